@@ -1,0 +1,693 @@
+// psl_api.cu -- the C ABI (include/pslb200.h): host logic above the kernels.
+//
+// Mirrors the reference's public surface (/root/reference/proj): parameter
+// defaults and validation (search.cpp:19-94), pow_int (sequence.cpp:95-105),
+// the ScanJob operator seam (search.cpp:156-175), neighborhood_scan
+// (search.cpp:296-321), evaluate_neighbor (sequence.cpp:180-196),
+// SidelobeTable::build (sequence.cpp:46-60), apply_flip
+// (sequence.cpp:198-224) and run_search (search.cpp:327-430), with the same
+// error classes (errors.hpp) mapped to status codes and the same messages.
+// There is no CPU fallback: without a CUDA device every compute entry point
+// returns PSL_ERR_CUDA.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "psl_internal.h"
+
+using namespace pslb;
+
+struct psl_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  uint32_t launches = 0;
+};
+
+struct psl_walks {
+  psl_ctx* ctx = nullptr;
+  psl_params params{};
+  uint32_t n_walks = 0;
+  RunArgs a{};
+  // device allocations
+  WalkState* st = nullptr;
+  int32_t* Cpiv = nullptr;
+  int32_t* Cloc = nullptr;
+  uint32_t* bits = nullptr;  // piv | loc | best | used, each n_walks * w_stride
+  int2* hlist = nullptr;
+  uint32_t* flips = nullptr;
+  psl_event* events = nullptr;
+  psl_trace* traces = nullptr;
+  uint64_t* seeds = nullptr;
+  uint32_t* init_bits = nullptr;
+};
+
+namespace {
+
+const char* kVersion = "0.1.0";  // version.hpp:5
+
+void set_err(char* err, size_t errlen, const std::string& msg) {
+  if (err && errlen) {
+    std::strncpy(err, msg.c_str(), errlen - 1);
+    err[errlen - 1] = 0;
+  }
+}
+
+int cuda_fail(char* err, size_t errlen, cudaError_t e, const char* what) {
+  set_err(err, errlen, std::string(what) + ": " + cudaGetErrorString(e));
+  return PSL_ERR_CUDA;
+}
+
+#define CK(call)                                                        \
+  do {                                                                  \
+    cudaError_t e_ = (call);                                            \
+    if (e_ != cudaSuccess) return cuda_fail(err, errlen, e_, #call);    \
+  } while (0)
+
+constexpr uint32_t kMinLength = 2;            // sequence.hpp:12
+constexpr uint32_t kMaxLength = 1u << 20;     // sequence.hpp:13
+
+std::string overflow_msg(bool neighbor, uint32_t L, uint32_t alpha) {
+  // search.cpp:276-280 (neighbour) / sequence.cpp:11-15 (fitness)
+  return std::string(neighbor ? "neighbor fitness is not finite at length "
+                              : "fitness sum is not finite at length ") +
+         std::to_string(L) + " with exponent " + std::to_string(alpha) +
+         "; lower the exponent (alpha2, then alpha1) until |C_k|^alpha sums stay "
+         "inside double range";
+}
+
+std::vector<uint32_t> pack_bits(const int8_t* s, uint32_t L, uint32_t pad) {
+  const uint32_t nw = (L + 31) / 32;
+  std::vector<uint32_t> b(nw + pad, 0u);
+  for (uint32_t i = 0; i < L; ++i)
+    if (s[i] < 0) b[i >> 5] |= 1u << (i & 31);
+  return b;
+}
+
+int check_sequence(const int8_t* s, uint32_t L, char* err, size_t errlen) {
+  // BinarySequence ctor (sequence.cpp:20-35)
+  if (L < kMinLength || L > kMaxLength) {
+    set_err(err, errlen, "sequence length " + std::to_string(L) + " out of supported range [" +
+                             std::to_string(kMinLength) + ", " + std::to_string(kMaxLength) + "]");
+    return PSL_ERR_CONFIG;
+  }
+  for (uint32_t i = 0; i < L; ++i) {
+    if (s[i] != 1 && s[i] != -1) {
+      set_err(err, errlen, "sequence element at position " + std::to_string(i) + " is " +
+                               std::to_string((int)s[i]) + "; elements must be +1 or -1");
+      return PSL_ERR_CONFIG;
+    }
+  }
+  return PSL_OK;
+}
+
+int device_ready(psl_ctx* ctx, char* err, size_t errlen) {
+  if (!ctx) { set_err(err, errlen, "null context"); return PSL_ERR_CUDA; }
+  CK(cudaSetDevice(ctx->device));
+  return PSL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* psl_version(void) { return kVersion; }
+
+int psl_ctx_create(int device, psl_ctx** out, char* err, size_t errlen) {
+  *out = nullptr;
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    set_err(err, errlen, std::string("no CUDA device available (") +
+                             (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices") +
+                             "); the B200 engine has no CPU fallback");
+    return PSL_ERR_CUDA;
+  }
+  if (device < 0 || device >= n) {
+    set_err(err, errlen, "device index " + std::to_string(device) + " out of range");
+    return PSL_ERR_CUDA;
+  }
+  CK(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10) {
+    set_err(err, errlen, std::string("device ") + prop.name +
+                             " is not sm_100 (Blackwell); this build targets sm_100a only");
+    return PSL_ERR_CUDA;
+  }
+  psl_ctx* c = new psl_ctx;
+  c->device = device;
+  CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
+  c->stream = c->own;
+  *out = c;
+  return PSL_OK;
+}
+
+void psl_ctx_destroy(psl_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->own) cudaStreamDestroy(ctx->own);
+  delete ctx;
+}
+
+int psl_ctx_set_stream(psl_ctx* ctx, void* stream) {
+  if (!ctx) return PSL_ERR_CUDA;
+  ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own;
+  return PSL_OK;
+}
+
+void* psl_ctx_stream(psl_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+uint32_t psl_kernel_launches(psl_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+// ---------------------------------------------------------------- params
+
+uint32_t psl_default_alpha2(uint32_t length) {
+  if (length < (1u << 18) - 1) return 13;
+  if (length < (1u << 19) - 1) return 11;
+  return 10;
+}
+uint32_t psl_default_n_lmt(uint32_t length) { return std::min(length, 1024u); }
+uint32_t psl_default_flip_lmt(uint32_t length) { return std::min(length, 10u); }
+
+void psl_default_params(uint32_t length, psl_params* p) {
+  std::memset(p, 0, sizeof(*p));
+  p->length = length;
+  p->seed = 1;
+  p->alpha1 = 4;
+  p->alpha2 = psl_default_alpha2(length);
+  p->ls_lmt = 2000;
+  p->flip_lmt = psl_default_flip_lmt(length);
+  p->n_lmt = psl_default_n_lmt(length);
+  p->workers = 1;
+}
+
+int psl_validate_params(const psl_params* in, psl_params* out, char* warning, size_t warnlen,
+                        char* err, size_t errlen) {
+  psl_params p = *in;
+  std::string warn;
+  auto fail = [&](const std::string& m) { set_err(err, errlen, m); return PSL_ERR_CONFIG; };
+  if (p.length < kMinLength || p.length > kMaxLength)
+    return fail("length " + std::to_string(p.length) + " out of supported range [" +
+                std::to_string(kMinLength) + ", " + std::to_string(kMaxLength) + "]");
+  if (p.alpha1 < 1 || p.alpha2 < 1) return fail("fitness exponents alpha1/alpha2 must be >= 1");
+  if (p.ls_lmt < 1) return fail("ls-lmt must be >= 1");
+  if (p.flip_lmt < 1) return fail("flip-lmt must be >= 1");
+  if (p.n_lmt < 1) return fail("n-lmt must be >= 1");
+  if (p.workers < 1 || p.workers > 4096) return fail("workers must be in [1, 4096]");
+  if (!p.has_max_nse && !p.has_max_seconds)
+    return fail("a stop condition is required: max-nse and/or max-seconds");
+  if (p.has_max_nse && p.max_nse < 1) return fail("max-nse must be >= 1");
+  if (p.has_max_seconds && !(std::isfinite(p.max_seconds) && p.max_seconds > 0))
+    return fail("max-seconds must be a positive finite number");
+  if (p.init) {
+    int rc = check_sequence(p.init, p.length, err, errlen);
+    if (rc) return rc;
+  }
+  if (p.n_lmt > p.length) {
+    warn += "n-lmt " + std::to_string(p.n_lmt) + " exceeds the " + std::to_string(p.length) +
+            " distinct one-flip neighbors; clamped to the length\n";
+    p.n_lmt = p.length;
+  }
+  if (p.flip_lmt > p.length) {
+    warn += "flip-lmt " + std::to_string(p.flip_lmt) + " exceeds the length; clamped to " +
+            std::to_string(p.length) + "\n";
+    p.flip_lmt = p.length;
+  }
+  if (warning && warnlen) set_err(warning, warnlen, warn);
+  if (out) *out = p;
+  return PSL_OK;
+}
+
+double psl_pow_int(double base, uint32_t exp) {
+  double result = 1.0, factor = base;
+  uint32_t e = exp;
+  while (e != 0) {
+    if (e & 1u) result *= factor;
+    e >>= 1;
+    if (e != 0) factor *= factor;
+  }
+  return result;
+}
+
+// ---------------------------------------------------------------- scans
+
+namespace {
+
+struct DevScan {
+  uint32_t* bits = nullptr;
+  int32_t* C = nullptr;
+  double* lut = nullptr;
+  int2* h = nullptr;
+  double* values = nullptr;
+  int32_t* psls = nullptr;
+  ~DevScan() {
+    cudaFree(bits); cudaFree(C); cudaFree(lut); cudaFree(h); cudaFree(values); cudaFree(psls);
+  }
+};
+
+// values[1..n], psls[1..n] of the n neighbours (start+i)%L of one pivot.
+int run_scan(psl_ctx* ctx, const int8_t* seq, const int32_t* table, uint32_t L, uint32_t start,
+             uint32_t n, const double* lut, uint32_t lut_size, double* values, int32_t* psls,
+             char* err, size_t errlen) {
+  int rc = device_ready(ctx, err, errlen);
+  if (rc) return rc;
+  const uint32_t nw = (L + 31) / 32;
+  std::vector<uint32_t> bits = pack_bits(seq, L, kBitsPad);
+  int32_t P = 0;
+  for (uint32_t k = 1; k < L; ++k) P = std::max(P, std::abs(table[k]));
+  std::vector<int2> h;
+  for (uint32_t k = 1; k < L; ++k)
+    if (std::abs(table[k]) >= P - 8) h.push_back(make_int2((int)k, table[k]));
+  DevScan d;
+  cudaStream_t s = ctx->stream;
+  CK(cudaMalloc(&d.bits, bits.size() * 4));
+  CK(cudaMalloc(&d.C, (size_t)L * 4));
+  CK(cudaMalloc(&d.lut, (size_t)lut_size * 8));
+  CK(cudaMalloc(&d.h, std::max<size_t>(h.size(), 1) * sizeof(int2)));
+  CK(cudaMalloc(&d.values, ((size_t)n + 1) * 8));
+  CK(cudaMalloc(&d.psls, ((size_t)n + 1) * 4));
+  CK(cudaMemcpyAsync(d.bits, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d.C, table, (size_t)L * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d.lut, lut, (size_t)lut_size * 8, cudaMemcpyHostToDevice, s));
+  if (!h.empty()) CK(cudaMemcpyAsync(d.h, h.data(), h.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+  ScanArgs a{};
+  a.L = L; a.n = n; a.start = start; a.nwords = nw;
+  a.nchunks = (L - 1 + kChunk - 1) / kChunk;
+  a.lut_size = lut_size; a.P = P; a.hcount = (uint32_t)h.size();
+  a.bits = d.bits; a.C = d.C; a.lut = d.lut; a.hlist = d.h; a.values = d.values; a.psls = d.psls;
+  if (launch_scan(a, s) < 0) return cuda_fail(err, errlen, cudaGetLastError(), "scan_kernel");
+  ctx->launches += 1;
+  CK(cudaMemcpyAsync(values + 1, d.values + 1, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(psls + 1, d.psls + 1, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return PSL_OK;
+}
+
+}  // namespace
+
+int psl_scan(psl_ctx* ctx, const psl_scan_job* job, char* err, size_t errlen) {
+  if (!job || !job->seq || !job->table || !job->lut || !job->values || !job->psls) {
+    set_err(err, errlen, "psl_scan: null pointer in job");
+    return PSL_ERR_CONFIG;
+  }
+  if (job->length < kMinLength || job->start >= job->length || job->n < 1 ||
+      job->n > job->length) {
+    set_err(err, errlen, "psl_scan: job out of range");
+    return PSL_ERR_CONFIG;
+  }
+  return run_scan(ctx, job->seq, job->table, job->length, job->start, job->n, job->lut,
+                  job->lut_size, job->values, job->psls, err, errlen);
+}
+
+int psl_neighborhood_scan(psl_ctx* ctx, const int8_t* seq, const int32_t* table,
+                          const double* lut, uint32_t lut_size, uint32_t alpha, uint32_t L,
+                          uint32_t start, uint32_t n, psl_scan_result* out, char* err,
+                          size_t errlen) {
+  int rc = check_sequence(seq, L, err, errlen);
+  if (rc) return rc;
+  // search.cpp:300-312
+  if (start >= L) {
+    set_err(err, errlen, "scan start position " + std::to_string(start) +
+                             " out of range for length " + std::to_string(L));
+    return PSL_ERR_CONFIG;
+  }
+  if (n < 1 || n > L) { set_err(err, errlen, "scan size must be in [1, length]"); return PSL_ERR_CONFIG; }
+  if (lut_size < L + 1) { set_err(err, errlen, "power table too small for sequence length"); return PSL_ERR_CONFIG; }
+  std::vector<double> values((size_t)n + 1);
+  std::vector<int32_t> psls((size_t)n + 1);
+  rc = run_scan(ctx, seq, table, L, start, n, lut, lut_size, values.data(), psls.data(), err, errlen);
+  if (rc) return rc;
+  // reduce_scan (search.cpp:271-292)
+  uint32_t bi = 1, pi = 1;
+  double v = values[1];
+  int32_t pm = psls[1];
+  for (uint32_t i = 1; i <= n; ++i) {
+    if (!std::isfinite(values[i])) {
+      set_err(err, errlen, overflow_msg(true, L, alpha));
+      return PSL_ERR_OVERFLOW;
+    }
+    if (values[i] < v) { v = values[i]; bi = i; }
+    if (psls[i] < pm) { pm = psls[i]; pi = i; }
+  }
+  out->best_index = (uint32_t)(((uint64_t)start + bi) % L);
+  out->value_step = v;
+  out->best_neighbor_psl = pm;
+  out->best_psl_index = (uint32_t)(((uint64_t)start + pi) % L);
+  return PSL_OK;
+}
+
+int psl_evaluate_neighbor(psl_ctx* ctx, const int8_t* seq, const int32_t* table,
+                          const double* lut, uint32_t lut_size, uint32_t alpha, uint32_t L,
+                          uint32_t j, double* fitness, int32_t* psl, char* err, size_t errlen) {
+  int rc = check_sequence(seq, L, err, errlen);
+  if (rc) return rc;
+  // sequence.cpp:182-192
+  if (j >= L) {
+    set_err(err, errlen, "neighbor position " + std::to_string(j) + " out of range for length " +
+                             std::to_string(L));
+    return PSL_ERR_CONFIG;
+  }
+  if (lut_size < L + 1) { set_err(err, errlen, "power table too small for sequence length"); return PSL_ERR_CONFIG; }
+  double values[2];
+  int32_t psls[2];
+  rc = run_scan(ctx, seq, table, L, (j + L - 1) % L, 1, lut, lut_size, values, psls, err, errlen);
+  if (rc) return rc;
+  if (!std::isfinite(values[1])) {
+    set_err(err, errlen, overflow_msg(false, L, alpha));
+    return PSL_ERR_OVERFLOW;
+  }
+  *fitness = values[1];
+  *psl = psls[1];
+  return PSL_OK;
+}
+
+int psl_build_table(psl_ctx* ctx, const int8_t* seq, uint32_t L, int32_t* table_out, char* err,
+                    size_t errlen) {
+  int rc = check_sequence(seq, L, err, errlen);
+  if (rc) return rc;
+  rc = device_ready(ctx, err, errlen);
+  if (rc) return rc;
+  const uint32_t nw = (L + 31) / 32;
+  std::vector<uint32_t> bits = pack_bits(seq, L, kBitsPad);
+  uint32_t* db = nullptr;
+  int32_t* dc = nullptr;
+  cudaStream_t s = ctx->stream;
+  CK(cudaMalloc(&db, bits.size() * 4));
+  CK(cudaMalloc(&dc, (size_t)L * 4));
+  CK(cudaMemcpyAsync(db, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice, s));
+  if (launch_table_only(db, dc, L, nw, s) < 0) {
+    cudaFree(db); cudaFree(dc);
+    return cuda_fail(err, errlen, cudaGetLastError(), "build_tables_kernel");
+  }
+  ctx->launches += 1;
+  cudaError_t e = cudaMemcpyAsync(table_out, dc, (size_t)L * 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(db);
+  cudaFree(dc);
+  if (e != cudaSuccess) return cuda_fail(err, errlen, e, "build_table");
+  return PSL_OK;
+}
+
+int psl_apply_flip(psl_ctx* ctx, int8_t* seq, int32_t* table, uint32_t L, uint32_t j, char* err,
+                   size_t errlen) {
+  int rc = check_sequence(seq, L, err, errlen);
+  if (rc) return rc;
+  if (j >= L) {
+    set_err(err, errlen, "flip position " + std::to_string(j) + " out of range for length " +
+                             std::to_string(L));
+    return PSL_ERR_CONFIG;
+  }
+  rc = device_ready(ctx, err, errlen);
+  if (rc) return rc;
+  std::vector<uint32_t> bits = pack_bits(seq, L, kBitsPad);
+  uint32_t* db = nullptr;
+  int32_t* dc = nullptr;
+  cudaStream_t s = ctx->stream;
+  CK(cudaMalloc(&db, bits.size() * 4));
+  CK(cudaMalloc(&dc, (size_t)L * 4));
+  CK(cudaMemcpyAsync(db, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dc, table, (size_t)L * 4, cudaMemcpyHostToDevice, s));
+  if (launch_apply_flip(db, dc, L, j, s) < 0) {
+    cudaFree(db); cudaFree(dc);
+    return cuda_fail(err, errlen, cudaGetLastError(), "apply_flip_kernel");
+  }
+  ctx->launches += 2;
+  cudaError_t e = cudaMemcpyAsync(table, dc, (size_t)L * 4, cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  cudaFree(db);
+  cudaFree(dc);
+  if (e != cudaSuccess) return cuda_fail(err, errlen, e, "apply_flip");
+  seq[j] = (int8_t)-seq[j];
+  return PSL_OK;
+}
+
+// ---------------------------------------------------------------- walks
+
+void psl_walks_destroy(psl_walks* w) {
+  if (!w) return;
+  cudaSetDevice(w->ctx->device);
+  cudaFree(w->st); cudaFree(w->Cpiv); cudaFree(w->Cloc); cudaFree(w->bits); cudaFree(w->hlist);
+  cudaFree(w->flips); cudaFree(w->events); cudaFree(w->traces); cudaFree(w->seeds);
+  cudaFree(w->init_bits);
+  delete w;
+}
+
+namespace {
+
+int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const uint64_t* seeds,
+                 const int8_t* inits, uint64_t events_cap, uint64_t traces_cap, psl_walks** out,
+                 char* err, size_t errlen) {
+  *out = nullptr;
+  psl_params p;
+  int rc = psl_validate_params(params, &p, nullptr, 0, err, errlen);
+  if (rc) return rc;
+  if (n_walks < 1) { set_err(err, errlen, "n_walks must be >= 1"); return PSL_ERR_CONFIG; }
+  if (inits) {
+    for (uint32_t w = 0; w < n_walks; ++w) {
+      rc = check_sequence(inits + (size_t)w * p.length, p.length, err, errlen);
+      if (rc) return rc;
+    }
+  }
+  rc = device_ready(ctx, err, errlen);
+  if (rc) return rc;
+  psl_walks* W = new psl_walks;
+  W->ctx = ctx;
+  W->params = p;
+  W->n_walks = n_walks;
+  const uint32_t L = p.length;
+  const uint32_t nw = (L + 31) / 32;
+  RunArgs& a = W->a;
+  a.L = L; a.n = p.n_lmt; a.alpha1 = p.alpha1; a.alpha2 = p.alpha2;
+  a.ls_lmt = p.ls_lmt; a.flip_lmt = p.flip_lmt;
+  a.nwords = nw;
+  a.nchunks = (L - 1 + kChunk - 1) / kChunk;
+  a.has_max_nse = p.has_max_nse; a.max_nse = p.max_nse;
+  a.has_max_seconds = p.has_max_seconds; a.max_seconds = p.max_seconds;
+  a.step_budget = 0xffffffffu;
+  a.record_events = events_cap > 0;
+  a.record_traces = traces_cap > 0;
+  a.events_cap = events_cap;
+  a.traces_cap = traces_cap;
+  a.c_stride = ((size_t)L + 31) & ~size_t(31);
+  a.w_stride = ((size_t)nw + kBitsPad + 3) & ~size_t(3);
+  a.h_stride = L;
+  a.f_stride = std::max<uint32_t>(p.flip_lmt, 1);
+  auto fail = [&](cudaError_t e, const char* what) {
+    psl_walks_destroy(W);
+    return cuda_fail(err, errlen, e, what);
+  };
+  cudaError_t e;
+#define AL(ptr, bytes) \
+  if ((e = cudaMalloc(&(ptr), (bytes))) != cudaSuccess) return fail(e, "cudaMalloc " #ptr);
+  AL(W->st, sizeof(WalkState) * n_walks);
+  AL(W->Cpiv, a.c_stride * 4 * n_walks);
+  AL(W->Cloc, a.c_stride * 4 * n_walks);
+  AL(W->bits, a.w_stride * 4 * n_walks * 4);
+  AL(W->hlist, a.h_stride * sizeof(int2) * n_walks);
+  AL(W->flips, a.f_stride * 4 * n_walks);
+  AL(W->seeds, 8ull * n_walks);
+  if (events_cap) AL(W->events, sizeof(psl_event) * events_cap * n_walks);
+  if (traces_cap) AL(W->traces, sizeof(psl_trace) * traces_cap * n_walks);
+  a.st = W->st; a.Cpiv = W->Cpiv; a.Cloc = W->Cloc;
+  a.bits_piv = W->bits;
+  a.bits_loc = W->bits + a.w_stride * n_walks;
+  a.bits_best = W->bits + 2 * a.w_stride * n_walks;
+  a.used = W->bits + 3 * a.w_stride * n_walks;
+  a.hlist = W->hlist; a.flips = W->flips; a.events = W->events; a.traces = W->traces;
+  cudaStream_t s = ctx->stream;
+  std::vector<uint64_t> sd(n_walks);
+  for (uint32_t w = 0; w < n_walks; ++w) sd[w] = seeds ? seeds[w] : p.seed + w;
+  if ((e = cudaMemcpyAsync(W->seeds, sd.data(), 8ull * n_walks, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+    return fail(e, "seeds");
+  const int8_t* init_src = inits ? inits : nullptr;
+  std::vector<uint32_t> ib;
+  if (!init_src && p.init) {
+    // run_search warm start: the same init for every walk
+    init_src = p.init;
+  }
+  if (init_src) {
+    ib.assign((size_t)nw * n_walks, 0u);
+    for (uint32_t w = 0; w < n_walks; ++w) {
+      const int8_t* sq = inits ? inits + (size_t)w * L : p.init;
+      for (uint32_t i = 0; i < L; ++i)
+        if (sq[i] < 0) ib[(size_t)w * nw + (i >> 5)] |= 1u << (i & 31);
+    }
+    AL(W->init_bits, ib.size() * 4);
+    if ((e = cudaMemcpyAsync(W->init_bits, ib.data(), ib.size() * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+      return fail(e, "init bits");
+  }
+#undef AL
+  if (launch_init_walks(a, n_walks, W->seeds, W->init_bits, s) < 0)
+    return fail(cudaGetLastError(), "init_walks_kernel");
+  if (launch_build_tables(a, n_walks, s) < 0) return fail(cudaGetLastError(), "build_tables_kernel");
+  ctx->launches += 2;
+  if (init_src) {
+    // the upload buffer is consumed by init_walks_kernel; keep it until sync
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(e, "init sync");
+  }
+  *out = W;
+  return PSL_OK;
+}
+
+int walks_launch(psl_walks* W, uint32_t steps, char* err, size_t errlen) {
+  RunArgs a = W->a;
+  a.step_budget = steps;
+  if (launch_run(a, W->n_walks, W->ctx->stream) < 0)
+    return cuda_fail(err, errlen, cudaGetLastError(), "run_kernel");
+  W->ctx->launches += 1;
+  return PSL_OK;
+}
+
+}  // namespace
+
+int psl_walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks,
+                     const uint64_t* seeds, const int8_t* inits, psl_walks** out, char* err,
+                     size_t errlen) {
+  return walks_create(ctx, params, n_walks, seeds, inits, 0, 0, out, err, errlen);
+}
+
+int psl_walks_step(psl_walks* w, uint32_t steps, char* err, size_t errlen) {
+  if (!w) return PSL_ERR_CONFIG;
+  int rc = device_ready(w->ctx, err, errlen);
+  if (rc) return rc;
+  return walks_launch(w, steps, err, errlen);
+}
+
+int psl_walks_run(psl_walks* w, char* err, size_t errlen) {
+  return psl_walks_step(w, 0xffffffffu, err, errlen);
+}
+
+int psl_walks_records(psl_walks* w, psl_walk_record* records, int8_t* solutions, char* err,
+                      size_t errlen) {
+  if (!w) return PSL_ERR_CONFIG;
+  int rc = device_ready(w->ctx, err, errlen);
+  if (rc) return rc;
+  cudaStream_t s = w->ctx->stream;
+  std::vector<WalkState> st(w->n_walks);
+  CK(cudaMemcpyAsync(st.data(), w->st, sizeof(WalkState) * w->n_walks, cudaMemcpyDeviceToHost, s));
+  std::vector<uint32_t> bb;
+  const uint32_t L = w->a.L, nw = w->a.nwords;
+  if (solutions) {
+    bb.resize(w->a.w_stride * w->n_walks);
+    CK(cudaMemcpyAsync(bb.data(), w->a.bits_best, bb.size() * 4, cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  (void)nw;
+  for (uint32_t i = 0; i < w->n_walks; ++i) {
+    const WalkState& S = st[i];
+    psl_walk_record& r = records[i];
+    r.seed = S.seed;
+    r.nse = S.nse;
+    const uint64_t end = S.end_ns ? S.end_ns : S.t0_ns;
+    r.elapsed_seconds = S.t0_ns ? (double)(end - S.t0_ns) * 1e-9 : 0.0;
+    r.psl_best = S.psl_best < 0 ? S.P : S.psl_best;
+    r.status = S.status;
+    r.energy = S.energy_best;
+    r.merit_factor = ((double)L * (double)L) / (2.0 * (double)S.energy_best);
+    r.switches = S.switches;
+    r.steps = S.steps;
+    if (solutions) {
+      const uint32_t* b = bb.data() + (size_t)i * w->a.w_stride;
+      int8_t* o = solutions + (size_t)i * L;
+      for (uint32_t k = 0; k < L; ++k) o[k] = ((b[k >> 5] >> (k & 31)) & 1u) ? -1 : 1;
+    }
+  }
+  return PSL_OK;
+}
+
+int psl_run_walks(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const uint64_t* seeds,
+                  const int8_t* inits, psl_walk_record* records, int8_t* solutions, char* err,
+                  size_t errlen) {
+  psl_walks* w = nullptr;
+  int rc = psl_walks_create(ctx, params, n_walks, seeds, inits, &w, err, errlen);
+  if (rc) return rc;
+  rc = psl_walks_run(w, err, errlen);
+  if (!rc) rc = psl_walks_records(w, records, solutions, err, errlen);
+  psl_walks_destroy(w);
+  return rc;
+}
+
+// ---------------------------------------------------------------- run_search
+
+int psl_run_search(psl_ctx* ctx, const psl_params* params, const psl_hooks* hooks,
+                   psl_run_record* out, int8_t* solution_best, char* err, size_t errlen) {
+  const bool want_traces = hooks && hooks->on_scan;
+  const uint64_t ecap = 1u << 16, tcap = want_traces ? (1u << 16) : 0;
+  psl_walks* W = nullptr;
+  int rc = walks_create(ctx, params, 1, nullptr, nullptr, ecap, tcap, &W, err, errlen);
+  if (rc) return rc;
+  cudaStream_t s = ctx->stream;
+  std::vector<psl_event> ev;
+  std::vector<psl_trace> tr;
+  uint64_t n_ev = 0, n_tr = 0;
+  WalkState S{};
+  for (;;) {
+    rc = walks_launch(W, 0xffffffffu, err, errlen);
+    if (rc) break;
+    cudaError_t e = cudaMemcpyAsync(&S, W->st, sizeof(S), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) { rc = cuda_fail(err, errlen, e, "run_search"); break; }
+    // drain (all buffered entries are final when the kernel returns)
+    ev.resize(S.n_events);
+    tr.resize(S.n_traces);
+    if (S.n_events)
+      e = cudaMemcpyAsync(ev.data(), W->events, sizeof(psl_event) * S.n_events, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && S.n_traces)
+      e = cudaMemcpyAsync(tr.data(), W->traces, sizeof(psl_trace) * S.n_traces, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) { rc = cuda_fail(err, errlen, e, "drain"); break; }
+    // hooks fire in event order; traces after the events of the same step are
+    // interleaved by nse (an event never has a larger nse than its step's trace)
+    size_t ie = 0, it = 0;
+    while (ie < ev.size() || it < tr.size()) {
+      if (ie < ev.size() && (it >= tr.size() || ev[ie].nse <= tr[it].nse)) {
+        if (hooks && hooks->on_event) hooks->on_event(&ev[ie], hooks->user);
+        ++ie;
+      } else {
+        if (hooks && hooks->on_scan) hooks->on_scan(&tr[it], hooks->user);
+        ++it;
+      }
+    }
+    n_ev += S.n_events;
+    n_tr += S.n_traces;
+    if (S.n_events || S.n_traces) {
+      WalkState reset = S;
+      reset.n_events = 0;
+      reset.n_traces = 0;
+      e = cudaMemcpyAsync(W->st, &reset, sizeof(reset), cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+      if (e != cudaSuccess) { rc = cuda_fail(err, errlen, e, "reset"); break; }
+    }
+    if (S.status != PSL_OK) {
+      const uint32_t L = W->a.L;
+      set_err(err, errlen, overflow_msg(S.err_kind == 2, L, S.err_alpha));
+      rc = PSL_ERR_OVERFLOW;
+      break;
+    }
+    if (S.done) break;
+  }
+  if (rc == PSL_OK) {
+    psl_walk_record r{};
+    rc = psl_walks_records(W, &r, solution_best, err, errlen);
+    if (rc == PSL_OK) {
+      out->nse = r.nse;
+      out->elapsed_seconds = r.elapsed_seconds;
+      out->psl_best = r.psl_best;
+      out->merit_factor = r.merit_factor;
+      out->energy = r.energy;
+      out->n_events = n_ev;
+      out->n_traces = n_tr;
+      out->switches = r.switches;
+    }
+  }
+  psl_walks_destroy(W);
+  return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,100 @@
+// psl_internal.h -- shared between the kernels (psl_kernels.cu) and the C-ABI
+// host layer (psl_api.cu).  Not part of the public boundary (include/pslb200.h).
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+#include "../../include/pslb200.h"
+
+namespace pslb {
+
+constexpr int kThreads = 1024;     // one CTA per walk; thread t scores neighbour i = t+1
+constexpr int kChunk = 512;        // k records staged in shared memory per chunk
+constexpr int kRecDoubles = 8;     // per-k record: BOTH[e4,e2,e2,e0] ONE[e3,e1,e1,e2]
+constexpr int kHCap = 1024;        // filtered high-sidelobe list kept in smem
+constexpr int kBitsPad = 8;        // zero words after each global bit array
+
+// Per-walk device state (global memory), resumable across launches.
+struct WalkState {
+  uint64_t rng[4];
+  uint64_t seed;
+  uint64_t nse;
+  uint64_t unimproved;
+  uint64_t switches;
+  uint64_t steps;
+  uint64_t t0_ns;
+  uint64_t end_ns;
+  uint64_t n_events;
+  uint64_t n_traces;
+  double value_local;
+  int64_t energy_best;
+  int32_t psl_best;
+  int32_t P;            // PSL of the pivot table after the last pass
+  int32_t P_local;      // PSL of the phase-local snapshot table
+  uint32_t phase;
+  uint32_t n_pending;   // pending flips the next pass folds into C
+  uint32_t src_local;   // next pass reads C from the local snapshot (restart)
+  uint32_t local_pending;    // next pass also writes the local snapshot C
+  uint32_t fitness_pending;  // next pass runs the serial pivot-fitness chain
+  int32_t status;       // PSL_OK / PSL_ERR_OVERFLOW
+  uint32_t err_alpha;
+  uint32_t err_kind;    // 1 fitness(), 2 reduce_scan()
+  uint32_t done;        // stop condition reached
+  uint32_t trace_patch; // 1: last trace waits for value_local
+  uint32_t switch_pending;  // 1: last event is a provisional phase-switch
+};
+
+struct RunArgs {
+  uint32_t L, n, alpha1, alpha2, ls_lmt, flip_lmt;
+  uint32_t nwords, nchunks;
+  int32_t has_max_nse, has_max_seconds;
+  uint64_t max_nse;
+  double max_seconds;
+  uint32_t step_budget;
+  int32_t record_events, record_traces;
+  uint64_t events_cap, traces_cap;
+  WalkState* st;
+  int32_t* Cpiv;
+  int32_t* Cloc;
+  size_t c_stride;
+  uint32_t* bits_piv;
+  uint32_t* bits_loc;
+  uint32_t* bits_best;
+  uint32_t* used;
+  size_t w_stride;
+  int2* hlist;
+  size_t h_stride;
+  uint32_t* flips;
+  size_t f_stride;
+  psl_event* events;
+  psl_trace* traces;
+};
+
+struct ScanArgs {
+  uint32_t L, n, start, nwords, nchunks, lut_size;
+  int32_t P;            // PSL of the given table
+  uint32_t hcount;
+  const uint32_t* bits;
+  const int32_t* C;
+  const double* lut;
+  const int2* hlist;    // all k with |C_k| >= P - 8
+  double* values;       // [n+1]
+  int32_t* psls;        // [n+1]
+};
+
+size_t run_smem_bytes(uint32_t nwords);
+
+// Launchers (return the number of kernels launched, or -1 on launch error).
+int launch_init_walks(const RunArgs& a, uint32_t n_walks, const uint64_t* d_seeds,
+                      const uint32_t* d_init_bits, cudaStream_t s);
+int launch_build_tables(const RunArgs& a, uint32_t n_walks, cudaStream_t s);
+int launch_run(const RunArgs& a, uint32_t n_walks, cudaStream_t s);
+int launch_scan(const ScanArgs& a, cudaStream_t s);
+int launch_table_only(const uint32_t* d_bits, int32_t* d_C, uint32_t L, uint32_t nwords,
+                      cudaStream_t s);
+int launch_apply_flip(uint32_t* d_bits, int32_t* d_C, uint32_t L, uint32_t j, cudaStream_t s);
+
+}  // namespace pslb

@@ -1,0 +1,989 @@
+// psl_kernels.cu -- sm_100a kernels for the two-phase low-PSL search hot path.
+//
+// Reference path (/root/reference/proj): detail::eval_flip (sequence.hpp:126-162)
+// called n_lmt times per step by scan_chunk/ScanPool (search.cpp:156-260),
+// reduce_scan (search.cpp:271-292), apply_flip (sequence.cpp:198-224) and the
+// run_search step loop (search.cpp:327-430).
+//
+// B200 design (DESIGN.md has the full derivation):
+//  * one persistent CTA (1024 threads) per walk; thread t scores neighbour
+//    i = t+1 of the pivot.  The whole step loop -- scan, argmin/PSL
+//    reduction, move, snapshots, restarts, RNG, events -- stays on device.
+//  * C_k lives in HBM/L2 and is streamed through shared memory in chunks of
+//    512 shifts.  While streaming, the builder threads fold the previous
+//    step's accepted flip(s) into C (the O(L) apply_flip is fused into the
+//    next sweep) and expand every C_k into a 64-byte record of the five
+//    possible terms |C_k + d|^alpha, d in {-4,-2,0,+2,+4}.
+//  * every neighbour's fitness is the reference's serial ascending-k double
+//    chain (one DADD per cell, RN, no reassociation), so values are
+//    bit-identical.  Per cell a thread only turns two sequence bits into a
+//    record offset (SHF + LOP3), loads the term (LDS.64) and adds it.
+//  * the sequence is bit-packed in shared memory (bit = 1 <-> -1); per
+//    32-shift block each lane slides two 32-bit windows (s_{j-k}, s_{j+k}).
+//  * neighbour PSL is exact but not computed per cell: only shifts with
+//    |C_k| >= PSL(pivot) - 8 can hold a neighbour's peak, and those are
+//    collected while streaming.
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "psl_internal.h"
+
+namespace pslb {
+
+namespace {
+
+constexpr uint32_t FULL = 0xffffffffu;
+
+// ------------------------------------------------------------ primitives
+
+__device__ __forceinline__ uint64_t rotl64(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+
+// rng.hpp:20-30
+__device__ __forceinline__ void rng_seed(uint64_t* s, uint64_t seed) {
+  uint64_t z = seed;
+  for (int i = 0; i < 4; ++i) {
+    z += 0x9e3779b97f4a7c15ull;
+    uint64_t x = z;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    s[i] = x ^ (x >> 31);
+  }
+}
+
+// rng.hpp:32-42
+__device__ __forceinline__ uint64_t rng_next(uint64_t* s) {
+  const uint64_t result = rotl64(s[1] * 5, 7) * 9;
+  const uint64_t t = s[1] << 17;
+  s[2] ^= s[0];
+  s[3] ^= s[1];
+  s[1] ^= s[2];
+  s[0] ^= s[3];
+  s[2] ^= t;
+  s[3] = rotl64(s[3], 45);
+  return result;
+}
+
+// rng.hpp:46-52
+__device__ __forceinline__ uint64_t rng_bounded(uint64_t* s, uint64_t n) {
+  const uint64_t mask = (n <= 1) ? 0ull : (~0ull >> __clzll((long long)(n - 1)));
+  for (;;) {
+    const uint64_t v = rng_next(s) & mask;
+    if (v < n) return v;
+  }
+}
+
+// sequence.cpp:95-105 -- same factor order, IEEE round-to-nearest multiplies.
+__device__ __forceinline__ double pow_int_dev(double base, uint32_t e) {
+  double result = 1.0, factor = base;
+  while (e != 0) {
+    if (e & 1u) result = __dmul_rn(result, factor);
+    e >>= 1;
+    if (e != 0) factor = __dmul_rn(factor, factor);
+  }
+  return result;
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// bits 0..15 / 16..31 of x to the even bit positions of a 32-bit word
+__device__ __forceinline__ uint32_t spread_lo(uint32_t x) {
+  x = __byte_perm(x, 0u, 0x4140);
+  x = (x | (x << 4)) & 0x0F0F0F0Fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
+__device__ __forceinline__ uint32_t spread_hi(uint32_t x) {
+  x = __byte_perm(x, 0u, 0x4342);
+  x = (x | (x << 4)) & 0x0F0F0F0Fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
+
+// sequence value at position x (0 <= x < L) from the padded smem bit array
+__device__ __forceinline__ int sval(const uint32_t* sb, uint32_t x) {
+  return 1 - 2 * (int)((sb[(x >> 5) + 1] >> (x & 31)) & 1u);
+}
+
+// padded word fetch; word index w may run past either end (reads a zero pad)
+__device__ __forceinline__ uint32_t sword(const uint32_t* sb, int w, int nwords) {
+  w = max(-1, min(w, nwords));
+  return sb[w + 1];
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+  for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+
+// ------------------------------------------------------------ shared layout
+
+struct Ctl {
+  WalkState st;
+  double rv[32];
+  uint32_t ri[32];
+  int32_t rp[32];
+  uint32_t rpi[32];
+  int32_t rbad[32];
+  int32_t rmax[32];
+  long long re[32];
+  double best_v, fit, cv;
+  uint32_t best_i, best_pi, ci, cpi;
+  int32_t best_psl, bad, cp, cbad;
+  uint32_t start, jstar, ppos;
+  int32_t do_scan, need_pass, imp, improve, restart;
+  uint32_t hcount, hf_count, steps_this_launch;
+  int32_t P_new;
+  long long energy;
+};
+
+constexpr size_t kTabBytes = 2ull * kChunk * kRecDoubles * sizeof(double);
+constexpr size_t kTailBytes = 2ull * kChunk * sizeof(double);
+constexpr size_t kHfBytes = (size_t)kHCap * sizeof(int2);
+constexpr size_t kCtlBytes = (sizeof(Ctl) + 15) & ~size_t(15);
+
+struct Smem {
+  double* tab;     // [2][kChunk][8]
+  double* tail;    // [2][kChunk]
+  int2* hf;        // [kHCap]
+  Ctl* ctl;
+  uint32_t* sb;    // [nwords + 2], sb[0] and sb[nwords+1] are zero pads
+};
+
+__device__ __forceinline__ Smem carve(unsigned char* base) {
+  Smem m;
+  m.tab = reinterpret_cast<double*>(base);
+  m.tail = reinterpret_cast<double*>(base + kTabBytes);
+  m.hf = reinterpret_cast<int2*>(base + kTabBytes + kTailBytes);
+  m.ctl = reinterpret_cast<Ctl*>(base + kTabBytes + kTailBytes + kHfBytes);
+  m.sb = reinterpret_cast<uint32_t*>(base + kTabBytes + kTailBytes + kHfBytes + kCtlBytes);
+  return m;
+}
+
+// ------------------------------------------------------------ the sweep
+
+struct SweepIO {
+  uint32_t L, nwords, nchunks;
+  const int32_t* Csrc;
+  int32_t* Cdst;             // nullptr: do not write C back
+  int32_t* Cloc;             // nullptr: no local-snapshot copy
+  const uint32_t* flips;     // pending flips folded into C while streaming
+  uint32_t F;
+  uint32_t alpha;            // terms = pow_int(a, alpha) ...
+  const double* lut;         // ... or lut[a] when non-null (ScanJob mode)
+  uint32_t lut_size;
+  int2* hlist;               // nullptr: no high-sidelobe collection
+  uint32_t* hcount;          // smem counter
+  int32_t hthr;
+  bool scan;                 // score neighbours
+  bool chain;                // thread 0 runs the pivot fitness chain
+};
+
+// apply_flip (sequence.cpp:198-224) folded into one C_k, for F pending flips
+// applied in order.  sb holds the sequence AFTER all of them.
+__device__ __forceinline__ int32_t fold_flips(int32_t cv, uint32_t k, const SweepIO& io,
+                                              const uint32_t* sb) {
+  for (uint32_t i = 0; i < io.F; ++i) {
+    const uint32_t f = io.flips[i];
+    int acc = 0;
+    if (k <= f) {
+      const uint32_t x = f - k;
+      int s = sval(sb, x);
+      for (uint32_t m = i + 1; m < io.F; ++m) s = (io.flips[m] == x) ? -s : s;
+      acc += s;
+    }
+    if (f + k < io.L) {
+      const uint32_t x = f + k;
+      int s = sval(sb, x);
+      for (uint32_t m = i + 1; m < io.F; ++m) s = (io.flips[m] == x) ? -s : s;
+      acc += s;
+    }
+    const int sf = -sval(sb, f);  // value of s_f before flip i
+    cv += -2 * sf * acc;
+  }
+  return cv;
+}
+
+__device__ __forceinline__ double term(const SweepIO& io, int32_t a) {
+  if (io.lut) return (uint32_t)a < io.lut_size ? io.lut[a] : 0.0;
+  return pow_int_dev((double)a, io.alpha);
+}
+
+// Expand chunk c of C into the per-k term records.
+__device__ __forceinline__ void build_chunk(const SweepIO& io, uint32_t c, double* tab,
+                                            double* tail, const uint32_t* sb, int32_t& pmax) {
+  const uint32_t t = threadIdx.x;
+  if (t >= (uint32_t)kChunk) return;
+  const uint32_t k = 1 + c * kChunk + t;
+  double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0, e4 = 0.0;
+  bool want = false;
+  int32_t cv = 0;
+  if (k < io.L) {
+    cv = io.Csrc[k];
+    if (io.F) cv = fold_flips(cv, k, io, sb);
+    if (io.Cdst) io.Cdst[k] = cv;
+    if (io.Cloc) io.Cloc[k] = cv;
+    const int32_t av = abs(cv);
+    pmax = max(pmax, av);
+    want = io.hlist != nullptr && av >= io.hthr;
+    e2 = term(io, av);
+    e4 = term(io, abs(cv - 4));
+    e3 = term(io, abs(cv - 2));
+    e1 = term(io, abs(cv + 2));
+    e0 = term(io, abs(cv + 4));
+  }
+  if (io.hlist) {
+    const uint32_t m = __ballot_sync(FULL, want);
+    if (m) {
+      const int lane = t & 31, leader = __ffs(m) - 1;
+      uint32_t base = 0;
+      if (lane == leader) base = atomicAdd(io.hcount, (uint32_t)__popc(m));
+      base = __shfl_sync(FULL, base, leader);
+      if (want) io.hlist[base + __popc(m & ((1u << lane) - 1))] = make_int2((int)k, cv);
+    }
+  }
+  double2* rec = reinterpret_cast<double2*>(tab + (size_t)t * kRecDoubles);
+  rec[0] = make_double2(e4, e2);   // BOTH slot = 2*bA' + bB'
+  rec[1] = make_double2(e2, e0);
+  rec[2] = make_double2(e3, e1);   // ONE  slot = one valid bit
+  rec[3] = make_double2(e1, e2);   // (slot 3: e2, unused)
+  tail[t] = e2;
+}
+
+enum : int { CLS_BOTH = 0, CLS_ONE = 1, CLS_TAIL = 2, CLS_MIXED = 3 };
+
+// One full sweep over k = 1..L-1.  Returns this lane's neighbour fitness.
+__device__ __forceinline__ double sweep(const SweepIO& io, const Smem& sm, bool active,
+                                        uint32_t j, int32_t& pmax, double& chain) {
+  const uint32_t L = io.L;
+  const int nwords = (int)io.nwords;
+  const uint32_t* sb = sm.sb;
+  // lane geometry (sequence.hpp:131-135)
+  const uint32_t left = j, right = L - 1 - j;
+  const uint32_t be = left < right ? left : right;   // both-sides range end
+  const uint32_t oe = left < right ? right : left;   // one-side range end
+  const bool sideA = left >= right;                  // one-side range uses s[j-k]
+  const uint32_t mbj = ((sb[(j >> 5) + 1] >> (j & 31)) & 1u) ? FULL : 0u;
+  // sliding windows: B covers positions j+k, A covers j-k (k = k0..k0+31)
+  int wB = (int)((j + 1) >> 5);
+  const uint32_t shB = (j + 1) & 31;
+  uint32_t Blo = sword(sb, wB, nwords), Bhi = sword(sb, wB + 1, nwords);
+  int wA = (int)(j >> 5) - 1;
+  const uint32_t shA = j & 31;
+  uint32_t Alo = sword(sb, wA, nwords), Ahi = sword(sb, wA + 1, nwords);
+
+  const uint32_t smask_one = sideA ? 0x10u : 0x08u;
+  double sum = 0.0;
+  const bool warp_scans = io.scan && __any_sync(FULL, active);
+
+  build_chunk(io, 0, sm.tab, sm.tail, sb, pmax);
+  __syncthreads();
+  for (uint32_t c = 0; c < io.nchunks; ++c) {
+    const uint32_t buf = c & 1;
+    double* tab = sm.tab + (size_t)buf * kChunk * kRecDoubles;
+    const double* tail = sm.tail + (size_t)buf * kChunk;
+    if (c + 1 < io.nchunks)
+      build_chunk(io, c + 1, sm.tab + (size_t)(buf ^ 1) * kChunk * kRecDoubles,
+                  sm.tail + (size_t)(buf ^ 1) * kChunk, sb, pmax);
+    if (warp_scans) {
+#pragma unroll 1
+      for (uint32_t blk = 0; blk < kChunk / 32; ++blk) {
+        const uint32_t k0 = 1 + c * kChunk + blk * 32;
+        const uint32_t kend = k0 + 31;
+        int cls;
+        if (!active) cls = CLS_TAIL;
+        else if (kend <= be) cls = CLS_BOTH;
+        else if (k0 > oe) cls = CLS_TAIL;
+        else if (k0 > be && kend <= oe) cls = CLS_ONE;
+        else cls = CLS_MIXED;
+        const uint32_t bm = __ballot_sync(FULL, cls == CLS_MIXED);
+        const uint32_t bb = __ballot_sync(FULL, cls == CLS_BOTH);
+        const uint32_t bo = __ballot_sync(FULL, cls == CLS_ONE);
+        const uint32_t Bp = __funnelshift_r(Blo, Bhi, shB) ^ mbj;
+        const uint32_t Ap = __brev(__funnelshift_r(Alo, Ahi, shA)) ^ mbj;
+        // prefetch the next block's window words
+        const uint32_t nB = sword(sb, wB + 2, nwords);
+        const uint32_t nA = sword(sb, wA - 1, nwords);
+        const char* rb = reinterpret_cast<const char*>(tab + (size_t)blk * 32 * kRecDoubles);
+        if (!(bm | bb | bo)) {
+          // every lane past its one-side range: the term is |C_k|^alpha for all
+          const double2* t2 = reinterpret_cast<const double2*>(tail + blk * 32);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const double2 v = t2[q];
+            sum = __dadd_rn(sum, v.x);
+            sum = __dadd_rn(sum, v.y);
+          }
+        } else if (!(bm | bb)) {
+          // one-side / tail lanes only: one bit per cell
+          const uint32_t P = sideA ? Ap : Bp;
+          const uint32_t mask = (cls == CLS_ONE) ? 0x08u : 0u;
+          const uint32_t base = (cls == CLS_ONE) ? 32u : 8u;
+#pragma unroll
+          for (int q = 0; q < 32; ++q) {
+            const uint32_t v = (q < 3) ? (P << (3 - q)) : (P >> (q - 3));
+            const uint32_t off = (v & mask) | base;
+            sum = __dadd_rn(sum, *reinterpret_cast<const double*>(rb + q * 64 + off));
+          }
+        } else {
+          const uint32_t Wlo = spread_lo(Bp) | (spread_lo(Ap) << 1);
+          const uint32_t Whi = spread_hi(Bp) | (spread_hi(Ap) << 1);
+          if (!bm) {
+            const uint32_t mask = cls == CLS_BOTH ? 0x18u : (cls == CLS_ONE ? smask_one : 0u);
+            const uint32_t base = cls == CLS_BOTH ? 0u : (cls == CLS_ONE ? 32u : 8u);
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+              const uint32_t x = q < 16 ? Wlo : Whi;
+              const int sh = 2 * (q & 15) - 3;
+              const uint32_t v = sh < 0 ? (x << (-sh)) : (x >> sh);
+              const uint32_t off = (v & mask) | base;
+              sum = __dadd_rn(sum, *reinterpret_cast<const double*>(rb + q * 64 + off));
+            }
+          } else {
+            // region boundary inside the block for some lane: per-cell region
+#pragma unroll 4
+            for (int q = 0; q < 32; ++q) {
+              const uint32_t k = k0 + q;
+              const uint32_t x = q < 16 ? Wlo : Whi;
+              const int sh = 2 * (q & 15) - 3;
+              const uint32_t v = sh < 0 ? (x << (-sh)) : (x >> sh);
+              const bool inb = active && k <= be;
+              const bool ino = active && k <= oe;
+              const uint32_t mask = inb ? 0x18u : (ino ? smask_one : 0u);
+              const uint32_t base = inb ? 0u : (ino ? 32u : 8u);
+              const uint32_t off = (v & mask) | base;
+              sum = __dadd_rn(sum, *reinterpret_cast<const double*>(rb + q * 64 + off));
+            }
+          }
+        }
+        Blo = Bhi; Bhi = nB; ++wB;
+        Ahi = Alo; Alo = nA; --wA;
+      }
+    }
+    if (io.chain && threadIdx.x == 0) {
+      // fitness(table, pow) (sequence.cpp:131-141): serial ascending k
+      const double2* t2 = reinterpret_cast<const double2*>(tail);
+      for (int r = 0; r < kChunk / 2; ++r) {
+        const double2 v = t2[r];
+        chain = __dadd_rn(chain, v.x);
+        chain = __dadd_rn(chain, v.y);
+      }
+    }
+    __syncthreads();
+  }
+  return sum;
+}
+
+// Exact neighbour PSL from the high-sidelobe list (entries (k, C_k)).
+__device__ __forceinline__ int32_t neighbour_psl(const int2* h, uint32_t nh, int32_t thr,
+                                                 bool filtered, uint32_t j, uint32_t L,
+                                                 const uint32_t* sb) {
+  const int sj = sval(sb, j);
+  int32_t peak = 0;
+  for (uint32_t e = 0; e < nh; ++e) {
+    const int2 kc = h[e];
+    if (!filtered && abs(kc.y) < thr) continue;
+    const uint32_t k = (uint32_t)kc.x;
+    const int sa = (k <= j) ? sval(sb, j - k) : 0;
+    const int sbv = (j + k < L) ? sval(sb, j + k) : 0;
+    const int32_t a = abs(kc.y - 2 * sj * (sa + sbv));
+    peak = max(peak, a);
+  }
+  return peak;
+}
+
+// Block-wide lexicographic (value, i) and (psl, i) minima + non-finite flag.
+// Result in ctl->best_* (valid after the trailing __syncthreads).
+__device__ __forceinline__ void block_reduce_scan(Ctl* ctl, bool active, double v, uint32_t i,
+                                                  int32_t p) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int bad = active && !isfinite(v);
+  if (!active) { v = __longlong_as_double(0x7ff0000000000000ll); i = 0xffffffffu; p = 0x7fffffff; }
+  uint32_t pi = i;
+  for (int o = 16; o; o >>= 1) {
+    const double v2 = __shfl_xor_sync(FULL, v, o);
+    const uint32_t i2 = __shfl_xor_sync(FULL, i, o);
+    const int32_t p2 = __shfl_xor_sync(FULL, p, o);
+    const uint32_t pi2 = __shfl_xor_sync(FULL, pi, o);
+    bad |= __shfl_xor_sync(FULL, bad, o);
+    if (v2 < v || (v2 == v && i2 < i)) { v = v2; i = i2; }
+    if (p2 < p || (p2 == p && pi2 < pi)) { p = p2; pi = pi2; }
+  }
+  if (lane == 0) { ctl->rv[warp] = v; ctl->ri[warp] = i; ctl->rp[warp] = p; ctl->rpi[warp] = pi; ctl->rbad[warp] = bad; }
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = blockDim.x >> 5;
+    v = lane < nw ? ctl->rv[lane] : __longlong_as_double(0x7ff0000000000000ll);
+    i = lane < nw ? ctl->ri[lane] : 0xffffffffu;
+    p = lane < nw ? ctl->rp[lane] : 0x7fffffff;
+    pi = lane < nw ? ctl->rpi[lane] : 0xffffffffu;
+    bad = lane < nw ? ctl->rbad[lane] : 0;
+    for (int o = 16; o; o >>= 1) {
+      const double v2 = __shfl_xor_sync(FULL, v, o);
+      const uint32_t i2 = __shfl_xor_sync(FULL, i, o);
+      const int32_t p2 = __shfl_xor_sync(FULL, p, o);
+      const uint32_t pi2 = __shfl_xor_sync(FULL, pi, o);
+      bad |= __shfl_xor_sync(FULL, bad, o);
+      if (v2 < v || (v2 == v && i2 < i)) { v = v2; i = i2; }
+      if (p2 < p || (p2 == p && pi2 < pi)) { p = p2; pi = pi2; }
+    }
+    if (lane == 0) { ctl->best_v = v; ctl->best_i = i; ctl->best_psl = p; ctl->best_pi = pi; ctl->bad = bad; }
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int32_t block_max(Ctl* ctl, int32_t v) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  v = warp_max(v);
+  if (lane == 0) ctl->rmax[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < (int)(blockDim.x >> 5) ? ctl->rmax[lane] : 0;
+    v = warp_max(v);
+    if (lane == 0) ctl->rmax[0] = v;
+  }
+  __syncthreads();
+  const int32_t r = ctl->rmax[0];
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ long long block_sum64(Ctl* ctl, long long v) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+  if (lane == 0) ctl->re[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    v = lane < (int)(blockDim.x >> 5) ? ctl->re[lane] : 0;
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    if (lane == 0) ctl->re[0] = v;
+  }
+  __syncthreads();
+  const long long r = ctl->re[0];
+  __syncthreads();
+  return r;
+}
+
+// merit_factor energy (sequence.cpp:143-152) of the pivot with position f
+// flipped (f < 0: unflipped).  sb holds the pivot.
+__device__ long long energy_sweep(Ctl* ctl, const int32_t* C, uint32_t L, const uint32_t* sb,
+                                  int64_t f) {
+  long long e = 0;
+  const int sf = f >= 0 ? sval(sb, (uint32_t)f) : 0;
+  for (uint32_t k = 1 + threadIdx.x; k < L; k += blockDim.x) {
+    long long cv = C[k];
+    if (f >= 0) {
+      const uint32_t fu = (uint32_t)f;
+      int acc = 0;
+      if (k <= fu) acc += sval(sb, fu - k);
+      if (fu + k < L) acc += sval(sb, fu + k);
+      cv += -2 * sf * acc;
+    }
+    e += cv * cv;
+  }
+  return block_sum64(ctl, e);
+}
+
+// ------------------------------------------------------------ kernels
+
+// Walk setup: RNG, pivot (random_sequence, search.cpp:120-129, or warm start),
+// snapshot copies.  One CTA per walk.
+__global__ void __launch_bounds__(256) init_walks_kernel(RunArgs a, const uint64_t* seeds,
+                                                         const uint32_t* init_bits) {
+  const uint32_t w = blockIdx.x;
+  WalkState* S = a.st + w;
+  uint32_t* bp = a.bits_piv + (size_t)w * a.w_stride;
+  uint32_t* bl = a.bits_loc + (size_t)w * a.w_stride;
+  uint32_t* bb = a.bits_best + (size_t)w * a.w_stride;
+  uint32_t* us = a.used + (size_t)w * a.w_stride;
+  const uint32_t nw = a.nwords;
+  if (threadIdx.x == 0) {
+    WalkState z = {};
+    rng_seed(z.rng, seeds[w]);
+    z.seed = seeds[w];
+    z.nse = 1;                 // the initial fitness evaluation (search.cpp:349)
+    z.phase = 1;
+    z.fitness_pending = 1;
+    z.psl_best = -1;           // set from P on the first pass
+    if (!init_bits) {
+      // L spin() draws in position order; bit = top bit of next() (1 <-> -1)
+      for (uint32_t wd = 0; wd < nw; ++wd) {
+        uint32_t word = 0;
+        const uint32_t nb = min(32u, a.L - wd * 32);
+        for (uint32_t b = 0; b < nb; ++b) word |= (uint32_t)(rng_next(z.rng) >> 63) << b;
+        bp[wd] = word;
+      }
+    }
+    *S = z;
+  }
+  if (init_bits) {
+    for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) bp[i] = init_bits[(size_t)w * nw + i];
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < nw + kBitsPad; i += blockDim.x) {
+    const uint32_t v = i < nw ? bp[i] : 0u;
+    if (i >= nw) bp[i] = 0u;
+    bl[i] = v;
+    bb[i] = v;
+    us[i] = 0u;
+  }
+}
+
+// SidelobeTable::build (sequence.cpp:46-60) in bit-parallel form:
+// C_k = (L-k) - 2 * popc(s[0..L-k) XOR s[k..L)).  Each warp owns 128
+// consecutive shifts (lane: k, k+32, k+64, k+96) and slides over the words.
+// Optionally reduces PSL and energy into the walk state and copies C to Cloc.
+constexpr int kTabR = 4;
+__global__ void __launch_bounds__(256) build_tables_kernel(const uint32_t* bits, size_t w_stride,
+                                                          int32_t* C, int32_t* Cloc,
+                                                          size_t c_stride, uint32_t L,
+                                                          WalkState* st) {
+  const uint32_t walk = blockIdx.y;
+  const uint32_t* S = bits + (size_t)walk * w_stride;
+  int32_t* Cw = C + (size_t)walk * c_stride;
+  int32_t* Cl = Cloc ? Cloc + (size_t)walk * c_stride : nullptr;
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const uint32_t kb = 1 + gw * 32 * kTabR;
+  if (gw == 0 && lane == 0) { Cw[0] = (int32_t)L; if (Cl) Cl[0] = (int32_t)L; }
+  if (kb >= L) return;
+  const uint32_t k0 = kb + lane;               // this lane's smallest shift
+  const uint32_t sh = k0 & 31;
+  const uint32_t base = k0 >> 5;
+  uint32_t win[kTabR + 1];
+#pragma unroll
+  for (int r = 0; r <= kTabR; ++r) win[r] = S[base + r];
+  uint32_t diff[kTabR] = {0, 0, 0, 0};
+  // pairs (p, p+k) exist for p < L-k; full words while 32(i+1) <= L - kmax_warp
+  const uint32_t kmax_warp = kb + 32 * kTabR - 1;
+  const uint32_t full = kmax_warp < L ? (L - kmax_warp) / 32 : 0;
+  uint32_t i = 0;
+  for (; i < full; ++i) {
+    const uint32_t s0 = S[i];
+#pragma unroll
+    for (int r = 0; r < kTabR; ++r) diff[r] += __popc(s0 ^ __funnelshift_r(win[r], win[r + 1], sh));
+#pragma unroll
+    for (int r = 0; r < kTabR; ++r) win[r] = win[r + 1];
+    win[kTabR] = S[i + 1 + base + kTabR];
+  }
+  // ragged end: mask by the per-shift pair count
+  const uint32_t kmin = k0;
+  const uint32_t last = kmin < L ? (L - kmin + 31) / 32 : 0;
+  for (; i < last; ++i) {
+    const uint32_t s0 = S[i];
+#pragma unroll
+    for (int r = 0; r < kTabR; ++r) {
+      const uint32_t k = k0 + 32 * r;
+      if (k < L) {
+        const int rem = (int)(L - k) - (int)(32 * i);
+        if (rem > 0) {
+          const uint32_t m = rem >= 32 ? FULL : ((1u << rem) - 1u);
+          diff[r] += __popc((s0 ^ __funnelshift_r(win[r], win[r + 1], sh)) & m);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kTabR; ++r) win[r] = win[r + 1];
+    win[kTabR] = S[i + 1 + base + kTabR];
+  }
+  int32_t pm = 0;
+  long long en = 0;
+#pragma unroll
+  for (int r = 0; r < kTabR; ++r) {
+    const uint32_t k = k0 + 32 * r;
+    if (k < L) {
+      const int32_t cv = (int32_t)(L - k) - 2 * (int32_t)diff[r];
+      Cw[k] = cv;
+      if (Cl) Cl[k] = cv;
+      pm = max(pm, abs(cv));
+      en += (long long)cv * cv;
+    }
+  }
+  if (st) {
+    pm = warp_max(pm);
+    for (int o = 16; o; o >>= 1) en += __shfl_xor_sync(FULL, en, o);
+    if (lane == 0) {
+      atomicMax(&st[walk].P, pm);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&st[walk].energy_best),
+                (unsigned long long)en);
+    }
+  }
+}
+
+// The device-resident run_search loop (search.cpp:327-430), one CTA per walk.
+__global__ void __launch_bounds__(kThreads, 1) run_kernel(RunArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Smem sm = carve(smem_raw);
+  Ctl* ctl = sm.ctl;
+  const uint32_t w = blockIdx.x, t = threadIdx.x;
+  const uint32_t L = a.L, nw = a.nwords;
+  WalkState* gst = a.st + w;
+  uint32_t* bits_piv = a.bits_piv + (size_t)w * a.w_stride;
+  uint32_t* bits_loc = a.bits_loc + (size_t)w * a.w_stride;
+  uint32_t* bits_best = a.bits_best + (size_t)w * a.w_stride;
+  uint32_t* used = a.used + (size_t)w * a.w_stride;
+  int32_t* Cpiv = a.Cpiv + (size_t)w * a.c_stride;
+  int32_t* Cloc = a.Cloc + (size_t)w * a.c_stride;
+  int2* hlist = a.hlist + (size_t)w * a.h_stride;
+  uint32_t* flips = a.flips + (size_t)w * a.f_stride;
+
+  if (t == 0) {
+    ctl->st = *gst;
+    ctl->steps_this_launch = 0;
+    if (ctl->st.t0_ns == 0) ctl->st.t0_ns = globaltimer();
+    if (ctl->st.psl_best < 0) { ctl->st.psl_best = ctl->st.P; ctl->st.P_local = ctl->st.P; }
+  }
+  sm.sb[0] = 0;
+  for (uint32_t i = t; i <= nw; i += kThreads) sm.sb[i + 1] = i < nw ? bits_piv[i] : 0u;
+  __syncthreads();
+  if (ctl->st.done || ctl->st.status != PSL_OK) return;
+
+  const uint32_t ngroups = (a.n + kThreads - 1) / kThreads;
+  for (;;) {
+    // ---- top of step: stop checks, max-nse first (search.cpp:371-374)
+    if (t == 0) {
+      WalkState& S = ctl->st;
+      const double elapsed = (double)(globaltimer() - S.t0_ns) * 1e-9;
+      const bool stop = (a.has_max_nse && S.nse >= a.max_nse) ||
+                        (a.has_max_seconds && elapsed >= a.max_seconds);
+      const bool room = ctl->steps_this_launch < a.step_budget &&
+                        (!a.record_events || S.n_events + 2 <= a.events_cap) &&
+                        (!a.record_traces || S.n_traces + 1 <= a.traces_cap);
+      ctl->do_scan = !stop && room;
+      if (stop) { S.done = 1; S.end_ns = globaltimer(); }
+      ctl->need_pass = ctl->do_scan || S.fitness_pending;
+      if (ctl->do_scan) ctl->start = (uint32_t)rng_bounded(S.rng, L);  // search.cpp:375
+      ctl->hcount = 0;
+      ctl->fit = 0.0;
+    }
+    __syncthreads();
+    if (!ctl->need_pass) break;
+    const bool do_scan = ctl->do_scan;
+    const uint32_t start = ctl->start;
+    const WalkState S0 = ctl->st;
+    const uint32_t alpha = S0.phase == 1 ? a.alpha1 : a.alpha2;
+
+    for (uint32_t g = 0; g < ngroups; ++g) {
+      const uint32_t i = g * kThreads + t + 1;
+      const bool active = do_scan && i <= a.n;
+      uint32_t j = 0;
+      if (active) { j = start + i; if (j >= L) j -= L; }
+      SweepIO io;
+      io.L = L; io.nwords = nw; io.nchunks = a.nchunks;
+      io.alpha = alpha; io.lut = nullptr; io.lut_size = 0;
+      io.scan = do_scan;
+      io.hcount = &ctl->hcount;
+      if (g == 0) {
+        io.Csrc = S0.src_local ? Cloc : Cpiv;
+        io.Cdst = Cpiv;
+        io.Cloc = S0.local_pending ? Cloc : nullptr;
+        io.flips = flips; io.F = S0.n_pending;
+        io.hlist = hlist;
+        const int32_t Psrc = S0.src_local ? S0.P_local : S0.P;
+        io.hthr = Psrc - 4 * (int32_t)S0.n_pending - 8;
+        io.chain = S0.fitness_pending != 0;
+      } else {
+        io.Csrc = Cpiv; io.Cdst = nullptr; io.Cloc = nullptr;
+        io.flips = flips; io.F = 0; io.hlist = nullptr; io.hthr = 0; io.chain = false;
+      }
+      int32_t pmax = 0;
+      double chain = 0.0;
+      const double val = sweep(io, sm, active, j, pmax, chain);
+      if (g == 0) {
+        const int32_t Pn = block_max(ctl, pmax);
+        if (t == 0) {
+          WalkState& S = ctl->st;
+          ctl->P_new = Pn;
+          S.P = Pn;
+          if (S.local_pending) { S.P_local = Pn; S.local_pending = 0; }
+          S.n_pending = 0;
+          S.src_local = 0;
+          if (S.fitness_pending) {
+            S.fitness_pending = 0;
+            if (!isfinite(chain)) {
+              // fitness() throws OverflowError (sequence.cpp:139); a provisional
+              // phase-switch event / trace from the restart step is withdrawn.
+              S.status = PSL_ERR_OVERFLOW; S.err_kind = 1; S.err_alpha = alpha;
+              if (S.switch_pending && S.n_events) --S.n_events;
+              if (S.trace_patch && S.n_traces) --S.n_traces;
+            } else {
+              S.value_local = chain;
+              if (S.trace_patch) {
+                a.traces[(size_t)w * a.traces_cap + S.n_traces - 1].value_local = chain;
+              }
+            }
+            S.trace_patch = 0;
+            S.switch_pending = 0;
+          }
+          // filter the high-sidelobe list into smem
+          ctl->hf_count = 0;
+        }
+        __syncthreads();
+        if (ctl->st.status != PSL_OK) break;
+        const int32_t thr = ctl->P_new - 8;
+        const uint32_t hc = ctl->hcount;
+        for (uint32_t e = t; e < hc; e += kThreads) {
+          const int2 kc = hlist[e];
+          if (abs(kc.y) >= thr) {
+            const uint32_t slot = atomicAdd(&ctl->hf_count, 1u);
+            if (slot < (uint32_t)kHCap) sm.hf[slot] = kc;
+          }
+        }
+        __syncthreads();
+      }
+      if (!do_scan) break;
+      const uint32_t nf = ctl->hf_count;
+      int32_t psl = 0;
+      if (active) {
+        psl = nf <= (uint32_t)kHCap
+                  ? neighbour_psl(sm.hf, nf, 0, true, j, L, sm.sb)
+                  : neighbour_psl(hlist, ctl->hcount, ctl->P_new - 8, false, j, L, sm.sb);
+      }
+      block_reduce_scan(ctl, active, val, i, psl);
+      if (t == 0) {
+        // combine groups in ascending offset order (strict <: smallest offset wins)
+        if (g == 0) {
+          ctl->cv = ctl->best_v; ctl->ci = ctl->best_i;
+          ctl->cp = ctl->best_psl; ctl->cpi = ctl->best_pi; ctl->cbad = ctl->bad;
+        } else {
+          if (ctl->best_v < ctl->cv) { ctl->cv = ctl->best_v; ctl->ci = ctl->best_i; }
+          if (ctl->best_psl < ctl->cp) { ctl->cp = ctl->best_psl; ctl->cpi = ctl->best_pi; }
+          ctl->cbad |= ctl->bad;
+        }
+      }
+      __syncthreads();
+    }
+    if (ctl->st.status != PSL_OK || !do_scan) break;
+
+    // ---- reduce_scan result + Algorithm 1 control (search.cpp:379-419)
+    if (t == 0) {
+      WalkState& S = ctl->st;
+      S.nse += a.n;                                            // :379
+      const double value_step = ctl->cv;
+      const uint32_t best_i = ctl->ci;
+      const int32_t psl_min = ctl->cp;
+      const uint32_t psl_i = ctl->cpi;
+      const double elapsed = (double)(globaltimer() - S.t0_ns) * 1e-9;
+      ctl->imp = ctl->improve = ctl->restart = 0;
+      if (ctl->cbad) {                                      // :275-281
+        S.status = PSL_ERR_OVERFLOW; S.err_kind = 2; S.err_alpha = alpha;
+      } else {
+        auto emit = [&](uint32_t kind) {
+          if (a.record_events) {
+            psl_event& ev = a.events[(size_t)w * a.events_cap + S.n_events];
+            ev.nse = S.nse; ev.elapsed_seconds = elapsed; ev.psl_best = S.psl_best;
+            ev.phase_index = S.phase; ev.kind = kind;
+          }
+          ++S.n_events;
+        };
+        const uint32_t jstar = (uint32_t)(((uint64_t)start + best_i) % L);
+        const uint32_t ppos = (uint32_t)(((uint64_t)start + psl_i) % L);
+        ctl->jstar = jstar; ctl->ppos = ppos;
+        if (psl_min < S.psl_best) {                            // :383-389
+          S.psl_best = psl_min;
+          ctl->imp = 1;
+          emit(PSL_EVENT_IMPROVED_PSL);
+        }
+        if (value_step < S.value_local) {                      // :394-399
+          S.value_local = value_step;
+          S.unimproved = 0;
+          ctl->improve = 1;
+          emit(PSL_EVENT_LOCAL_BEST_IMPROVED);
+        } else if (value_step > S.value_local) {               // :400-413
+          if (++S.unimproved > a.ls_lmt) {
+            ctl->restart = 1;
+            S.phase = (S.phase == 1) ? 2u : 1u;
+            S.nse += 1;
+            S.unimproved = 0;
+            S.switches += 1;
+            S.fitness_pending = 1;
+            S.switch_pending = 1;
+            emit(PSL_EVENT_PHASE_SWITCH);
+          }
+        }
+        if (a.record_traces) {                                 // :417-419
+          psl_trace& tr = a.traces[(size_t)w * a.traces_cap + S.n_traces];
+          tr.nse = S.nse; tr.value_step = value_step; tr.value_local = S.value_local;
+          tr.psl_best = S.psl_best; tr.phase_index = S.phase;
+          ++S.n_traces;
+          S.trace_patch = ctl->restart ? 1u : 0u;
+        }
+        S.steps += 1;
+        ctl->steps_this_launch += 1;
+      }
+    }
+    __syncthreads();
+    if (ctl->st.status != PSL_OK) break;
+
+    if (ctl->imp) {
+      // best_seq = pivot with the best-PSL neighbour's flip (:385-387)
+      const uint32_t pp = ctl->ppos;
+      for (uint32_t i = t; i < nw; i += kThreads) {
+        uint32_t v = sm.sb[i + 1];
+        if (i == (pp >> 5)) v ^= 1u << (pp & 31);
+        bits_best[i] = v;
+      }
+      const long long e = energy_sweep(ctl, Cpiv, L, sm.sb, (int64_t)pp);
+      if (t == 0) ctl->st.energy_best = e;
+    }
+    __syncthreads();
+    if (ctl->restart) {
+      // back to the phase-local best (:405-406): bits from the snapshot, C via
+      // the next pass (src_local); then flip_random_distinct (:407, :131-148)
+      for (uint32_t i = t; i < nw; i += kThreads) sm.sb[i + 1] = bits_loc[i];
+      __syncthreads();
+      if (t == 0) {
+        WalkState& S = ctl->st;
+        uint32_t done = 0;
+        while (done < a.flip_lmt) {
+          const uint32_t pos = (uint32_t)rng_bounded(S.rng, L);
+          const uint32_t bit = 1u << (pos & 31);
+          if (used[pos >> 5] & bit) continue;
+          used[pos >> 5] |= bit;
+          flips[done++] = pos;
+          sm.sb[(pos >> 5) + 1] ^= bit;
+        }
+        for (uint32_t m = 0; m < done; ++m) used[flips[m] >> 5] = 0u;
+        S.n_pending = done;
+        S.src_local = 1;
+      }
+    } else if (t == 0) {
+      // the pivot always moves to the argmin neighbour (:392)
+      const uint32_t js = ctl->jstar;
+      sm.sb[(js >> 5) + 1] ^= 1u << (js & 31);
+      flips[0] = js;
+      ctl->st.n_pending = 1;
+      ctl->st.src_local = 0;
+      if (ctl->improve) ctl->st.local_pending = 1;
+    }
+    __syncthreads();
+    if (ctl->improve) {
+      for (uint32_t i = t; i < nw; i += kThreads) bits_loc[i] = sm.sb[i + 1];
+    }
+    __syncthreads();
+  }
+
+  // ---- persist
+  __syncthreads();
+  if (t == 0) {
+    if (ctl->st.status != PSL_OK) ctl->st.end_ns = globaltimer();
+    *gst = ctl->st;
+  }
+  for (uint32_t i = t; i < nw; i += kThreads) bits_piv[i] = sm.sb[i + 1];
+}
+
+// ScanJob / neighborhood_scan: neighbours of one given pivot, group g of 1024
+// per CTA, terms from the caller's PowerTable.
+__global__ void __launch_bounds__(kThreads, 1) scan_kernel(ScanArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const Smem sm = carve(smem_raw);
+  const uint32_t t = threadIdx.x;
+  const uint32_t nw = a.nwords;
+  sm.sb[0] = 0;
+  for (uint32_t i = t; i <= nw; i += kThreads) sm.sb[i + 1] = i < nw ? a.bits[i] : 0u;
+  const bool in_smem = a.hcount <= (uint32_t)kHCap;
+  if (in_smem)
+    for (uint32_t e = t; e < a.hcount; e += kThreads) sm.hf[e] = a.hlist[e];
+  __syncthreads();
+  const uint32_t i = blockIdx.x * kThreads + t + 1;
+  const bool active = i <= a.n;
+  uint32_t j = 0;
+  if (active) { j = a.start + i; if (j >= a.L) j -= a.L; }
+  SweepIO io;
+  io.L = a.L; io.nwords = nw; io.nchunks = a.nchunks;
+  io.Csrc = a.C; io.Cdst = nullptr; io.Cloc = nullptr; io.flips = nullptr; io.F = 0;
+  io.alpha = 0; io.lut = a.lut; io.lut_size = a.lut_size;
+  io.hlist = nullptr; io.hcount = nullptr; io.hthr = 0;
+  io.scan = true; io.chain = false;
+  int32_t pmax = 0;
+  double chain = 0.0;
+  const double v = sweep(io, sm, active, j, pmax, chain);
+  if (active) {
+    const int32_t p = in_smem ? neighbour_psl(sm.hf, a.hcount, 0, true, j, a.L, sm.sb)
+                              : neighbour_psl(a.hlist, a.hcount, 0, true, j, a.L, sm.sb);
+    a.values[i] = v;
+    a.psls[i] = p;
+  }
+}
+
+// apply_flip (sequence.cpp:198-224) for the C-ABI: C_k += delta_k, then s_j flips.
+__global__ void apply_flip_kernel(uint32_t* bits, int32_t* C, uint32_t L, uint32_t j) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x + 1;
+  auto sv = [&](uint32_t x) { return 1 - 2 * (int)((bits[x >> 5] >> (x & 31)) & 1u); };
+  if (k < L) {
+    int acc = 0;
+    if (k <= j) acc += sv(j - k);
+    if (j + k < L) acc += sv(j + k);
+    C[k] += -2 * sv(j) * acc;
+  }
+}
+__global__ void flip_bit_kernel(uint32_t* bits, uint32_t j) { bits[j >> 5] ^= 1u << (j & 31); }
+
+}  // namespace
+
+size_t run_smem_bytes(uint32_t nwords) {
+  return kTabBytes + kTailBytes + kHfBytes + kCtlBytes + (size_t)(nwords + 2) * 4;
+}
+
+int launch_init_walks(const RunArgs& a, uint32_t n_walks, const uint64_t* d_seeds,
+                      const uint32_t* d_init_bits, cudaStream_t s) {
+  init_walks_kernel<<<n_walks, 256, 0, s>>>(a, d_seeds, d_init_bits);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_build_tables(const RunArgs& a, uint32_t n_walks, cudaStream_t s) {
+  const uint32_t per_block = 8 * 32 * kTabR;
+  dim3 grid((a.L + per_block - 1) / per_block, n_walks);
+  build_tables_kernel<<<grid, 256, 0, s>>>(a.bits_piv, a.w_stride, a.Cpiv, a.Cloc, a.c_stride,
+                                           a.L, a.st);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_table_only(const uint32_t* d_bits, int32_t* d_C, uint32_t L, uint32_t nwords,
+                      cudaStream_t s) {
+  const uint32_t per_block = 8 * 32 * kTabR;
+  dim3 grid((L + per_block - 1) / per_block, 1);
+  build_tables_kernel<<<grid, 256, 0, s>>>(d_bits, nwords + kBitsPad, d_C, nullptr, L, L, nullptr);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_run(const RunArgs& a, uint32_t n_walks, cudaStream_t s) {
+  const size_t smem = run_smem_bytes(a.nwords);
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(run_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)run_smem_bytes((1u << 20) / 32 + 1)) != cudaSuccess)
+      return -1;
+    attr = true;
+  }
+  run_kernel<<<n_walks, kThreads, smem, s>>>(a);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_scan(const ScanArgs& a, cudaStream_t s) {
+  const size_t smem = run_smem_bytes(a.nwords);
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)run_smem_bytes((1u << 20) / 32 + 1)) != cudaSuccess)
+      return -1;
+    attr = true;
+  }
+  const uint32_t groups = (a.n + kThreads - 1) / kThreads;
+  scan_kernel<<<groups, kThreads, smem, s>>>(a);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_apply_flip(uint32_t* d_bits, int32_t* d_C, uint32_t L, uint32_t j, cudaStream_t s) {
+  apply_flip_kernel<<<(L + 255) / 256, 256, 0, s>>>(d_bits, d_C, L, j);
+  flip_bit_kernel<<<1, 1, 0, s>>>(d_bits, j);
+  return cudaGetLastError() == cudaSuccess ? 2 : -1;
+}
+
+}  // namespace pslb

@@ -1,0 +1,278 @@
+"""Generate tests/golden/*.json from the UNMODIFIED reference.
+
+Runs here (where /root/reference exists) against oracle/_ref/libpslref.so, which
+oracle/Makefile compiles from the reference sources.  The fixtures are small and
+committed; the GPU box never reads /root/reference.
+
+    make -C oracle && python tests/golden/make_golden.py [--big]
+
+Doubles are stored as float.hex() strings so comparisons are bit-exact;
+sequences as '+'/'-' strings (formats.md alphabet).  --big adds the m18/m20
+known-answer runs (the reference needs ~2.5 min for the m20 O(L^2) build).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.join(HERE, "..", ".."))
+from oracle import oracle_py as O  # noqa: E402
+
+R = O.ref()
+
+
+def seq_str(s) -> str:
+    return "".join("+" if int(x) > 0 else "-" for x in s)
+
+
+def hx(x: float) -> str:
+    return float(x).hex()
+
+
+def sha(a: np.ndarray) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def ref_seq(seed: int, L: int) -> np.ndarray:
+    s = np.empty(L, np.int8)
+    R.ref_random_sequence(seed, L, s)
+    return s
+
+
+def ref_table(s: np.ndarray) -> np.ndarray:
+    c = np.empty(len(s), np.int32)
+    assert R.ref_build_table(s, len(s), c) == 0
+    return c
+
+
+def ref_lut(L: int, alpha: int) -> np.ndarray:
+    return np.array([R.ref_pow_int(float(a), alpha) for a in range(L + 1)], np.float64)
+
+
+def run(L, seed, a1, a2, ls, flip, n, max_nse, init=None, traces=True, cap=1 << 20):
+    sol = np.zeros(L, np.int8)
+    psl, mf, el = C.c_int32(), C.c_double(), C.c_double()
+    nse, ne, nt = C.c_uint64(), C.c_uint64(), C.c_uint64()
+    ev = (O.RefEvent * cap)()
+    tr = (O.RefTrace * cap)() if traces else None
+    err = C.create_string_buffer(512)
+    init_arr = np.ascontiguousarray(init, np.int8) if init is not None else None
+    rc = R.ref_run_search(L, seed, a1, a2, ls, flip, n, 1, max_nse, 0.0,
+                          init_arr.ctypes.data if init_arr is not None else None, sol,
+                          C.byref(psl), C.byref(mf), C.byref(nse), C.byref(el),
+                          C.cast(ev, C.c_void_p), cap, C.byref(ne),
+                          C.cast(tr, C.c_void_p) if tr else None, cap if tr else 0,
+                          C.byref(nt), err, 512)
+    out = {"status": rc, "error": err.value.decode()}
+    out["events"] = [[ev[i].nse, ev[i].psl_best, ev[i].phase, ev[i].kind]
+                     for i in range(min(ne.value, cap))]
+    if rc == 0:
+        out.update(nse=nse.value, psl_best=psl.value, merit_factor=hx(mf.value),
+                   solution_best=seq_str(sol))
+    if tr is not None:
+        out["traces"] = [[tr[i].nse, hx(tr[i].value_step), hx(tr[i].value_local),
+                          tr[i].psl_best, tr[i].phase] for i in range(min(nt.value, cap))]
+    return out
+
+
+def gen_rng():
+    out = {}
+    for seed in (42, 1, 2, 7, 123456789, 2**64 - 1):
+        v = np.zeros(16, np.uint64)
+        R.ref_rng(seed, 16, v)
+        out[str(seed)] = [int(x) for x in v]
+    seqs = {str(seed): seq_str(ref_seq(seed, 64)) for seed in (1, 3, 9, 10, 123)}
+    return {"next16": out, "random_sequence64": seqs}
+
+
+def gen_hand():
+    ones = np.ones(4, np.int8)
+    alt = np.array([1, -1, 1, -1], np.int8)
+    b13 = np.array([1, 1, 1, 1, 1, -1, -1, 1, 1, -1, 1, -1, 1], np.int8)
+    out = {
+        "ones4_table": [int(x) for x in ref_table(ones)],
+        "alt4_table": [int(x) for x in ref_table(alt)],
+        "barker13_table": [int(x) for x in ref_table(b13)],
+        "pow_int": {},
+    }
+    for a in (0, 1, 2, 3, 5, 7, 100, 1000, 5073, 1048575):
+        out["pow_int"][str(a)] = [hx(R.ref_pow_int(float(a), al)) for al in range(0, 17)]
+    # neighborhood_scan tie-break case (unit_search.cpp:149-171)
+    res = []
+    for (start, n, alpha) in ((2, 4, 2), (1, 1, 2), (0, 4, 2), (3, 2, 5)):
+        bi, bp, bpi = C.c_uint32(), C.c_int32(), C.c_uint32()
+        v = C.c_double()
+        err = C.create_string_buffer(256)
+        rc = R.ref_neighborhood_scan(ones, 4, alpha, start, n, C.byref(bi), C.byref(v),
+                                     C.byref(bp), C.byref(bpi), err, 256)
+        res.append({"start": start, "n": n, "alpha": alpha, "status": rc,
+                    "best_index": bi.value, "value_step": hx(v.value),
+                    "best_neighbor_psl": bp.value, "best_psl_index": bpi.value})
+    out["ones4_scans"] = res
+    return out
+
+
+def gen_scans():
+    rng = np.random.default_rng(20251018)
+    cases = []
+    lengths = [2, 3, 4, 5, 7, 8, 13, 16, 31, 32, 33, 63, 64, 65, 100, 127, 128, 129, 255,
+               257, 300, 1023, 1024, 1025, 2047, 4095]
+    for L in lengths:
+        for rep in range(3 if L < 1000 else 2):
+            seed = int(rng.integers(1, 2**31))
+            s = ref_seq(seed, L)
+            c = ref_table(s)
+            alpha = int(rng.integers(1, 14))
+            start = int(rng.integers(0, L))
+            n = int(rng.integers(1, L + 1)) if rep else L
+            lut = ref_lut(L, alpha)
+            values = np.zeros(n + 1, np.float64)
+            psls = np.zeros(n + 1, np.int32)
+            R.ref_scan_values(s, c, L, start, n, lut, values, psls)
+            bi, bp, bpi = C.c_uint32(), C.c_int32(), C.c_uint32()
+            v = C.c_double()
+            err = C.create_string_buffer(256)
+            rc = R.ref_neighborhood_scan(s, L, alpha, start, n, C.byref(bi), C.byref(v),
+                                         C.byref(bp), C.byref(bpi), err, 256)
+            case = {"L": L, "seed": seed, "alpha": alpha, "start": start, "n": n,
+                    "table_sha": sha(c), "status": rc, "best_index": bi.value,
+                    "value_step": hx(v.value), "best_neighbor_psl": bp.value,
+                    "best_psl_index": bpi.value, "values_sha": sha(values[1:]),
+                    "psls_sha": sha(psls[1:])}
+            if L <= 300:
+                case["values"] = [hx(x) for x in values[1:]]
+                case["psls"] = [int(x) for x in psls[1:]]
+            cases.append(case)
+    return cases
+
+
+def gen_c1():
+    """acceptance.cpp:75-99 (C1): 1000 (S, j, alpha) triples, seed 20250816."""
+    out = []
+    state = np.zeros(1, np.uint64)  # regenerate the exact draws with the ref RNG via seqs
+    del state
+    # Reproduce acceptance's draw order with the oracle RNG (pinned to the ref
+    # by test_oracle), then evaluate with the reference.
+    r = O.OrcRng()
+    O.lib().orc_rng_seed(C.byref(r), 20250816)
+    lengths = (16, 64, 257)
+    for i in range(1000):
+        L = lengths[i % 3]
+        s = np.array([1 if (O.lib().orc_rng_next(C.byref(r)) >> 63) == 0 else -1
+                      for _ in range(L)], np.int8)
+        j = O.lib().orc_rng_bounded(C.byref(r), L)
+        alpha = 1 + O.lib().orc_rng_bounded(C.byref(r), 13)
+        f, p = C.c_double(), C.c_int32()
+        assert R.ref_evaluate_neighbor(s, L, j, alpha, C.byref(f), C.byref(p)) == 0
+        flipped = s.copy()
+        flipped[j] = -flipped[j]
+        brute = R.ref_brute_fitness(flipped, L, alpha)
+        assert brute == f.value
+        out.append([L, int(j), int(alpha), hx(f.value), p.value])
+    return out
+
+
+def gen_trajectories():
+    cases = [(16, 16, 5, 3, 4, 13, 1, 2000), (31, 8, 3, 5, 2, 7, 7, 3000),
+             (32, 1, 2, 10, 4, 13, 42, 1500), (24, 24, 1, 24, 3, 5, 99, 2500),
+             (64, 11, 4, 2, 4, 13, 5, 3000)]
+    out = []
+    for (L, n, ls, flip, a1, a2, seed, max_nse) in cases:
+        sol = np.zeros(L, np.int8)
+        psl, nse, sw, nt = C.c_int32(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        cap = 1 << 16
+        tr = (O.RefTrace * cap)()
+        R.ref_naive_search(L, seed, a1, a2, ls, flip, n, max_nse, sol, C.byref(psl),
+                           C.byref(nse), C.byref(sw), C.cast(tr, C.c_void_p), cap, C.byref(nt))
+        naive = [[tr[i].nse, hx(tr[i].value_step), hx(tr[i].value_local), tr[i].psl_best,
+                  tr[i].phase] for i in range(nt.value)]
+        rec = run(L, seed, a1, a2, ls, flip, n, max_nse)
+        assert rec["traces"] == naive, f"reference run_search != naive oracle for L={L}"
+        rec.update(params=[L, seed, a1, a2, ls, flip, n, max_nse], switches=sw.value)
+        out.append(rec)
+    # extra small cases exercising clamps, full neighbourhoods and warm starts
+    extra = [(2, 5, 4, 13, 2, 10, 1024, 500), (3, 6, 1, 2, 1, 3, 3, 300),
+             (48, 1, 4, 13, 3, 5, 7, 5000), (96, 2, 4, 13, 4, 10, 96, 40000),
+             (128, 11, 4, 13, 2000, 10, 128, 50000), (257, 3, 4, 13, 2000, 10, 257, 100000),
+             (100, 4, 1, 1, 2, 7, 100, 20000), (200, 9, 13, 4, 3, 200, 50, 20000)]
+    for (L, seed, a1, a2, ls, flip, n, max_nse) in extra:
+        rec = run(L, seed, a1, a2, ls, flip, n, max_nse)
+        rec.update(params=[L, seed, a1, a2, ls, flip, n, max_nse])
+        out.append(rec)
+    return out
+
+
+def gen_records():
+    out = {}
+    # docs/formats.md:31-55 golden record
+    out["formats_md"] = run(16, 3, 4, 13, 2000, 10, 16, 400)
+    out["formats_md"]["params"] = [16, 3, 4, 13, 2000, 10, 16, 400]
+    # acceptance C6 configuration (acceptance.cpp:232-254)
+    c6 = run(4095, 1, 4, 13, 2000, 10, 1024, 1000000)
+    c6["params"] = [4095, 1, 4, 13, 2000, 10, 1024, 1000000]
+    tr = c6.pop("traces")
+    c6["n_traces"] = len(tr)
+    c6["traces_head"] = tr[:50]
+    c6["traces_sha"] = hashlib.sha256(json.dumps(tr).encode()).hexdigest()
+    out["c6"] = c6
+    # warm start (unit_search.cpp:323-341)
+    init = ref_seq(123, 32)
+    ws = run(32, 77, 4, 13, 2000, 10, 32, 1, init=init)
+    ws.update(params=[32, 77, 4, 13, 2000, 10, 32, 1], init=seq_str(init))
+    out["warm_start_nse1"] = ws
+    init2 = ref_seq(5, 200)
+    ws2 = run(200, 8, 4, 13, 5, 10, 60, 30000, init=init2)
+    ws2.update(params=[200, 8, 4, 13, 5, 10, 60, 30000], init=seq_str(init2))
+    out["warm_start_200"] = ws2
+    # overflow in phase two / initial fitness (unit_search.cpp:343-365)
+    out["overflow_alpha2"] = run(64, 1, 4, 1100, 1, 10, 64, 1000000)
+    out["overflow_alpha2"]["params"] = [64, 1, 4, 1100, 1, 10, 64, 1000000]
+    out["overflow_alpha1"] = run(64, 1, 1100, 1100, 1, 10, 64, 1000000)
+    out["overflow_alpha1"]["params"] = [64, 1, 1100, 1100, 1, 10, 64, 1000000]
+    return out
+
+
+def gen_kats(big: bool):
+    out = {}
+    configs = [(16383, 300), (65535, 100)] + ([(262143, 8), (1048575, 3)] if big else [])
+    for (L, scans) in configs:
+        a2 = O.lib().orc_default_alpha2(L)
+        n = min(L, 1024)
+        s = ref_seq(1, L)
+        c = O.build_table(s, fast=True)  # bit-parallel oracle; pinned below at m14
+        if L <= 16383:
+            assert np.array_equal(c, ref_table(s))
+        lut1 = ref_lut(L, 4)
+        rec = run(L, 1, 4, a2, 2000, 10, n, 1 + scans * n)
+        rec.update(params=[L, 1, 4, a2, 2000, min(L, 10), n, 1 + scans * n],
+                   initial_psl=int(np.abs(c[1:]).max()),
+                   initial_fitness=hx(O.fitness(c, lut1)),
+                   table_sha=sha(c), c1=int(c[1]), c2=int(c[2]), c_last=int(c[-1]))
+        out[str(L)] = rec
+        print(f"KAT L={L}: psl {rec.get('psl_best')} nse {rec.get('nse')}", flush=True)
+    return out
+
+
+def main():
+    big = "--big" in sys.argv
+    def dump(name, obj):
+        with open(os.path.join(HERE, name), "w") as f:
+            json.dump(obj, f, separators=(",", ":"))
+        print("wrote", name, os.path.getsize(os.path.join(HERE, name)), "bytes", flush=True)
+    dump("rng.json", gen_rng())
+    dump("hand.json", gen_hand())
+    dump("scans.json", gen_scans())
+    dump("c1.json", gen_c1())
+    dump("trajectories.json", gen_trajectories())
+    dump("records.json", gen_records())
+    dump("kats_big.json" if big else "kats.json", gen_kats(big))
+
+
+if __name__ == "__main__":
+    main()
