@@ -1,0 +1,337 @@
+#!/usr/bin/env python
+"""Benchmark: flip-evaluations/s (NSE/s) of the two-phase low-PSL search at
+L = 2^20 - 1 (BASELINE.json metric), one JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+A step = one search step of every walk on every GPU: each walk scans its
+n_lmt = 1024 one-flip neighbours (1024 x (L-1) flip x shift cells), reduces,
+moves (and restarts when the phase rule fires), all on the device.  Walks are
+independent (seed = seed0 + global walk id), one CTA per SM, so per-GPU work is
+fixed as N grows ("scaling": "weak").  Inputs are synthetic random start
+sequences (random_sequence(L, Rng(seed))), the reference's own start.
+
+--impl reference times the reference's CPU implementation of the same path
+(oracle/_ref/libpslref.so, compiled from the unmodified reference sources) on
+all host cores: each step, every host thread scores the 1024 one-flip
+neighbours of an L = 2^20 - 1 pivot with the reference's detail::eval_flip.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L_DEFAULT = (1 << 20) - 1
+A100_M20_NSE = 85062.0   # BASELINE.md / PAPER.md:342-359, A100, L = 1048575 (N_lmt = 6912)
+METRIC = "flip-evals/sec (NSE/s) at L=2^20-1"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--length", type=int, default=L_DEFAULT)
+    ap.add_argument("--walks", type=int, default=0, help="walks per GPU (0 = one per SM)")
+    ap.add_argument("--n-lmt", type=int, default=1024)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--cpu-reps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- CPU reference
+
+def reference_sample(L: int, n: int, reps: int, threads: int, seed: int):
+    """The reference's own kernel (detail::eval_flip) on all host threads:
+    each thread scores n neighbours of an L pivot `reps` times.  Returns
+    (NSE/s, seconds, description).  The pivot's table comes from the oracle's
+    threaded bit-parallel build (setup, untimed)."""
+    from oracle import oracle_py as O
+    R = O.ref()
+    s = O.random_sequence(seed, L)
+    c = O.build_table(s, threads=threads)
+    lut = O.power_table(L + 4, 4)
+    secs = C_double()
+    rate = R.ref_bench_eval(s, c, L, 1, lut, n, reps, threads, secs)
+    desc = (f"{threads} host threads x {reps} x {n} one-flip neighbour evaluations "
+            f"(reference detail::eval_flip, sequence.hpp:126-162) of an L={L} random pivot, "
+            f"alpha=4; table built by the oracle (untimed)")
+    return rate, secs.value, desc
+
+
+def C_double():
+    import ctypes
+    return ctypes.c_double()
+
+
+def run_reference_arm(args, rank: int):
+    if rank != 0:
+        return
+    from oracle import oracle_py as O
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libpslref.so not built (needs /root/reference at build time)"}))
+        return
+    L, n = args.length, args.n_lmt
+    threads = os.cpu_count() or 1
+    R = O.ref()
+    s = O.random_sequence(args.seed, L)
+    c = O.build_table(s, threads=threads)
+    lut = O.power_table(L + 4, 4)
+    secs = C_double()
+    for _ in range(args.warmup):
+        R.ref_bench_eval(s, c, L, 1, lut, n, 1, threads, secs)
+    total = 0.0
+    for _ in range(args.steps):
+        R.ref_bench_eval(s, c, L, 1, lut, n, 1, threads, secs)
+        total += secs.value
+    nse = float(threads) * n * args.steps
+    value = nse / total
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "NSE/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": value / A100_M20_NSE, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"m20: L={L}, {threads} walks (one per host core), n_lmt={n}",
+                   "L": L, "n_lmt": n, "host_threads": threads,
+                   "step": "every host thread scores the n one-flip neighbours of its pivot"},
+        "cpu_baseline": {"value": value, "unit": "NSE/s", "cores": threads, "kind": "reference",
+                         "sample": f"{threads} threads x {n} eval_flip per step, L={L}"},
+        "e2e": {"value": value, "unit": "NSE/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "cells_per_s": value * (L - 1),
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------- ours
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2107_09801_b200 as P
+    from paper_2107_09801_b200 import dist as D
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    ctx = P.Context(local_rank)
+    # a dedicated (non-default) stream shared by the engine and the CUDA events
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    nsm = torch.cuda.get_device_properties(local_rank).multi_processor_count
+    n_walks = args.walks or nsm
+    L, n = args.length, args.n_lmt
+    total_steps = args.warmup + args.steps + 4
+    params = P.SearchParams(length=L, seed=args.seed, alpha1=4, alpha2=P.default_alpha2(L),
+                            ls_lmt=2000, flip_lmt=min(L, 10), n_lmt=n,
+                            stop=P.StopCondition(max_nse=1 + total_steps * (n + 1)))
+    seeds = [args.seed + rank * n_walks + w for w in range(n_walks)]
+
+    # roofline denominators measured on this GPU, now
+    import ctypes
+    dadd, lds, mhz = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+    err = ctypes.create_string_buffer(256)
+    P._lib.lib().psl_probe_peaks(ctx.handle, ctypes.byref(dadd), ctypes.byref(lds),
+                                 ctypes.byref(mhz), err, 256)
+
+    # setup: pivots (random_sequence), O(L^2) tables -- untimed, like the reference
+    t_setup = time.perf_counter()
+    walks = P.Walks(params, n_walks, seeds=seeds, ctx=ctx)
+    torch.cuda.synchronize()
+    setup_s = time.perf_counter() - t_setup
+
+    for _ in range(args.warmup):
+        walks.step(1)
+    torch.cuda.synchronize()
+    r0 = walks.records()
+    nse0 = sum(r.nse for r in r0)
+    launches0 = ctx.kernel_launches()
+    e_start = torch.cuda.Event(enable_timing=True)
+    e_end = torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local_rank) as clocks:
+        e_start.record(stream)
+        for _ in range(args.steps):
+            walks.step(1)
+        e_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = e_start.elapsed_time(e_end)
+    launches = ctx.kernel_launches() - launches0
+    r1 = walks.records(solutions=True)
+    nse_local = sum(r.nse for r in r1) - nse0
+    max_ms = D.max_over_ranks(ms, dev)
+    nse_total = D.sum_over_ranks(float(nse_local), dev)
+    value = nse_total / (max_ms * 1e-3)
+    # end-of-run best-PSL reduction across GPUs (outside the timed region)
+    best_psl, best_walk, _ = D.reduce_best([r.psl_best for r in r1], seeds,
+                                           [r.solution_best for r in r1], L, device=dev)
+    walks.close()
+
+    # dominant kernel: run_kernel, one launch per step; algorithmic work per
+    # launch = walks x n x (L-1) cells (one exact DADD-chain term each)
+    cells_per_launch = n_walks * n * (L - 1)
+    per_launch_s = (ms * 1e-3) / args.steps
+    achieved = cells_per_launch / per_launch_s
+    roofline = {
+        "bound": "fp64",
+        "achieved": achieved / 1e9, "peak": dadd.value / 1e9, "unit": "Gcell/s",
+        "frac": achieved / dadd.value if dadd.value else None,
+        "traffic": None,
+        "peak_source": "measured live: FP64-add pipe (one dependent DADD per cell is the "
+                       "serial fitness chain's floor), psl_probe_peaks",
+        "lds_table_roof_gcell_s": lds.value / 1e9,
+        "probe_sm_mhz": mhz.value,
+        "hbm_gbs_achieved": n_walks * 8.0 * L / per_launch_s / 1e9,
+    }
+
+    # e2e through the public API: host start sequences in, records + best
+    # sequences out, table build + e2e_steps search steps inside the region
+    e2e = None
+    if rank == 0 or True:
+        rng = np.random.default_rng(1234 + rank)
+        inits = np.where(rng.integers(0, 2, (n_walks, L)) == 1, -1, 1).astype(np.int8)
+        inits_t = torch.from_numpy(inits).pin_memory()
+        inits_pinned = inits_t.numpy()
+        p2 = P.SearchParams(length=L, seed=args.seed, alpha1=4, alpha2=P.default_alpha2(L),
+                            ls_lmt=2000, flip_lmt=min(L, 10), n_lmt=n,
+                            stop=P.StopCondition(max_nse=1 + args.e2e_steps * n))
+        torch.cuda.synchronize()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ea.record(stream)
+        recs = P.run_walks(p2, n_walks, seeds=seeds, inits=inits_pinned, ctx=ctx, solutions=True)
+        eb.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = D.max_over_ranks(ea.elapsed_time(eb), dev)
+        e2e_nse = D.sum_over_ranks(float(sum(r.nse for r in recs)), dev)
+        e2e = {"value": e2e_nse / (e2e_ms * 1e-3), "unit": "NSE/s",
+               "h2d_bytes_per_step": int(inits.nbytes + 8 * n_walks),
+               "d2h_bytes_per_step": int(n_walks * L + n_walks * 80),
+               "step": f"one psl_run_walks call: {n_walks} host start sequences -> "
+                       f"O(L^2) table build + {args.e2e_steps} search steps -> records + "
+                       f"best sequences on the host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import oracle_py as O
+            if O.ref_available():
+                rate, secs, desc = reference_sample(L, n, args.cpu_reps, os.cpu_count() or 1,
+                                                    args.seed)
+                cpu = {"value": rate, "unit": "NSE/s", "cores": os.cpu_count() or 1,
+                       "kind": "reference", "sample": desc, "seconds": secs}
+        except Exception as e:  # the baseline is reported, never required
+            cpu = {"value": None, "unit": "NSE/s", "cores": os.cpu_count() or 1,
+                   "kind": "reference", "sample": f"failed: {e}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "NSE/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": max_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": value / A100_M20_NSE,
+            "dtype": "f64", "data": "synthetic",
+            "config": {
+                "workload": f"m20 two-phase search: L={L}, {n_walks} independent walks per GPU "
+                            f"(one CTA per SM), alpha1=4, alpha2={P.default_alpha2(L)}, "
+                            f"ls_lmt=2000, flip_lmt=10, n_lmt={n}",
+                "L": L, "walks_per_gpu": n_walks, "n_lmt": n, "parallelism": f"walks x{world}",
+                "l2": "inputs larger than L2: each step streams every walk's 4 MB C_k table "
+                      f"({n_walks * 4 * L / 2**20:.0f} MiB per GPU per step) through L2",
+                "vs_baseline_ref": "A100 solver 85062 NSE/s at L=1048575 (PAPER.md:342-359, "
+                                   "N_lmt=6912)",
+                "setup_seconds": setup_s},
+            "cells_per_s": value * (L - 1),
+            "roofline": roofline,
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "best_psl": best_psl, "best_walk": best_walk,
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -146,6 +146,11 @@ int psl_ctx_set_stream(psl_ctx* ctx, void* stream);
 void* psl_ctx_stream(psl_ctx* ctx);
 const char* psl_version(void);                         /* version.hpp:5 */
 uint32_t psl_kernel_launches(psl_ctx* ctx);            /* kernels launched so far */
+/* Measurement helper for the roofline (bench.py): FP64-add pipe throughput
+ * (cells/s at one DADD per cell), the divergent-LDS.64+DADD loop rate, and the
+ * SM clock seen by the probe. */
+int psl_probe_peaks(psl_ctx* ctx, double* dadd_cells_per_s, double* lds_cells_per_s,
+                    double* sm_mhz, char* err, size_t errlen);
 
 /* ---- parameters (host logic, search.cpp:19-94, sequence.cpp:95-105) ---- */
 uint32_t psl_default_alpha2(uint32_t length);          /* search.cpp:19-23 */

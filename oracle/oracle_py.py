@@ -77,6 +77,7 @@ def lib():
         L.orc_power_table.argtypes = [C.c_uint32, C.c_uint32, _f64p]
         L.orc_build_table.argtypes = [_i8p, C.c_uint32, _i32p]
         L.orc_build_table_fast.argtypes = [_i8p, C.c_uint32, _i32p]
+        L.orc_build_table_mt.argtypes = [_i8p, C.c_uint32, _i32p, C.c_uint32]
         L.orc_psl.argtypes = [_i32p, C.c_uint32]
         L.orc_psl.restype = C.c_int32
         L.orc_fitness.argtypes = [_i32p, C.c_uint32, _f64p]
@@ -183,13 +184,16 @@ def power_table(max_abs: int, alpha: int) -> np.ndarray:
     return lut
 
 
-def build_table(s: np.ndarray, fast: bool | None = None) -> np.ndarray:
+def build_table(s: np.ndarray, fast: bool | None = None, threads: int = 0) -> np.ndarray:
     s = np.ascontiguousarray(s, np.int8)
     L = len(s)
     c = np.empty(L, np.int32)
     if fast is None:
         fast = L > 4096
-    (lib().orc_build_table_fast if fast else lib().orc_build_table)(s, L, c)
+    if threads > 1:
+        lib().orc_build_table_mt(s, L, c, threads)
+    else:
+        (lib().orc_build_table_fast if fast else lib().orc_build_table)(s, L, c)
     return c
 
 

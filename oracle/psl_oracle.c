@@ -9,6 +9,7 @@
 #include "psl_oracle.h"
 
 #include <math.h>
+#include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -108,6 +109,53 @@ void orc_build_table_fast(const int8_t* s, uint32_t L, int32_t* c) {
     c[k] = (int32_t)n - 2 * (int32_t)diff;
   }
   free(b);
+}
+
+/* orc_build_table_fast split over threads (shift k handled by thread
+ * k % nthreads, so the O(L-k) work per shift is balanced). */
+typedef struct { const uint64_t* b; uint32_t L; int32_t* c; uint32_t t, nt; } orc_tb_job;
+
+static void* orc_tb_worker(void* arg) {
+  const orc_tb_job* j = (const orc_tb_job*)arg;
+  const uint64_t* b = j->b;
+  const uint32_t L = j->L;
+  for (uint32_t k = 1 + j->t; k < L; k += j->nt) {
+    const uint32_t n = L - k;
+    const uint32_t ws = k >> 6, sh = k & 63;
+    int64_t diff = 0;
+    const uint32_t full = n / 64;
+    uint32_t w = 0;
+    if (sh) {
+      for (; w < full; ++w)
+        diff += __builtin_popcountll(b[w] ^ ((b[w + ws] >> sh) | (b[w + ws + 1] << (64 - sh))));
+    } else {
+      for (; w < full; ++w) diff += __builtin_popcountll(b[w] ^ b[w + ws]);
+    }
+    if (n & 63) {
+      uint64_t hi = b[w + ws];
+      uint64_t shifted = sh ? ((hi >> sh) | (b[w + ws + 1] << (64 - sh))) : hi;
+      diff += __builtin_popcountll((b[w] ^ shifted) & ((1ull << (n & 63)) - 1));
+    }
+    j->c[k] = (int32_t)n - 2 * (int32_t)diff;
+  }
+  return NULL;
+}
+
+void orc_build_table_mt(const int8_t* s, uint32_t L, int32_t* c, uint32_t nthreads) {
+  const uint32_t W = (L + 63) / 64;
+  uint64_t* b = (uint64_t*)calloc((size_t)W + 2, sizeof(uint64_t));
+  for (uint32_t i = 0; i < L; ++i)
+    if (s[i] < 0) b[i >> 6] |= 1ull << (i & 63);
+  c[0] = (int32_t)L;
+  if (nthreads < 1) nthreads = 1;
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * nthreads);
+  orc_tb_job* jobs = (orc_tb_job*)malloc(sizeof(orc_tb_job) * nthreads);
+  for (uint32_t t = 0; t < nthreads; ++t) {
+    jobs[t].b = b; jobs[t].L = L; jobs[t].c = c; jobs[t].t = t; jobs[t].nt = nthreads;
+    pthread_create(&th[t], NULL, orc_tb_worker, &jobs[t]);
+  }
+  for (uint32_t t = 0; t < nthreads; ++t) pthread_join(th[t], NULL);
+  free(th); free(jobs); free(b);
 }
 
 /* sequence.cpp:84-93 */

@@ -36,6 +36,7 @@ double orc_pow_int(double base, uint32_t exp);                       /* :95-105 
 void orc_power_table(uint32_t max_abs, uint32_t alpha, double* lut); /* :107-115 */
 void orc_build_table(const int8_t* s, uint32_t L, int32_t* c);       /* :46-60   */
 void orc_build_table_fast(const int8_t* s, uint32_t L, int32_t* c);  /* same result, bit-parallel */
+void orc_build_table_mt(const int8_t* s, uint32_t L, int32_t* c, uint32_t nthreads);
 int32_t orc_psl(const int32_t* c, uint32_t L);                       /* :84-93   */
 double orc_fitness(const int32_t* c, uint32_t L, const double* lut); /* :131-141 */
 double orc_merit_factor(const int32_t* c, uint32_t L);               /* :143-152 */

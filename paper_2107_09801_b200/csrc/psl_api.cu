@@ -165,6 +165,18 @@ void* psl_ctx_stream(psl_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; 
 
 uint32_t psl_kernel_launches(psl_ctx* ctx) { return ctx ? ctx->launches : 0; }
 
+int psl_probe_peaks(psl_ctx* ctx, double* dadd_cells_per_s, double* lds_cells_per_s,
+                    double* sm_mhz, char* err, size_t errlen) {
+  int rc = device_ready(ctx, err, errlen);
+  if (rc) return rc;
+  int nsm = 0;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
+  const int n = probe_peaks(nsm, ctx->stream, dadd_cells_per_s, lds_cells_per_s, sm_mhz);
+  if (n < 0) return cuda_fail(err, errlen, cudaGetLastError(), "probe_peaks");
+  ctx->launches += (uint32_t)n;
+  return PSL_OK;
+}
+
 // ---------------------------------------------------------------- params
 
 uint32_t psl_default_alpha2(uint32_t length) {

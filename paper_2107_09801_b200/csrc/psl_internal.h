@@ -96,5 +96,6 @@ int launch_scan(const ScanArgs& a, cudaStream_t s);
 int launch_table_only(const uint32_t* d_bits, int32_t* d_C, uint32_t L, uint32_t nwords,
                       cudaStream_t s);
 int launch_apply_flip(uint32_t* d_bits, int32_t* d_C, uint32_t L, uint32_t j, cudaStream_t s);
+int probe_peaks(int nsm, cudaStream_t s, double* dadd_cps, double* lds_cps, double* mhz);
 
 }  // namespace pslb

@@ -987,3 +987,83 @@ int launch_apply_flip(uint32_t* d_bits, int32_t* d_C, uint32_t L, uint32_t j, cu
 }
 
 }  // namespace pslb
+
+// ---------------------------------------------------------------- probes
+// Roofline denominators measured live (bench.py): the FP64 add pipe (the
+// serial fitness chain needs exactly one dependent DADD per cell) and the
+// divergent-LDS.64 + DADD rate of a per-cell table-lookup loop.
+namespace pslb {
+namespace {
+__global__ void __launch_bounds__(1024, 1) probe_dadd_kernel(int reps, double* out, long long* cyc) {
+  double s1 = threadIdx.x * 1e-3, s2 = 0.5, s3 = 0.25, s4 = 1.0;
+  const double x = 1.0000001 + threadIdx.x * 1e-9;
+  const long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      s1 = __dadd_rn(s1, x); s2 = __dadd_rn(s2, x); s3 = __dadd_rn(s3, x); s4 = __dadd_rn(s4, x);
+    }
+  }
+  const long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s1 + s2 + s3 + s4;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+__global__ void __launch_bounds__(1024, 1) probe_lds_kernel(int reps, double* out, long long* cyc) {
+  __shared__ __align__(16) double tab[512 * 8];
+  for (int i = threadIdx.x; i < 512 * 8; i += blockDim.x) tab[i] = 1.0 + (i & 7) * 0.25;
+  __syncthreads();
+  uint32_t w = 0x9E3779B9u * (threadIdx.x + 1);
+  double sum = 0.0;
+  const long long t0 = clock64();
+  for (int r = 0; r < reps; ++r) {
+#pragma unroll 1
+    for (int kb = 0; kb < 512; kb += 16) {
+      const char* rb = reinterpret_cast<const char*>(tab + kb * 8);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const uint32_t v = q < 2 ? (w << (3 - 2 * q)) : (w >> (2 * q - 3));
+        sum = __dadd_rn(sum, *reinterpret_cast<const double*>(rb + q * 64 + (v & 0x18u)));
+      }
+      w = w * 1664525u + 1013904223u;
+    }
+  }
+  const long long t1 = clock64();
+  out[blockIdx.x * blockDim.x + threadIdx.x] = sum;
+  if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
+}
+}  // namespace
+
+int probe_peaks(int nsm, cudaStream_t s, double* dadd_cps, double* lds_cps, double* mhz) {
+  double* out = nullptr;
+  long long* cyc = nullptr;
+  if (cudaMalloc(&out, sizeof(double) * nsm * 1024) != cudaSuccess) return -1;
+  if (cudaMalloc(&cyc, sizeof(long long) * nsm) != cudaSuccess) { cudaFree(out); return -1; }
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int reps = 2000;
+  float ms = 0.f;
+  long long c0 = 0;
+  probe_dadd_kernel<<<nsm, 1024, 0, s>>>(10, out, cyc);
+  cudaEventRecord(a, s);
+  probe_dadd_kernel<<<nsm, 1024, 0, s>>>(reps, out, cyc);
+  cudaEventRecord(b, s);
+  cudaEventSynchronize(b);
+  cudaEventElapsedTime(&ms, a, b);
+  cudaMemcpy(&c0, cyc, sizeof(c0), cudaMemcpyDeviceToHost);
+  *dadd_cps = (double)nsm * 1024 * reps * 64 / (ms * 1e-3);
+  *mhz = (double)c0 / (ms * 1e-3) / 1e6;
+  probe_lds_kernel<<<nsm, 1024, 0, s>>>(10, out, cyc);
+  cudaEventRecord(a, s);
+  probe_lds_kernel<<<nsm, 1024, 0, s>>>(reps / 10, out, cyc);
+  cudaEventRecord(b, s);
+  cudaEventSynchronize(b);
+  cudaEventElapsedTime(&ms, a, b);
+  *lds_cps = (double)nsm * 1024 * (reps / 10) * 512 / (ms * 1e-3);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  cudaFree(cyc);
+  return cudaGetLastError() == cudaSuccess ? 4 : -1;
+}
+}  // namespace pslb
