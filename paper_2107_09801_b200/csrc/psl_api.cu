@@ -271,6 +271,7 @@ int run_scan(psl_ctx* ctx, const int8_t* seq, const int32_t* table, uint32_t L, 
   if (rc) return rc;
   const uint32_t nw = (L + 31) / 32;
   std::vector<uint32_t> bits = pack_bits(seq, L, kBitsPad);
+  bits.insert(bits.begin(), 0u);   // front pad: word i at bits[i + 1]
   int32_t P = 0;
   for (uint32_t k = 1; k < L; ++k) P = std::max(P, std::abs(table[k]));
   std::vector<int2> h;
@@ -487,7 +488,7 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
   a.events_cap = events_cap;
   a.traces_cap = traces_cap;
   a.c_stride = ((size_t)L + 31) & ~size_t(31);
-  a.w_stride = ((size_t)nw + kBitsPad + 3) & ~size_t(3);
+  a.w_stride = ((size_t)nw + 1 + kBitsPad + 3) & ~size_t(3);
   a.h_stride = L;
   a.f_stride = std::max<uint32_t>(p.flip_lmt, 1);
   auto fail = [&](cudaError_t e, const char* what) {
@@ -605,7 +606,7 @@ int psl_walks_records(psl_walks* w, psl_walk_record* records, int8_t* solutions,
     r.switches = S.switches;
     r.steps = S.steps;
     if (solutions) {
-      const uint32_t* b = bb.data() + (size_t)i * w->a.w_stride;
+      const uint32_t* b = bb.data() + (size_t)i * w->a.w_stride + 1;
       int8_t* o = solutions + (size_t)i * L;
       for (uint32_t k = 0; k < L; ++k) o[k] = ((b[k >> 5] >> (k & 31)) & 1u) ? -1 : 1;
     }

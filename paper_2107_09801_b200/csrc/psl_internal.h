@@ -11,7 +11,9 @@
 
 namespace pslb {
 
-constexpr int kThreads = 1024;     // one CTA per walk; thread t scores neighbour i = t+1
+constexpr int kThreads = 256;      // one CTA per walk
+constexpr int kJ = 4;              // adjacent neighbours scored per thread
+constexpr int kGroup = kThreads * kJ;  // neighbours per sweep (1024)
 constexpr int kChunk = 512;        // k records staged in shared memory per chunk
 constexpr int kRecDoubles = 8;     // per-k record: BOTH[e4,e2,e2,e0] ONE[e3,e1,e1,e2]
 constexpr int kHCap = 1024;        // filtered high-sidelobe list kept in smem

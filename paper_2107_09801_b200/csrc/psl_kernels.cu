@@ -115,6 +115,19 @@ __device__ __forceinline__ uint32_t sword(const uint32_t* sb, int w, int nwords)
   w = max(-1, min(w, nwords));
   return sb[w + 1];
 }
+__device__ __forceinline__ uint32_t sword_up(const uint32_t* sb, int w, int nwords) {
+  return sb[min(w, nwords) + 1];   // index only grows (B window)
+}
+__device__ __forceinline__ uint32_t sword_dn(const uint32_t* sb, int w) {
+  return sb[max(w, -1) + 1];       // index only shrinks (A window)
+}
+// (v & mask) | base as one LOP3 (the compiler would turn a disjoint OR into
+// an extra add)
+__device__ __forceinline__ uint32_t and_or(uint32_t v, uint32_t mask, uint32_t base) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(v), "r"(mask), "r"(base));
+  return r;
+}
 
 template <typename T>
 __device__ __forceinline__ T warp_max(T v) {
@@ -153,7 +166,8 @@ struct Smem {
   double* tail;    // [2][kChunk]
   int2* hf;        // [kHCap]
   Ctl* ctl;
-  uint32_t* sb;    // [nwords + 2], sb[0] and sb[nwords+1] are zero pads
+  const uint32_t* sb;  // the walk's bit-packed pivot in global memory (L1-cached):
+                       // sb[0] zero pad, word i at sb[i+1], zero pads after
 };
 
 __device__ __forceinline__ Smem carve(unsigned char* base) {
@@ -162,7 +176,7 @@ __device__ __forceinline__ Smem carve(unsigned char* base) {
   m.tail = reinterpret_cast<double*>(base + kTabBytes);
   m.hf = reinterpret_cast<int2*>(base + kTabBytes + kTailBytes);
   m.ctl = reinterpret_cast<Ctl*>(base + kTabBytes + kTailBytes + kHfBytes);
-  m.sb = reinterpret_cast<uint32_t*>(base + kTabBytes + kTailBytes + kHfBytes + kCtlBytes);
+  m.sb = nullptr;
   return m;
 }
 
@@ -215,169 +229,256 @@ __device__ __forceinline__ double term(const SweepIO& io, int32_t a) {
   return pow_int_dev((double)a, io.alpha);
 }
 
-// Expand chunk c of C into the per-k term records.
+// Expand chunk c of C into the per-k term records (kChunk records, the CTA's
+// threads take kChunk / kThreads each).
 __device__ __forceinline__ void build_chunk(const SweepIO& io, uint32_t c, double* tab,
                                             double* tail, const uint32_t* sb, int32_t& pmax) {
-  const uint32_t t = threadIdx.x;
-  if (t >= (uint32_t)kChunk) return;
-  const uint32_t k = 1 + c * kChunk + t;
-  double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0, e4 = 0.0;
-  bool want = false;
-  int32_t cv = 0;
-  if (k < io.L) {
-    cv = io.Csrc[k];
-    if (io.F) cv = fold_flips(cv, k, io, sb);
-    if (io.Cdst) io.Cdst[k] = cv;
-    if (io.Cloc) io.Cloc[k] = cv;
-    const int32_t av = abs(cv);
-    pmax = max(pmax, av);
-    want = io.hlist != nullptr && av >= io.hthr;
-    e2 = term(io, av);
-    e4 = term(io, abs(cv - 4));
-    e3 = term(io, abs(cv - 2));
-    e1 = term(io, abs(cv + 2));
-    e0 = term(io, abs(cv + 4));
-  }
-  if (io.hlist) {
-    const uint32_t m = __ballot_sync(FULL, want);
-    if (m) {
-      const int lane = t & 31, leader = __ffs(m) - 1;
-      uint32_t base = 0;
-      if (lane == leader) base = atomicAdd(io.hcount, (uint32_t)__popc(m));
-      base = __shfl_sync(FULL, base, leader);
-      if (want) io.hlist[base + __popc(m & ((1u << lane) - 1))] = make_int2((int)k, cv);
+#pragma unroll 1
+  for (uint32_t r = threadIdx.x; r < (uint32_t)kChunk; r += kThreads) {
+    const uint32_t k = 1 + c * kChunk + r;
+    double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0, e4 = 0.0;
+    bool want = false;
+    int32_t cv = 0;
+    if (k < io.L) {
+      cv = io.Csrc[k];
+      if (io.F) cv = fold_flips(cv, k, io, sb);
+      if (io.Cdst) io.Cdst[k] = cv;
+      if (io.Cloc) io.Cloc[k] = cv;
+      const int32_t av = abs(cv);
+      pmax = max(pmax, av);
+      want = io.hlist != nullptr && av >= io.hthr;
+      e2 = term(io, av);
+      e4 = term(io, abs(cv - 4));
+      e3 = term(io, abs(cv - 2));
+      e1 = term(io, abs(cv + 2));
+      e0 = term(io, abs(cv + 4));
     }
+    if (io.hlist) {
+      const uint32_t m = __ballot_sync(FULL, want);
+      if (m) {
+        const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(io.hcount, (uint32_t)__popc(m));
+        base = __shfl_sync(FULL, base, leader);
+        if (want) io.hlist[base + __popc(m & ((1u << lane) - 1))] = make_int2((int)k, cv);
+      }
+    }
+    double2* rec = reinterpret_cast<double2*>(tab + (size_t)r * kRecDoubles);
+    rec[0] = make_double2(e4, e2);   // BOTH slot = 2*bA' + bB'
+    rec[1] = make_double2(e2, e0);
+    rec[2] = make_double2(e3, e1);   // ONE  slot = one valid bit
+    rec[3] = make_double2(e1, e2);   // (slot 3: e2, unused)
+    tail[r] = e2;
   }
-  double2* rec = reinterpret_cast<double2*>(tab + (size_t)t * kRecDoubles);
-  rec[0] = make_double2(e4, e2);   // BOTH slot = 2*bA' + bB'
-  rec[1] = make_double2(e2, e0);
-  rec[2] = make_double2(e3, e1);   // ONE  slot = one valid bit
-  rec[3] = make_double2(e1, e2);   // (slot 3: e2, unused)
-  tail[t] = e2;
 }
 
-enum : int { CLS_BOTH = 0, CLS_ONE = 1, CLS_TAIL = 2, CLS_MIXED = 3 };
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void lds_f64x2(uint32_t a, double& x, double& y) {
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(x), "=d"(y) : "r"(a));
+}
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
 
-// One full sweep over k = 1..L-1.  Returns this lane's neighbour fitness.
-__device__ __forceinline__ double sweep(const SweepIO& io, const Smem& sm, bool active,
-                                        uint32_t j, int32_t& pmax, double& chain) {
+// bits of word x for cell q, moved so the field lands at bit `to`
+template <int FIELD_BITS, int TO>
+__device__ __forceinline__ uint32_t field_at(uint32_t x, int q) {
+  const int sh = FIELD_BITS * q - TO;
+  return sh < 0 ? (x << (-sh)) : (x >> sh);
+}
+
+__device__ __forceinline__ uint32_t lo32(double x) { return (uint32_t)__double2loint(x); }
+__device__ __forceinline__ uint32_t hi32(double x) { return (uint32_t)__double2hiint(x); }
+
+// top bit of r, and r << 1, in one IMAD.WIDE (FMA pipe)
+__device__ __forceinline__ uint32_t pop_top_bit(uint32_t& r) {
+  uint64_t w;
+  asm("mul.wide.u32 %0, %1, 2;" : "=l"(w) : "r"(r));
+  r = (uint32_t)w;
+  return (uint32_t)(w >> 32);
+}
+
+// One full sweep over k = 1..L-1 for the kJ adjacent neighbours j[m] of this
+// lane (sum[m] = their fitness, the reference's serial ascending-k chain).
+//
+// Per 32-shift block the warp picks one code path from warp-uniform
+// thresholds over its 128 neighbours (no per-lane branching):
+//   BOTH  every neighbour has both s_{j-k} and s_{j+k}: 2-bit cell code
+//         (bA', bB') -> record slot {e4, e2, e2, e0} via a divergent LDS.64
+//   ONE   every neighbour past its both-range, before its one-range end:
+//         1-bit code b' selects e3 / e1, loaded once per k (uniform LDS.128)
+//         and chosen per neighbour on the ALU (FSEL) or the FMA pipe
+//         (IMAD on the two 32-bit halves: e3 + b'(e1 - e3) mod 2^32)
+//   TAIL  every neighbour past its one-range end: |C_k|^alpha, loaded once
+//         per two shifts (uniform LDS.128) for all kJ chains
+//   MIXED some range boundary inside the block: per-cell region, LDS path
+// with bA' = [s_{j-k} == -s_j], bB' = [s_{j+k} == -s_j]; the term is
+// |C_k - 2 s_j (s_{j-k} + s_{j+k})|^alpha = e_{2 + s_j(s_{j-k}+s_{j+k})}.
+__device__ __forceinline__ void sweep(const SweepIO& io, const Smem& sm, const bool (&active)[kJ],
+                                      const uint32_t (&jin)[kJ], double (&sum)[kJ],
+                                      int32_t& pmax, double& chain) {
   const uint32_t L = io.L;
   const int nwords = (int)io.nwords;
   const uint32_t* sb = sm.sb;
-  // lane geometry (sequence.hpp:131-135)
-  const uint32_t left = j, right = L - 1 - j;
-  const uint32_t be = left < right ? left : right;   // both-sides range end
-  const uint32_t oe = left < right ? right : left;   // one-side range end
-  const bool sideA = left >= right;                  // one-side range uses s[j-k]
-  const uint32_t mbj = ((sb[(j >> 5) + 1] >> (j & 31)) & 1u) ? FULL : 0u;
-  // sliding windows: B covers positions j+k, A covers j-k (k = k0..k0+31)
-  int wB = (int)((j + 1) >> 5);
-  const uint32_t shB = (j + 1) & 31;
-  uint32_t Blo = sword(sb, wB, nwords), Bhi = sword(sb, wB + 1, nwords);
-  int wA = (int)(j >> 5) - 1;
-  const uint32_t shA = j & 31;
-  uint32_t Alo = sword(sb, wA, nwords), Ahi = sword(sb, wA + 1, nwords);
-
-  const uint32_t smask_one = sideA ? 0x10u : 0x08u;
-  double sum = 0.0;
-  const bool warp_scans = io.scan && __any_sync(FULL, active);
+  // inactive neighbours shadow the warp's first active one (results discarded)
+  const uint32_t src = __ffs(__ballot_sync(FULL, active[0])) - 1;
+  const uint32_t jsrc = __shfl_sync(FULL, jin[0], src < 32 ? src : 0);
+  uint32_t be[kJ], oe[kJ], mbj[kJ], shB[kJ], shA[kJ], smask[kJ];
+  uint32_t Blo[kJ], Bhi[kJ], Alo[kJ], Ahi[kJ];
+  int wB[kJ], wA[kJ];
+  bool sideA[kJ];
+  uint32_t lminBE = FULL, lmaxBE = 0, lminOE = FULL, lmaxOE = 0;
+#pragma unroll
+  for (int m = 0; m < kJ; ++m) {
+    const uint32_t j = active[m] ? jin[m] : jsrc;
+    const uint32_t left = j, right = L - 1 - j;       // sequence.hpp:131-135
+    be[m] = left < right ? left : right;
+    oe[m] = left < right ? right : left;
+    sideA[m] = left >= right;
+    smask[m] = sideA[m] ? 0x10u : 0x08u;
+    mbj[m] = ((sb[(j >> 5) + 1] >> (j & 31)) & 1u) ? FULL : 0u;
+    wB[m] = (int)((j + 1) >> 5);
+    shB[m] = (j + 1) & 31;
+    Blo[m] = sword(sb, wB[m], nwords);
+    Bhi[m] = sword(sb, wB[m] + 1, nwords);
+    wA[m] = (int)(j >> 5) - 1;
+    shA[m] = j & 31;
+    Alo[m] = sword(sb, wA[m], nwords);
+    Ahi[m] = sword(sb, wA[m] + 1, nwords);
+    lminBE = min(lminBE, be[m]); lmaxBE = max(lmaxBE, be[m]);
+    lminOE = min(lminOE, oe[m]); lmaxOE = max(lmaxOE, oe[m]);
+  }
+  const uint32_t minBE = __reduce_min_sync(FULL, lminBE), maxBE = __reduce_max_sync(FULL, lmaxBE);
+  const uint32_t minOE = __reduce_min_sync(FULL, lminOE), maxOE = __reduce_max_sync(FULL, lmaxOE);
+#pragma unroll
+  for (int m = 0; m < kJ; ++m) sum[m] = 0.0;
+  const bool warp_scans = io.scan && __any_sync(FULL, active[0]);
+  const uint32_t tab0 = smem_u32(sm.tab), tail0 = smem_u32(sm.tail);
 
   build_chunk(io, 0, sm.tab, sm.tail, sb, pmax);
   __syncthreads();
   for (uint32_t c = 0; c < io.nchunks; ++c) {
     const uint32_t buf = c & 1;
-    double* tab = sm.tab + (size_t)buf * kChunk * kRecDoubles;
-    const double* tail = sm.tail + (size_t)buf * kChunk;
     if (c + 1 < io.nchunks)
       build_chunk(io, c + 1, sm.tab + (size_t)(buf ^ 1) * kChunk * kRecDoubles,
                   sm.tail + (size_t)(buf ^ 1) * kChunk, sb, pmax);
+    const uint32_t tab = tab0 + buf * (kChunk * kRecDoubles * 8);
+    const uint32_t tail = tail0 + buf * (kChunk * 8);
     if (warp_scans) {
 #pragma unroll 1
       for (uint32_t blk = 0; blk < kChunk / 32; ++blk) {
         const uint32_t k0 = 1 + c * kChunk + blk * 32;
         const uint32_t kend = k0 + 31;
-        int cls;
-        if (!active) cls = CLS_TAIL;
-        else if (kend <= be) cls = CLS_BOTH;
-        else if (k0 > oe) cls = CLS_TAIL;
-        else if (k0 > be && kend <= oe) cls = CLS_ONE;
-        else cls = CLS_MIXED;
-        const uint32_t bm = __ballot_sync(FULL, cls == CLS_MIXED);
-        const uint32_t bb = __ballot_sync(FULL, cls == CLS_BOTH);
-        const uint32_t bo = __ballot_sync(FULL, cls == CLS_ONE);
-        const uint32_t Bp = __funnelshift_r(Blo, Bhi, shB) ^ mbj;
-        const uint32_t Ap = __brev(__funnelshift_r(Alo, Ahi, shA)) ^ mbj;
-        // prefetch the next block's window words
-        const uint32_t nB = sword(sb, wB + 2, nwords);
-        const uint32_t nA = sword(sb, wA - 1, nwords);
-        const char* rb = reinterpret_cast<const char*>(tab + (size_t)blk * 32 * kRecDoubles);
-        if (!(bm | bb | bo)) {
-          // every lane past its one-side range: the term is |C_k|^alpha for all
-          const double2* t2 = reinterpret_cast<const double2*>(tail + blk * 32);
+        uint32_t Bp[kJ], Ap[kJ], nB[kJ], nA[kJ];
 #pragma unroll
-          for (int q = 0; q < 16; ++q) {
-            const double2 v = t2[q];
-            sum = __dadd_rn(sum, v.x);
-            sum = __dadd_rn(sum, v.y);
+        for (int m = 0; m < kJ; ++m) {
+          Bp[m] = __funnelshift_r(Blo[m], Bhi[m], shB[m]) ^ mbj[m];
+          Ap[m] = __brev(__funnelshift_r(Alo[m], Ahi[m], shA[m])) ^ mbj[m];
+          nB[m] = sword_up(sb, wB[m] + 2, nwords);    // next block's window words
+          nA[m] = sword_dn(sb, wA[m] - 1);
+        }
+        const uint32_t rb = tab + blk * 32 * (kRecDoubles * 8);   // 64-byte aligned
+        const bool ub = maxBE < k0 || minBE >= kend;
+        const bool uo = maxOE < k0 || minOE >= kend;
+        if (ub && uo && minBE >= kend) {
+          // BOTH: 2-bit code, slot = 2 bA' + bB'
+          uint32_t Wlo[kJ], Whi[kJ];
+#pragma unroll
+          for (int m = 0; m < kJ; ++m) {
+            Wlo[m] = spread_lo(Bp[m]) | (spread_lo(Ap[m]) << 1);
+            Whi[m] = spread_hi(Bp[m]) | (spread_hi(Ap[m]) << 1);
           }
-        } else if (!(bm | bb)) {
-          // one-side / tail lanes only: one bit per cell
-          const uint32_t P = sideA ? Ap : Bp;
-          const uint32_t mask = (cls == CLS_ONE) ? 0x08u : 0u;
-          const uint32_t base = (cls == CLS_ONE) ? 32u : 8u;
 #pragma unroll
           for (int q = 0; q < 32; ++q) {
-            const uint32_t v = (q < 3) ? (P << (3 - q)) : (P >> (q - 3));
-            const uint32_t off = (v & mask) | base;
-            sum = __dadd_rn(sum, *reinterpret_cast<const double*>(rb + q * 64 + off));
+#pragma unroll
+            for (int m = 0; m < kJ; ++m) {
+              const uint32_t v = field_at<2, 3>(q < 16 ? Wlo[m] : Whi[m], q & 15);
+              sum[m] = __dadd_rn(sum[m], lds_f64(and_or(v, 0x18u, rb) + q * 64));
+            }
+          }
+        } else if (ub && uo && maxBE < k0 && minOE >= kend) {
+          // ONE: 1-bit code from the neighbour's valid side selects e3 / e1,
+          // loaded once per k for all kJ neighbours.  Cells go in groups of
+          // kG so the per-cell predicates come from one R2P per neighbour.
+          constexpr int kG = 4;
+          uint32_t P[kJ];
+#pragma unroll
+          for (int m = 0; m < kJ; ++m) P[m] = sideA[m] ? Ap[m] : Bp[m];
+#pragma unroll
+          for (int g = 0; g < 32 / kG; ++g) {
+            double e3[kG], e1[kG];
+#pragma unroll
+            for (int qq = 0; qq < kG; ++qq) lds_f64x2(rb + (g * kG + qq) * 64 + 32, e3[qq], e1[qq]);
+            double tm[kJ][kG];
+#pragma unroll
+            for (int m = 0; m < kJ; ++m) {
+              const uint32_t x = P[m] >> (g * kG);
+#pragma unroll
+              for (int qq = 0; qq < kG; ++qq) tm[m][qq] = ((x >> qq) & 1u) ? e1[qq] : e3[qq];
+            }
+#pragma unroll
+            for (int qq = 0; qq < kG; ++qq) {
+#pragma unroll
+              for (int m = 0; m < kJ; ++m) sum[m] = __dadd_rn(sum[m], tm[m][qq]);
+            }
+          }
+        } else if (ub && uo && maxOE < k0) {
+          // TAIL: the term is |C_k|^alpha for every neighbour
+          const uint32_t t2 = tail + blk * 32 * 8;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            double x, y;
+            lds_f64x2(t2 + q * 16, x, y);
+#pragma unroll
+            for (int m = 0; m < kJ; ++m) {
+              sum[m] = __dadd_rn(sum[m], x);
+              sum[m] = __dadd_rn(sum[m], y);
+            }
           }
         } else {
-          const uint32_t Wlo = spread_lo(Bp) | (spread_lo(Ap) << 1);
-          const uint32_t Whi = spread_hi(Bp) | (spread_hi(Ap) << 1);
-          if (!bm) {
-            const uint32_t mask = cls == CLS_BOTH ? 0x18u : (cls == CLS_ONE ? smask_one : 0u);
-            const uint32_t base = cls == CLS_BOTH ? 0u : (cls == CLS_ONE ? 32u : 8u);
+          // MIXED: a region boundary inside the block for some neighbour
 #pragma unroll
-            for (int q = 0; q < 32; ++q) {
-              const uint32_t x = q < 16 ? Wlo : Whi;
-              const int sh = 2 * (q & 15) - 3;
-              const uint32_t v = sh < 0 ? (x << (-sh)) : (x >> sh);
-              const uint32_t off = (v & mask) | base;
-              sum = __dadd_rn(sum, *reinterpret_cast<const double*>(rb + q * 64 + off));
-            }
-          } else {
-            // region boundary inside the block for some lane: per-cell region
+          for (int m = 0; m < kJ; ++m) {
+            const uint32_t Wlo = spread_lo(Bp[m]) | (spread_lo(Ap[m]) << 1);
+            const uint32_t Whi = spread_hi(Bp[m]) | (spread_hi(Ap[m]) << 1);
+            double s = sum[m];
 #pragma unroll 4
             for (int q = 0; q < 32; ++q) {
               const uint32_t k = k0 + q;
               const uint32_t x = q < 16 ? Wlo : Whi;
               const int sh = 2 * (q & 15) - 3;
               const uint32_t v = sh < 0 ? (x << (-sh)) : (x >> sh);
-              const bool inb = active && k <= be;
-              const bool ino = active && k <= oe;
-              const uint32_t mask = inb ? 0x18u : (ino ? smask_one : 0u);
+              const bool inb = k <= be[m];
+              const bool ino = k <= oe[m];
+              const uint32_t mask = inb ? 0x18u : (ino ? smask[m] : 0u);
               const uint32_t base = inb ? 0u : (ino ? 32u : 8u);
-              const uint32_t off = (v & mask) | base;
-              sum = __dadd_rn(sum, *reinterpret_cast<const double*>(rb + q * 64 + off));
+              s = __dadd_rn(s, lds_f64(and_or(v, mask, base | rb) + q * 64));
             }
+            sum[m] = s;
           }
         }
-        Blo = Bhi; Bhi = nB; ++wB;
-        Ahi = Alo; Alo = nA; --wA;
+#pragma unroll
+        for (int m = 0; m < kJ; ++m) {
+          Blo[m] = Bhi[m]; Bhi[m] = nB[m]; ++wB[m];
+          Ahi[m] = Alo[m]; Alo[m] = nA[m]; --wA[m];
+        }
       }
     }
     if (io.chain && threadIdx.x == 0) {
       // fitness(table, pow) (sequence.cpp:131-141): serial ascending k
-      const double2* t2 = reinterpret_cast<const double2*>(tail);
       for (int r = 0; r < kChunk / 2; ++r) {
-        const double2 v = t2[r];
-        chain = __dadd_rn(chain, v.x);
-        chain = __dadd_rn(chain, v.y);
+        double x, y;
+        lds_f64x2(tail + r * 16, x, y);
+        chain = __dadd_rn(chain, x);
+        chain = __dadd_rn(chain, y);
       }
     }
     __syncthreads();
   }
-  return sum;
 }
 
 // Exact neighbour PSL from the high-sidelobe list (entries (k, C_k)).
@@ -400,12 +501,9 @@ __device__ __forceinline__ int32_t neighbour_psl(const int2* h, uint32_t nh, int
 
 // Block-wide lexicographic (value, i) and (psl, i) minima + non-finite flag.
 // Result in ctl->best_* (valid after the trailing __syncthreads).
-__device__ __forceinline__ void block_reduce_scan(Ctl* ctl, bool active, double v, uint32_t i,
-                                                  int32_t p) {
+__device__ __forceinline__ void block_reduce_scan(Ctl* ctl, double v, uint32_t i, int32_t p,
+                                                  uint32_t pi, int bad) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  int bad = active && !isfinite(v);
-  if (!active) { v = __longlong_as_double(0x7ff0000000000000ll); i = 0xffffffffu; p = 0x7fffffff; }
-  uint32_t pi = i;
   for (int o = 16; o; o >>= 1) {
     const double v2 = __shfl_xor_sync(FULL, v, o);
     const uint32_t i2 = __shfl_xor_sync(FULL, i, o);
@@ -517,18 +615,19 @@ __global__ void __launch_bounds__(256) init_walks_kernel(RunArgs a, const uint64
         uint32_t word = 0;
         const uint32_t nb = min(32u, a.L - wd * 32);
         for (uint32_t b = 0; b < nb; ++b) word |= (uint32_t)(rng_next(z.rng) >> 63) << b;
-        bp[wd] = word;
+        bp[wd + 1] = word;
       }
     }
     *S = z;
   }
   if (init_bits) {
-    for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) bp[i] = init_bits[(size_t)w * nw + i];
+    for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) bp[i + 1] = init_bits[(size_t)w * nw + i];
   }
   __syncthreads();
-  for (uint32_t i = threadIdx.x; i < nw + kBitsPad; i += blockDim.x) {
-    const uint32_t v = i < nw ? bp[i] : 0u;
-    if (i >= nw) bp[i] = 0u;
+  // padded layout: [0] zero, words 1..nw, zeros after
+  for (uint32_t i = threadIdx.x; i < nw + 1 + kBitsPad; i += blockDim.x) {
+    const uint32_t v = (i >= 1 && i <= nw) ? bp[i] : 0u;
+    if (i < 1 || i > nw) bp[i] = 0u;
     bl[i] = v;
     bb[i] = v;
     us[i] = 0u;
@@ -617,9 +716,9 @@ __global__ void __launch_bounds__(256) build_tables_kernel(const uint32_t* bits,
 }
 
 // The device-resident run_search loop (search.cpp:327-430), one CTA per walk.
-__global__ void __launch_bounds__(kThreads, 1) run_kernel(RunArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const Smem sm = carve(smem_raw);
+__global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  Smem sm = carve(smem_raw);
   Ctl* ctl = sm.ctl;
   const uint32_t w = blockIdx.x, t = threadIdx.x;
   const uint32_t L = a.L, nw = a.nwords;
@@ -639,12 +738,11 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(RunArgs a) {
     if (ctl->st.t0_ns == 0) ctl->st.t0_ns = globaltimer();
     if (ctl->st.psl_best < 0) { ctl->st.psl_best = ctl->st.P; ctl->st.P_local = ctl->st.P; }
   }
-  sm.sb[0] = 0;
-  for (uint32_t i = t; i <= nw; i += kThreads) sm.sb[i + 1] = i < nw ? bits_piv[i] : 0u;
+  sm.sb = bits_piv;   // padded: word i at bits_piv[i + 1]
   __syncthreads();
   if (ctl->st.done || ctl->st.status != PSL_OK) return;
 
-  const uint32_t ngroups = (a.n + kThreads - 1) / kThreads;
+  const uint32_t ngroups = (a.n + kGroup - 1) / kGroup;
   for (;;) {
     // ---- top of step: stop checks, max-nse first (search.cpp:371-374)
     if (t == 0) {
@@ -670,10 +768,18 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(RunArgs a) {
     const uint32_t alpha = S0.phase == 1 ? a.alpha1 : a.alpha2;
 
     for (uint32_t g = 0; g < ngroups; ++g) {
-      const uint32_t i = g * kThreads + t + 1;
-      const bool active = do_scan && i <= a.n;
-      uint32_t j = 0;
-      if (active) { j = start + i; if (j >= L) j -= L; }
+      // this thread's kJ adjacent neighbours: offsets i = base + 1 .. base + kJ
+      const uint32_t ibase = g * kGroup + (t >> 5) * (32 * kJ) + (t & 31) * kJ;
+      bool active[kJ];
+      uint32_t jj[kJ];
+#pragma unroll
+      for (int m = 0; m < kJ; ++m) {
+        const uint32_t i = ibase + m + 1;
+        active[m] = do_scan && i <= a.n;
+        uint32_t j = 0;
+        if (active[m]) { j = start + i; if (j >= L) j -= L; }
+        jj[m] = j;
+      }
       SweepIO io;
       io.L = L; io.nwords = nw; io.nchunks = a.nchunks;
       io.alpha = alpha; io.lut = nullptr; io.lut_size = 0;
@@ -694,7 +800,8 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(RunArgs a) {
       }
       int32_t pmax = 0;
       double chain = 0.0;
-      const double val = sweep(io, sm, active, j, pmax, chain);
+      double val[kJ];
+      sweep(io, sm, active, jj, val, pmax, chain);
       if (g == 0) {
         const int32_t Pn = block_max(ctl, pmax);
         if (t == 0) {
@@ -739,13 +846,23 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(RunArgs a) {
       }
       if (!do_scan) break;
       const uint32_t nf = ctl->hf_count;
-      int32_t psl = 0;
-      if (active) {
-        psl = nf <= (uint32_t)kHCap
-                  ? neighbour_psl(sm.hf, nf, 0, true, j, L, sm.sb)
-                  : neighbour_psl(hlist, ctl->hcount, ctl->P_new - 8, false, j, L, sm.sb);
+      // thread-local reduce_scan over its kJ neighbours (ascending offset)
+      double bv = __longlong_as_double(0x7ff0000000000000ll);
+      uint32_t bi = 0xffffffffu, bpi = 0xffffffffu;
+      int32_t bp = 0x7fffffff;
+      int bad = 0;
+#pragma unroll
+      for (int m = 0; m < kJ; ++m) {
+        if (!active[m]) continue;
+        const uint32_t i = ibase + m + 1;
+        const int32_t psl = nf <= (uint32_t)kHCap
+            ? neighbour_psl(sm.hf, nf, 0, true, jj[m], L, sm.sb)
+            : neighbour_psl(hlist, ctl->hcount, ctl->P_new - 8, false, jj[m], L, sm.sb);
+        bad |= !isfinite(val[m]);
+        if (bi == 0xffffffffu || val[m] < bv) { bv = val[m]; bi = i; }
+        if (psl < bp) { bp = psl; bpi = i; }
       }
-      block_reduce_scan(ctl, active, val, i, psl);
+      block_reduce_scan(ctl, bv, bi, bp, bpi, bad);
       if (t == 0) {
         // combine groups in ascending offset order (strict <: smallest offset wins)
         if (g == 0) {
@@ -825,9 +942,9 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(RunArgs a) {
       // best_seq = pivot with the best-PSL neighbour's flip (:385-387)
       const uint32_t pp = ctl->ppos;
       for (uint32_t i = t; i < nw; i += kThreads) {
-        uint32_t v = sm.sb[i + 1];
+        uint32_t v = bits_piv[i + 1];
         if (i == (pp >> 5)) v ^= 1u << (pp & 31);
-        bits_best[i] = v;
+        bits_best[i + 1] = v;
       }
       const long long e = energy_sweep(ctl, Cpiv, L, sm.sb, (int64_t)pp);
       if (t == 0) ctl->st.energy_best = e;
@@ -836,7 +953,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(RunArgs a) {
     if (ctl->restart) {
       // back to the phase-local best (:405-406): bits from the snapshot, C via
       // the next pass (src_local); then flip_random_distinct (:407, :131-148)
-      for (uint32_t i = t; i < nw; i += kThreads) sm.sb[i + 1] = bits_loc[i];
+      for (uint32_t i = t; i < nw; i += kThreads) bits_piv[i + 1] = bits_loc[i + 1];
       __syncthreads();
       if (t == 0) {
         WalkState& S = ctl->st;
@@ -847,7 +964,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(RunArgs a) {
           if (used[pos >> 5] & bit) continue;
           used[pos >> 5] |= bit;
           flips[done++] = pos;
-          sm.sb[(pos >> 5) + 1] ^= bit;
+          bits_piv[(pos >> 5) + 1] ^= bit;
         }
         for (uint32_t m = 0; m < done; ++m) used[flips[m] >> 5] = 0u;
         S.n_pending = done;
@@ -856,7 +973,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(RunArgs a) {
     } else if (t == 0) {
       // the pivot always moves to the argmin neighbour (:392)
       const uint32_t js = ctl->jstar;
-      sm.sb[(js >> 5) + 1] ^= 1u << (js & 31);
+      bits_piv[(js >> 5) + 1] ^= 1u << (js & 31);
       flips[0] = js;
       ctl->st.n_pending = 1;
       ctl->st.src_local = 0;
@@ -864,7 +981,7 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(RunArgs a) {
     }
     __syncthreads();
     if (ctl->improve) {
-      for (uint32_t i = t; i < nw; i += kThreads) bits_loc[i] = sm.sb[i + 1];
+      for (uint32_t i = t; i < nw; i += kThreads) bits_loc[i + 1] = bits_piv[i + 1];
     }
     __syncthreads();
   }
@@ -875,26 +992,31 @@ __global__ void __launch_bounds__(kThreads, 1) run_kernel(RunArgs a) {
     if (ctl->st.status != PSL_OK) ctl->st.end_ns = globaltimer();
     *gst = ctl->st;
   }
-  for (uint32_t i = t; i < nw; i += kThreads) bits_piv[i] = sm.sb[i + 1];
 }
 
-// ScanJob / neighborhood_scan: neighbours of one given pivot, group g of 1024
-// per CTA, terms from the caller's PowerTable.
-__global__ void __launch_bounds__(kThreads, 1) scan_kernel(ScanArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const Smem sm = carve(smem_raw);
+// ScanJob / neighborhood_scan: neighbours of one given pivot, kGroup per CTA,
+// terms from the caller's PowerTable.
+__global__ void __launch_bounds__(kThreads, 2) scan_kernel(ScanArgs a) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  Smem sm = carve(smem_raw);
   const uint32_t t = threadIdx.x;
   const uint32_t nw = a.nwords;
-  sm.sb[0] = 0;
-  for (uint32_t i = t; i <= nw; i += kThreads) sm.sb[i + 1] = i < nw ? a.bits[i] : 0u;
+  sm.sb = a.bits;     // padded: word i at a.bits[i + 1]
   const bool in_smem = a.hcount <= (uint32_t)kHCap;
   if (in_smem)
     for (uint32_t e = t; e < a.hcount; e += kThreads) sm.hf[e] = a.hlist[e];
   __syncthreads();
-  const uint32_t i = blockIdx.x * kThreads + t + 1;
-  const bool active = i <= a.n;
-  uint32_t j = 0;
-  if (active) { j = a.start + i; if (j >= a.L) j -= a.L; }
+  const uint32_t ibase = blockIdx.x * kGroup + (t >> 5) * (32 * kJ) + (t & 31) * kJ;
+  bool active[kJ];
+  uint32_t jj[kJ];
+#pragma unroll
+  for (int m = 0; m < kJ; ++m) {
+    const uint32_t i = ibase + m + 1;
+    active[m] = i <= a.n;
+    uint32_t j = 0;
+    if (active[m]) { j = a.start + i; if (j >= a.L) j -= a.L; }
+    jj[m] = j;
+  }
   SweepIO io;
   io.L = a.L; io.nwords = nw; io.nchunks = a.nchunks;
   io.Csrc = a.C; io.Cdst = nullptr; io.Cloc = nullptr; io.flips = nullptr; io.F = 0;
@@ -903,11 +1025,15 @@ __global__ void __launch_bounds__(kThreads, 1) scan_kernel(ScanArgs a) {
   io.scan = true; io.chain = false;
   int32_t pmax = 0;
   double chain = 0.0;
-  const double v = sweep(io, sm, active, j, pmax, chain);
-  if (active) {
-    const int32_t p = in_smem ? neighbour_psl(sm.hf, a.hcount, 0, true, j, a.L, sm.sb)
-                              : neighbour_psl(a.hlist, a.hcount, 0, true, j, a.L, sm.sb);
-    a.values[i] = v;
+  double v[kJ];
+  sweep(io, sm, active, jj, v, pmax, chain);
+#pragma unroll
+  for (int m = 0; m < kJ; ++m) {
+    if (!active[m]) continue;
+    const uint32_t i = ibase + m + 1;
+    const int32_t p = in_smem ? neighbour_psl(sm.hf, a.hcount, 0, true, jj[m], a.L, sm.sb)
+                              : neighbour_psl(a.hlist, a.hcount, 0, true, jj[m], a.L, sm.sb);
+    a.values[i] = v[m];
     a.psls[i] = p;
   }
 }
@@ -927,9 +1053,7 @@ __global__ void flip_bit_kernel(uint32_t* bits, uint32_t j) { bits[j >> 5] ^= 1u
 
 }  // namespace
 
-size_t run_smem_bytes(uint32_t nwords) {
-  return kTabBytes + kTailBytes + kHfBytes + kCtlBytes + (size_t)(nwords + 2) * 4;
-}
+size_t run_smem_bytes(uint32_t) { return kTabBytes + kTailBytes + kHfBytes + kCtlBytes; }
 
 int launch_init_walks(const RunArgs& a, uint32_t n_walks, const uint64_t* d_seeds,
                       const uint32_t* d_init_bits, cudaStream_t s) {
@@ -940,8 +1064,8 @@ int launch_init_walks(const RunArgs& a, uint32_t n_walks, const uint64_t* d_seed
 int launch_build_tables(const RunArgs& a, uint32_t n_walks, cudaStream_t s) {
   const uint32_t per_block = 8 * 32 * kTabR;
   dim3 grid((a.L + per_block - 1) / per_block, n_walks);
-  build_tables_kernel<<<grid, 256, 0, s>>>(a.bits_piv, a.w_stride, a.Cpiv, a.Cloc, a.c_stride,
-                                           a.L, a.st);
+  build_tables_kernel<<<grid, 256, 0, s>>>(a.bits_piv + 1, a.w_stride, a.Cpiv, a.Cloc,
+                                           a.c_stride, a.L, a.st);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -975,7 +1099,7 @@ int launch_scan(const ScanArgs& a, cudaStream_t s) {
       return -1;
     attr = true;
   }
-  const uint32_t groups = (a.n + kThreads - 1) / kThreads;
+  const uint32_t groups = (a.n + kGroup - 1) / kGroup;
   scan_kernel<<<groups, kThreads, smem, s>>>(a);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }

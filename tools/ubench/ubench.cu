@@ -247,7 +247,7 @@ __global__ void __launch_bounds__(1024, 1) k_cells(int reps, double* out, long l
           else if (MODE == 22) off = (l / 8) * 8;
           else if (MODE == 23) off = (l & 1) * 16;
           else if (MODE == 24) off = (l & 1) * 24;
-          else if (MODE == 25) off = (l & 1) * 128;
+          else if (MODE == 25) off = (l & 1) * 128 % 64 + (l & 1) * 0;
           else if (MODE == 26) off = l * 8;
           else if (MODE == 27) off = (l % 16) * 8;
           else if (MODE == 28) off = (r2 & 1) * 8;
@@ -258,6 +258,32 @@ __global__ void __launch_bounds__(1024, 1) k_cells(int reps, double* out, long l
           uint32_t lo, hi;
           if (MODE == 31) { asm volatile("ld.shared.u32 %0, [%1];" : "=r"(lo) : "r"(rec + q * REC + off)); hi = 0; }
           else asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(rec + q * REC + off));
+          acc = acc + lo + hi;
+        }
+        sum += (double)acc;
+      }
+
+      if (MODE >= 40 && MODE < 60) {
+        uint32_t acc = 0;
+        const uint32_t l = threadIdx.x & 31;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const uint32_t w = q < 16 ? wlo : whi; const int qq = q & 15;
+          // per-lane random bit for this q, then forced structure
+          auto rb = [&](uint32_t lane) { return (__shfl_sync(0xffffffffu, w, lane) >> (2 * qq)) & 1u; };
+          uint32_t off;
+          if (MODE == 40) off = ((l >> 1) & 1) * 8;
+          else if (MODE == 41) off = ((l >> 2) & 1) * 8;
+          else if (MODE == 42) off = rb(l & ~1u) * 8;          // pair-uniform random
+          else if (MODE == 43) off = rb(l & 15u) * 8;          // l and l+16 equal
+          else if (MODE == 44) off = rb(l & ~3u) * 8;          // quad-uniform random
+          else if (MODE == 45) off = rb(l & ~7u) * 8;          // octet-uniform random
+          else if (MODE == 46) off = rb(l) * 16;               // random X / X+16
+          else if (MODE == 47) off = rb(l) * 64;               // random X / X+64 (next record)
+          else if (MODE == 48) off = rb(l) * 8 + (l & 16) * 2; // random within half-warp-specific pairs
+          else off = rb(l) * 8;                                 // random (T9)
+          uint32_t lo, hi;
+          asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(rec + q * REC + off));
           acc = acc + lo + hi;
         }
         sum += (double)acc;
@@ -276,7 +302,7 @@ int run(const char* name, int nsm, int threads, int reps, double cells_per_block
   double* out; long long* cyc;
   CK(cudaMalloc(&out, sizeof(double) * nsm * 1024));
   CK(cudaMalloc(&cyc, sizeof(long long) * nsm));
-  const int smem = KC * REC;
+  const int smem = KC * REC + 1024;
   CK(cudaFuncSetAttribute(k_cells<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   k_cells<MODE><<<nsm, threads, smem>>>(2, out, cyc);
   CK(cudaDeviceSynchronize());
@@ -300,18 +326,16 @@ int main() {
   printf("%s SMs=%d cc=%d.%d\n", p.name, p.multiProcessorCount, p.major, p.minor);
   const int nsm = p.multiProcessorCount;
   for (int th : {1024}) {
-    run<20>("T1 3 addr 0,8,16 lane%3", nsm, th, 200, 32);
-    run<21>("T2 4 addr 0..24 lane%4", nsm, th, 200, 32);
-    run<22>("T3 4 addr quarter-warp", nsm, th, 200, 32);
-    run<23>("T4 2 addr 0,16", nsm, th, 200, 32);
-    run<24>("T5 2 addr 0,24", nsm, th, 200, 32);
-    run<25>("T6 2 addr 0,128 (conflict)", nsm, th, 200, 32);
-    run<26>("T7 32 distinct 256B", nsm, th, 200, 32);
-    run<27>("T8 16 distinct", nsm, th, 200, 32);
-    run<28>("T9 2 addr random", nsm, th, 200, 32);
-    run<29>("T10 3 addr random", nsm, th, 200, 32);
-    run<30>("T11 4 addr random", nsm, th, 200, 32);
-    run<31>("T12 LDS.32 4 addr lane%4", nsm, th, 200, 32);
+    run<49>("U0 random 0/8 (+shfl cost)", nsm, th, 100, 32);
+    run<40>("U1 (l>>1)&1", nsm, th, 100, 32);
+    run<41>("U2 (l>>2)&1", nsm, th, 100, 32);
+    run<42>("U4 pair-uniform random", nsm, th, 100, 32);
+    run<43>("U5 l==l+16 random", nsm, th, 100, 32);
+    run<44>("U6 quad-uniform random", nsm, th, 100, 32);
+    run<45>("U7 octet-uniform random", nsm, th, 100, 32);
+    run<46>("U8 random 0/16", nsm, th, 100, 32);
+    run<47>("U9 random 0/64", nsm, th, 100, 32);
+    run<48>("U10 halfwarp-specific pairs", nsm, th, 100, 32);
   }
   return 0;
 }
