@@ -327,31 +327,37 @@ __device__ __forceinline__ void sweep(const SweepIO& io, const Smem& sm, const b
   // inactive neighbours shadow the warp's first active one (results discarded)
   const uint32_t src = __ffs(__ballot_sync(FULL, active[0])) - 1;
   const uint32_t jsrc = __shfl_sync(FULL, jin[0], src < 32 ? src : 0);
-  uint32_t be[kJ], oe[kJ], mbj[kJ], shB[kJ], shA[kJ], smask[kJ];
-  uint32_t Blo[kJ], Bhi[kJ], Alo[kJ], Ahi[kJ];
-  int wB[kJ], wA[kJ];
+  uint32_t be[kJ], oe[kJ], mbj[kJ], smask[kJ], jm[kJ];
   bool sideA[kJ];
   uint32_t lminBE = FULL, lmaxBE = 0, lminOE = FULL, lmaxOE = 0;
 #pragma unroll
   for (int m = 0; m < kJ; ++m) {
     const uint32_t j = active[m] ? jin[m] : jsrc;
+    jm[m] = j;
     const uint32_t left = j, right = L - 1 - j;       // sequence.hpp:131-135
     be[m] = left < right ? left : right;
     oe[m] = left < right ? right : left;
     sideA[m] = left >= right;
     smask[m] = sideA[m] ? 0x10u : 0x08u;
     mbj[m] = ((sb[(j >> 5) + 1] >> (j & 31)) & 1u) ? FULL : 0u;
-    wB[m] = (int)((j + 1) >> 5);
-    shB[m] = (j + 1) & 31;
-    Blo[m] = sword(sb, wB[m], nwords);
-    Bhi[m] = sword(sb, wB[m] + 1, nwords);
-    wA[m] = (int)(j >> 5) - 1;
-    shA[m] = j & 31;
-    Alo[m] = sword(sb, wA[m], nwords);
-    Ahi[m] = sword(sb, wA[m] + 1, nwords);
     lminBE = min(lminBE, be[m]); lmaxBE = max(lmaxBE, be[m]);
     lminOE = min(lminOE, oe[m]); lmaxOE = max(lmaxOE, oe[m]);
   }
+  // The kJ neighbours of a lane are consecutive positions except when the
+  // neighbourhood wraps past L-1 inside the lane (or lanes shadow inactive
+  // neighbours): such lanes rebuild their planes from memory each block.
+  bool adj = true;
+#pragma unroll
+  for (int m = 1; m < kJ; ++m) adj = adj && jm[m] == jm[0] + m;
+  // shared sliding windows (3 words each) of an adjacent lane:
+  //   B: positions j0 + k0 .. j0 + k0 + 34      (s_{j+k})
+  //   A: positions j0 - k0 - 31 .. j0 - k0 + 3  (s_{j-k}, reversed by BREV)
+  int wb = (int)((jm[0] + 1) >> 5);
+  const uint32_t shB = (jm[0] + 1) & 31;
+  uint32_t b0 = sword(sb, wb, nwords), b1 = sword(sb, wb + 1, nwords), b2 = sword(sb, wb + 2, nwords);
+  int wa = (int)(jm[0] >> 5) - 1;
+  const uint32_t shA = jm[0] & 31;
+  uint32_t a0 = sword(sb, wa, nwords), a1 = sword(sb, wa + 1, nwords), a2 = sword(sb, wa + 2, nwords);
   const uint32_t minBE = __reduce_min_sync(FULL, lminBE), maxBE = __reduce_max_sync(FULL, lmaxBE);
   const uint32_t minOE = __reduce_min_sync(FULL, lminOE), maxOE = __reduce_max_sync(FULL, lmaxOE);
 #pragma unroll
@@ -373,13 +379,26 @@ __device__ __forceinline__ void sweep(const SweepIO& io, const Smem& sm, const b
       for (uint32_t blk = 0; blk < kChunk / 32; ++blk) {
         const uint32_t k0 = 1 + c * kChunk + blk * 32;
         const uint32_t kend = k0 + 31;
-        uint32_t Bp[kJ], Ap[kJ], nB[kJ], nA[kJ];
+        uint32_t Bp[kJ], Ap[kJ];
+        const uint32_t nb = sword_up(sb, wb + 3, nwords);   // next block's window words
+        const uint32_t na = sword_dn(sb, wa - 1);
+        if (adj) {
+          const uint32_t XB = __funnelshift_r(b0, b1, shB), YB = __funnelshift_r(b1, b2, shB);
+          const uint32_t XA = __funnelshift_r(a0, a1, shA), YA = __funnelshift_r(a1, a2, shA);
 #pragma unroll
-        for (int m = 0; m < kJ; ++m) {
-          Bp[m] = __funnelshift_r(Blo[m], Bhi[m], shB[m]) ^ mbj[m];
-          Ap[m] = __brev(__funnelshift_r(Alo[m], Ahi[m], shA[m])) ^ mbj[m];
-          nB[m] = sword_up(sb, wB[m] + 2, nwords);    // next block's window words
-          nA[m] = sword_dn(sb, wA[m] - 1);
+          for (int m = 0; m < kJ; ++m) {
+            Bp[m] = __funnelshift_r(XB, YB, m) ^ mbj[m];
+            Ap[m] = __brev(__funnelshift_r(XA, YA, m)) ^ mbj[m];
+          }
+        } else {
+#pragma unroll
+          for (int m = 0; m < kJ; ++m) {
+            const int pbB = (int)(jm[m] + k0), pbA = (int)jm[m] - (int)k0 - 31;
+            const int wB = pbB >> 5, wA = pbA >> 5;       // arithmetic shift = floor
+            Bp[m] = __funnelshift_r(sword(sb, wB, nwords), sword(sb, wB + 1, nwords), pbB & 31) ^ mbj[m];
+            Ap[m] = __brev(__funnelshift_r(sword(sb, wA, nwords), sword(sb, wA + 1, nwords),
+                                           pbA & 31)) ^ mbj[m];
+          }
         }
         const uint32_t rb = tab + blk * 32 * (kRecDoubles * 8);   // 64-byte aligned
         const bool ub = maxBE < k0 || minBE >= kend;
@@ -461,11 +480,8 @@ __device__ __forceinline__ void sweep(const SweepIO& io, const Smem& sm, const b
             sum[m] = s;
           }
         }
-#pragma unroll
-        for (int m = 0; m < kJ; ++m) {
-          Blo[m] = Bhi[m]; Bhi[m] = nB[m]; ++wB[m];
-          Ahi[m] = Alo[m]; Alo[m] = nA[m]; --wA[m];
-        }
+        b0 = b1; b1 = b2; b2 = nb; ++wb;
+        a2 = a1; a1 = a0; a0 = na; --wa;
       }
     }
     if (io.chain && threadIdx.x == 0) {
