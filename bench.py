@@ -227,8 +227,9 @@ def main():
     torch.cuda.synchronize()
     with ClockSampler(local_rank) as clocks:
         e_start.record(stream)
-        for _ in range(args.steps):
-            walks.step(1)
+        # one persistent launch advances every walk by exactly K steps (walks
+        # progress independently inside it; no per-step host round trip)
+        walks.step(args.steps)
         e_end.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -245,10 +246,10 @@ def main():
                                            [r.solution_best for r in r1], L, device=dev)
     walks.close()
 
-    # dominant kernel: run_kernel, one launch per step; algorithmic work per
-    # launch = walks x n x (L-1) cells (one exact DADD-chain term each)
-    cells_per_launch = n_walks * n * (L - 1)
-    per_launch_s = (ms * 1e-3) / args.steps
+    # dominant kernel: run_kernel, one launch for the K timed steps; algorithmic
+    # work = walks x n x (L-1) cells per step (one exact DADD-chain term each)
+    cells_per_launch = n_walks * n * (L - 1)      # per step
+    per_launch_s = (ms * 1e-3) / args.steps       # per step
     achieved = cells_per_launch / per_launch_s
     roofline = {
         "bound": "fp64",

@@ -44,7 +44,9 @@ struct psl_walks {
   psl_event* events = nullptr;
   psl_trace* traces = nullptr;
   uint64_t* seeds = nullptr;
-  uint32_t* init_bits = nullptr;
+  int8_t* inits = nullptr;      // device copy of warm starts (int8 +-1)
+  uint32_t* bad = nullptr;      // [first bad flat index + 1, value]
+  int8_t* sol = nullptr;        // unpack scratch for solutions
 };
 
 namespace {
@@ -447,7 +449,9 @@ void psl_walks_destroy(psl_walks* w) {
   cudaSetDevice(w->ctx->device);
   cudaFree(w->st); cudaFree(w->Cpiv); cudaFree(w->Cloc); cudaFree(w->bits); cudaFree(w->hlist);
   cudaFree(w->flips); cudaFree(w->events); cudaFree(w->traces); cudaFree(w->seeds);
-  cudaFree(w->init_bits);
+  cudaFree(w->inits);
+  cudaFree(w->bad);
+  cudaFree(w->sol);
   delete w;
 }
 
@@ -461,12 +465,6 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
   int rc = psl_validate_params(params, &p, nullptr, 0, err, errlen);
   if (rc) return rc;
   if (n_walks < 1) { set_err(err, errlen, "n_walks must be >= 1"); return PSL_ERR_CONFIG; }
-  if (inits) {
-    for (uint32_t w = 0; w < n_walks; ++w) {
-      rc = check_sequence(inits + (size_t)w * p.length, p.length, err, errlen);
-      if (rc) return rc;
-    }
-  }
   rc = device_ready(ctx, err, errlen);
   if (rc) return rc;
   psl_walks* W = new psl_walks;
@@ -518,31 +516,44 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
   for (uint32_t w = 0; w < n_walks; ++w) sd[w] = seeds ? seeds[w] : p.seed + w;
   if ((e = cudaMemcpyAsync(W->seeds, sd.data(), 8ull * n_walks, cudaMemcpyHostToDevice, s)) != cudaSuccess)
     return fail(e, "seeds");
-  const int8_t* init_src = inits ? inits : nullptr;
-  std::vector<uint32_t> ib;
-  if (!init_src && p.init) {
-    // run_search warm start: the same init for every walk
-    init_src = p.init;
-  }
-  if (init_src) {
-    ib.assign((size_t)nw * n_walks, 0u);
-    for (uint32_t w = 0; w < n_walks; ++w) {
-      const int8_t* sq = inits ? inits + (size_t)w * L : p.init;
-      for (uint32_t i = 0; i < L; ++i)
-        if (sq[i] < 0) ib[(size_t)w * nw + (i >> 5)] |= 1u << (i & 31);
+  // warm starts travel as int8 and are validated + packed on the device
+  AL(W->bad, 8);
+  if ((e = cudaMemsetAsync(W->bad, 0xff, 4, s)) != cudaSuccess) return fail(e, "bad flag");
+  if ((e = cudaMemsetAsync(W->bad + 1, 0, 4, s)) != cudaSuccess) return fail(e, "bad flag");
+  if (inits || p.init) {
+    const size_t bytes = (size_t)n_walks * L;
+    AL(W->inits, bytes);
+    if (inits) {
+      if ((e = cudaMemcpyAsync(W->inits, inits, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return fail(e, "inits");
+    } else {
+      for (uint32_t w = 0; w < n_walks; ++w)
+        if ((e = cudaMemcpyAsync(W->inits + (size_t)w * L, p.init, L, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+          return fail(e, "init");
     }
-    AL(W->init_bits, ib.size() * 4);
-    if ((e = cudaMemcpyAsync(W->init_bits, ib.data(), ib.size() * 4, cudaMemcpyHostToDevice, s)) != cudaSuccess)
-      return fail(e, "init bits");
   }
 #undef AL
-  if (launch_init_walks(a, n_walks, W->seeds, W->init_bits, s) < 0)
+  if (launch_init_walks(a, n_walks, W->seeds, W->inits, W->bad, s) < 0)
     return fail(cudaGetLastError(), "init_walks_kernel");
-  if (launch_build_tables(a, n_walks, s) < 0) return fail(cudaGetLastError(), "build_tables_kernel");
-  ctx->launches += 2;
-  if (init_src) {
-    // the upload buffer is consumed by init_walks_kernel; keep it until sync
-    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail(e, "init sync");
+  // SidelobeTable::build: exact NTT correlation for long sequences (O(L log L)),
+  // bit-parallel popcount kernel (O(L^2/32)) for short ones
+  const int nb = L >= 8192 ? launch_build_tables_ntt(a, n_walks, s) : launch_build_tables(a, n_walks, s);
+  if (nb < 0) return fail(cudaGetLastError(), "build_tables");
+  ctx->launches += 1 + (uint32_t)nb;
+  if (W->inits) {
+    uint32_t bad[2];
+    if ((e = cudaMemcpyAsync(bad, W->bad, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(s)) != cudaSuccess)
+      return fail(e, "init check");
+    if (bad[0] != 0xffffffffu) {
+      const uint32_t flat = bad[0] - 1;
+      psl_walks_destroy(W);
+      set_err(err, errlen, "sequence element at position " + std::to_string(flat % L) + " is " +
+                               std::to_string((int)(int32_t)bad[1]) + "; elements must be +1 or -1");
+      return PSL_ERR_CONFIG;
+    }
+    cudaFree(W->inits);
+    W->inits = nullptr;
   }
   *out = W;
   return PSL_OK;
@@ -584,14 +595,16 @@ int psl_walks_records(psl_walks* w, psl_walk_record* records, int8_t* solutions,
   cudaStream_t s = w->ctx->stream;
   std::vector<WalkState> st(w->n_walks);
   CK(cudaMemcpyAsync(st.data(), w->st, sizeof(WalkState) * w->n_walks, cudaMemcpyDeviceToHost, s));
-  std::vector<uint32_t> bb;
-  const uint32_t L = w->a.L, nw = w->a.nwords;
+  const uint32_t L = w->a.L;
   if (solutions) {
-    bb.resize(w->a.w_stride * w->n_walks);
-    CK(cudaMemcpyAsync(bb.data(), w->a.bits_best, bb.size() * 4, cudaMemcpyDeviceToHost, s));
+    // unpack on the device, one D2H of n_walks * L int8
+    if (!w->sol) CK(cudaMalloc(&w->sol, (size_t)w->n_walks * L));
+    if (launch_unpack(w->a.bits_best, w->a.w_stride, L, w->n_walks, w->sol, s) < 0)
+      return cuda_fail(err, errlen, cudaGetLastError(), "unpack_kernel");
+    w->ctx->launches += 1;
+    CK(cudaMemcpyAsync(solutions, w->sol, (size_t)w->n_walks * L, cudaMemcpyDeviceToHost, s));
   }
   CK(cudaStreamSynchronize(s));
-  (void)nw;
   for (uint32_t i = 0; i < w->n_walks; ++i) {
     const WalkState& S = st[i];
     psl_walk_record& r = records[i];
@@ -605,11 +618,6 @@ int psl_walks_records(psl_walks* w, psl_walk_record* records, int8_t* solutions,
     r.merit_factor = ((double)L * (double)L) / (2.0 * (double)S.energy_best);
     r.switches = S.switches;
     r.steps = S.steps;
-    if (solutions) {
-      const uint32_t* b = bb.data() + (size_t)i * w->a.w_stride + 1;
-      int8_t* o = solutions + (size_t)i * L;
-      for (uint32_t k = 0; k < L; ++k) o[k] = ((b[k >> 5] >> (k & 31)) & 1u) ? -1 : 1;
-    }
   }
   return PSL_OK;
 }

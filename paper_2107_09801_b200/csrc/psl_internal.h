@@ -91,8 +91,11 @@ size_t run_smem_bytes(uint32_t nwords);
 
 // Launchers (return the number of kernels launched, or -1 on launch error).
 int launch_init_walks(const RunArgs& a, uint32_t n_walks, const uint64_t* d_seeds,
-                      const uint32_t* d_init_bits, cudaStream_t s);
+                      const int8_t* d_inits, uint32_t* d_bad, cudaStream_t s);
+int launch_unpack(const uint32_t* bits, size_t w_stride, uint32_t L, uint32_t n_walks, int8_t* out,
+                  cudaStream_t s);
 int launch_build_tables(const RunArgs& a, uint32_t n_walks, cudaStream_t s);
+int launch_build_tables_ntt(const RunArgs& a, uint32_t n_walks, cudaStream_t s);
 int launch_run(const RunArgs& a, uint32_t n_walks, cudaStream_t s);
 int launch_scan(const ScanArgs& a, cudaStream_t s);
 int launch_table_only(const uint32_t* d_bits, int32_t* d_C, uint32_t L, uint32_t nwords,

@@ -23,6 +23,7 @@
 //  * neighbour PSL is exact but not computed per cell: only shifts with
 //    |C_k| >= PSL(pivot) - 8 can hold a neighbour's peak, and those are
 //    collected while streaming.
+#include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -609,7 +610,7 @@ __device__ long long energy_sweep(Ctl* ctl, const int32_t* C, uint32_t L, const 
 // Walk setup: RNG, pivot (random_sequence, search.cpp:120-129, or warm start),
 // snapshot copies.  One CTA per walk.
 __global__ void __launch_bounds__(256) init_walks_kernel(RunArgs a, const uint64_t* seeds,
-                                                         const uint32_t* init_bits) {
+                                                         const int8_t* inits, uint32_t* bad) {
   const uint32_t w = blockIdx.x;
   WalkState* S = a.st + w;
   uint32_t* bp = a.bits_piv + (size_t)w * a.w_stride;
@@ -625,7 +626,7 @@ __global__ void __launch_bounds__(256) init_walks_kernel(RunArgs a, const uint64
     z.phase = 1;
     z.fitness_pending = 1;
     z.psl_best = -1;           // set from P on the first pass
-    if (!init_bits) {
+    if (!inits) {
       // L spin() draws in position order; bit = top bit of next() (1 <-> -1)
       for (uint32_t wd = 0; wd < nw; ++wd) {
         uint32_t word = 0;
@@ -636,8 +637,23 @@ __global__ void __launch_bounds__(256) init_walks_kernel(RunArgs a, const uint64
     }
     *S = z;
   }
-  if (init_bits) {
-    for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) bp[i + 1] = init_bits[(size_t)w * nw + i];
+  if (inits) {
+    // warm starts: validate (BinarySequence ctor, sequence.cpp:20-35) and pack;
+    // bad[0] = first offending flat index + 1, bad[1] = its value
+    const int8_t* src = inits + (size_t)w * a.L;
+    for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) {
+      uint32_t word = 0;
+      const uint32_t nb = min(32u, a.L - i * 32);
+      for (uint32_t b = 0; b < nb; ++b) {
+        const int8_t v = src[i * 32 + b];
+        if (v != 1 && v != -1) {
+          const uint32_t flat = (uint32_t)((size_t)w * a.L + i * 32 + b) + 1;
+          if (atomicMin(&bad[0], flat) > flat) bad[1] = (uint32_t)(int32_t)v;
+        }
+        word |= (uint32_t)(v < 0) << b;
+      }
+      bp[i + 1] = word;
+    }
   }
   __syncthreads();
   // padded layout: [0] zero, words 1..nw, zeros after
@@ -1072,8 +1088,8 @@ __global__ void flip_bit_kernel(uint32_t* bits, uint32_t j) { bits[j >> 5] ^= 1u
 size_t run_smem_bytes(uint32_t) { return kTabBytes + kTailBytes + kHfBytes + kCtlBytes; }
 
 int launch_init_walks(const RunArgs& a, uint32_t n_walks, const uint64_t* d_seeds,
-                      const uint32_t* d_init_bits, cudaStream_t s) {
-  init_walks_kernel<<<n_walks, 256, 0, s>>>(a, d_seeds, d_init_bits);
+                      const int8_t* d_inits, uint32_t* d_bad, cudaStream_t s) {
+  init_walks_kernel<<<n_walks, 256, 0, s>>>(a, d_seeds, d_inits, d_bad);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
@@ -1205,5 +1221,23 @@ int probe_peaks(int nsm, cudaStream_t s, double* dadd_cps, double* lds_cps, doub
   cudaFree(out);
   cudaFree(cyc);
   return cudaGetLastError() == cudaSuccess ? 4 : -1;
+}
+}  // namespace pslb
+
+namespace pslb {
+namespace {
+// bit-packed best sequences -> int8 +-1 (one walk per blockIdx.y)
+__global__ void unpack_kernel(const uint32_t* bits, size_t w_stride, uint32_t L, int8_t* out) {
+  const uint32_t w = blockIdx.y;
+  const uint32_t* b = bits + (size_t)w * w_stride + 1;
+  int8_t* o = out + (size_t)w * L;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x)
+    o[i] = ((b[i >> 5] >> (i & 31)) & 1u) ? (int8_t)-1 : (int8_t)1;
+}
+}  // namespace
+int launch_unpack(const uint32_t* bits, size_t w_stride, uint32_t L, uint32_t n_walks, int8_t* out,
+                  cudaStream_t s) {
+  unpack_kernel<<<dim3(std::min<uint32_t>((L + 255) / 256, 512), n_walks), 256, 0, s>>>(bits, w_stride, L, out);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 }  // namespace pslb

@@ -317,3 +317,23 @@ def test_max_seconds_stop(engine):
     assert rec.nse > 1
     assert rec.elapsed_seconds >= 0.05
     assert rec.elapsed_seconds < 5.0
+
+
+def test_walks_warm_starts(engine):
+    """Per-walk warm starts (validated and packed on the device) == run_search(init)."""
+    L = 300
+    rng = np.random.default_rng(8)
+    inits = np.where(rng.integers(0, 2, (3, L)) == 1, -1, 1).astype(np.int8)
+    p = _params(engine, L, 5, 4, 13, 6, 10, 100, 1 + 40 * 100)
+    recs = engine.run_walks(p, 3, inits=inits)
+    for w, r in enumerate(recs):
+        q = _params(engine, L, 5 + w, 4, 13, 6, 10, 100, 1 + 40 * 100, init=inits[w])
+        single = engine.run_search(q)
+        rc, orec, osol, _, _ = O.run_search(L, 5 + w, 4, 13, 6, 10, 100, 1 + 40 * 100,
+                                            init=inits[w])
+        assert (r.nse, r.psl_best) == (single.nse, single.psl_best) == (orec.nse, orec.psl_best)
+        assert np.array_equal(r.solution_best, osol)
+    bad = inits.copy()
+    bad[1, 17] = 0
+    with pytest.raises(engine.ConfigError, match="position 17 is 0"):
+        engine.run_walks(p, 3, inits=bad)
