@@ -285,9 +285,9 @@ def main():
         e2e = {"value": e2e_nse / (e2e_ms * 1e-3), "unit": "NSE/s",
                "h2d_bytes_per_step": int(inits.nbytes + 8 * n_walks),
                "d2h_bytes_per_step": int(n_walks * L + n_walks * 80),
-               "step": f"one psl_run_walks call: {n_walks} host start sequences -> "
-                       f"O(L^2) table build + {args.e2e_steps} search steps -> records + "
-                       f"best sequences on the host"}
+               "step": f"one psl_run_walks call: {n_walks} host start sequences (pinned int8) -> "
+                       f"device validation/packing + NTT table build + {args.e2e_steps} search "
+                       f"steps -> records + best sequences (int8) on the host"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -146,6 +146,12 @@ int psl_ctx_create(int device, psl_ctx** out, char* err, size_t errlen) {
   c->device = device;
   CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
   c->stream = c->own;
+  // keep freed walk buffers in the pool (no release back to the OS between calls)
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
   *out = c;
   return PSL_OK;
 }
@@ -447,11 +453,11 @@ int psl_apply_flip(psl_ctx* ctx, int8_t* seq, int32_t* table, uint32_t L, uint32
 void psl_walks_destroy(psl_walks* w) {
   if (!w) return;
   cudaSetDevice(w->ctx->device);
-  cudaFree(w->st); cudaFree(w->Cpiv); cudaFree(w->Cloc); cudaFree(w->bits); cudaFree(w->hlist);
-  cudaFree(w->flips); cudaFree(w->events); cudaFree(w->traces); cudaFree(w->seeds);
-  cudaFree(w->inits);
-  cudaFree(w->bad);
-  cudaFree(w->sol);
+  cudaStream_t s = w->ctx->stream;
+  for (void* p : {(void*)w->st, (void*)w->Cpiv, (void*)w->Cloc, (void*)w->bits, (void*)w->hlist,
+                  (void*)w->flips, (void*)w->events, (void*)w->traces, (void*)w->seeds,
+                  (void*)w->inits, (void*)w->bad, (void*)w->sol})
+    if (p) cudaFreeAsync(p, s);
   delete w;
 }
 
@@ -489,13 +495,16 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
   a.w_stride = ((size_t)nw + 1 + kBitsPad + 3) & ~size_t(3);
   a.h_stride = L;
   a.f_stride = std::max<uint32_t>(p.flip_lmt, 1);
+  cudaStream_t s = ctx->stream;
   auto fail = [&](cudaError_t e, const char* what) {
     psl_walks_destroy(W);
     return cuda_fail(err, errlen, e, what);
   };
   cudaError_t e;
+  // stream-ordered allocations from the device's default pool: repeated
+  // psl_run_walks calls reuse the memory instead of re-mapping gigabytes
 #define AL(ptr, bytes) \
-  if ((e = cudaMalloc(&(ptr), (bytes))) != cudaSuccess) return fail(e, "cudaMalloc " #ptr);
+  if ((e = cudaMallocAsync(&(ptr), (bytes), s)) != cudaSuccess) return fail(e, "cudaMallocAsync " #ptr);
   AL(W->st, sizeof(WalkState) * n_walks);
   AL(W->Cpiv, a.c_stride * 4 * n_walks);
   AL(W->Cloc, a.c_stride * 4 * n_walks);
@@ -511,7 +520,6 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
   a.bits_best = W->bits + 2 * a.w_stride * n_walks;
   a.used = W->bits + 3 * a.w_stride * n_walks;
   a.hlist = W->hlist; a.flips = W->flips; a.events = W->events; a.traces = W->traces;
-  cudaStream_t s = ctx->stream;
   std::vector<uint64_t> sd(n_walks);
   for (uint32_t w = 0; w < n_walks; ++w) sd[w] = seeds ? seeds[w] : p.seed + w;
   if ((e = cudaMemcpyAsync(W->seeds, sd.data(), 8ull * n_walks, cudaMemcpyHostToDevice, s)) != cudaSuccess)
@@ -552,7 +560,7 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
                                std::to_string((int)(int32_t)bad[1]) + "; elements must be +1 or -1");
       return PSL_ERR_CONFIG;
     }
-    cudaFree(W->inits);
+    cudaFreeAsync(W->inits, s);
     W->inits = nullptr;
   }
   *out = W;
@@ -598,7 +606,7 @@ int psl_walks_records(psl_walks* w, psl_walk_record* records, int8_t* solutions,
   const uint32_t L = w->a.L;
   if (solutions) {
     // unpack on the device, one D2H of n_walks * L int8
-    if (!w->sol) CK(cudaMalloc(&w->sol, (size_t)w->n_walks * L));
+    if (!w->sol) CK(cudaMallocAsync(&w->sol, (size_t)w->n_walks * L, s));
     if (launch_unpack(w->a.bits_best, w->a.w_stride, L, w->n_walks, w->sol, s) < 0)
       return cuda_fail(err, errlen, cudaGetLastError(), "unpack_kernel");
     w->ctx->launches += 1;

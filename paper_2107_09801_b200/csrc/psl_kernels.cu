@@ -292,17 +292,6 @@ __device__ __forceinline__ uint32_t field_at(uint32_t x, int q) {
   return sh < 0 ? (x << (-sh)) : (x >> sh);
 }
 
-__device__ __forceinline__ uint32_t lo32(double x) { return (uint32_t)__double2loint(x); }
-__device__ __forceinline__ uint32_t hi32(double x) { return (uint32_t)__double2hiint(x); }
-
-// top bit of r, and r << 1, in one IMAD.WIDE (FMA pipe)
-__device__ __forceinline__ uint32_t pop_top_bit(uint32_t& r) {
-  uint64_t w;
-  asm("mul.wide.u32 %0, %1, 2;" : "=l"(w) : "r"(r));
-  r = (uint32_t)w;
-  return (uint32_t)(w >> 32);
-}
-
 // One full sweep over k = 1..L-1 for the kJ adjacent neighbours j[m] of this
 // lane (sum[m] = their fitness, the reference's serial ascending-k chain).
 //
