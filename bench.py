@@ -251,11 +251,24 @@ def main():
     cells_per_launch = n_walks * n * (L - 1)      # per step
     per_launch_s = (ms * 1e-3) / args.steps       # per step
     achieved = cells_per_launch / per_launch_s
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "r01_run_kernel.json")
+    if os.path.exists(prof) and L == L_DEFAULT and n == 1024:
+        try:
+            pj = json.load(open(prof))
+            # ncu --set full capture of run_kernel on this workload, scaled to one
+            # step of this run's walk count (profiles/r01_run_kernel.txt)
+            traffic = pj["dram_bytes_per_launch"] / pj.get("steps_per_launch", 1) \
+                * n_walks / float(pj.get("launch__grid_size", n_walks))
+        except Exception:
+            traffic = None
     roofline = {
         "bound": "fp64",
         "achieved": achieved / 1e9, "peak": dadd.value / 1e9, "unit": "Gcell/s",
         "frac": achieved / dadd.value if dadd.value else None,
-        "traffic": None,
+        "traffic": traffic,
+        "traffic_unit": "DRAM bytes per step (ncu capture, profiles/r01_run_kernel.json)",
+        "algorithmic_bytes_per_step": n_walks * 8.0 * L,
         "peak_source": "measured live: FP64-add pipe (one dependent DADD per cell is the "
                        "serial fitness chain's floor), psl_probe_peaks",
         "lds_table_roof_gcell_s": lds.value / 1e9,
