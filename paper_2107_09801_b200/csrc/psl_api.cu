@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -647,7 +648,11 @@ int psl_run_walks(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, cons
 int psl_run_search(psl_ctx* ctx, const psl_params* params, const psl_hooks* hooks,
                    psl_run_record* out, int8_t* solution_best, char* err, size_t errlen) {
   const bool want_traces = hooks && hooks->on_scan;
-  const uint64_t ecap = 1u << 16, tcap = want_traces ? (1u << 16) : 0;
+  // device event/trace buffer capacity per drain (PSLB200_DRAIN_CAP overrides,
+  // used by the tests to force many drain/resume cycles)
+  uint64_t cap = 1u << 16;
+  if (const char* env = std::getenv("PSLB200_DRAIN_CAP")) cap = std::max<uint64_t>(2, std::strtoull(env, nullptr, 10));
+  const uint64_t ecap = cap, tcap = want_traces ? cap : 0;
   psl_walks* W = nullptr;
   int rc = walks_create(ctx, params, 1, nullptr, nullptr, ecap, tcap, &W, err, errlen);
   if (rc) return rc;

@@ -337,3 +337,13 @@ def test_walks_warm_starts(engine):
     bad[1, 17] = 0
     with pytest.raises(engine.ConfigError, match="position 17 is 0"):
         engine.run_walks(p, 3, inits=bad)
+
+
+def test_drain_and_resume(engine, golden, monkeypatch):
+    """Tiny device event/trace buffers: run_search drains and relaunches many
+    times; hooks must still see the reference's exact event/trace stream."""
+    monkeypatch.setenv("PSLB200_DRAIN_CAP", "3")
+    for key in ("formats_md", "warm_start_200"):
+        _run_and_compare(engine, golden("records.json")[key])
+    for g in golden("trajectories.json")[:3]:
+        _run_and_compare(engine, g)
