@@ -493,7 +493,10 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
   a.events_cap = events_cap;
   a.traces_cap = traces_cap;
   a.c_stride = ((size_t)L + 31) & ~size_t(31);
-  a.w_stride = ((size_t)nw + 1 + kBitsPad + 3) & ~size_t(3);
+  // per-walk bit regions: nw+48 zero words in front and behind the sequence, so
+  // the scan's sliding windows never need bounds clamps
+  a.w_front = (size_t)nw + 48 - 1;
+  a.w_stride = ((size_t)nw + 48 + nw + (size_t)nw + 48 + kBitsPad + 3) & ~size_t(3);
   a.h_stride = L;
   a.f_stride = std::max<uint32_t>(p.flip_lmt, 1);
   cudaStream_t s = ctx->stream;
@@ -608,7 +611,7 @@ int psl_walks_records(psl_walks* w, psl_walk_record* records, int8_t* solutions,
   if (solutions) {
     // unpack on the device, one D2H of n_walks * L int8
     if (!w->sol) CK(cudaMallocAsync(&w->sol, (size_t)w->n_walks * L, s));
-    if (launch_unpack(w->a.bits_best, w->a.w_stride, L, w->n_walks, w->sol, s) < 0)
+    if (launch_unpack(w->a.bits_best + w->a.w_front + 1, w->a.w_stride, L, w->n_walks, w->sol, s) < 0)
       return cuda_fail(err, errlen, cudaGetLastError(), "unpack_kernel");
     w->ctx->launches += 1;
     CK(cudaMemcpyAsync(solutions, w->sol, (size_t)w->n_walks * L, cudaMemcpyDeviceToHost, s));

@@ -66,7 +66,8 @@ struct RunArgs {
   uint32_t* bits_loc;
   uint32_t* bits_best;
   uint32_t* used;
-  size_t w_stride;
+  size_t w_stride;   // words per walk region: [front pad][nwords][back pad]
+  size_t w_front;    // walk base = region + w_front, word i at base[i + 1]
   int2* hlist;
   size_t h_stride;
   uint32_t* flips;

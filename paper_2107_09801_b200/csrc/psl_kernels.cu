@@ -342,12 +342,12 @@ __device__ __forceinline__ void sweep(const SweepIO& io, const Smem& sm, const b
   // shared sliding windows (3 words each) of an adjacent lane:
   //   B: positions j0 + k0 .. j0 + k0 + 34      (s_{j+k})
   //   A: positions j0 - k0 - 31 .. j0 - k0 + 3  (s_{j-k}, reversed by BREV)
-  int wb = (int)((jm[0] + 1) >> 5);
+  // (the walk's bit array carries >= nwords+48 zero words on both sides, so
+  // these pointers slide past either end without clamps)
   const uint32_t shB = (jm[0] + 1) & 31;
-  uint32_t b0 = sword(sb, wb, nwords), b1 = sword(sb, wb + 1, nwords), b2 = sword(sb, wb + 2, nwords);
-  int wa = (int)(jm[0] >> 5) - 1;
   const uint32_t shA = jm[0] & 31;
-  uint32_t a0 = sword(sb, wa, nwords), a1 = sword(sb, wa + 1, nwords), a2 = sword(sb, wa + 2, nwords);
+  const uint32_t* pB = sb + (int)((jm[0] + 1) >> 5) + 1;          // word of j0 + k0
+  const uint32_t* pA = sb + ((int)(jm[0] >> 5) - 1) + 1;          // word of j0 - k0 - 31
   const uint32_t minBE = __reduce_min_sync(FULL, lminBE), maxBE = __reduce_max_sync(FULL, lmaxBE);
   const uint32_t minOE = __reduce_min_sync(FULL, lminOE), maxOE = __reduce_max_sync(FULL, lmaxOE);
 #pragma unroll
@@ -370,9 +370,9 @@ __device__ __forceinline__ void sweep(const SweepIO& io, const Smem& sm, const b
         const uint32_t k0 = 1 + c * kChunk + blk * 32;
         const uint32_t kend = k0 + 31;
         uint32_t Bp[kJ], Ap[kJ];
-        const uint32_t nb = sword_up(sb, wb + 3, nwords);   // next block's window words
-        const uint32_t na = sword_dn(sb, wa - 1);
         if (adj) {
+          const uint32_t b0 = pB[0], b1 = pB[1], b2 = pB[2];
+          const uint32_t a0 = pA[0], a1 = pA[1], a2 = pA[2];
           const uint32_t XB = __funnelshift_r(b0, b1, shB), YB = __funnelshift_r(b1, b2, shB);
           const uint32_t XA = __funnelshift_r(a0, a1, shA), YA = __funnelshift_r(a1, a2, shA);
 #pragma unroll
@@ -470,8 +470,8 @@ __device__ __forceinline__ void sweep(const SweepIO& io, const Smem& sm, const b
             sum[m] = s;
           }
         }
-        b0 = b1; b1 = b2; b2 = nb; ++wb;
-        a2 = a1; a1 = a0; a0 = na; --wa;
+        ++pB;
+        --pA;
       }
     }
     if (io.chain && threadIdx.x == 0) {
@@ -602,10 +602,10 @@ __global__ void __launch_bounds__(256) init_walks_kernel(RunArgs a, const uint64
                                                          const int8_t* inits, uint32_t* bad) {
   const uint32_t w = blockIdx.x;
   WalkState* S = a.st + w;
-  uint32_t* bp = a.bits_piv + (size_t)w * a.w_stride;
-  uint32_t* bl = a.bits_loc + (size_t)w * a.w_stride;
-  uint32_t* bb = a.bits_best + (size_t)w * a.w_stride;
-  uint32_t* us = a.used + (size_t)w * a.w_stride;
+  uint32_t* bp = a.bits_piv + (size_t)w * a.w_stride + a.w_front;
+  uint32_t* bl = a.bits_loc + (size_t)w * a.w_stride + a.w_front;
+  uint32_t* bb = a.bits_best + (size_t)w * a.w_stride + a.w_front;
+  uint32_t* us = a.used + (size_t)w * a.w_stride + a.w_front;
   const uint32_t nw = a.nwords;
   if (threadIdx.x == 0) {
     WalkState z = {};
@@ -645,10 +645,13 @@ __global__ void __launch_bounds__(256) init_walks_kernel(RunArgs a, const uint64
     }
   }
   __syncthreads();
-  // padded layout: [0] zero, words 1..nw, zeros after
-  for (uint32_t i = threadIdx.x; i < nw + 1 + kBitsPad; i += blockDim.x) {
-    const uint32_t v = (i >= 1 && i <= nw) ? bp[i] : 0u;
-    if (i < 1 || i > nw) bp[i] = 0u;
+  // padded layout: zero pads around words 1..nw (relative to the walk base);
+  // the pads let the scan's sliding windows run off either end unclamped
+  const long long lo = -(long long)a.w_front, hi = (long long)(a.w_stride - a.w_front);
+  for (long long i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const bool in = i >= 1 && i <= (long long)nw;
+    const uint32_t v = in ? bp[i] : 0u;
+    if (!in) bp[i] = 0u;
     bl[i] = v;
     bb[i] = v;
     us[i] = 0u;
@@ -744,10 +747,10 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
   const uint32_t w = blockIdx.x, t = threadIdx.x;
   const uint32_t L = a.L, nw = a.nwords;
   WalkState* gst = a.st + w;
-  uint32_t* bits_piv = a.bits_piv + (size_t)w * a.w_stride;
-  uint32_t* bits_loc = a.bits_loc + (size_t)w * a.w_stride;
-  uint32_t* bits_best = a.bits_best + (size_t)w * a.w_stride;
-  uint32_t* used = a.used + (size_t)w * a.w_stride;
+  uint32_t* bits_piv = a.bits_piv + (size_t)w * a.w_stride + a.w_front;
+  uint32_t* bits_loc = a.bits_loc + (size_t)w * a.w_stride + a.w_front;
+  uint32_t* bits_best = a.bits_best + (size_t)w * a.w_stride + a.w_front;
+  uint32_t* used = a.used + (size_t)w * a.w_stride + a.w_front;
   int32_t* Cpiv = a.Cpiv + (size_t)w * a.c_stride;
   int32_t* Cloc = a.Cloc + (size_t)w * a.c_stride;
   int2* hlist = a.hlist + (size_t)w * a.h_stride;
@@ -1085,7 +1088,7 @@ int launch_init_walks(const RunArgs& a, uint32_t n_walks, const uint64_t* d_seed
 int launch_build_tables(const RunArgs& a, uint32_t n_walks, cudaStream_t s) {
   const uint32_t per_block = 8 * 32 * kTabR;
   dim3 grid((a.L + per_block - 1) / per_block, n_walks);
-  build_tables_kernel<<<grid, 256, 0, s>>>(a.bits_piv + 1, a.w_stride, a.Cpiv, a.Cloc,
+  build_tables_kernel<<<grid, 256, 0, s>>>(a.bits_piv + a.w_front + 1, a.w_stride, a.Cpiv, a.Cloc,
                                            a.c_stride, a.L, a.st);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
@@ -1218,7 +1221,7 @@ namespace {
 // bit-packed best sequences -> int8 +-1 (one walk per blockIdx.y)
 __global__ void unpack_kernel(const uint32_t* bits, size_t w_stride, uint32_t L, int8_t* out) {
   const uint32_t w = blockIdx.y;
-  const uint32_t* b = bits + (size_t)w * w_stride + 1;
+  const uint32_t* b = bits + (size_t)w * w_stride;   // caller passes word 0 of walk 0
   int8_t* o = out + (size_t)w * L;
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x)
     o[i] = ((b[i >> 5] >> (i & 31)) & 1u) ? (int8_t)-1 : (int8_t)1;

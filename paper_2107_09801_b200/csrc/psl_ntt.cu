@@ -164,7 +164,7 @@ int launch_build_tables_ntt(const RunArgs& a, uint32_t n_walks, cudaStream_t s) 
   ntt_twiddle_kernel<<<(N / 2 + 255) / 256, 256, 0, s>>>(twi, N / 2, to_mont(iroot));
   launches += 2;
   const dim3 gl(std::min<uint32_t>((N + 255) / 256, 256), n_walks);
-  ntt_load_kernel<<<gl, 256, 0, s>>>(a.bits_piv + 1, a.w_stride, L, N, x, y);
+  ntt_load_kernel<<<gl, 256, 0, s>>>(a.bits_piv + a.w_front + 1, a.w_stride, L, N, x, y);
   launches += 1;
   const uint32_t bx = std::min<uint32_t>((N / 2 + 255) / 256, 1024);
   for (uint32_t h = N / 2; h >= 1; h >>= 1) {

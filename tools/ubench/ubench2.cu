@@ -197,6 +197,34 @@ __global__ void kern(int reps, double* out, long long* cyc) {
             for (int m = 0; m < J; ++m) s[m] = __dadd_rn(s[m], tm[m][qq]);
           }
         }
+      } else if (MODE == 13 || MODE == 14) {  // ONE: predicated DADD pairs (NP neighbours), FSEL for the rest
+        constexpr int NP = (MODE == 13) ? 4 : 2;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          constexpr int G = 4;
+          double e3[G], e1[G];
+#pragma unroll
+          for (int qq = 0; qq < G; ++qq) lds_f64x2(rec + (G * g + qq) * REC + 32, e3[qq], e1[qq]);
+          double tm[J][G];
+#pragma unroll
+          for (int m = NP; m < J; ++m) {
+            const uint32_t x = P[m] >> (G * g);
+#pragma unroll
+            for (int qq = 0; qq < G; ++qq) tm[m][qq] = ((x >> qq) & 1u) ? e1[qq] : e3[qq];
+          }
+#pragma unroll
+          for (int qq = 0; qq < G; ++qq) {
+#pragma unroll
+            for (int m = 0; m < NP; ++m) {
+              const uint32_t bit = (P[m] >> (G * g + qq)) & 1u;
+              asm volatile("{ .reg .pred p; setp.ne.u32 p, %1, 0;\n"
+                           "  @p add.rn.f64 %0, %0, %2;\n"
+                           "  @!p add.rn.f64 %0, %0, %3; }" : "+d"(s[m]) : "r"(bit), "d"(e1[qq]), "d"(e3[qq]));
+            }
+#pragma unroll
+            for (int m = NP; m < J; ++m) s[m] = __dadd_rn(s[m], tm[m][qq]);
+          }
+        }
       } else if (MODE == 3) {   // BOTH via select: candidates (e4,e2),(e0,x) uniform
 #pragma unroll
         for (int q = 0; q < 32; ++q) {
@@ -244,11 +272,11 @@ int run(const char* name, int nsm, int threads, int ctas_per_sm, int reps) {
 int main() {
   cudaDeviceProp p; cudaGetDeviceProperties(&p, 0);
   const int nsm = p.multiProcessorCount;
-  for (int cps = 1; cps <= 2; ++cps) {
+  for (int cps = 2; cps <= 2; ++cps) {
     const int th = 256;
-        run<10>("ONE 4xFSEL R2P v2", nsm, th, cps, 100);
-    run<11>("ONE 3FSEL R2P + 1 IMAD", nsm, th, cps, 100);
-    run<12>("ONE 2FSEL R2P + 2 IMAD", nsm, th, cps, 100);
+    run<10>("ONE 4xFSEL R2P v2", nsm, th, cps, 100);
+    run<13>("ONE 4x pred-DADD", nsm, th, cps, 100);
+    run<14>("ONE 2 FSEL + 2 pred-DADD", nsm, th, cps, 100);
   }
   return 0;
 }
