@@ -273,6 +273,8 @@ __device__ __forceinline__ void build_chunk(const SweepIO& io, uint32_t c, doubl
   }
 }
 
+enum : int { CLS_BOTH = 0, CLS_ONE = 1, CLS_TAIL = 2, CLS_MIXED = 3 };
+
 __device__ __forceinline__ double lds_f64(uint32_t a) {
   double v;
   asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a));
@@ -369,37 +371,63 @@ __device__ __forceinline__ void sweep(const SweepIO& io, const Smem& sm, const b
       for (uint32_t blk = 0; blk < kChunk / 32; ++blk) {
         const uint32_t k0 = 1 + c * kChunk + blk * 32;
         const uint32_t kend = k0 + 31;
-        uint32_t Bp[kJ], Ap[kJ];
-        if (adj) {
-          const uint32_t b0 = pB[0], b1 = pB[1], b2 = pB[2];
-          const uint32_t a0 = pA[0], a1 = pA[1], a2 = pA[2];
-          const uint32_t XB = __funnelshift_r(b0, b1, shB), YB = __funnelshift_r(b1, b2, shB);
-          const uint32_t XA = __funnelshift_r(a0, a1, shA), YA = __funnelshift_r(a1, a2, shA);
-#pragma unroll
-          for (int m = 0; m < kJ; ++m) {
-            Bp[m] = __funnelshift_r(XB, YB, m) ^ mbj[m];
-            Ap[m] = __brev(__funnelshift_r(XA, YA, m)) ^ mbj[m];
-          }
-        } else {
-#pragma unroll
-          for (int m = 0; m < kJ; ++m) {
-            const int pbB = (int)(jm[m] + k0), pbA = (int)jm[m] - (int)k0 - 31;
-            const int wB = pbB >> 5, wA = pbA >> 5;       // arithmetic shift = floor
-            Bp[m] = __funnelshift_r(sword(sb, wB, nwords), sword(sb, wB + 1, nwords), pbB & 31) ^ mbj[m];
-            Ap[m] = __brev(__funnelshift_r(sword(sb, wA, nwords), sword(sb, wA + 1, nwords),
-                                           pbA & 31)) ^ mbj[m];
-          }
-        }
         const uint32_t rb = tab + blk * 32 * (kRecDoubles * 8);   // 64-byte aligned
         const bool ub = maxBE < k0 || minBE >= kend;
         const bool uo = maxOE < k0 || minOE >= kend;
-        if (ub && uo && minBE >= kend) {
-          // BOTH: 2-bit code, slot = 2 bA' + bB'
-          uint32_t Wlo[kJ], Whi[kJ];
+        const int cls = !(ub && uo) ? CLS_MIXED
+                        : minBE >= kend ? CLS_BOTH : (maxOE < k0 ? CLS_TAIL : CLS_ONE);
+        // bit planes of the block: Bp[m] bit q = bB'(k0+q), Ap[m] bit q = bA'(k0+q)
+        // (shared 64-bit windows XB:YB / XA:YA for a lane of adjacent neighbours)
+        uint32_t XB = 0, YB = 0, XA = 0, YA = 0;
+        uint32_t Bp[kJ], Ap[kJ];
+        if (cls != CLS_TAIL) {
+          if (adj) {
+            const uint32_t b0 = pB[0], b1 = pB[1], b2 = pB[2];
+            const uint32_t a0 = pA[0], a1 = pA[1], a2 = pA[2];
+            XB = __funnelshift_r(b0, b1, shB); YB = __funnelshift_r(b1, b2, shB);
+            XA = __funnelshift_r(a0, a1, shA); YA = __funnelshift_r(a1, a2, shA);
+            if (cls != CLS_BOTH) {
 #pragma unroll
-          for (int m = 0; m < kJ; ++m) {
-            Wlo[m] = spread_lo(Bp[m]) | (spread_lo(Ap[m]) << 1);
-            Whi[m] = spread_hi(Bp[m]) | (spread_hi(Ap[m]) << 1);
+              for (int m = 0; m < kJ; ++m) {
+                Bp[m] = __funnelshift_r(XB, YB, m) ^ mbj[m];
+                Ap[m] = __brev(__funnelshift_r(XA, YA, m)) ^ mbj[m];
+              }
+            }
+          } else {
+#pragma unroll
+            for (int m = 0; m < kJ; ++m) {
+              const int pbB = (int)(jm[m] + k0), pbA = (int)jm[m] - (int)k0 - 31;
+              const int wB = pbB >> 5, wA = pbA >> 5;       // arithmetic shift = floor
+              Bp[m] = __funnelshift_r(sword(sb, wB, nwords), sword(sb, wB + 1, nwords), pbB & 31) ^ mbj[m];
+              Ap[m] = __brev(__funnelshift_r(sword(sb, wA, nwords), sword(sb, wA + 1, nwords),
+                                             pbA & 31)) ^ mbj[m];
+            }
+          }
+        }
+        if (cls == CLS_BOTH) {
+          // BOTH: 2-bit code, slot = 2 bA' + bB'; W[m] interleaves (bB', bA')
+          uint32_t Wlo[kJ], Whi[kJ];
+          if (adj) {
+            // spread the shared windows once; neighbour m is a 2m-bit funnel
+            const uint32_t SB0 = spread_lo(XB), SB1 = spread_hi(XB), SB2 = spread_lo(YB);
+            const uint32_t RL = __brev(YA), RH = __brev(XA);   // bit-reversed A window
+            const uint32_t SA1 = spread_hi(RL) << 1, SA2 = spread_lo(RH) << 1,
+                           SA3 = spread_hi(RH) << 1;
+#pragma unroll
+            for (int m = 0; m < kJ; ++m) {
+              const uint32_t blo = m ? __funnelshift_r(SB0, SB1, 2 * m) : SB0;
+              const uint32_t bhi = m ? __funnelshift_r(SB1, SB2, 2 * m) : SB1;
+              const uint32_t alo = m ? __funnelshift_r(SA1, SA2, 32 - 2 * m) : SA2;
+              const uint32_t ahi = m ? __funnelshift_r(SA2, SA3, 32 - 2 * m) : SA3;
+              Wlo[m] = (blo | alo) ^ mbj[m];
+              Whi[m] = (bhi | ahi) ^ mbj[m];
+            }
+          } else {
+#pragma unroll
+            for (int m = 0; m < kJ; ++m) {
+              Wlo[m] = spread_lo(Bp[m]) | (spread_lo(Ap[m]) << 1);
+              Whi[m] = spread_hi(Bp[m]) | (spread_hi(Ap[m]) << 1);
+            }
           }
 #pragma unroll
           for (int q = 0; q < 32; ++q) {
@@ -409,7 +437,7 @@ __device__ __forceinline__ void sweep(const SweepIO& io, const Smem& sm, const b
               sum[m] = __dadd_rn(sum[m], lds_f64(and_or(v, 0x18u, rb) + q * 64));
             }
           }
-        } else if (ub && uo && maxBE < k0 && minOE >= kend) {
+        } else if (cls == CLS_ONE) {
           // ONE: 1-bit code from the neighbour's valid side selects e3 / e1,
           // loaded once per k for all kJ neighbours.  Cells go in groups of
           // kG so the per-cell predicates come from one R2P per neighbour.
@@ -435,7 +463,7 @@ __device__ __forceinline__ void sweep(const SweepIO& io, const Smem& sm, const b
               for (int m = 0; m < kJ; ++m) sum[m] = __dadd_rn(sum[m], tm[m][qq]);
             }
           }
-        } else if (ub && uo && maxOE < k0) {
+        } else if (cls == CLS_TAIL) {
           // TAIL: the term is |C_k|^alpha for every neighbour
           const uint32_t t2 = tail + blk * 32 * 8;
 #pragma unroll
