@@ -319,21 +319,20 @@ __device__ __forceinline__ void sweep(const SweepIO& io, const Smem& sm, const b
   // inactive neighbours shadow the warp's first active one (results discarded)
   const uint32_t src = __ffs(__ballot_sync(FULL, active[0])) - 1;
   const uint32_t jsrc = __shfl_sync(FULL, jin[0], src < 32 ? src : 0);
-  uint32_t be[kJ], oe[kJ], mbj[kJ], smask[kJ], jm[kJ];
-  bool sideA[kJ];
+  uint32_t mbj[kJ], jm[kJ];
+  uint32_t sideA_bits = 0;           // bit m: neighbour m's one-side range uses s[j-k]
   uint32_t lminBE = FULL, lmaxBE = 0, lminOE = FULL, lmaxOE = 0;
 #pragma unroll
   for (int m = 0; m < kJ; ++m) {
     const uint32_t j = active[m] ? jin[m] : jsrc;
     jm[m] = j;
     const uint32_t left = j, right = L - 1 - j;       // sequence.hpp:131-135
-    be[m] = left < right ? left : right;
-    oe[m] = left < right ? right : left;
-    sideA[m] = left >= right;
-    smask[m] = sideA[m] ? 0x10u : 0x08u;
+    const uint32_t be = left < right ? left : right;
+    const uint32_t oe = left < right ? right : left;
+    sideA_bits |= (left >= right ? 1u : 0u) << m;
     mbj[m] = ((sb[(j >> 5) + 1] >> (j & 31)) & 1u) ? FULL : 0u;
-    lminBE = min(lminBE, be[m]); lmaxBE = max(lmaxBE, be[m]);
-    lminOE = min(lminOE, oe[m]); lmaxOE = max(lmaxOE, oe[m]);
+    lminBE = min(lminBE, be); lmaxBE = max(lmaxBE, be);
+    lminOE = min(lminOE, oe); lmaxOE = max(lmaxOE, oe);
   }
   // The kJ neighbours of a lane are consecutive positions except when the
   // neighbourhood wraps past L-1 inside the lane (or lanes shadow inactive
@@ -444,23 +443,20 @@ __device__ __forceinline__ void sweep(const SweepIO& io, const Smem& sm, const b
           constexpr int kG = 4;
           uint32_t P[kJ];
 #pragma unroll
-          for (int m = 0; m < kJ; ++m) P[m] = sideA[m] ? Ap[m] : Bp[m];
+          for (int m = 0; m < kJ; ++m) P[m] = ((sideA_bits >> m) & 1u) ? Ap[m] : Bp[m];
 #pragma unroll
           for (int g = 0; g < 32 / kG; ++g) {
             double e3[kG], e1[kG];
 #pragma unroll
             for (int qq = 0; qq < kG; ++qq) lds_f64x2(rb + (g * kG + qq) * 64 + 32, e3[qq], e1[qq]);
-            double tm[kJ][kG];
 #pragma unroll
             for (int m = 0; m < kJ; ++m) {
+              // predicates of kG cells of one neighbour from one R2P; the kJ
+              // chains are independent, each still adds in ascending k
               const uint32_t x = P[m] >> (g * kG);
 #pragma unroll
-              for (int qq = 0; qq < kG; ++qq) tm[m][qq] = ((x >> qq) & 1u) ? e1[qq] : e3[qq];
-            }
-#pragma unroll
-            for (int qq = 0; qq < kG; ++qq) {
-#pragma unroll
-              for (int m = 0; m < kJ; ++m) sum[m] = __dadd_rn(sum[m], tm[m][qq]);
+              for (int qq = 0; qq < kG; ++qq)
+                sum[m] = __dadd_rn(sum[m], ((x >> qq) & 1u) ? e1[qq] : e3[qq]);
             }
           }
         } else if (cls == CLS_TAIL) {
@@ -489,9 +485,10 @@ __device__ __forceinline__ void sweep(const SweepIO& io, const Smem& sm, const b
               const uint32_t x = q < 16 ? Wlo : Whi;
               const int sh = 2 * (q & 15) - 3;
               const uint32_t v = sh < 0 ? (x << (-sh)) : (x >> sh);
-              const bool inb = k <= be[m];
-              const bool ino = k <= oe[m];
-              const uint32_t mask = inb ? 0x18u : (ino ? smask[m] : 0u);
+              const uint32_t jl = jm[m], jr = L - 1 - jm[m];
+              const bool inb = k <= min(jl, jr);
+              const bool ino = k <= max(jl, jr);
+              const uint32_t mask = inb ? 0x18u : (ino ? (((sideA_bits >> m) & 1u) ? 0x10u : 0x08u) : 0u);
               const uint32_t base = inb ? 0u : (ino ? 32u : 8u);
               s = __dadd_rn(s, lds_f64(and_or(v, mask, base | rb) + q * 64));
             }
@@ -816,8 +813,11 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
     if (!ctl->need_pass) break;
     const bool do_scan = ctl->do_scan;
     const uint32_t start = ctl->start;
-    const WalkState S0 = ctl->st;
-    const uint32_t alpha = S0.phase == 1 ? a.alpha1 : a.alpha2;
+    // the few walk-state fields the pass needs (not the whole struct: registers)
+    const uint32_t alpha = ctl->st.phase == 1 ? a.alpha1 : a.alpha2;
+    const uint32_t s_src_local = ctl->st.src_local, s_local_pending = ctl->st.local_pending;
+    const uint32_t s_n_pending = ctl->st.n_pending, s_fitness_pending = ctl->st.fitness_pending;
+    const int32_t s_Psrc = s_src_local ? ctl->st.P_local : ctl->st.P;
 
     for (uint32_t g = 0; g < ngroups; ++g) {
       // this thread's kJ adjacent neighbours: offsets i = base + 1 .. base + kJ
@@ -838,14 +838,13 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
       io.scan = do_scan;
       io.hcount = &ctl->hcount;
       if (g == 0) {
-        io.Csrc = S0.src_local ? Cloc : Cpiv;
+        io.Csrc = s_src_local ? Cloc : Cpiv;
         io.Cdst = Cpiv;
-        io.Cloc = S0.local_pending ? Cloc : nullptr;
-        io.flips = flips; io.F = S0.n_pending;
+        io.Cloc = s_local_pending ? Cloc : nullptr;
+        io.flips = flips; io.F = s_n_pending;
         io.hlist = hlist;
-        const int32_t Psrc = S0.src_local ? S0.P_local : S0.P;
-        io.hthr = Psrc - 4 * (int32_t)S0.n_pending - 8;
-        io.chain = S0.fitness_pending != 0;
+        io.hthr = s_Psrc - 4 * (int32_t)s_n_pending - 8;
+        io.chain = s_fitness_pending != 0;
       } else {
         io.Csrc = Cpiv; io.Cdst = nullptr; io.Cloc = nullptr;
         io.flips = flips; io.F = 0; io.hlist = nullptr; io.hthr = 0; io.chain = false;

@@ -288,6 +288,33 @@ __global__ void __launch_bounds__(1024, 1) k_cells(int reps, double* out, long l
         }
         sum += (double)acc;
       }
+
+      if (MODE >= 60 && MODE < 80) {
+        uint32_t acc = 0;
+        const uint32_t l = threadIdx.x & 31;
+        // per-block patterns prepared once (shuffles outside the cell loop)
+        const uint32_t wpair = __shfl_sync(0xffffffffu, wlo, l & ~1u);
+        const uint32_t wquad = __shfl_sync(0xffffffffu, wlo, l & ~3u);
+        const uint32_t whalf = __shfl_sync(0xffffffffu, wlo, l & 15u);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+          const int qq = q & 15;
+          uint32_t off;
+          if (MODE == 60) off = ((wlo >> (2 * qq)) & 1u) * 8;            // random 0/8
+          else if (MODE == 61) off = ((wpair >> (2 * qq)) & 1u) * 8;     // pair-uniform random 0/8
+          else if (MODE == 62) off = ((wquad >> (2 * qq)) & 1u) * 8;     // quad-uniform random
+          else if (MODE == 63) off = ((whalf >> (2 * qq)) & 1u) * 8;     // lane l == lane l+16
+          else if (MODE == 64) off = ((wlo >> (2 * qq)) & 3u) * 8;       // random 4 slots
+          else if (MODE == 65) off = ((wpair >> (2 * qq)) & 3u) * 8;     // pair-uniform 4 slots
+          else if (MODE == 66) off = ((wlo >> (2 * qq)) & 1u) * 8 + (l & 1u) * 16; // random, pair parity picks half
+          else if (MODE == 67) off = ((wlo >> (2 * qq)) & 1u) * 16 + (l & 1u) * 8; // (X|X+16)+parity*8
+          else off = 0;
+          uint32_t lo, hi;
+          asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(rec + q * REC + off));
+          acc = acc + lo + hi;
+        }
+        sum += (double)acc;
+      }
       // rotate W so the pattern changes per block
       const uint32_t t = wlo; wlo = whi ^ (wlo << 7); whi = t ^ (whi >> 3);
     }
@@ -326,16 +353,15 @@ int main() {
   printf("%s SMs=%d cc=%d.%d\n", p.name, p.multiProcessorCount, p.major, p.minor);
   const int nsm = p.multiProcessorCount;
   for (int th : {1024}) {
-    run<49>("U0 random 0/8 (+shfl cost)", nsm, th, 100, 32);
-    run<40>("U1 (l>>1)&1", nsm, th, 100, 32);
-    run<41>("U2 (l>>2)&1", nsm, th, 100, 32);
-    run<42>("U4 pair-uniform random", nsm, th, 100, 32);
-    run<43>("U5 l==l+16 random", nsm, th, 100, 32);
-    run<44>("U6 quad-uniform random", nsm, th, 100, 32);
-    run<45>("U7 octet-uniform random", nsm, th, 100, 32);
-    run<46>("U8 random 0/16", nsm, th, 100, 32);
-    run<47>("U9 random 0/64", nsm, th, 100, 32);
-    run<48>("U10 halfwarp-specific pairs", nsm, th, 100, 32);
+    run<60>("R0 random 0/8", nsm, th, 100, 32);
+    run<61>("R1 pair-uniform 0/8", nsm, th, 100, 32);
+    run<62>("R2 quad-uniform 0/8", nsm, th, 100, 32);
+    run<63>("R3 l==l+16 0/8", nsm, th, 100, 32);
+    run<64>("R4 random 4 slots", nsm, th, 100, 32);
+    run<65>("R5 pair-uniform 4 slots", nsm, th, 100, 32);
+    run<66>("R6 random + parity*16", nsm, th, 100, 32);
+    run<67>("R7 random*16 + parity*8", nsm, th, 100, 32);
+    run<7>("H uniform", nsm, th, 100, 32);
   }
   return 0;
 }
