@@ -177,6 +177,12 @@ int psl_evaluate_neighbor(psl_ctx* ctx, const int8_t* seq, const int32_t* table,
 /* SidelobeTable::build (sequence.cpp:46-60); table_out[0] = length. */
 int psl_build_table(psl_ctx* ctx, const int8_t* seq, uint32_t length, int32_t* table_out,
                     char* err, size_t errlen);
+/* oracle::verify_sequence (oracle.cpp:172-197): table on the device, then PSL,
+ * merit factor (exact int64 energy), and the |C_k| histogram (entries 0..
+ * min(hist_cap, L+1)-1; may be NULL). */
+int psl_verify_sequence(psl_ctx* ctx, const int8_t* seq, uint32_t length, int32_t* psl,
+                        double* merit_factor, int64_t* energy, uint64_t* histogram,
+                        uint32_t hist_cap, char* err, size_t errlen);
 /* apply_flip (sequence.cpp:198-224), in place on host buffers. */
 int psl_apply_flip(psl_ctx* ctx, int8_t* seq, int32_t* table, uint32_t length, uint32_t j,
                    char* err, size_t errlen);

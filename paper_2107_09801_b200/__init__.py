@@ -12,6 +12,6 @@ from .pslopt import (  # noqa: F401
     ScanTrace, SearchHooks, SearchParams, StopCondition, WalkRecord, Walks, apply_flip,
     build_table, default_alpha2, default_context, default_flip_lmt, default_n_lmt, default_params,
     evaluate_neighbor, fitness, kVersion, merit_factor, neighborhood_scan, pow_int, psl,
-    run_search, run_walks, scan_values, validate_params)
+    run_search, run_walks, scan_values, validate_params, verify_sequence, SequenceReport)
 
 __version__ = kVersion

@@ -92,6 +92,9 @@ SIGNATURES = {
                                         C.c_size_t]),
     "psl_build_table": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_char_p,
                                   C.c_size_t]),
+    "psl_verify_sequence": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.POINTER(C.c_int32),
+                                      C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_void_p,
+                                      C.c_uint32, C.c_char_p, C.c_size_t]),
     "psl_apply_flip": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32,
                                  C.c_char_p, C.c_size_t]),
     "psl_run_search": (C.c_int, [C.c_void_p, C.POINTER(psl_params), C.POINTER(psl_hooks),

@@ -416,6 +416,48 @@ int psl_build_table(psl_ctx* ctx, const int8_t* seq, uint32_t L, int32_t* table_
   return PSL_OK;
 }
 
+int psl_verify_sequence(psl_ctx* ctx, const int8_t* seq, uint32_t L, int32_t* psl,
+                        double* merit_factor, int64_t* energy, uint64_t* histogram,
+                        uint32_t hist_cap, char* err, size_t errlen) {
+  int rc = check_sequence(seq, L, err, errlen);
+  if (rc) return rc;
+  rc = device_ready(ctx, err, errlen);
+  if (rc) return rc;
+  const uint32_t nw = (L + 31) / 32;
+  std::vector<uint32_t> bits = pack_bits(seq, L, kBitsPad);
+  cudaStream_t s = ctx->stream;
+  uint32_t* db = nullptr;
+  int32_t* dc = nullptr;
+  int32_t* dpsl = nullptr;
+  unsigned long long* den = nullptr;
+  unsigned long long* dh = nullptr;
+  CK(cudaMallocAsync(&db, bits.size() * 4, s));
+  CK(cudaMallocAsync(&dc, (size_t)L * 4, s));
+  CK(cudaMallocAsync(&dpsl, 4, s));
+  CK(cudaMallocAsync(&den, 8, s));
+  CK(cudaMallocAsync(&dh, ((size_t)L + 1) * 8, s));
+  CK(cudaMemcpyAsync(db, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemsetAsync(dpsl, 0, 4, s));
+  CK(cudaMemsetAsync(den, 0, 8, s));
+  CK(cudaMemsetAsync(dh, 0, ((size_t)L + 1) * 8, s));
+  if (launch_table_only(db, dc, L, nw, s) < 0 || launch_verify(dc, L, dpsl, den, dh, s) < 0)
+    return cuda_fail(err, errlen, cudaGetLastError(), "verify");
+  ctx->launches += 2;
+  int32_t hpsl = 0;
+  unsigned long long hen = 0;
+  CK(cudaMemcpyAsync(&hpsl, dpsl, 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(&hen, den, 8, cudaMemcpyDeviceToHost, s));
+  if (histogram && hist_cap)
+    CK(cudaMemcpyAsync(histogram, dh, std::min<size_t>(hist_cap, (size_t)L + 1) * 8,
+                       cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  for (void* p : {(void*)db, (void*)dc, (void*)dpsl, (void*)den, (void*)dh}) cudaFreeAsync(p, s);
+  *psl = hpsl;
+  if (energy) *energy = (int64_t)hen;
+  if (merit_factor) *merit_factor = ((double)L * (double)L) / (2.0 * (double)(int64_t)hen);
+  return PSL_OK;
+}
+
 int psl_apply_flip(psl_ctx* ctx, int8_t* seq, int32_t* table, uint32_t L, uint32_t j, char* err,
                    size_t errlen) {
   int rc = check_sequence(seq, L, err, errlen);

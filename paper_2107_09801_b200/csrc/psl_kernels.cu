@@ -1260,3 +1260,34 @@ int launch_unpack(const uint32_t* bits, size_t w_stride, uint32_t L, uint32_t n_
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 }  // namespace pslb
+
+namespace pslb {
+namespace {
+// oracle::verify_sequence (oracle.cpp:172-197) reductions over a device table:
+// PSL, exact energy, |C_k| histogram (k = 1..L-1).
+__global__ void verify_kernel(const int32_t* C, uint32_t L, int32_t* psl, unsigned long long* energy,
+                              unsigned long long* hist) {
+  int32_t pm = 0;
+  unsigned long long en = 0;
+  for (uint32_t k = 1 + blockIdx.x * blockDim.x + threadIdx.x; k < L; k += gridDim.x * blockDim.x) {
+    const int32_t a = abs(C[k]);
+    pm = max(pm, a);
+    en += (unsigned long long)((long long)C[k] * C[k]);
+    atomicAdd(&hist[a], 1ull);
+  }
+  for (int o = 16; o; o >>= 1) {
+    pm = max(pm, __shfl_xor_sync(0xffffffffu, pm, o));
+    en += __shfl_xor_sync(0xffffffffu, en, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(psl, pm);
+    atomicAdd(energy, en);
+  }
+}
+}  // namespace
+int launch_verify(const int32_t* C, uint32_t L, int32_t* psl, unsigned long long* energy,
+                  unsigned long long* hist, cudaStream_t s) {
+  verify_kernel<<<std::min<uint32_t>((L + 255) / 256, 1184), 256, 0, s>>>(C, L, psl, energy, hist);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+}  // namespace pslb

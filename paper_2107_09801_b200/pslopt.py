@@ -347,6 +347,29 @@ def fitness(table, pow_or_alpha) -> float:           # sequence.cpp:117-141
     return total
 
 
+@dataclass
+class SequenceReport:                                # oracle.hpp SequenceReport
+    length: int
+    psl: int
+    merit_factor: float
+    sidelobe_histogram: np.ndarray
+
+
+def verify_sequence(seq, ctx: Context | None = None) -> SequenceReport:
+    """oracle::verify_sequence (oracle.cpp:172-197) on the device."""
+    s = _seq(seq)
+    ctx = ctx or default_context()
+    L = len(s)
+    psl_, mf, en = C.c_int32(), C.c_double(), C.c_int64()
+    hist = np.zeros(L + 1, np.uint64)
+    err = _err()
+    rc = B.lib().psl_verify_sequence(ctx.handle, s.ctypes.data, L, C.byref(psl_), C.byref(mf),
+                                     C.byref(en), hist.ctypes.data, L + 1, err, len(err))
+    if rc:
+        _raise(rc, err)
+    return SequenceReport(L, psl_.value, mf.value, hist[:psl_.value + 1].copy())
+
+
 def apply_flip(seq: np.ndarray, table: np.ndarray, j: int, ctx: Context | None = None) -> None:
     """apply_flip (sequence.cpp:198-224), in place, on the device."""
     if seq.dtype != np.int8 or table.dtype != np.int32 or not seq.flags.c_contiguous:

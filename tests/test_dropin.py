@@ -36,3 +36,83 @@ def test_acceptance_criterion(crit):
 def test_acceptance_quality(crit):
     rc, out = run(crit, 1800)
     assert rc == 0 and "PASS" in out, out
+
+
+CLI = os.path.join(ROOT, "oracle", "_ref", "pslopt_b200")
+
+# docs/formats.md:31-55 (the reference's own golden record); elapsed masked
+FORMATS_MD_RECORD = """pslopt-run v1
+length: 16
+seed: 3
+alpha1: 4
+alpha2: 13
+ls-lmt: 2000
+flip-lmt: 10
+n-lmt: 16
+workers: 1
+max-nse: 400
+max-seconds: none
+init: none
+solver-version: 0.1.0
+nse: 401
+elapsed-seconds: *
+psl-best: 2
+merit-factor: 4.571428571428571
+solution-best: +-+-++--++-----+
+events: 4
+event: 17 * 3 1 improved-psl
+event: 17 * 3 1 local-best-improved
+event: 49 * 2 1 improved-psl
+event: 49 * 2 1 local-best-improved
+"""
+
+
+def _mask(text):
+    out = []
+    for line in text.splitlines():
+        if line.startswith("elapsed-seconds:"):
+            line = "elapsed-seconds: *"
+        elif line.startswith("event:"):
+            f = line.split()
+            f[2] = "*"
+            line = " ".join(f)
+        out.append(line)
+    return "\n".join(out) + "\n"
+
+
+@pytest.mark.skipif(not os.path.exists(CLI), reason="pslopt_b200 not built")
+def test_cli_solve_writes_reference_record(tmp_path):
+    out, best, log = tmp_path / "rec.txt", tmp_path / "best.txt", tmp_path / "log.csv"
+    p = subprocess.run([CLI, "solve", "-L", "16", "--seed", "3", "--n-lmt", "16", "--max-nse", "400",
+                        "--out", str(out), "--best", str(best), "--log", str(log)],
+                       capture_output=True, text=True, timeout=120)
+    assert p.returncode == 0, p.stderr
+    assert p.stdout.startswith("PSL=2 NSE=401 MF=4.571429 elapsed=")
+    assert _mask(out.read_text()) == FORMATS_MD_RECORD
+    assert best.read_text().strip() == "+-+-++--++-----+"
+    rows = log.read_text().splitlines()
+    assert rows[0] == "nse,elapsed_seconds,psl_best,phase_index,kind" and len(rows) == 5
+    v = subprocess.run([CLI, "verify", str(best), "--histogram"], capture_output=True, text=True,
+                       timeout=120)
+    assert v.returncode == 0 and v.stdout.startswith("L=16 PSL=2 MF=4.571429 PSL<sqrt(L): yes")
+
+
+@pytest.mark.skipif(not os.path.exists(CLI), reason="pslopt_b200 not built")
+def test_cli_bench_matches_reference_readme():
+    # proj/README.md:172-175: L=1023, 1e7 NSE, seeds 1-10 -> two-phase mean 28.5
+    p = subprocess.run([CLI, "bench", "-L", "1023", "--runs", "10", "--max-nse", "10000000"],
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr
+    assert "psl mean=28.500 min=28 max=29" in p.stdout, p.stdout
+
+
+@pytest.mark.skipif(not os.path.exists(CLI), reason="pslopt_b200 not built")
+def test_cli_exit_codes(tmp_path):
+    r = subprocess.run([CLI, "solve", "-L", "64", "--max-nse", "100000", "--alpha2", "1100",
+                        "--ls-lmt", "1"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 2 and "1100" in r.stderr and "alpha2" in r.stderr
+    r = subprocess.run([CLI, "solve", "-L", "1", "--max-nse", "10"], capture_output=True, text=True)
+    assert r.returncode == 1
+    r = subprocess.run([CLI, "solve", "-L", "16", "--max-nse", "10", "--init",
+                        str(tmp_path / "missing.txt")], capture_output=True, text=True)
+    assert r.returncode == 3

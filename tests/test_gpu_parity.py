@@ -347,3 +347,16 @@ def test_drain_and_resume(engine, golden, monkeypatch):
         _run_and_compare(engine, golden("records.json")[key])
     for g in golden("trajectories.json")[:3]:
         _run_and_compare(engine, g)
+
+
+def test_verify_sequence_matches_oracle(engine):
+    """oracle::verify_sequence on the device: PSL, merit factor, histogram."""
+    rng = np.random.default_rng(12)
+    for L in (2, 13, 100, 4097, 70000):
+        s = rng.choice(np.array([-1, 1], np.int8), L)
+        c = O.build_table(s, fast=True)
+        rep = engine.verify_sequence(s)
+        assert rep.psl == O.psl(c)
+        assert rep.merit_factor == O.lib().orc_merit_factor(c, L)
+        hist = np.bincount(np.abs(c[1:]), minlength=rep.psl + 1)
+        assert np.array_equal(rep.sidelobe_histogram, hist)
