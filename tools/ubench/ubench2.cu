@@ -225,6 +225,57 @@ __global__ void kern(int reps, double* out, long long* cyc) {
             for (int m = NP; m < J; ++m) s[m] = __dadd_rn(s[m], tm[m][qq]);
           }
         }
+      } else if (MODE == 15) {  // ONE: 3 FSEL (R2P order) + 1 divergent-LDS neighbour
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          constexpr int G = 4;
+          double e3[G], e1[G];
+#pragma unroll
+          for (int qq = 0; qq < G; ++qq) lds_f64x2(rec + (G * g + qq) * REC + 32, e3[qq], e1[qq]);
+#pragma unroll
+          for (int m = 0; m < 3; ++m) {
+            const uint32_t x = P[m] >> (G * g);
+#pragma unroll
+            for (int qq = 0; qq < G; ++qq) s[m] = __dadd_rn(s[m], ((x >> qq) & 1u) ? e1[qq] : e3[qq]);
+          }
+#pragma unroll
+          for (int qq = 0; qq < G; ++qq) {
+            const int q = G * g + qq;
+            const uint32_t v = q < 3 ? (P[3] << (3 - q)) : (P[3] >> (q - 3));
+            uint32_t a; asm("lop3.b32 %0, %1, 8, %2, 0xEA;" : "=r"(a) : "r"(v), "r"(rec + 32));
+            s[3] = __dadd_rn(s[3], lds_f64(a + q * REC));
+          }
+        }
+      } else if (MODE == 16) {  // BOTH: 2 LDS neighbours + 2 FSEL 2-level neighbours
+        uint32_t X[J], Y[J];
+#pragma unroll
+        for (int m = 0; m < J; ++m) { X[m] = P[m]; Y[m] = P[m] * 2654435761u; }
+#pragma unroll
+        for (int g = 0; g < 8; ++g) {
+          constexpr int G = 4;
+          double e4[G], e2[G], e0[G];
+#pragma unroll
+          for (int qq = 0; qq < G; ++qq) { lds_f64x2(rec + (G * g + qq) * REC, e4[qq], e2[qq]); e0[qq] = lds_f64(rec + (G * g + qq) * REC + 24); }
+#pragma unroll
+          for (int m = 2; m < 4; ++m) {
+            const uint32_t x = X[m] >> (G * g), y = Y[m] >> (G * g);
+#pragma unroll
+            for (int qq = 0; qq < G; ++qq)
+              s[m] = __dadd_rn(s[m], ((x >> qq) & 1u) ? e2[qq] : (((y >> qq) & 1u) ? e0[qq] : e4[qq]));
+          }
+#pragma unroll
+          for (int qq = 0; qq < G; ++qq) {
+            const int q = G * g + qq;
+#pragma unroll
+            for (int m = 0; m < 2; ++m) {
+              const uint32_t w = P[m];
+              const int sh = (2 * q - 3) & 31;
+              const uint32_t v = q < 2 ? (w << (3 - 2 * q)) : (w >> sh);
+              uint32_t a; asm("lop3.b32 %0, %1, 0x18, %2, 0xEA;" : "=r"(a) : "r"(v), "r"(rec));
+              s[m] = __dadd_rn(s[m], lds_f64(a + q * REC));
+            }
+          }
+        }
       } else if (MODE == 3) {   // BOTH via select: candidates (e4,e2),(e0,x) uniform
 #pragma unroll
         for (int q = 0; q < 32; ++q) {
@@ -275,8 +326,9 @@ int main() {
   for (int cps = 2; cps <= 2; ++cps) {
     const int th = 256;
     run<10>("ONE 4xFSEL R2P v2", nsm, th, cps, 100);
-    run<13>("ONE 4x pred-DADD", nsm, th, cps, 100);
-    run<14>("ONE 2 FSEL + 2 pred-DADD", nsm, th, cps, 100);
+    run<15>("ONE 3 FSEL + 1 LDS", nsm, th, cps, 100);
+    run<2>("BOTH 4 LDS", nsm, th, cps, 100);
+    run<16>("BOTH 2 LDS + 2 FSEL", nsm, th, cps, 100);
   }
   return 0;
 }
