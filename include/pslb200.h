@@ -146,6 +146,21 @@ int psl_ctx_set_stream(psl_ctx* ctx, void* stream);
 void* psl_ctx_stream(psl_ctx* ctx);
 const char* psl_version(void);                         /* version.hpp:5 */
 uint32_t psl_kernel_launches(psl_ctx* ctx);            /* kernels launched so far */
+/* Scan mode of subsequent runs.  PSL_SCAN_AUTO (default): steps are scored by
+ * the certified tensor-core scan wherever it can decide them and by the exact
+ * serial-chain sweep otherwise (records, events and solutions are identical
+ * to the reference either way; runs with an on_scan hook always use the exact
+ * sweep, since ScanTrace carries the serial doubles).  PSL_SCAN_EXACT: exact
+ * sweep on every step.  The PSLB200_SCAN=exact environment variable sets the
+ * default. */
+#define PSL_SCAN_AUTO 0
+#define PSL_SCAN_EXACT 1
+int psl_ctx_set_scan_mode(psl_ctx* ctx, int mode);
+int psl_ctx_scan_mode(psl_ctx* ctx);
+/* Totals over the walks whose records were read on this context: steps decided
+ * by the certified scan alone, certified steps re-scored exactly, and exact
+ * value_local chains. */
+int psl_ctx_scan_stats(psl_ctx* ctx, uint64_t* certified, uint64_t* refined, uint64_t* chains);
 /* Measurement helper for the roofline (bench.py): FP64-add pipe throughput
  * (cells/s at one DADD per cell), the divergent-LDS.64+DADD loop rate, and the
  * SM clock seen by the probe. */

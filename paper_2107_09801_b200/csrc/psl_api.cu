@@ -28,6 +28,8 @@ struct psl_ctx {
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
   uint32_t launches = 0;
+  int scan_mode = PSL_SCAN_AUTO;
+  uint64_t stats[3] = {0, 0, 0};
 };
 
 struct psl_walks {
@@ -145,6 +147,8 @@ int psl_ctx_create(int device, psl_ctx** out, char* err, size_t errlen) {
   }
   psl_ctx* c = new psl_ctx;
   c->device = device;
+  if (const char* env = std::getenv("PSLB200_SCAN"))
+    c->scan_mode = std::string(env) == "exact" ? PSL_SCAN_EXACT : PSL_SCAN_AUTO;
   CK(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking));
   c->stream = c->own;
   // keep freed walk buffers in the pool (no release back to the OS between calls)
@@ -173,6 +177,22 @@ int psl_ctx_set_stream(psl_ctx* ctx, void* stream) {
 void* psl_ctx_stream(psl_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
 
 uint32_t psl_kernel_launches(psl_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int psl_ctx_set_scan_mode(psl_ctx* ctx, int mode) {
+  if (!ctx || (mode != PSL_SCAN_AUTO && mode != PSL_SCAN_EXACT)) return PSL_ERR_CONFIG;
+  ctx->scan_mode = mode;
+  return PSL_OK;
+}
+
+int psl_ctx_scan_mode(psl_ctx* ctx) { return ctx ? ctx->scan_mode : -1; }
+
+int psl_ctx_scan_stats(psl_ctx* ctx, uint64_t* certified, uint64_t* refined, uint64_t* chains) {
+  if (!ctx) return PSL_ERR_CONFIG;
+  if (certified) *certified = ctx->stats[0];
+  if (refined) *refined = ctx->stats[1];
+  if (chains) *chains = ctx->stats[2];
+  return PSL_OK;
+}
 
 int psl_probe_peaks(psl_ctx* ctx, double* dadd_cells_per_s, double* lds_cells_per_s,
                     double* sm_mhz, char* err, size_t errlen) {
@@ -532,6 +552,7 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
   a.step_budget = 0xffffffffu;
   a.record_events = events_cap > 0;
   a.record_traces = traces_cap > 0;
+  a.cert = ctx->scan_mode == PSL_SCAN_AUTO && !a.record_traces;
   a.events_cap = events_cap;
   a.traces_cap = traces_cap;
   a.c_stride = ((size_t)L + 31) & ~size_t(31);
@@ -672,6 +693,9 @@ int psl_walks_records(psl_walks* w, psl_walk_record* records, int8_t* solutions,
     r.merit_factor = ((double)L * (double)L) / (2.0 * (double)S.energy_best);
     r.switches = S.switches;
     r.steps = S.steps;
+    w->ctx->stats[0] += S.n_cert;
+    w->ctx->stats[1] += S.n_refine;
+    w->ctx->stats[2] += S.n_vlchain;
   }
   return PSL_OK;
 }

@@ -1,0 +1,384 @@
+// psl_cert.cuh -- the certified (decision-exact) neighbourhood scan.
+// Included by psl_kernels.cu inside its anonymous namespace (after the exact
+// sweep helpers).
+//
+// The reference scores neighbour j by the serial double chain
+//   V(j) = fl( sum_{k=1}^{L-1} E_k(2 + s_j (s_{j-k} + s_{j+k})) )       (sequence.hpp:126-162)
+// with E_k(x) = pow_int(|C_k - 2(x-2)|, alpha) and out-of-range s = 0.  The
+// serial chain only matters through the DECISIONS run_search takes from it
+// (argmin with smallest-offset ties, value_step vs value_local; search.cpp:
+// 383-413), so this scan computes an approximation of the exact real sum T(j)
+// with a rigorous error bound, turns it into an interval that provably holds
+// V(j) (|V - T| <= gamma_{L} T for a serial sum of L-1 nonnegative terms), and
+// hands the step to the exact sweep whenever the intervals cannot decide.
+//
+// Per shift k the term is affine in u = s_j s_{j+k}, v = s_j s_{j-k} and uv:
+//   both sides in range: 4E = 4P + 4Q (u + v) + 4R uv,  4P = e4+e0+2e2,
+//                        4Q = e4-e0, 4R = e4+e0-2e2        (e_x = E_k(x))
+//   one side in range:   4E = 4M + 4N (u or v),          4M = 2(e3+e1), 4N = 2(e3-e1)
+//   none:                4E = 4 e2
+// so with zones over the 1024-row window (m_j = min(j, L-1-j), M_j = L-1-m_j):
+//   4T(j) = S_P + S_M + S_E                       (window-wide constants, k in Z1/Z3/Z5)
+//         + s_j sum_k H4_k (s_{j+k} + s_{j-k})    (H4 = 4Q in Z1, 4N in Z3: a correlation)
+//         + sum_{k in Z1} 4R_k s_{j+k} s_{j-k}    (the both-sides cross term)
+//         + 4 * (exact terms of the two <= n-wide bands where the zone depends on j)
+// The two correlations run on the tensor cores (mma.sync s8): the sequence as
+// +-1 bytes (A, rows = neighbours, Hankel in k), H4 / R4 as 8 balanced base-256
+// digits of a fixed-point value (B, one digit per column), int32 accumulation
+// (exact).  Everything else is per-k work in the builder.
+#pragma once
+
+constexpr int kCertTiles = 8;                 // m16 row tiles per warp (128 rows)
+constexpr int kCertCols = kChunk / 32;        // k columns of 32 per chunk
+constexpr int kLimbStride = kChunk + 16;      // bytes per digit row (bank spread)
+constexpr int kWinBytes = 1568;               // staged bytes per copy (392 words, = 8 mod 32)
+constexpr int kY0 = 1031;                     // origin of the reversed window
+constexpr size_t kLimbBuf = 8ull * kLimbStride;          // one table, one buffer
+constexpr size_t kWinBuf = 4ull * kWinBytes;             // one direction (4 copies), one buffer
+constexpr size_t kCertRecBuf = (size_t)kChunk * sizeof(int32_t);
+constexpr size_t kCertRowBytes = (size_t)kGroup * sizeof(double);
+// [limbH 2][limbR 2][win_f 2][win_r 2][rec 2][xrow]
+constexpr size_t kCertBytes = 4 * kLimbBuf + 4 * kWinBuf + 2 * kCertRecBuf + kCertRowBytes;
+constexpr uint32_t kCertMinL = 4096;
+
+struct CertIO {
+  uint32_t L, n, nchunks, j0;                 // rows j = j0 + rho, rho < 1024 (active: rho < n)
+  const int32_t* Csrc;
+  int32_t* Cdst;
+  int32_t* Cloc;
+  const uint32_t* flips;
+  uint32_t F;
+  uint32_t alpha;
+  int2* hlist;
+  uint32_t* hcount;
+  int32_t hthr;
+  double scale;                               // 2^-q
+  uint32_t m_lo, m_hi, M_lo, M_hi;            // zone bounds (see above)
+};
+
+struct CertSmem {
+  unsigned char* limbH;   // [2][8][kLimbStride]
+  unsigned char* limbR;
+  unsigned char* winF;    // [2][4][kWinBytes]  F[x] = s_{j0+kb+x}
+  unsigned char* winV;    // [2][4][kWinBytes]  V[y] = s_{j0-kb+kY0-y}
+  int32_t* rec;           // [2][kChunk]        C_k (band chunks only)
+  double* xrow;           // [1024]             cross-term sums per row
+};
+
+__device__ __forceinline__ CertSmem cert_carve(unsigned char* base) {
+  CertSmem m;
+  m.limbH = base;
+  m.limbR = base + 2 * kLimbBuf;
+  m.winF = base + 4 * kLimbBuf;
+  m.winV = base + 4 * kLimbBuf + 2 * kWinBuf;
+  m.rec = reinterpret_cast<int32_t*>(base + 4 * kLimbBuf + 4 * kWinBuf);
+  m.xrow = reinterpret_cast<double*>(base + 4 * kLimbBuf + 4 * kWinBuf + 2 * kCertRecBuf);
+  return m;
+}
+
+__device__ __forceinline__ bool cert_band_chunk(const CertIO& io, uint32_t c) {
+  const uint32_t kb = 1 + c * kChunk, ke = kb + kChunk - 1;
+  return (kb <= io.m_hi && ke > io.m_lo) || (kb <= io.M_hi && ke > io.M_lo);
+}
+
+// any k column with nonzero H4 / R4 (zones Z1, Z3) in the chunk starting at kb
+__device__ __forceinline__ bool cert_mma_work(const CertIO& io, uint32_t kb) {
+  return kb <= io.m_lo || (kb + kChunk - 1 > io.m_hi && kb <= io.M_lo);
+}
+
+// +-1 / 0 bytes of the staged windows
+__device__ __forceinline__ uint32_t nib_bytes(uint32_t nib) {
+  return ((nib * 0x00204081u) & 0x01010101u) * 0xFEu + 0x01010101u;
+}
+__device__ __forceinline__ uint32_t sbyte(const uint32_t* sb, long long p, uint32_t L) {
+  if (p < 0 || p >= (long long)L) return 0u;
+  return ((sb[(p >> 5) + 1] >> (p & 31)) & 1u) ? 0xFFu : 0x01u;
+}
+
+// Builder for chunk c into buffer b: fold pending flips into C, write C back,
+// collect high sidelobes, expand into the fixed-point digit rows of H4 / R4,
+// the window constants and (band chunks) the exact term records; stage the
+// sequence windows the MMAs read.
+__device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs, uint32_t c,
+                                           uint32_t b, const uint32_t* sb, int32_t& pmax,
+                                           double (&part)[5]) {
+  const uint32_t t = threadIdx.x;
+  const uint32_t kb = 1 + c * kChunk;
+  const bool band = cert_band_chunk(io, c);
+  int32_t* rec = cs.rec + (size_t)b * kChunk;
+  uint64_t VH[2], VR[2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const uint32_t r = 2 * t + i;
+    const uint32_t k = kb + r;
+    double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0, e4 = 0.0;
+    bool want = false;
+    int32_t cv = 0;
+    if (k < io.L) {
+      cv = io.Csrc[k];
+      if (io.F) {
+        SweepIO fio;
+        fio.L = io.L; fio.flips = io.flips; fio.F = io.F;
+        cv = fold_flips(cv, k, fio, sb);
+      }
+      if (io.Cdst) io.Cdst[k] = cv;
+      if (io.Cloc) io.Cloc[k] = cv;
+      const int32_t a = abs(cv);
+      pmax = max(pmax, a);
+      want = io.hlist != nullptr && a >= io.hthr;
+      e2 = pow_int_dev((double)a, io.alpha);
+      e4 = pow_int_dev((double)abs(cv - 4), io.alpha);
+      e3 = pow_int_dev((double)abs(cv - 2), io.alpha);
+      e1 = pow_int_dev((double)abs(cv + 2), io.alpha);
+      e0 = pow_int_dev((double)abs(cv + 4), io.alpha);
+    }
+    if (io.hlist) {
+      const uint32_t m = __ballot_sync(FULL, want);
+      if (m) {
+        const int lane = t & 31, leader = __ffs(m) - 1;
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(io.hcount, (uint32_t)__popc(m));
+        base = __shfl_sync(FULL, base, leader);
+        if (want) io.hlist[base + __popc(m & ((1u << lane) - 1))] = make_int2((int)k, cv);
+      }
+    }
+    double H = 0.0, R = 0.0;
+    if (k < io.L) {
+      if (k <= io.m_lo) {                               // Z1: both sides for every row
+        H = __dsub_rn(e4, e0);
+        R = __dsub_rn(__dadd_rn(e4, e0), __dmul_rn(2.0, e2));
+        part[0] = __dadd_rn(part[0], __dadd_rn(__dadd_rn(e4, e0), __dmul_rn(2.0, e2)));
+      } else if (k <= io.m_hi) {                        // band 1: exact terms per row
+      } else if (k <= io.M_lo) {                        // Z3: one side for every row
+        H = __dmul_rn(2.0, __dsub_rn(e3, e1));
+        part[1] = __dadd_rn(part[1], __dmul_rn(2.0, __dadd_rn(e3, e1)));
+      } else if (k <= io.M_hi) {                        // band 2
+      } else {                                          // Z5: no side for any row
+        part[2] = __dadd_rn(part[2], __dmul_rn(4.0, e2));
+      }
+      part[3] = __dadd_rn(part[3], fabs(H));
+      part[4] = __dadd_rn(part[4], fabs(R));
+    }
+    // fixed point (|V| < 2^62) -> 8 balanced base-256 digits, as bytes
+    const long long hv = __double2ll_rn(__dmul_rn(H, io.scale));
+    const long long rv = __double2ll_rn(__dmul_rn(R, io.scale));
+    VH[i] = ((unsigned long long)hv + 0x8080808080808080ull) ^ 0x8080808080808080ull;
+    VR[i] = ((unsigned long long)rv + 0x8080808080808080ull) ^ 0x8080808080808080ull;
+    if (band) rec[r] = cv;
+  }
+  unsigned char* lh = cs.limbH + (size_t)b * kLimbBuf + 2 * t;
+  unsigned char* lr = cs.limbR + (size_t)b * kLimbBuf + 2 * t;
+#pragma unroll
+  for (int d = 0; d < 8; ++d) {
+    const uint32_t h = (uint32_t)((VH[0] >> (8 * d)) & 0xFF) | ((uint32_t)((VH[1] >> (8 * d)) & 0xFF) << 8);
+    const uint32_t r = (uint32_t)((VR[0] >> (8 * d)) & 0xFF) | ((uint32_t)((VR[1] >> (8 * d)) & 0xFF) << 8);
+    *reinterpret_cast<uint16_t*>(lh + d * kLimbStride) = (uint16_t)h;
+    *reinterpret_cast<uint16_t*>(lr + d * kLimbStride) = (uint16_t)r;
+  }
+  // sequence windows: 2 directions x 4 copies x 392 words (only chunks with MMA work)
+  if (!cert_mma_work(io, kb)) return;
+  const uint32_t L = io.L;
+  for (uint32_t idx = t; idx < 2u * 4u * (kWinBytes / 4); idx += kThreads) {
+    const uint32_t dir = idx / (4 * (kWinBytes / 4));
+    const uint32_t rem = idx - dir * (4 * (kWinBytes / 4));
+    const uint32_t a = rem / (kWinBytes / 4), q = rem - a * (kWinBytes / 4);
+    // fwd: byte i <-> position p0 + i; rev: byte i <-> position p0 - i
+    const long long p0 = dir == 0 ? (long long)io.j0 + kb + a + 4ll * q
+                                  : (long long)io.j0 - kb + kY0 - a - 4ll * q;
+    const long long lo = dir == 0 ? p0 : p0 - 3, hi = dir == 0 ? p0 + 3 : p0;
+    uint32_t val = 0;
+    if (hi >= 0 && lo < (long long)L) {
+      if (lo >= 0 && hi < (long long)L) {
+        const uint32_t w = (uint32_t)(lo >> 5), sh = (uint32_t)(lo & 31);
+        const uint32_t x = __funnelshift_r(sb[w + 1], sb[w + 2], sh) & 0xFu;
+        val = nib_bytes(dir == 0 ? x : __brev(x) >> 28);
+      } else {
+        for (int i = 0; i < 4; ++i) val |= sbyte(sb, dir == 0 ? p0 + i : p0 - i, L) << (8 * i);
+      }
+    }
+    unsigned char* dst = (dir == 0 ? cs.winF : cs.winV) + (size_t)b * kWinBuf + a * kWinBytes + 4 * q;
+    *reinterpret_cast<uint32_t*>(dst) = val;
+  }
+}
+
+__device__ __forceinline__ void imma_s8(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                        uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// s_{j+k} s_{j-k} as +-1 bytes from two +-1 byte words
+__device__ __forceinline__ uint32_t uv_bytes(uint32_t f, uint32_t v) { return (f ^ v) | 0x01010101u; }
+
+template <int OFF>
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1+%2];" : "=r"(v) : "r"(addr), "n"(OFF));
+  return v;
+}
+
+// Per-lane shared addresses (buffer 0) of this warp's MMA operands.  Row rho =
+// 128 w + 16 r + g (+8 for a1/a3), fragment layout of mma.m16n8k32 (row.col):
+//   forward word m (bytes 8m..8m+3 past base_f = 128w + g + 4t) = s_{j+k} for
+//     m = 2r + 4c + {0: a0, 1: a1, 2: a2, 3: a3}
+//   reversed word m' (past base_v = kY0 - 128w - g + 4t) = s_{j-k} for
+//     m' = 4c - 2r + {0: a0, -1: a1, 2: a2, 1: a3}
+struct CertLane {
+  uint32_t f, v, bh, br;
+};
+__device__ __forceinline__ CertLane cert_lane(const CertSmem& cs) {
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t gid = lane >> 2, tig = lane & 3;
+  const uint32_t base_f = 128 * w + gid + 4 * tig, af = gid & 3;
+  const uint32_t base_v = kY0 - 128 * w - gid + 4 * tig, av = base_v & 3;
+  CertLane l;
+  l.f = smem_u32(cs.winF) + af * kWinBytes + (base_f - af);
+  l.v = smem_u32(cs.winV) + av * kWinBytes + (base_v - av);
+  l.bh = smem_u32(cs.limbH) + gid * kLimbStride + 4 * tig;
+  l.br = smem_u32(cs.limbR) + gid * kLimbStride + 4 * tig;
+  return l;
+}
+
+// ncols consecutive 32-k columns with one warp-uniform mode
+template <bool FWD, bool REV, bool CRS>
+__device__ __forceinline__ void cert_cols(uint32_t f, uint32_t v, uint32_t bh, uint32_t br, int ncols,
+                                          int (&accL)[kCertTiles][4], int (&accX)[kCertTiles][4]) {
+#pragma unroll 1
+  for (int cc = 0; cc < ncols; ++cc, f += 32, v += 32, bh += 32, br += 32) {
+    uint32_t b0 = 0, b1 = 0, r0 = 0, r1 = 0;
+    if (FWD || REV) { b0 = lds32<0>(bh); b1 = lds32<16>(bh); }
+    if (CRS) { r0 = lds32<0>(br); r1 = lds32<16>(br); }
+#pragma unroll
+    for (int r = 0; r < kCertTiles; ++r) {
+      uint32_t f0 = 0, f1 = 0, f2 = 0, f3 = 0, v0 = 0, v1 = 0, v2 = 0, v3 = 0;
+      switch (r) {   // immediate offsets: 16r + {0,8,16,24} / -16r + {0,-8,16,8}
+#define CERT_LOADS(R)                                                                    \
+  case R:                                                                                \
+    if (FWD || CRS) {                                                                    \
+      f0 = lds32<16 * R>(f); f1 = lds32<16 * R + 8>(f);                                  \
+      f2 = lds32<16 * R + 16>(f); f3 = lds32<16 * R + 24>(f);                            \
+    }                                                                                    \
+    if (REV || CRS) {                                                                    \
+      v0 = lds32<-16 * R>(v); v1 = lds32<-16 * R - 8>(v);                                \
+      v2 = lds32<-16 * R + 16>(v); v3 = lds32<-16 * R + 8>(v);                           \
+    }                                                                                    \
+    break;
+        CERT_LOADS(0) CERT_LOADS(1) CERT_LOADS(2) CERT_LOADS(3)
+        CERT_LOADS(4) CERT_LOADS(5) CERT_LOADS(6) CERT_LOADS(7)
+#undef CERT_LOADS
+      }
+      if (FWD) imma_s8(accL[r], f0, f1, f2, f3, b0, b1);
+      if (CRS) imma_s8(accX[r], uv_bytes(f0, v0), uv_bytes(f1, v1), uv_bytes(f2, v2), uv_bytes(f3, v3), r0, r1);
+      if (REV) imma_s8(accL[r], v0, v1, v2, v3, b0, b1);
+    }
+  }
+}
+
+// The tensor-core part of chunk c (buffer b) for this warp's 128 rows:
+// accL += digits of H4 x (s_{j+k} + s_{j-k}), accX += digits of R4 x s_{j+k} s_{j-k}.
+// Columns are grouped into runs of one mode (zones and row ranges are
+// monotone in k, so a chunk has at most a few runs).
+template <bool kCross>
+__device__ __forceinline__ void cert_mma_chunk(const CertIO& io, const CertLane& ln, uint32_t c,
+                                               uint32_t b, int (&accL)[kCertTiles][4],
+                                               int (&accX)[kCertTiles][4]) {
+  const uint32_t kb = 1 + c * kChunk;
+  if (!cert_mma_work(io, kb)) return;
+  const uint32_t w = threadIdx.x >> 5;
+  const uint32_t jw_lo = io.j0 + 128 * w, jw_hi = jw_lo + 127;
+  const uint32_t fo = b * (uint32_t)kWinBuf, bo = b * (uint32_t)kLimbBuf;
+  auto mode = [&](int cc) -> int {
+    const uint32_t k0 = kb + 32 * cc, k1 = k0 + 31;
+    if (k0 >= io.L) return 0;
+    const bool lin = k0 <= io.m_lo || (k1 > io.m_hi && k0 <= io.M_lo);
+    const bool fwd = lin && jw_lo + k0 < io.L;
+    const bool rev = lin && k0 <= jw_hi;
+    const bool crs = kCross && k0 <= io.m_lo;
+    return (fwd ? 1 : 0) | (rev ? 2 : 0) | (crs ? 4 : 0);
+  };
+  int cc = 0;
+  while (cc < kCertCols) {
+    const int md = mode(cc);
+    int ce = cc + 1;
+    while (ce < kCertCols && mode(ce) == md) ++ce;
+    const uint32_t f = ln.f + fo + 32 * cc, v = ln.v + fo + 32 * cc;
+    const uint32_t bh = ln.bh + bo + 32 * cc, br = ln.br + bo + 32 * cc;
+    const int n = ce - cc;
+    switch (md) {
+      case 1: cert_cols<true, false, false>(f, v, bh, br, n, accL, accX); break;
+      case 2: cert_cols<false, true, false>(f, v, bh, br, n, accL, accX); break;
+      case 3: cert_cols<true, true, false>(f, v, bh, br, n, accL, accX); break;
+      case 7: if (kCross) cert_cols<true, true, true>(f, v, bh, br, n, accL, accX); break;
+      case 5: if (kCross) cert_cols<true, false, true>(f, v, bh, br, n, accL, accX); break;
+      case 6: if (kCross) cert_cols<false, true, true>(f, v, bh, br, n, accL, accX); break;
+      case 4: if (kCross) cert_cols<false, false, true>(f, v, bh, br, n, accL, accX); break;
+      default: break;
+    }
+    cc = ce;
+  }
+}
+
+// Accumulator digits -> per-row doubles (rows 128w + 16r + g (+8)); the quad
+// holds digits 2 tig, 2 tig + 1 (weights 256^d), times the unit 2^q.
+__device__ __forceinline__ void cert_rows(const int (&acc)[kCertTiles][4], double unit, double* row) {
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gid = lane >> 2, tig = lane & 3;
+  const double w0 = ldexp(1.0, 16 * tig), w1 = ldexp(1.0, 16 * tig + 8);
+#pragma unroll
+  for (int r = 0; r < kCertTiles; ++r) {
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      double p = __dadd_rn(__dmul_rn((double)acc[r][2 * hh], w0), __dmul_rn((double)acc[r][2 * hh + 1], w1));
+      p = __dadd_rn(p, __shfl_xor_sync(FULL, p, 1));
+      p = __dadd_rn(p, __shfl_xor_sync(FULL, p, 2));
+      if (tig == 0) row[128 * warp + 16 * r + gid + 8 * hh] = __dmul_rn(p, unit);
+    }
+  }
+}
+
+// Exact band terms of chunk c for this thread's rows rho = 4t + m: per cell
+// pow_int(|C_k - 2x|, alpha), x = s_j (s_{j-k} [k <= j] + s_{j+k} [j+k < L]).
+__device__ __forceinline__ void cert_band_cells(const CertIO& io, const CertSmem& cs, uint32_t c,
+                                                uint32_t b, const uint32_t* __restrict__ sb,
+                                                double (&Bs)[kJ]) {
+  const uint32_t kb = 1 + c * kChunk;
+  const uint32_t ke = min(kb + kChunk - 1, io.L - 1);
+  const int32_t* rec = cs.rec + (size_t)b * kChunk;
+  const uint32_t L = io.L, alpha = io.alpha;
+#pragma unroll 1
+  for (int band = 0; band < 2; ++band) {
+    const uint32_t blo = max(kb, (band ? io.M_lo : io.m_lo) + 1);
+    const uint32_t bhi = min(ke, band ? io.M_hi : io.m_hi);
+    if (blo > bhi) continue;
+#pragma unroll
+    for (int m = 0; m < kJ; ++m) {
+      const uint32_t rho = 4 * threadIdx.x + m;
+      if (rho >= io.n) continue;
+      const uint32_t j = io.j0 + rho;
+      const uint32_t sjb = (sb[(j >> 5) + 1] >> (j & 31)) & 1u;
+      double s = Bs[m];
+#pragma unroll 1
+      for (uint32_t k0 = blo; k0 <= bhi; k0 += 32) {
+        // bit q: s_{j+k0+q} and s_{j-k0-q} (1 <-> -1; zero pads beyond the ends)
+        const long long pB = (long long)j + k0, pA = (long long)j - k0 - 31;
+        const long long wB = pB >> 5, wA = pA >> 5;
+        const uint32_t Bw = __funnelshift_r(sb[wB + 1], sb[wB + 2], (uint32_t)(pB & 31));
+        const uint32_t Aw = __brev(__funnelshift_r(sb[wA + 1], sb[wA + 2], (uint32_t)(pA & 31)));
+        const uint32_t nq = min(32u, bhi - k0 + 1);
+        for (uint32_t q = 0; q < nq; ++q) {
+          const uint32_t k = k0 + q;
+          const int u = ((Bw >> q) & 1u) == sjb ? 1 : -1;
+          const int v = ((Aw >> q) & 1u) == sjb ? 1 : -1;
+          const int x = (k <= j ? v : 0) + (j + k < L ? u : 0);
+          s = __dadd_rn(s, pow_int_dev((double)abs(rec[k - kb] - 2 * x), alpha));
+        }
+      }
+      Bs[m] = s;
+    }
+  }
+}
+
+// gamma_n = n u / (1 - n u), u = 2^-53 (Higham)
+__device__ __forceinline__ double gamma_n(double n) {
+  const double u = 0x1p-53;
+  return n * u / (1.0 - n * u);
+}

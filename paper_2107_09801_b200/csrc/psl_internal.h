@@ -47,6 +47,12 @@ struct WalkState {
   uint32_t done;        // stop condition reached
   uint32_t trace_patch; // 1: last trace waits for value_local
   uint32_t switch_pending;  // 1: last event is a provisional phase-switch
+  uint32_t vl_exact;    // value_local is the serial double (else only [vl_lo, vl_hi] is known,
+                        // and the exact value is fitness() of the local snapshot table)
+  double vl_lo, vl_hi;
+  uint64_t n_cert;      // steps decided by the certified scan alone
+  uint64_t n_refine;    // certified steps that needed the exact sweep
+  uint64_t n_vlchain;   // exact value_local chains over the local snapshot
 };
 
 struct RunArgs {
@@ -57,6 +63,7 @@ struct RunArgs {
   double max_seconds;
   uint32_t step_budget;
   int32_t record_events, record_traces;
+  int32_t cert;         // certified scan allowed (decision-exact; never with traces)
   uint64_t events_cap, traces_cap;
   WalkState* st;
   int32_t* Cpiv;

@@ -155,12 +155,22 @@ struct Ctl {
   uint32_t hcount, hf_count, steps_this_launch;
   int32_t P_new;
   long long energy;
+  // certified scan (psl_cert.cuh)
+  int32_t cert, need_exact, need_vl, cmp, cv_exact, c_q;
+  double cv_lo, cv_hi;
+  double c_scale, c_unit, c_sconst, c_errconst;
+  uint32_t m_lo, m_hi, M_lo, M_hi;
+  double rs5[5][8];
 };
 
 constexpr size_t kTabBytes = 2ull * kChunk * kRecDoubles * sizeof(double);
 constexpr size_t kTailBytes = 2ull * kChunk * sizeof(double);
 constexpr size_t kHfBytes = (size_t)kHCap * sizeof(int2);
 constexpr size_t kCtlBytes = (sizeof(Ctl) + 15) & ~size_t(15);
+// the exact sweep's records and the certified scan's buffers share one region
+// (psl_cert.cuh: 4 digit rows + 4 window copies + 2 record buffers)
+constexpr size_t kCertRegion = 4ull * 8 * (kChunk + 16) + 4ull * 4 * 1568 + 2ull * kChunk * 4 + 8ull * kGroup;
+constexpr size_t kMainBytes = (kTabBytes + kTailBytes) > kCertRegion ? (kTabBytes + kTailBytes) : kCertRegion;
 
 struct Smem {
   double* tab;     // [2][kChunk][8]
@@ -175,8 +185,8 @@ __device__ __forceinline__ Smem carve(unsigned char* base) {
   Smem m;
   m.tab = reinterpret_cast<double*>(base);
   m.tail = reinterpret_cast<double*>(base + kTabBytes);
-  m.hf = reinterpret_cast<int2*>(base + kTabBytes + kTailBytes);
-  m.ctl = reinterpret_cast<Ctl*>(base + kTabBytes + kTailBytes + kHfBytes);
+  m.hf = reinterpret_cast<int2*>(base + kMainBytes);
+  m.ctl = reinterpret_cast<Ctl*>(base + kMainBytes + kHfBytes);
   m.sb = nullptr;
   return m;
 }
@@ -764,7 +774,94 @@ __global__ void __launch_bounds__(256) build_tables_kernel(const uint32_t* bits,
   }
 }
 
+#include "psl_cert.cuh"
+static_assert(kCertBytes <= kMainBytes, "certified buffers exceed the shared region");
+
+// Neighbour PSL + thread-local reduce_scan over this thread's kJ neighbours
+// (ascending offset) + the block-wide lexicographic minima (ctl->best_*).
+__device__ __forceinline__ void reduce_group(Ctl* ctl, const Smem& sm, const int2* hlist,
+                                             const bool (&active)[kJ], const uint32_t (&jj)[kJ],
+                                             const double (&val)[kJ], uint32_t ibase, uint32_t L) {
+  const uint32_t nf = ctl->hf_count;
+  double bv = __longlong_as_double(0x7ff0000000000000ll);
+  uint32_t bi = 0xffffffffu, bpi = 0xffffffffu;
+  int32_t bp = 0x7fffffff;
+  int bad = 0;
+#pragma unroll
+  for (int m = 0; m < kJ; ++m) {
+    if (!active[m]) continue;
+    const uint32_t i = ibase + m + 1;
+    const int32_t psl = nf <= (uint32_t)kHCap
+        ? neighbour_psl(sm.hf, nf, 0, true, jj[m], L, sm.sb)
+        : neighbour_psl(hlist, ctl->hcount, ctl->P_new - 8, false, jj[m], L, sm.sb);
+    bad |= !isfinite(val[m]);
+    if (bi == 0xffffffffu || val[m] < bv) { bv = val[m]; bi = i; }
+    if (psl < bp) { bp = psl; bpi = i; }
+  }
+  block_reduce_scan(ctl, bv, bi, bp, bpi, bad);
+}
+
+// First-pass bookkeeping shared by the exact and certified passes: the new
+// pivot PSL, consumed pending flips, the restart fitness chain.
+__device__ __forceinline__ void first_pass_state(Ctl* ctl, const RunArgs& a, uint32_t w,
+                                                 int32_t Pn, double chain, uint32_t alpha) {
+  WalkState& S = ctl->st;
+  ctl->P_new = Pn;
+  S.P = Pn;
+  if (S.local_pending) { S.P_local = Pn; S.local_pending = 0; }
+  S.n_pending = 0;
+  S.src_local = 0;
+  if (S.fitness_pending) {
+    S.fitness_pending = 0;
+    if (!isfinite(chain)) {
+      // fitness() throws OverflowError (sequence.cpp:139); a provisional
+      // phase-switch event / trace from the restart step is withdrawn.
+      S.status = PSL_ERR_OVERFLOW; S.err_kind = 1; S.err_alpha = alpha;
+      if (S.switch_pending && S.n_events) --S.n_events;
+      if (S.trace_patch && S.n_traces) --S.n_traces;
+    } else {
+      S.value_local = chain;
+      S.vl_exact = 1; S.vl_lo = chain; S.vl_hi = chain;
+      if (S.trace_patch) {
+        a.traces[(size_t)w * a.traces_cap + S.n_traces - 1].value_local = chain;
+      }
+    }
+    S.trace_patch = 0;
+    S.switch_pending = 0;
+  }
+  ctl->hf_count = 0;
+}
+
+// Filter the pass's high-sidelobe list into smem (entries that can still
+// carry a neighbour's peak: |C_k| >= P - 8).
+__device__ __forceinline__ void filter_hlist(Ctl* ctl, const Smem& sm, const int2* hlist) {
+  const int32_t thr = ctl->P_new - 8;
+  const uint32_t hc = ctl->hcount;
+  for (uint32_t e = threadIdx.x; e < hc; e += kThreads) {
+    const int2 kc = hlist[e];
+    if (abs(kc.y) >= thr) {
+      const uint32_t slot = atomicAdd(&ctl->hf_count, 1u);
+      if (slot < (uint32_t)kHCap) sm.hf[slot] = kc;
+    }
+  }
+}
+
+// value_step vs value_local: -1 less, 0 equal, +1 greater, 2 undecided
+__device__ __forceinline__ int compare_local(const WalkState& S, double lo, double hi, bool exact,
+                                             double v) {
+  if (exact && S.vl_exact) return v < S.value_local ? -1 : (v > S.value_local ? 1 : 0);
+  const double vlo = S.vl_exact ? S.value_local : S.vl_lo;
+  const double vhi = S.vl_exact ? S.value_local : S.vl_hi;
+  if (hi < vlo) return -1;
+  if (lo > vhi) return 1;
+  return 2;
+}
+
 // The device-resident run_search loop (search.cpp:327-430), one CTA per walk.
+// kCert: steps may be decided by the certified scan (psl_cert.cuh); any step
+// it cannot decide is re-scored by the exact sweep, so every decision (and
+// the RunRecord) is the reference's.
+template <bool kCert>
 __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   Smem sm = carve(smem_raw);
@@ -808,6 +905,31 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
       if (ctl->do_scan) ctl->start = (uint32_t)rng_bounded(S.rng, L);  // search.cpp:375
       ctl->hcount = 0;
       ctl->fit = 0.0;
+      ctl->cert = 0;
+      ctl->need_exact = 0;
+      ctl->need_vl = 0;
+      if (kCert && a.cert && ctl->do_scan && !S.fitness_pending && a.n <= (uint32_t)kGroup &&
+          L >= kCertMinL && ctl->start + a.n < L) {
+        // fixed-point scale: every |H4|, |R4| <= 2 pow(Amax, alpha) < 2^(62+q)
+        const uint32_t alpha = S.phase == 1 ? a.alpha1 : a.alpha2;
+        const int32_t Psrc = S.src_local ? S.P_local : S.P;
+        const double amax = (double)Psrc + 4.0 * S.n_pending + 4.0;
+        const double fa = pow_int_dev(amax, alpha);
+        if (isfinite(fa) && fa * 8.0 * (double)L < 1e300) {
+          const int q = fa > 0.0 ? max(0, ilogb(2.0 * fa) - 61) : 0;
+          ctl->c_scale = ldexp(1.0, -q);
+          ctl->c_unit = ldexp(1.0, q);
+          ctl->c_q = q;
+          const uint32_t j0 = ctl->start + 1, jl = ctl->start + a.n;   // active rows
+          const uint32_t h = (L - 1) / 2;
+          const uint32_t m0 = min(j0, L - 1 - j0), m1 = min(jl, L - 1 - jl);
+          ctl->m_lo = min(m0, m1);
+          ctl->m_hi = (j0 <= L - 1 - h && jl >= h) ? h : max(m0, m1);
+          ctl->M_lo = L - 1 - ctl->m_hi;
+          ctl->M_hi = L - 1 - ctl->m_lo;
+          ctl->cert = 1;
+        }
+      }
     }
     __syncthreads();
     if (!ctl->need_pass) break;
@@ -819,115 +941,258 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
     const uint32_t s_n_pending = ctl->st.n_pending, s_fitness_pending = ctl->st.fitness_pending;
     const int32_t s_Psrc = s_src_local ? ctl->st.P_local : ctl->st.P;
 
-    for (uint32_t g = 0; g < ngroups; ++g) {
-      // this thread's kJ adjacent neighbours: offsets i = base + 1 .. base + kJ
-      const uint32_t ibase = g * kGroup + (t >> 5) * (32 * kJ) + (t & 31) * kJ;
-      bool active[kJ];
-      uint32_t jj[kJ];
+    if (kCert && ctl->cert) {
+      // ================= certified pass (psl_cert.cuh)
+      CertIO io;
+      io.L = L; io.n = a.n; io.nchunks = a.nchunks; io.j0 = start + 1;
+      io.Csrc = s_src_local ? Cloc : Cpiv;
+      io.Cdst = Cpiv;
+      io.Cloc = s_local_pending ? Cloc : nullptr;
+      io.flips = flips; io.F = s_n_pending;
+      io.alpha = alpha;
+      io.hlist = hlist; io.hcount = &ctl->hcount;
+      io.hthr = s_Psrc - 4 * (int32_t)s_n_pending - 8;
+      io.scale = ctl->c_scale;
+      io.m_lo = ctl->m_lo; io.m_hi = ctl->m_hi; io.M_lo = ctl->M_lo; io.M_hi = ctl->M_hi;
+      const CertSmem cs = cert_carve(smem_raw);
+      int accL[kCertTiles][4], accX[kCertTiles][4];
 #pragma unroll
-      for (int m = 0; m < kJ; ++m) {
-        const uint32_t i = ibase + m + 1;
-        active[m] = do_scan && i <= a.n;
-        uint32_t j = 0;
-        if (active[m]) { j = start + i; if (j >= L) j -= L; }
-        jj[m] = j;
-      }
-      SweepIO io;
-      io.L = L; io.nwords = nw; io.nchunks = a.nchunks;
-      io.alpha = alpha; io.lut = nullptr; io.lut_size = 0;
-      io.scan = do_scan;
-      io.hcount = &ctl->hcount;
-      if (g == 0) {
-        io.Csrc = s_src_local ? Cloc : Cpiv;
-        io.Cdst = Cpiv;
-        io.Cloc = s_local_pending ? Cloc : nullptr;
-        io.flips = flips; io.F = s_n_pending;
-        io.hlist = hlist;
-        io.hthr = s_Psrc - 4 * (int32_t)s_n_pending - 8;
-        io.chain = s_fitness_pending != 0;
-      } else {
-        io.Csrc = Cpiv; io.Cdst = nullptr; io.Cloc = nullptr;
-        io.flips = flips; io.F = 0; io.hlist = nullptr; io.hthr = 0; io.chain = false;
-      }
+      for (int r = 0; r < kCertTiles; ++r)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) { accL[r][e] = 0; accX[r][e] = 0; }
+      double part[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+      double Bs[kJ] = {0.0, 0.0, 0.0, 0.0};
       int32_t pmax = 0;
-      double chain = 0.0;
-      double val[kJ];
-      sweep(io, sm, active, jj, val, pmax, chain);
-      if (g == 0) {
-        const int32_t Pn = block_max(ctl, pmax);
-        if (t == 0) {
-          WalkState& S = ctl->st;
-          ctl->P_new = Pn;
-          S.P = Pn;
-          if (S.local_pending) { S.P_local = Pn; S.local_pending = 0; }
-          S.n_pending = 0;
-          S.src_local = 0;
-          if (S.fitness_pending) {
-            S.fitness_pending = 0;
-            if (!isfinite(chain)) {
-              // fitness() throws OverflowError (sequence.cpp:139); a provisional
-              // phase-switch event / trace from the restart step is withdrawn.
-              S.status = PSL_ERR_OVERFLOW; S.err_kind = 1; S.err_alpha = alpha;
-              if (S.switch_pending && S.n_events) --S.n_events;
-              if (S.trace_patch && S.n_traces) --S.n_traces;
-            } else {
-              S.value_local = chain;
-              if (S.trace_patch) {
-                a.traces[(size_t)w * a.traces_cap + S.n_traces - 1].value_local = chain;
-              }
-            }
-            S.trace_patch = 0;
-            S.switch_pending = 0;
-          }
-          // filter the high-sidelobe list into smem
-          ctl->hf_count = 0;
-        }
-        __syncthreads();
-        if (ctl->st.status != PSL_OK) break;
-        const int32_t thr = ctl->P_new - 8;
-        const uint32_t hc = ctl->hcount;
-        for (uint32_t e = t; e < hc; e += kThreads) {
-          const int2 kc = hlist[e];
-          if (abs(kc.y) >= thr) {
-            const uint32_t slot = atomicAdd(&ctl->hf_count, 1u);
-            if (slot < (uint32_t)kHCap) sm.hf[slot] = kc;
-          }
-        }
+      const CertLane ln = cert_lane(cs);
+      cert_build(io, cs, 0, 0, sm.sb, pmax, part);
+      __syncthreads();
+      uint32_t c = 0;
+      // phase 1: chunks holding k <= m_lo (both sides for every row: cross term)
+      for (; c < io.nchunks && 1 + c * kChunk <= io.m_lo; ++c) {
+        const uint32_t b = c & 1;
+        if (c + 1 < io.nchunks) cert_build(io, cs, c + 1, b ^ 1, sm.sb, pmax, part);
+        cert_mma_chunk<true>(io, ln, c, b, accL, accX);
+        if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, b, sm.sb, Bs);
         __syncthreads();
       }
-      if (!do_scan) break;
-      const uint32_t nf = ctl->hf_count;
-      // thread-local reduce_scan over its kJ neighbours (ascending offset)
-      double bv = __longlong_as_double(0x7ff0000000000000ll);
-      uint32_t bi = 0xffffffffu, bpi = 0xffffffffu;
-      int32_t bp = 0x7fffffff;
-      int bad = 0;
+      cert_rows(accX, ctl->c_unit, cs.xrow);   // the cross term is complete
+      for (; c < io.nchunks; ++c) {
+        const uint32_t b = c & 1;
+        if (c + 1 < io.nchunks) cert_build(io, cs, c + 1, b ^ 1, sm.sb, pmax, part);
+        cert_mma_chunk<false>(io, ln, c, b, accL, accX);
+        if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, b, sm.sb, Bs);
+        __syncthreads();
+      }
+      const int32_t Pn = block_max(ctl, pmax);
+      // window constants: warp sums, then a fixed-order sum over warps
+      {
+        const int lane = t & 31, warp = t >> 5;
 #pragma unroll
-      for (int m = 0; m < kJ; ++m) {
-        if (!active[m]) continue;
-        const uint32_t i = ibase + m + 1;
-        const int32_t psl = nf <= (uint32_t)kHCap
-            ? neighbour_psl(sm.hf, nf, 0, true, jj[m], L, sm.sb)
-            : neighbour_psl(hlist, ctl->hcount, ctl->P_new - 8, false, jj[m], L, sm.sb);
-        bad |= !isfinite(val[m]);
-        if (bi == 0xffffffffu || val[m] < bv) { bv = val[m]; bi = i; }
-        if (psl < bp) { bp = psl; bpi = i; }
+        for (int i = 0; i < 5; ++i) {
+          double v = part[i];
+          for (int o = 16; o; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, o));
+          if (lane == 0) ctl->rs5[i][warp] = v;
+        }
       }
-      block_reduce_scan(ctl, bv, bi, bp, bpi, bad);
+      double* linrow = reinterpret_cast<double*>(cs.winF);   // [1024]
+      const double* xrow = cs.xrow;
+      cert_rows(accL, ctl->c_unit, linrow);
+      if (t == 0) first_pass_state(ctl, a, w, Pn, 0.0, alpha);
+      __syncthreads();
       if (t == 0) {
-        // combine groups in ascending offset order (strict <: smallest offset wins)
-        if (g == 0) {
+        double sm5[5];
+        for (int i = 0; i < 5; ++i) {
+          double v = 0.0;
+          for (int x = 0; x < kThreads / 32; ++x) v = __dadd_rn(v, ctl->rs5[i][x]);
+          sm5[i] = v;
+        }
+        const double u = 0x1p-53;
+        const double Sc = __dadd_rn(__dadd_rn(sm5[0], sm5[1]), sm5[2]);
+        ctl->c_sconst = Sc;
+        ctl->c_errconst = 2.0 * gamma_n((double)L / 256.0 + 80.0) * Sc + 8.0 * u * sm5[0] +
+                          64.0 * u * (sm5[3] + sm5[4]) +
+                          (ctl->c_q > 0 ? ((double)L + (double)ctl->m_lo) * ctl->c_unit : 0.0) +
+                          1024.0 * u * (double)L * ctl->c_unit;
+      }
+      filter_hlist(ctl, sm, hlist);
+      __syncthreads();
+      // per-row intervals [lo, hi] that provably hold the serial double V(j)
+      {
+        const double u = 0x1p-53;
+        const double gL = gamma_n((double)L), gB = gamma_n(2100.0), g8 = gamma_n(8.0);
+        const double Sc = ctl->c_sconst, E0 = ctl->c_errconst;
+        bool active[kJ];
+        uint32_t jj[kJ];
+        double mid[kJ], lo[kJ], hi[kJ];
+        const uint32_t ibase = kJ * t;
+#pragma unroll
+        for (int m = 0; m < kJ; ++m) {
+          const uint32_t rho = kJ * t + m;
+          active[m] = rho < a.n;
+          jj[m] = start + 1 + rho;
+          const double lin = linrow[rho], xv = xrow[rho];
+          const double B4 = __dmul_rn(4.0, Bs[m]);
+          const int sj = active[m] ? sval(sm.sb, jj[m]) : 1;
+          const double T4 = __dadd_rn(__dadd_rn(__dadd_rn(Sc, B4), sj > 0 ? lin : -lin), xv);
+          const double Abs = Sc + B4 + fabs(lin) + fabs(xv);
+          const double Err = E0 + 2.0 * gB * B4 + 2.0 * g8 * Abs + u * (fabs(lin) + fabs(xv));
+          mid[m] = 0.25 * T4;
+          lo[m] = fmax(0.0, 0.25 * (T4 - Err)) * (1.0 - gL) * (1.0 - 8.0 * u);
+          hi[m] = 0.25 * (T4 + Err) * (1.0 + gL) * (1.0 + 8.0 * u);
+          if (!isfinite(hi[m])) mid[m] = __longlong_as_double(0x7ff8000000000000ll);   // -> bad
+        }
+        reduce_group(ctl, sm, hlist, active, jj, mid, ibase, L);
+        const uint32_t bi = ctl->best_i;
+#pragma unroll
+        for (int m = 0; m < kJ; ++m)
+          if (active[m] && ibase + m + 1 == bi) { ctl->cv_lo = lo[m]; ctl->cv_hi = hi[m]; }
+        __syncthreads();
+        const double hs = ctl->cv_hi;
+        int amb = 0;
+#pragma unroll
+        for (int m = 0; m < kJ; ++m) amb |= active[m] && ibase + m + 1 != bi && lo[m] <= hs;
+        amb = __syncthreads_or(amb);
+        if (t == 0) {
           ctl->cv = ctl->best_v; ctl->ci = ctl->best_i;
           ctl->cp = ctl->best_psl; ctl->cpi = ctl->best_pi; ctl->cbad = ctl->bad;
-        } else {
-          if (ctl->best_v < ctl->cv) { ctl->cv = ctl->best_v; ctl->ci = ctl->best_i; }
-          if (ctl->best_psl < ctl->cp) { ctl->cp = ctl->best_psl; ctl->cpi = ctl->best_pi; }
-          ctl->cbad |= ctl->bad;
+          ctl->cv_exact = 0;
+          const WalkState& S = ctl->st;
+          int need = amb || ctl->bad;
+          if (!need) {
+            ctl->cmp = compare_local(S, ctl->cv_lo, ctl->cv_hi, false, ctl->cv);
+            need = ctl->cmp == 2;
+          }
+          ctl->need_exact = need;
+          ctl->st.n_cert += need ? 0 : 1;
+          ctl->st.n_refine += need ? 1 : 0;
         }
+        __syncthreads();
+      }
+      if (ctl->need_exact) {
+        // exact re-score of the same pivot (flips already folded into Cpiv)
+        const uint32_t ibase = (t >> 5) * (32 * kJ) + (t & 31) * kJ;
+        bool active[kJ];
+        uint32_t jj[kJ];
+#pragma unroll
+        for (int m = 0; m < kJ; ++m) {
+          const uint32_t i = ibase + m + 1;
+          active[m] = i <= a.n;
+          uint32_t j = 0;
+          if (active[m]) { j = start + i; if (j >= L) j -= L; }
+          jj[m] = j;
+        }
+        SweepIO sio;
+        sio.L = L; sio.nwords = nw; sio.nchunks = a.nchunks;
+        sio.alpha = alpha; sio.lut = nullptr; sio.lut_size = 0;
+        sio.scan = true; sio.hcount = &ctl->hcount;
+        sio.Csrc = Cpiv; sio.Cdst = nullptr; sio.Cloc = nullptr;
+        sio.flips = flips; sio.F = 0; sio.hlist = nullptr; sio.hthr = 0; sio.chain = false;
+        int32_t pm = 0;
+        double chain = 0.0;
+        double val[kJ];
+        sweep(sio, sm, active, jj, val, pm, chain);
+        reduce_group(ctl, sm, hlist, active, jj, val, ibase, L);
+        if (t == 0) {
+          ctl->cv = ctl->best_v; ctl->ci = ctl->best_i;
+          ctl->cp = ctl->best_psl; ctl->cpi = ctl->best_pi; ctl->cbad = ctl->bad;
+          ctl->cv_exact = 1; ctl->cv_lo = ctl->cv; ctl->cv_hi = ctl->cv;
+          ctl->cmp = compare_local(ctl->st, ctl->cv, ctl->cv, true, ctl->cv);
+          ctl->need_vl = !ctl->cbad && ctl->cmp == 2;
+        }
+        __syncthreads();
+      }
+    } else {
+      // ================= exact pass(es)
+      for (uint32_t g = 0; g < ngroups; ++g) {
+        // this thread's kJ adjacent neighbours: offsets i = base + 1 .. base + kJ
+        const uint32_t ibase = g * kGroup + (t >> 5) * (32 * kJ) + (t & 31) * kJ;
+        bool active[kJ];
+        uint32_t jj[kJ];
+#pragma unroll
+        for (int m = 0; m < kJ; ++m) {
+          const uint32_t i = ibase + m + 1;
+          active[m] = do_scan && i <= a.n;
+          uint32_t j = 0;
+          if (active[m]) { j = start + i; if (j >= L) j -= L; }
+          jj[m] = j;
+        }
+        SweepIO io;
+        io.L = L; io.nwords = nw; io.nchunks = a.nchunks;
+        io.alpha = alpha; io.lut = nullptr; io.lut_size = 0;
+        io.scan = do_scan;
+        io.hcount = &ctl->hcount;
+        if (g == 0) {
+          io.Csrc = s_src_local ? Cloc : Cpiv;
+          io.Cdst = Cpiv;
+          io.Cloc = s_local_pending ? Cloc : nullptr;
+          io.flips = flips; io.F = s_n_pending;
+          io.hlist = hlist;
+          io.hthr = s_Psrc - 4 * (int32_t)s_n_pending - 8;
+          io.chain = s_fitness_pending != 0;
+        } else {
+          io.Csrc = Cpiv; io.Cdst = nullptr; io.Cloc = nullptr;
+          io.flips = flips; io.F = 0; io.hlist = nullptr; io.hthr = 0; io.chain = false;
+        }
+        int32_t pmax = 0;
+        double chain = 0.0;
+        double val[kJ];
+        sweep(io, sm, active, jj, val, pmax, chain);
+        if (g == 0) {
+          const int32_t Pn = block_max(ctl, pmax);
+          if (t == 0) first_pass_state(ctl, a, w, Pn, chain, alpha);
+          __syncthreads();
+          if (ctl->st.status != PSL_OK) break;
+          filter_hlist(ctl, sm, hlist);
+          __syncthreads();
+        }
+        if (!do_scan) break;
+        reduce_group(ctl, sm, hlist, active, jj, val, ibase, L);
+        if (t == 0) {
+          // combine groups in ascending offset order (strict <: smallest offset wins)
+          if (g == 0) {
+            ctl->cv = ctl->best_v; ctl->ci = ctl->best_i;
+            ctl->cp = ctl->best_psl; ctl->cpi = ctl->best_pi; ctl->cbad = ctl->bad;
+          } else {
+            if (ctl->best_v < ctl->cv) { ctl->cv = ctl->best_v; ctl->ci = ctl->best_i; }
+            if (ctl->best_psl < ctl->cp) { ctl->cp = ctl->best_psl; ctl->cpi = ctl->best_pi; }
+            ctl->cbad |= ctl->bad;
+          }
+        }
+        __syncthreads();
+      }
+      if (t == 0 && do_scan && ctl->st.status == PSL_OK) {
+        ctl->cv_exact = 1; ctl->cv_lo = ctl->cv; ctl->cv_hi = ctl->cv;
+        ctl->cmp = compare_local(ctl->st, ctl->cv, ctl->cv, true, ctl->cv);
+        ctl->need_vl = !ctl->cbad && ctl->cmp == 2;
       }
       __syncthreads();
     }
     if (ctl->st.status != PSL_OK || !do_scan) break;
+
+    if (ctl->need_vl) {
+      // value_local is only known as an interval: its exact value is the serial
+      // fitness of the local snapshot table (the argmin neighbour's chain is
+      // fitness() of the moved table, term for term)
+      const bool none[kJ] = {false, false, false, false};
+      const uint32_t zj[kJ] = {0, 0, 0, 0};
+      SweepIO sio;
+      sio.L = L; sio.nwords = nw; sio.nchunks = a.nchunks;
+      sio.alpha = alpha; sio.lut = nullptr; sio.lut_size = 0;
+      sio.scan = false; sio.hcount = &ctl->hcount;
+      sio.Csrc = Cloc; sio.Cdst = nullptr; sio.Cloc = nullptr;
+      sio.flips = flips; sio.F = 0; sio.hlist = nullptr; sio.hthr = 0; sio.chain = true;
+      int32_t pm = 0;
+      double chain = 0.0;
+      double val[kJ];
+      sweep(sio, sm, none, zj, val, pm, chain);
+      if (t == 0) {
+        WalkState& S = ctl->st;
+        S.value_local = chain; S.vl_exact = 1; S.vl_lo = chain; S.vl_hi = chain;
+        S.n_vlchain += 1;
+        ctl->cmp = compare_local(S, ctl->cv, ctl->cv, true, ctl->cv);
+      }
+      __syncthreads();
+    }
 
     // ---- reduce_scan result + Algorithm 1 control (search.cpp:379-419)
     if (t == 0) {
@@ -958,12 +1223,13 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
           ctl->imp = 1;
           emit(PSL_EVENT_IMPROVED_PSL);
         }
-        if (value_step < S.value_local) {                      // :394-399
+        if (ctl->cmp < 0) {                                    // :394-399
           S.value_local = value_step;
+          S.vl_exact = ctl->cv_exact; S.vl_lo = ctl->cv_lo; S.vl_hi = ctl->cv_hi;
           S.unimproved = 0;
           ctl->improve = 1;
           emit(PSL_EVENT_LOCAL_BEST_IMPROVED);
-        } else if (value_step > S.value_local) {               // :400-413
+        } else if (ctl->cmp > 0) {                             // :400-413
           if (++S.unimproved > a.ls_lmt) {
             ctl->restart = 1;
             S.phase = (S.phase == 1) ? 2u : 1u;
@@ -1104,7 +1370,7 @@ __global__ void flip_bit_kernel(uint32_t* bits, uint32_t j) { bits[j >> 5] ^= 1u
 
 }  // namespace
 
-size_t run_smem_bytes(uint32_t) { return kTabBytes + kTailBytes + kHfBytes + kCtlBytes; }
+size_t run_smem_bytes(uint32_t) { return kMainBytes + kHfBytes + kCtlBytes; }
 
 int launch_init_walks(const RunArgs& a, uint32_t n_walks, const uint64_t* d_seeds,
                       const int8_t* d_inits, uint32_t* d_bad, cudaStream_t s) {
@@ -1132,12 +1398,15 @@ int launch_run(const RunArgs& a, uint32_t n_walks, cudaStream_t s) {
   const size_t smem = run_smem_bytes(a.nwords);
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(run_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(run_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)run_smem_bytes((1u << 20) / 32 + 1)) != cudaSuccess ||
+        cudaFuncSetAttribute(run_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)run_smem_bytes((1u << 20) / 32 + 1)) != cudaSuccess)
       return -1;
     attr = true;
   }
-  run_kernel<<<n_walks, kThreads, smem, s>>>(a);
+  if (a.cert) run_kernel<true><<<n_walks, kThreads, smem, s>>>(a);
+  else run_kernel<false><<<n_walks, kThreads, smem, s>>>(a);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 

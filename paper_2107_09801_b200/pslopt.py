@@ -90,6 +90,24 @@ class Context:
     def kernel_launches(self) -> int:
         return B.lib().psl_kernel_launches(self._h)
 
+    SCAN_AUTO, SCAN_EXACT = 0, 1
+
+    def set_scan_mode(self, mode: int) -> None:
+        """SCAN_AUTO: certified tensor-core scan where it decides the step,
+        exact sweep otherwise (identical results); SCAN_EXACT: exact sweep only."""
+        if B.lib().psl_ctx_set_scan_mode(self._h, int(mode)):
+            raise ConfigError(f"unknown scan mode {mode}")
+
+    def scan_mode(self) -> int:
+        return B.lib().psl_ctx_scan_mode(self._h)
+
+    def scan_stats(self) -> dict:
+        """Totals over records read on this context: certified steps, certified
+        steps re-scored by the exact sweep, exact value_local chains."""
+        a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        B.lib().psl_ctx_scan_stats(self._h, C.byref(a), C.byref(b), C.byref(c))
+        return {"certified": a.value, "refined": b.value, "chains": c.value}
+
     def close(self) -> None:
         if self._h:
             B.lib().psl_ctx_destroy(self._h)
