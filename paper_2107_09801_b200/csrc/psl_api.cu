@@ -50,6 +50,7 @@ struct psl_walks {
   int8_t* inits = nullptr;      // device copy of warm starts (int8 +-1)
   uint32_t* bad = nullptr;      // [first bad flat index + 1, value]
   int8_t* sol = nullptr;        // unpack scratch for solutions
+  double* lut = nullptr;        // [2][lut_n] power tables
 };
 
 namespace {
@@ -519,7 +520,7 @@ void psl_walks_destroy(psl_walks* w) {
   cudaStream_t s = w->ctx->stream;
   for (void* p : {(void*)w->st, (void*)w->Cpiv, (void*)w->Cloc, (void*)w->bits, (void*)w->hlist,
                   (void*)w->flips, (void*)w->events, (void*)w->traces, (void*)w->seeds,
-                  (void*)w->inits, (void*)w->bad, (void*)w->sol})
+                  (void*)w->inits, (void*)w->bad, (void*)w->sol, (void*)w->lut})
     if (p) cudaFreeAsync(p, s);
   delete w;
 }
@@ -581,6 +582,9 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
   AL(W->seeds, 8ull * n_walks);
   if (events_cap) AL(W->events, sizeof(psl_event) * events_cap * n_walks);
   if (traces_cap) AL(W->traces, sizeof(psl_trace) * traces_cap * n_walks);
+  a.lut_n = L + 8;
+  AL(W->lut, 2ull * a.lut_n * sizeof(double));
+  a.lut1 = W->lut; a.lut2 = W->lut + a.lut_n;
   a.st = W->st; a.Cpiv = W->Cpiv; a.Cloc = W->Cloc;
   a.bits_piv = W->bits;
   a.bits_loc = W->bits + a.w_stride * n_walks;
@@ -610,6 +614,9 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
 #undef AL
   if (launch_init_walks(a, n_walks, W->seeds, W->inits, W->bad, s) < 0)
     return fail(cudaGetLastError(), "init_walks_kernel");
+  if (launch_power_tables(W->lut, a.lut_n, p.alpha1, p.alpha2, s) < 0)
+    return fail(cudaGetLastError(), "power_tables_kernel");
+  ctx->launches += 1;
   // SidelobeTable::build: exact NTT correlation for long sequences (O(L log L)),
   // bit-parallel popcount kernel (O(L^2/32)) for short ones
   const int nb = L >= 8192 ? launch_build_tables_ntt(a, n_walks, s) : launch_build_tables(a, n_walks, s);

@@ -49,6 +49,7 @@ struct CertIO {
   const uint32_t* flips;
   uint32_t F;
   uint32_t alpha;
+  const double* lut;                          // PowerTable of the phase (covers |C_k| + 4)
   int2* hlist;
   uint32_t* hcount;
   int32_t hthr;
@@ -126,11 +127,11 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
       const int32_t a = abs(cv);
       pmax = max(pmax, a);
       want = io.hlist != nullptr && a >= io.hthr;
-      e2 = pow_int_dev((double)a, io.alpha);
-      e4 = pow_int_dev((double)abs(cv - 4), io.alpha);
-      e3 = pow_int_dev((double)abs(cv - 2), io.alpha);
-      e1 = pow_int_dev((double)abs(cv + 2), io.alpha);
-      e0 = pow_int_dev((double)abs(cv + 4), io.alpha);
+      e2 = __ldg(io.lut + a);
+      e4 = __ldg(io.lut + abs(cv - 4));
+      e3 = __ldg(io.lut + abs(cv - 2));
+      e1 = __ldg(io.lut + abs(cv + 2));
+      e0 = __ldg(io.lut + abs(cv + 4));
     }
     if (io.hlist) {
       const uint32_t m = __ballot_sync(FULL, want);
@@ -175,25 +176,27 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
     *reinterpret_cast<uint16_t*>(lh + d * kLimbStride) = (uint16_t)h;
     *reinterpret_cast<uint16_t*>(lr + d * kLimbStride) = (uint16_t)r;
   }
-  // sequence windows: 2 directions x 4 copies x 392 words (only chunks with MMA work)
+  // sequence windows: 4 copies x 392 words per direction, only for chunks with
+  // MMA work and only the directions some row still has in range
   if (!cert_mma_work(io, kb)) return;
-  const uint32_t L = io.L;
-  for (uint32_t idx = t; idx < 2u * 4u * (kWinBytes / 4); idx += kThreads) {
-    const uint32_t dir = idx / (4 * (kWinBytes / 4));
-    const uint32_t rem = idx - dir * (4 * (kWinBytes / 4));
-    const uint32_t a = rem / (kWinBytes / 4), q = rem - a * (kWinBytes / 4);
+  const int L = (int)io.L, j0 = (int)io.j0;
+  const bool nf = j0 + (int)kb < L, nv = (int)kb <= j0 + kGroup - 1;
+  constexpr int kW = kWinBytes / 4;
+  const int total = (nf ? 4 * kW : 0) + (nv ? 4 * kW : 0);
+  for (int idx = (int)t; idx < total; idx += kThreads) {
+    const int dir = nf ? (idx >= 4 * kW ? 1 : 0) : 1;
+    const int rem = nf && dir ? idx - 4 * kW : idx;
+    const int a = rem / kW, q = rem - a * kW;
     // fwd: byte i <-> position p0 + i; rev: byte i <-> position p0 - i
-    const long long p0 = dir == 0 ? (long long)io.j0 + kb + a + 4ll * q
-                                  : (long long)io.j0 - kb + kY0 - a - 4ll * q;
-    const long long lo = dir == 0 ? p0 : p0 - 3, hi = dir == 0 ? p0 + 3 : p0;
+    const int p0 = dir == 0 ? j0 + (int)kb + a + 4 * q : j0 - (int)kb + kY0 - a - 4 * q;
+    const int lo = dir == 0 ? p0 : p0 - 3, hi = lo + 3;
     uint32_t val = 0;
-    if (hi >= 0 && lo < (long long)L) {
-      if (lo >= 0 && hi < (long long)L) {
-        const uint32_t w = (uint32_t)(lo >> 5), sh = (uint32_t)(lo & 31);
-        const uint32_t x = __funnelshift_r(sb[w + 1], sb[w + 2], sh) & 0xFu;
+    if (hi >= 0 && lo < L) {
+      if (lo >= 0 && hi < L) {
+        const uint32_t x = __funnelshift_r(sb[(lo >> 5) + 1], sb[(lo >> 5) + 2], (uint32_t)lo & 31) & 0xFu;
         val = nib_bytes(dir == 0 ? x : __brev(x) >> 28);
       } else {
-        for (int i = 0; i < 4; ++i) val |= sbyte(sb, dir == 0 ? p0 + i : p0 - i, L) << (8 * i);
+        for (int i = 0; i < 4; ++i) val |= sbyte(sb, dir == 0 ? p0 + i : p0 - i, io.L) << (8 * i);
       }
     }
     unsigned char* dst = (dir == 0 ? cs.winF : cs.winV) + (size_t)b * kWinBuf + a * kWinBytes + 4 * q;
@@ -296,11 +299,16 @@ __device__ __forceinline__ void cert_mma_chunk(const CertIO& io, const CertLane&
     const bool crs = kCross && k0 <= io.m_lo;
     return (fwd ? 1 : 0) | (rev ? 2 : 0) | (crs ? 4 : 0);
   };
-  int cc = 0;
-  while (cc < kCertCols) {
-    const int md = mode(cc);
-    int ce = cc + 1;
-    while (ce < kCertCols && mode(ce) == md) ++ce;
+  // runs of equal mode: lane l < 16 evaluates column l, run starts by ballot
+  const uint32_t lane = threadIdx.x & 31;
+  const int my = mode((int)(lane & 15));
+  const int prev = __shfl_up_sync(FULL, my, 1);
+  uint32_t starts = __ballot_sync(FULL, lane < 16 && (lane == 0 || my != prev));
+  while (starts) {
+    const int cc = __ffs(starts) - 1;
+    starts &= starts - 1;
+    const int ce = starts ? __ffs(starts) - 1 : kCertCols;
+    const int md = __shfl_sync(FULL, my, cc);
     const uint32_t f = ln.f + fo + 32 * cc, v = ln.v + fo + 32 * cc;
     const uint32_t bh = ln.bh + bo + 32 * cc, br = ln.br + bo + 32 * cc;
     const int n = ce - cc;
@@ -314,7 +322,6 @@ __device__ __forceinline__ void cert_mma_chunk(const CertIO& io, const CertLane&
       case 4: if (kCross) cert_cols<false, false, true>(f, v, bh, br, n, accL, accX); break;
       default: break;
     }
-    cc = ce;
   }
 }
 
@@ -343,7 +350,8 @@ __device__ __forceinline__ void cert_band_cells(const CertIO& io, const CertSmem
   const uint32_t kb = 1 + c * kChunk;
   const uint32_t ke = min(kb + kChunk - 1, io.L - 1);
   const int32_t* rec = cs.rec + (size_t)b * kChunk;
-  const uint32_t L = io.L, alpha = io.alpha;
+  const uint32_t L = io.L;
+  const double* __restrict__ lut = io.lut;
 #pragma unroll 1
   for (int band = 0; band < 2; ++band) {
     const uint32_t blo = max(kb, (band ? io.M_lo : io.m_lo) + 1);
@@ -369,7 +377,7 @@ __device__ __forceinline__ void cert_band_cells(const CertIO& io, const CertSmem
           const int u = ((Bw >> q) & 1u) == sjb ? 1 : -1;
           const int v = ((Aw >> q) & 1u) == sjb ? 1 : -1;
           const int x = (k <= j ? v : 0) + (j + k < L ? u : 0);
-          s = __dadd_rn(s, pow_int_dev((double)abs(rec[k - kb] - 2 * x), alpha));
+          s = __dadd_rn(s, __ldg(lut + abs(rec[k - kb] - 2 * x)));
         }
       }
       Bs[m] = s;

@@ -81,6 +81,9 @@ struct RunArgs {
   size_t f_stride;
   psl_event* events;
   psl_trace* traces;
+  const double* lut1;   // PowerTable(L, alpha1) / (L, alpha2) on the device (sequence.hpp:72-84)
+  const double* lut2;
+  uint32_t lut_n;       // entries per table (> max |C_k| + 4)
 };
 
 struct ScanArgs {
@@ -110,6 +113,8 @@ int launch_run(const RunArgs& a, uint32_t n_walks, cudaStream_t s);
 int launch_scan(const ScanArgs& a, cudaStream_t s);
 int launch_table_only(const uint32_t* d_bits, int32_t* d_C, uint32_t L, uint32_t nwords,
                       cudaStream_t s);
+int launch_power_tables(double* lut, uint32_t lut_n, uint32_t alpha1, uint32_t alpha2,
+                        cudaStream_t s);
 int launch_apply_flip(uint32_t* d_bits, int32_t* d_C, uint32_t L, uint32_t j, cudaStream_t s);
 int probe_peaks(int nsm, cudaStream_t s, double* dadd_cps, double* lds_cps, double* mhz);
 

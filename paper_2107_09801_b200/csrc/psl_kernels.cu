@@ -937,6 +937,7 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
     const uint32_t start = ctl->start;
     // the few walk-state fields the pass needs (not the whole struct: registers)
     const uint32_t alpha = ctl->st.phase == 1 ? a.alpha1 : a.alpha2;
+    const double* lut = ctl->st.phase == 1 ? a.lut1 : a.lut2;
     const uint32_t s_src_local = ctl->st.src_local, s_local_pending = ctl->st.local_pending;
     const uint32_t s_n_pending = ctl->st.n_pending, s_fitness_pending = ctl->st.fitness_pending;
     const int32_t s_Psrc = s_src_local ? ctl->st.P_local : ctl->st.P;
@@ -949,7 +950,7 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
       io.Cdst = Cpiv;
       io.Cloc = s_local_pending ? Cloc : nullptr;
       io.flips = flips; io.F = s_n_pending;
-      io.alpha = alpha;
+      io.alpha = alpha; io.lut = lut;
       io.hlist = hlist; io.hcount = &ctl->hcount;
       io.hthr = s_Psrc - 4 * (int32_t)s_n_pending - 8;
       io.scale = ctl->c_scale;
@@ -1083,7 +1084,7 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
         }
         SweepIO sio;
         sio.L = L; sio.nwords = nw; sio.nchunks = a.nchunks;
-        sio.alpha = alpha; sio.lut = nullptr; sio.lut_size = 0;
+        sio.alpha = alpha; sio.lut = lut; sio.lut_size = a.lut_n;
         sio.scan = true; sio.hcount = &ctl->hcount;
         sio.Csrc = Cpiv; sio.Cdst = nullptr; sio.Cloc = nullptr;
         sio.flips = flips; sio.F = 0; sio.hlist = nullptr; sio.hthr = 0; sio.chain = false;
@@ -1118,7 +1119,7 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
         }
         SweepIO io;
         io.L = L; io.nwords = nw; io.nchunks = a.nchunks;
-        io.alpha = alpha; io.lut = nullptr; io.lut_size = 0;
+        io.alpha = alpha; io.lut = lut; io.lut_size = a.lut_n;
         io.scan = do_scan;
         io.hcount = &ctl->hcount;
         if (g == 0) {
@@ -1177,7 +1178,7 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
       const uint32_t zj[kJ] = {0, 0, 0, 0};
       SweepIO sio;
       sio.L = L; sio.nwords = nw; sio.nchunks = a.nchunks;
-      sio.alpha = alpha; sio.lut = nullptr; sio.lut_size = 0;
+      sio.alpha = alpha; sio.lut = lut; sio.lut_size = a.lut_n;
       sio.scan = false; sio.hcount = &ctl->hcount;
       sio.Csrc = Cloc; sio.Cdst = nullptr; sio.Cloc = nullptr;
       sio.flips = flips; sio.F = 0; sio.hlist = nullptr; sio.hthr = 0; sio.chain = true;
@@ -1368,6 +1369,15 @@ __global__ void apply_flip_kernel(uint32_t* bits, int32_t* C, uint32_t L, uint32
 }
 __global__ void flip_bit_kernel(uint32_t* bits, uint32_t j) { bits[j >> 5] ^= 1u << (j & 31); }
 
+// PowerTable(L, alpha) for both phases (sequence.hpp:72-84): lut[a] = pow_int(a, alpha)
+__global__ void power_tables_kernel(double* lut, uint32_t n, uint32_t alpha1, uint32_t alpha2) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) {
+    lut[i] = pow_int_dev((double)i, alpha1);
+    lut[n + i] = pow_int_dev((double)i, alpha2);
+  }
+}
+
 }  // namespace
 
 size_t run_smem_bytes(uint32_t) { return kMainBytes + kHfBytes + kCtlBytes; }
@@ -1421,6 +1431,12 @@ int launch_scan(const ScanArgs& a, cudaStream_t s) {
   }
   const uint32_t groups = (a.n + kGroup - 1) / kGroup;
   scan_kernel<<<groups, kThreads, smem, s>>>(a);
+  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+}
+
+int launch_power_tables(double* lut, uint32_t lut_n, uint32_t alpha1, uint32_t alpha2,
+                        cudaStream_t s) {
+  power_tables_kernel<<<(lut_n + 255) / 256, 256, 0, s>>>(lut, lut_n, alpha1, alpha2);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
