@@ -48,6 +48,8 @@ struct CertIO {
   int32_t* Cloc;
   const uint32_t* flips;
   uint32_t F;
+  uint32_t f1;                                // flips[0] and s_{f1} (after) when F == 1
+  int sf1;
   uint32_t alpha;
   const double* lut;                          // PowerTable of the phase (covers |C_k| + 4)
   int2* hlist;
@@ -117,7 +119,12 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
     int32_t cv = 0;
     if (k < io.L) {
       cv = io.Csrc[k];
-      if (io.F) {
+      if (io.F == 1) {
+        // the common single move: C_k += 2 s_f (s_{f-k} + s_{f+k}), s_f after the flip
+        const uint32_t f = io.f1;
+        const int acc = (k <= f ? sval(sb, f - k) : 0) + (f + k < io.L ? sval(sb, f + k) : 0);
+        cv += 2 * io.sf1 * acc;
+      } else if (io.F) {
         SweepIO fio;
         fio.L = io.L; fio.flips = io.flips; fio.F = io.F;
         cv = fold_flips(cv, k, fio, sb);
@@ -157,8 +164,6 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
       } else {                                          // Z5: no side for any row
         part[2] = __dadd_rn(part[2], __dmul_rn(4.0, e2));
       }
-      part[3] = __dadd_rn(part[3], fabs(H));
-      part[4] = __dadd_rn(part[4], fabs(R));
     }
     // fixed point (|V| < 2^62) -> 8 balanced base-256 digits, as bytes
     const long long hv = __double2ll_rn(__dmul_rn(H, io.scale));
@@ -167,12 +172,18 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
     VR[i] = ((unsigned long long)rv + 0x8080808080808080ull) ^ 0x8080808080808080ull;
     if (band) rec[r] = cv;
   }
+  // digit d of the two k's -> one u16 per digit row (PRMT gathers byte d of each)
   unsigned char* lh = cs.limbH + (size_t)b * kLimbBuf + 2 * t;
   unsigned char* lr = cs.limbR + (size_t)b * kLimbBuf + 2 * t;
+  const uint32_t h0l = (uint32_t)VH[0], h0h = (uint32_t)(VH[0] >> 32);
+  const uint32_t h1l = (uint32_t)VH[1], h1h = (uint32_t)(VH[1] >> 32);
+  const uint32_t r0l = (uint32_t)VR[0], r0h = (uint32_t)(VR[0] >> 32);
+  const uint32_t r1l = (uint32_t)VR[1], r1h = (uint32_t)(VR[1] >> 32);
 #pragma unroll
   for (int d = 0; d < 8; ++d) {
-    const uint32_t h = (uint32_t)((VH[0] >> (8 * d)) & 0xFF) | ((uint32_t)((VH[1] >> (8 * d)) & 0xFF) << 8);
-    const uint32_t r = (uint32_t)((VR[0] >> (8 * d)) & 0xFF) | ((uint32_t)((VR[1] >> (8 * d)) & 0xFF) << 8);
+    const uint32_t sel = (uint32_t)(d & 3) | ((uint32_t)(4 + (d & 3)) << 4);
+    const uint32_t h = __byte_perm(d < 4 ? h0l : h0h, d < 4 ? h1l : h1h, sel);
+    const uint32_t r = __byte_perm(d < 4 ? r0l : r0h, d < 4 ? r1l : r1h, sel);
     *reinterpret_cast<uint16_t*>(lh + d * kLimbStride) = (uint16_t)h;
     *reinterpret_cast<uint16_t*>(lr + d * kLimbStride) = (uint16_t)r;
   }
@@ -182,25 +193,34 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
   const int L = (int)io.L, j0 = (int)io.j0;
   const bool nf = j0 + (int)kb < L, nv = (int)kb <= j0 + kGroup - 1;
   constexpr int kW = kWinBytes / 4;
-  const int total = (nf ? 4 * kW : 0) + (nv ? 4 * kW : 0);
+  // thread -> base word q of one direction: bytes 4q..4q+7 of the base copy
+  // from one bit window, copy a word q = base bytes 4q+a..4q+a+3
+  const int total = (nf ? kW : 0) + (nv ? kW : 0);
   for (int idx = (int)t; idx < total; idx += kThreads) {
-    const int dir = nf ? (idx >= 4 * kW ? 1 : 0) : 1;
-    const int rem = nf && dir ? idx - 4 * kW : idx;
-    const int a = rem / kW, q = rem - a * kW;
-    // fwd: byte i <-> position p0 + i; rev: byte i <-> position p0 - i
-    const int p0 = dir == 0 ? j0 + (int)kb + a + 4 * q : j0 - (int)kb + kY0 - a - 4 * q;
-    const int lo = dir == 0 ? p0 : p0 - 3, hi = lo + 3;
-    uint32_t val = 0;
+    const int dir = nf ? (idx >= kW ? 1 : 0) : 1;
+    const int q = nf && dir ? idx - kW : idx;
+    // fwd: byte i <-> position p0 + i; rev: byte i <-> position p0 - i (i = 0..7)
+    const int p0 = dir == 0 ? j0 + (int)kb + 4 * q : j0 - (int)kb + kY0 - 4 * q;
+    const int lo = dir == 0 ? p0 : p0 - 7, hi = lo + 7;
+    uint32_t w0 = 0, w1 = 0;
     if (hi >= 0 && lo < L) {
       if (lo >= 0 && hi < L) {
-        const uint32_t x = __funnelshift_r(sb[(lo >> 5) + 1], sb[(lo >> 5) + 2], (uint32_t)lo & 31) & 0xFu;
-        val = nib_bytes(dir == 0 ? x : __brev(x) >> 28);
+        uint32_t x = __funnelshift_r(sb[(lo >> 5) + 1], sb[(lo >> 5) + 2], (uint32_t)lo & 31) & 0xFFu;
+        if (dir) x = __brev(x) >> 24;
+        w0 = nib_bytes(x & 0xFu);
+        w1 = nib_bytes(x >> 4);
       } else {
-        for (int i = 0; i < 4; ++i) val |= sbyte(sb, dir == 0 ? p0 + i : p0 - i, io.L) << (8 * i);
+        for (int i = 0; i < 4; ++i) {
+          w0 |= sbyte(sb, dir == 0 ? p0 + i : p0 - i, io.L) << (8 * i);
+          w1 |= sbyte(sb, dir == 0 ? p0 + 4 + i : p0 - 4 - i, io.L) << (8 * i);
+        }
       }
     }
-    unsigned char* dst = (dir == 0 ? cs.winF : cs.winV) + (size_t)b * kWinBuf + a * kWinBytes + 4 * q;
-    *reinterpret_cast<uint32_t*>(dst) = val;
+    unsigned char* dst = (dir == 0 ? cs.winF : cs.winV) + (size_t)b * kWinBuf + 4 * q;
+    *reinterpret_cast<uint32_t*>(dst) = w0;
+    *reinterpret_cast<uint32_t*>(dst + kWinBytes) = __funnelshift_r(w0, w1, 8);
+    *reinterpret_cast<uint32_t*>(dst + 2 * kWinBytes) = __funnelshift_r(w0, w1, 16);
+    *reinterpret_cast<uint32_t*>(dst + 3 * kWinBytes) = __funnelshift_r(w0, w1, 24);
   }
 }
 

@@ -950,6 +950,8 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
       io.Cdst = Cpiv;
       io.Cloc = s_local_pending ? Cloc : nullptr;
       io.flips = flips; io.F = s_n_pending;
+      io.f1 = s_n_pending == 1 ? flips[0] : 0u;
+      io.sf1 = s_n_pending == 1 ? sval(sm.sb, io.f1) : 0;
       io.alpha = alpha; io.lut = lut;
       io.hlist = hlist; io.hcount = &ctl->hcount;
       io.hthr = s_Psrc - 4 * (int32_t)s_n_pending - 8;
@@ -1011,7 +1013,7 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
         const double Sc = __dadd_rn(__dadd_rn(sm5[0], sm5[1]), sm5[2]);
         ctl->c_sconst = Sc;
         ctl->c_errconst = 2.0 * gamma_n((double)L / 256.0 + 80.0) * Sc + 8.0 * u * sm5[0] +
-                          64.0 * u * (sm5[3] + sm5[4]) +
+                          64.0 * u * (2.0 * sm5[0] + sm5[1]) +   // sum|H4| <= S_P + S_M, sum|R4| <= S_P
                           (ctl->c_q > 0 ? ((double)L + (double)ctl->m_lo) * ctl->c_unit : 0.0) +
                           1024.0 * u * (double)L * ctl->c_unit;
       }
