@@ -554,6 +554,8 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
   a.record_events = events_cap > 0;
   a.record_traces = traces_cap > 0;
   a.cert = ctx->scan_mode == PSL_SCAN_AUTO && !a.record_traces;
+  a.cert_slack = 0.0;
+  if (const char* env = std::getenv("PSLB200_CERT_SLACK")) a.cert_slack = std::max(0.0, std::atof(env));
   a.events_cap = events_cap;
   a.traces_cap = traces_cap;
   a.c_stride = ((size_t)L + 31) & ~size_t(31);

@@ -39,7 +39,7 @@ constexpr size_t kCertRecBuf = (size_t)kChunk * sizeof(int32_t);
 constexpr size_t kCertRowBytes = (size_t)kGroup * sizeof(double);
 // [limbH 2][limbR 2][win_f 2][win_r 2][rec 2][xrow]
 constexpr size_t kCertBytes = 4 * kLimbBuf + 4 * kWinBuf + 2 * kCertRecBuf + kCertRowBytes;
-constexpr uint32_t kCertMinL = 4096;
+constexpr uint32_t kCertMinL = 2048;
 
 struct CertIO {
   uint32_t L, n, nchunks, j0;                 // rows j = j0 + rho, rho < 1024 (active: rho < n)

@@ -64,6 +64,7 @@ struct RunArgs {
   uint32_t step_budget;
   int32_t record_events, record_traces;
   int32_t cert;         // certified scan allowed (decision-exact; never with traces)
+  double cert_slack;    // test hook: extra relative interval width (forces the exact fallbacks)
   uint64_t events_cap, traces_cap;
   WalkState* st;
   int32_t* Cpiv;

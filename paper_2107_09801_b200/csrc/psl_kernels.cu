@@ -1038,7 +1038,8 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
           const int sj = active[m] ? sval(sm.sb, jj[m]) : 1;
           const double T4 = __dadd_rn(__dadd_rn(__dadd_rn(Sc, B4), sj > 0 ? lin : -lin), xv);
           const double Abs = Sc + B4 + fabs(lin) + fabs(xv);
-          const double Err = E0 + 2.0 * gB * B4 + 2.0 * g8 * Abs + u * (fabs(lin) + fabs(xv));
+          const double Err = E0 + 2.0 * gB * B4 + 2.0 * g8 * Abs + u * (fabs(lin) + fabs(xv)) +
+                             a.cert_slack * Abs;
           mid[m] = 0.25 * T4;
           lo[m] = fmax(0.0, 0.25 * (T4 - Err)) * (1.0 - gL) * (1.0 - 8.0 * u);
           hi[m] = 0.25 * (T4 + Err) * (1.0 + gL) * (1.0 + 8.0 * u);
