@@ -207,6 +207,7 @@ def main():
     err = ctypes.create_string_buffer(256)
     P._lib.lib().psl_probe_peaks(ctx.handle, ctypes.byref(dadd), ctypes.byref(lds),
                                  ctypes.byref(mhz), err, 256)
+    mma_per_s = ctx.probe_imma()
 
     # setup: pivots (random_sequence), O(L^2) tables -- untimed, like the reference
     t_setup = time.perf_counter()
@@ -219,6 +220,7 @@ def main():
     torch.cuda.synchronize()
     r0 = walks.records()
     nse0 = sum(r.nse for r in r0)
+    stats0 = ctx.scan_stats()
     launches0 = ctx.kernel_launches()
     e_start = torch.cuda.Event(enable_timing=True)
     e_end = torch.cuda.Event(enable_timing=True)
@@ -237,6 +239,8 @@ def main():
     ms = e_start.elapsed_time(e_end)
     launches = ctx.kernel_launches() - launches0
     r1 = walks.records(solutions=True)
+    stats1 = ctx.scan_stats()
+    scan = {k: stats1[k] - stats0[k] for k in stats1}
     nse_local = sum(r.nse for r in r1) - nse0
     max_ms = D.max_over_ranks(ms, dev)
     nse_total = D.sum_over_ranks(float(nse_local), dev)
@@ -246,11 +250,17 @@ def main():
                                            [r.solution_best for r in r1], L, device=dev)
     walks.close()
 
-    # dominant kernel: run_kernel, one launch for the K timed steps; algorithmic
-    # work = walks x n x (L-1) cells per step (one exact DADD-chain term each)
-    cells_per_launch = n_walks * n * (L - 1)      # per step
-    per_launch_s = (ms * 1e-3) / args.steps       # per step
-    achieved = cells_per_launch / per_launch_s
+    # dominant kernel: run_kernel, one launch for the K timed steps.  Steps are
+    # scored by the certified scan (int8 mma.sync correlations)
+    # and fall back to the exact DADD sweep where the intervals cannot decide;
+    # the bound is the legacy tensor pipe: achieved = int8 ops of the mma.sync
+    # instructions the kernel issued (device counter) / time, peak = the same
+    # instruction's measured throughput on this GPU.
+    cells_per_step = n_walks * n * (L - 1)
+    per_step_s = (ms * 1e-3) / args.steps
+    mma_ops = scan["mma"] * 16 * 8 * 32 * 2.0          # m16n8k32: 4096 MACs
+    achieved = mma_ops / (ms * 1e-3)
+    peak = mma_per_s * 16 * 8 * 32 * 2.0
     traffic = None
     prof = os.path.join(ROOT, "profiles", "r01_run_kernel.json")
     if os.path.exists(prof) and L == L_DEFAULT and n == 1024:
@@ -263,17 +273,21 @@ def main():
         except Exception:
             traffic = None
     roofline = {
-        "bound": "fp64",
-        "achieved": achieved / 1e9, "peak": dadd.value / 1e9, "unit": "Gcell/s",
-        "frac": achieved / dadd.value if dadd.value else None,
+        "bound": "tensor",
+        "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TOP/s (int8)",
+        "frac": achieved / peak if peak else None,
         "traffic": traffic,
         "traffic_unit": "DRAM bytes per step (ncu capture, profiles/r01_run_kernel.json)",
         "algorithmic_bytes_per_step": n_walks * 8.0 * L,
-        "peak_source": "measured live: FP64-add pipe (one dependent DADD per cell is the "
-                       "serial fitness chain's floor), psl_probe_peaks",
-        "lds_table_roof_gcell_s": lds.value / 1e9,
+        "peak_source": "measured live: mma.sync m16n8k32 s8 issue rate of this GPU "
+                       "(psl_probe_imma); the kernel's MMAs are counted on the device",
+        "mma_per_step": scan["mma"] / args.steps,
+        "cells_per_s": cells_per_step / per_step_s,
+        "fp64_dadd_peak_gcell_s": dadd.value / 1e9,
         "probe_sm_mhz": mhz.value,
-        "hbm_gbs_achieved": n_walks * 8.0 * L / per_launch_s / 1e9,
+        "hbm_gbs_achieved": n_walks * 8.0 * L / per_step_s / 1e9,
+        "scan_steps": {"certified": scan["certified"], "refined": scan["refined"],
+                       "value_local_chains": scan["chains"]},
     }
 
     # e2e through the public API: host start sequences in, records + best

@@ -158,9 +158,12 @@ uint32_t psl_kernel_launches(psl_ctx* ctx);            /* kernels launched so fa
 int psl_ctx_set_scan_mode(psl_ctx* ctx, int mode);
 int psl_ctx_scan_mode(psl_ctx* ctx);
 /* Totals over the walks whose records were read on this context: steps decided
- * by the certified scan alone, certified steps re-scored exactly, and exact
- * value_local chains. */
-int psl_ctx_scan_stats(psl_ctx* ctx, uint64_t* certified, uint64_t* refined, uint64_t* chains);
+ * by the certified scan alone, certified steps re-scored exactly, exact
+ * value_local chains, and tensor-core mma.sync (m16n8k32 s8) instructions. */
+int psl_ctx_scan_stats(psl_ctx* ctx, uint64_t* certified, uint64_t* refined, uint64_t* chains,
+                       uint64_t* mma);
+/* Measurement helper: mma.sync m16n8k32 s8 instructions per second (all SMs). */
+int psl_probe_imma(psl_ctx* ctx, double* mma_per_s, char* err, size_t errlen);
 /* Measurement helper for the roofline (bench.py): FP64-add pipe throughput
  * (cells/s at one DADD per cell), the divergent-LDS.64+DADD loop rate, and the
  * SM clock seen by the probe. */

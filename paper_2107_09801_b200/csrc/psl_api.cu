@@ -29,7 +29,7 @@ struct psl_ctx {
   cudaStream_t stream = nullptr;
   uint32_t launches = 0;
   int scan_mode = PSL_SCAN_AUTO;
-  uint64_t stats[3] = {0, 0, 0};
+  uint64_t stats[4] = {0, 0, 0, 0};
 };
 
 struct psl_walks {
@@ -51,6 +51,7 @@ struct psl_walks {
   uint32_t* bad = nullptr;      // [first bad flat index + 1, value]
   int8_t* sol = nullptr;        // unpack scratch for solutions
   double* lut = nullptr;        // [2][lut_n] power tables
+  uint64_t stats_read[4] = {0, 0, 0, 0};   // scan statistics already added to ctx->stats
 };
 
 namespace {
@@ -187,11 +188,24 @@ int psl_ctx_set_scan_mode(psl_ctx* ctx, int mode) {
 
 int psl_ctx_scan_mode(psl_ctx* ctx) { return ctx ? ctx->scan_mode : -1; }
 
-int psl_ctx_scan_stats(psl_ctx* ctx, uint64_t* certified, uint64_t* refined, uint64_t* chains) {
+int psl_ctx_scan_stats(psl_ctx* ctx, uint64_t* certified, uint64_t* refined, uint64_t* chains,
+                       uint64_t* mma) {
   if (!ctx) return PSL_ERR_CONFIG;
   if (certified) *certified = ctx->stats[0];
   if (refined) *refined = ctx->stats[1];
   if (chains) *chains = ctx->stats[2];
+  if (mma) *mma = ctx->stats[3];
+  return PSL_OK;
+}
+
+int psl_probe_imma(psl_ctx* ctx, double* mma_per_s, char* err, size_t errlen) {
+  int rc = device_ready(ctx, err, errlen);
+  if (rc) return rc;
+  int nsm = 0;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
+  const int n = probe_imma(nsm, ctx->stream, mma_per_s);
+  if (n < 0) return cuda_fail(err, errlen, cudaGetLastError(), "probe_imma");
+  ctx->launches += (uint32_t)n;
   return PSL_OK;
 }
 
@@ -702,9 +716,14 @@ int psl_walks_records(psl_walks* w, psl_walk_record* records, int8_t* solutions,
     r.merit_factor = ((double)L * (double)L) / (2.0 * (double)S.energy_best);
     r.switches = S.switches;
     r.steps = S.steps;
-    w->ctx->stats[0] += S.n_cert;
-    w->ctx->stats[1] += S.n_refine;
-    w->ctx->stats[2] += S.n_vlchain;
+  }
+  uint64_t tot[4] = {0, 0, 0, 0};
+  for (const WalkState& S : st) {
+    tot[0] += S.n_cert; tot[1] += S.n_refine; tot[2] += S.n_vlchain; tot[3] += S.n_mma;
+  }
+  for (int i = 0; i < 4; ++i) {
+    w->ctx->stats[i] += tot[i] - w->stats_read[i];
+    w->stats_read[i] = tot[i];
   }
   return PSL_OK;
 }

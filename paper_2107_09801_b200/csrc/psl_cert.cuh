@@ -304,7 +304,7 @@ __device__ __forceinline__ void cert_cols(uint32_t f, uint32_t v, uint32_t bh, u
 template <bool kCross>
 __device__ __forceinline__ void cert_mma_chunk(const CertIO& io, const CertLane& ln, uint32_t c,
                                                uint32_t b, int (&accL)[kCertTiles][4],
-                                               int (&accX)[kCertTiles][4]) {
+                                               int (&accX)[kCertTiles][4], uint32_t& nmma) {
   const uint32_t kb = 1 + c * kChunk;
   if (!cert_mma_work(io, kb)) return;
   const uint32_t w = threadIdx.x >> 5;
@@ -332,6 +332,7 @@ __device__ __forceinline__ void cert_mma_chunk(const CertIO& io, const CertLane&
     const uint32_t f = ln.f + fo + 32 * cc, v = ln.v + fo + 32 * cc;
     const uint32_t bh = ln.bh + bo + 32 * cc, br = ln.br + bo + 32 * cc;
     const int n = ce - cc;
+    nmma += (uint32_t)(n * kCertTiles) * (uint32_t)(((md & 1) && true) + ((md >> 1) & 1) + (kCross ? (md >> 2) & 1 : 0));
     switch (md) {
       case 1: cert_cols<true, false, false>(f, v, bh, br, n, accL, accX); break;
       case 2: cert_cols<false, true, false>(f, v, bh, br, n, accL, accX); break;

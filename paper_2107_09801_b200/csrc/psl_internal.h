@@ -53,6 +53,7 @@ struct WalkState {
   uint64_t n_cert;      // steps decided by the certified scan alone
   uint64_t n_refine;    // certified steps that needed the exact sweep
   uint64_t n_vlchain;   // exact value_local chains over the local snapshot
+  uint64_t n_mma;       // tensor-core mma.sync m16n8k32 instructions (per warp) issued
 };
 
 struct RunArgs {
@@ -118,5 +119,6 @@ int launch_power_tables(double* lut, uint32_t lut_n, uint32_t alpha1, uint32_t a
                         cudaStream_t s);
 int launch_apply_flip(uint32_t* d_bits, int32_t* d_C, uint32_t L, uint32_t j, cudaStream_t s);
 int probe_peaks(int nsm, cudaStream_t s, double* dadd_cps, double* lds_cps, double* mhz);
+int probe_imma(int nsm, cudaStream_t s, double* mma_per_s);
 
 }  // namespace pslb

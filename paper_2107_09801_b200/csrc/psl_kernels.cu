@@ -966,6 +966,7 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
       double part[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
       double Bs[kJ] = {0.0, 0.0, 0.0, 0.0};
       int32_t pmax = 0;
+      uint32_t nmma = 0;
       const CertLane ln = cert_lane(cs);
       cert_build(io, cs, 0, 0, sm.sb, pmax, part);
       __syncthreads();
@@ -974,7 +975,7 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
       for (; c < io.nchunks && 1 + c * kChunk <= io.m_lo; ++c) {
         const uint32_t b = c & 1;
         if (c + 1 < io.nchunks) cert_build(io, cs, c + 1, b ^ 1, sm.sb, pmax, part);
-        cert_mma_chunk<true>(io, ln, c, b, accL, accX);
+        cert_mma_chunk<true>(io, ln, c, b, accL, accX, nmma);
         if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, b, sm.sb, Bs);
         __syncthreads();
       }
@@ -982,10 +983,12 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
       for (; c < io.nchunks; ++c) {
         const uint32_t b = c & 1;
         if (c + 1 < io.nchunks) cert_build(io, cs, c + 1, b ^ 1, sm.sb, pmax, part);
-        cert_mma_chunk<false>(io, ln, c, b, accL, accX);
+        cert_mma_chunk<false>(io, ln, c, b, accL, accX, nmma);
         if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, b, sm.sb, Bs);
         __syncthreads();
       }
+      if ((t & 31) == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&ctl->st.n_mma),
+                                   (unsigned long long)nmma);
       const int32_t Pn = block_max(ctl, pmax);
       // window constants: warp sums, then a fixed-order sum over warps
       {
@@ -1495,6 +1498,45 @@ __global__ void __launch_bounds__(1024, 1) probe_lds_kernel(int reps, double* ou
   if (threadIdx.x == 0) cyc[blockIdx.x] = t1 - t0;
 }
 }  // namespace
+
+// legacy tensor pipe: mma.sync m16n8k32 s8 throughput (8 independent accumulators per warp)
+__global__ void __launch_bounds__(256) probe_imma_kernel(int reps, int* out) {
+  uint32_t a0 = 0x01010101u * (threadIdx.x + 1), a1 = a0 ^ 0x5a5a5a5au, a2 = ~a0, a3 = a0 + 7;
+  const uint32_t b0 = 0x03030303u * threadIdx.x, b1 = ~b0;
+  int d[8][4] = {};
+  for (int r = 0; r < reps; ++r) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      asm volatile("mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+                   : "+r"(d[q][0]), "+r"(d[q][1]), "+r"(d[q][2]), "+r"(d[q][3])
+                   : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+    a0 += 1;
+  }
+  int s = 0;
+  for (int q = 0; q < 8; ++q) s += d[q][0] + d[q][1] + d[q][2] + d[q][3];
+  if (s == 0x7fffffff) out[0] = s;
+}
+
+int probe_imma(int nsm, cudaStream_t s, double* mma_per_s) {
+  int* out = nullptr;
+  if (cudaMalloc(&out, 64) != cudaSuccess) return -1;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int reps = 2048, blocks = nsm * 4;
+  probe_imma_kernel<<<blocks, 256, 0, s>>>(8, out);
+  cudaEventRecord(a, s);
+  probe_imma_kernel<<<blocks, 256, 0, s>>>(reps, out);
+  cudaEventRecord(b, s);
+  cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  *mma_per_s = (double)blocks * 8 * reps * 8 / (ms * 1e-3);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  return cudaGetLastError() == cudaSuccess ? 2 : -1;
+}
 
 int probe_peaks(int nsm, cudaStream_t s, double* dadd_cps, double* lds_cps, double* mhz) {
   double* out = nullptr;

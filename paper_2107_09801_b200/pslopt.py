@@ -104,9 +104,18 @@ class Context:
     def scan_stats(self) -> dict:
         """Totals over records read on this context: certified steps, certified
         steps re-scored by the exact sweep, exact value_local chains."""
-        a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
-        B.lib().psl_ctx_scan_stats(self._h, C.byref(a), C.byref(b), C.byref(c))
-        return {"certified": a.value, "refined": b.value, "chains": c.value}
+        a, b, c, d = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        B.lib().psl_ctx_scan_stats(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d))
+        return {"certified": a.value, "refined": b.value, "chains": c.value, "mma": d.value}
+
+    def probe_imma(self) -> float:
+        """mma.sync m16n8k32 s8 instructions per second on this GPU (all SMs)."""
+        v = C.c_double()
+        err = _err()
+        rc = B.lib().psl_probe_imma(self._h, C.byref(v), err, len(err))
+        if rc:
+            _raise(rc, err)
+        return v.value
 
     def close(self) -> None:
         if self._h:
