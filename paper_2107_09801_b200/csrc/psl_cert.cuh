@@ -42,7 +42,9 @@ constexpr size_t kCertBytes = 4 * kLimbBuf + 4 * kWinBuf + 2 * kCertRecBuf + kCe
 constexpr uint32_t kCertMinL = 2048;
 
 struct CertIO {
-  uint32_t L, n, nchunks, j0;                 // rows j = j0 + rho, rho < 1024 (active: rho < n)
+  uint32_t L, n, nchunks;
+  int32_t j0;                                 // rows j = j0 + rho (may be < 0 for inactive rows)
+  uint32_t r_lo, r_hi;                        // active rows of this pass: r_lo <= rho < r_hi
   const int32_t* Csrc;
   int32_t* Cdst;
   int32_t* Cloc;
@@ -98,13 +100,19 @@ __device__ __forceinline__ uint32_t sbyte(const uint32_t* sb, long long p, uint3
   return ((sb[(p >> 5) + 1] >> (p & 31)) & 1u) ? 0xFFu : 0x01u;
 }
 
+// C_k of this thread's two shifts of chunk c (prefetched one chunk ahead)
+__device__ __forceinline__ int2 cert_load(const CertIO& io, uint32_t c) {
+  const uint32_t k = 1 + c * kChunk + 2 * threadIdx.x;
+  return make_int2(k < io.L ? io.Csrc[k] : 0, k + 1 < io.L ? io.Csrc[k + 1] : 0);
+}
+
 // Builder for chunk c into buffer b: fold pending flips into C, write C back,
 // collect high sidelobes, expand into the fixed-point digit rows of H4 / R4,
 // the window constants and (band chunks) the exact term records; stage the
 // sequence windows the MMAs read.
 __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs, uint32_t c,
                                            uint32_t b, const uint32_t* sb, int32_t& pmax,
-                                           double (&part)[5]) {
+                                           double (&part)[5], int2 cpre) {
   const uint32_t t = threadIdx.x;
   const uint32_t kb = 1 + c * kChunk;
   const bool band = cert_band_chunk(io, c);
@@ -118,7 +126,7 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
     bool want = false;
     int32_t cv = 0;
     if (k < io.L) {
-      cv = io.Csrc[k];
+      cv = i == 0 ? cpre.x : cpre.y;
       if (io.F == 1) {
         // the common single move: C_k += 2 s_f (s_{f-k} + s_{f+k}), s_f after the flip
         const uint32_t f = io.f1;
@@ -190,8 +198,8 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
   // sequence windows: 4 copies x 392 words per direction, only for chunks with
   // MMA work and only the directions some row still has in range
   if (!cert_mma_work(io, kb)) return;
-  const int L = (int)io.L, j0 = (int)io.j0;
-  const bool nf = j0 + (int)kb < L, nv = (int)kb <= j0 + kGroup - 1;
+  const int L = (int)io.L, j0 = io.j0;
+  const bool nf = j0 + (int)io.r_lo + (int)kb < L, nv = (int)kb <= j0 + (int)io.r_hi - 1;
   constexpr int kW = kWinBytes / 4;
   // thread -> base word q of one direction: bytes 4q..4q+7 of the base copy
   // from one bit window, copy a word q = base bytes 4q+a..4q+a+3
@@ -308,14 +316,17 @@ __device__ __forceinline__ void cert_mma_chunk(const CertIO& io, const CertLane&
   const uint32_t kb = 1 + c * kChunk;
   if (!cert_mma_work(io, kb)) return;
   const uint32_t w = threadIdx.x >> 5;
-  const uint32_t jw_lo = io.j0 + 128 * w, jw_hi = jw_lo + 127;
+  // this warp's active rows (none: no MMAs)
+  const int rw_lo = max(128 * (int)w, (int)io.r_lo), rw_hi = min(128 * (int)w + 127, (int)io.r_hi - 1);
+  if (rw_lo > rw_hi) return;
+  const long long jw_lo = (long long)io.j0 + rw_lo, jw_hi = (long long)io.j0 + rw_hi;
   const uint32_t fo = b * (uint32_t)kWinBuf, bo = b * (uint32_t)kLimbBuf;
   auto mode = [&](int cc) -> int {
     const uint32_t k0 = kb + 32 * cc, k1 = k0 + 31;
     if (k0 >= io.L) return 0;
     const bool lin = k0 <= io.m_lo || (k1 > io.m_hi && k0 <= io.M_lo);
-    const bool fwd = lin && jw_lo + k0 < io.L;
-    const bool rev = lin && k0 <= jw_hi;
+    const bool fwd = lin && jw_lo + k0 < (long long)io.L;
+    const bool rev = lin && (long long)k0 <= jw_hi;
     const bool crs = kCross && k0 <= io.m_lo;
     return (fwd ? 1 : 0) | (rev ? 2 : 0) | (crs ? 4 : 0);
   };
@@ -381,8 +392,8 @@ __device__ __forceinline__ void cert_band_cells(const CertIO& io, const CertSmem
 #pragma unroll
     for (int m = 0; m < kJ; ++m) {
       const uint32_t rho = 4 * threadIdx.x + m;
-      if (rho >= io.n) continue;
-      const uint32_t j = io.j0 + rho;
+      if (rho < io.r_lo || rho >= io.r_hi) continue;
+      const uint32_t j = (uint32_t)(io.j0 + (int32_t)rho);
       const uint32_t sjb = (sb[(j >> 5) + 1] >> (j & 31)) & 1u;
       double s = Bs[m];
 #pragma unroll 1

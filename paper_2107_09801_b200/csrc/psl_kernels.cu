@@ -615,16 +615,25 @@ __device__ long long energy_sweep(Ctl* ctl, const int32_t* C, uint32_t L, const 
                                   int64_t f) {
   long long e = 0;
   const int sf = f >= 0 ? sval(sb, (uint32_t)f) : 0;
-  for (uint32_t k = 1 + threadIdx.x; k < L; k += blockDim.x) {
-    long long cv = C[k];
-    if (f >= 0) {
-      const uint32_t fu = (uint32_t)f;
-      int acc = 0;
-      if (k <= fu) acc += sval(sb, fu - k);
-      if (fu + k < L) acc += sval(sb, fu + k);
-      cv += -2 * sf * acc;
+  // four shifts per thread and load (C is 16-byte aligned per walk; slots
+  // k = 0 and k >= L of the padded row are skipped)
+  for (uint32_t q = threadIdx.x; 4 * q < L; q += blockDim.x) {
+    const int4 c4 = reinterpret_cast<const int4*>(C)[q];
+    const int32_t cs[4] = {c4.x, c4.y, c4.z, c4.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t k = 4 * q + i;
+      if (k == 0 || k >= L) continue;
+      long long cv = cs[i];
+      if (f >= 0) {
+        const uint32_t fu = (uint32_t)f;
+        int acc = 0;
+        if (k <= fu) acc += sval(sb, fu - k);
+        if (fu + k < L) acc += sval(sb, fu + k);
+        cv += -2 * sf * acc;
+      }
+      e += cv * cv;
     }
-    e += cv * cv;
   }
   return block_sum64(ctl, e);
 }
@@ -909,7 +918,7 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
       ctl->need_exact = 0;
       ctl->need_vl = 0;
       if (kCert && a.cert && ctl->do_scan && !S.fitness_pending && a.n <= (uint32_t)kGroup &&
-          L >= kCertMinL && ctl->start + a.n < L) {
+          L >= kCertMinL) {
         // fixed-point scale: every |H4|, |R4| <= 2 pow(Amax, alpha) < 2^(62+q)
         const uint32_t alpha = S.phase == 1 ? a.alpha1 : a.alpha2;
         const int32_t Psrc = S.src_local ? S.P_local : S.P;
@@ -920,13 +929,6 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
           ctl->c_scale = ldexp(1.0, -q);
           ctl->c_unit = ldexp(1.0, q);
           ctl->c_q = q;
-          const uint32_t j0 = ctl->start + 1, jl = ctl->start + a.n;   // active rows
-          const uint32_t h = (L - 1) / 2;
-          const uint32_t m0 = min(j0, L - 1 - j0), m1 = min(jl, L - 1 - jl);
-          ctl->m_lo = min(m0, m1);
-          ctl->m_hi = (j0 <= L - 1 - h && jl >= h) ? h : max(m0, m1);
-          ctl->M_lo = L - 1 - ctl->m_hi;
-          ctl->M_hi = L - 1 - ctl->m_lo;
           ctl->cert = 1;
         }
       }
@@ -943,110 +945,158 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
     const int32_t s_Psrc = s_src_local ? ctl->st.P_local : ctl->st.P;
 
     if (kCert && ctl->cert) {
-      // ================= certified pass (psl_cert.cuh)
-      CertIO io;
-      io.L = L; io.n = a.n; io.nchunks = a.nchunks; io.j0 = start + 1;
-      io.Csrc = s_src_local ? Cloc : Cpiv;
-      io.Cdst = Cpiv;
-      io.Cloc = s_local_pending ? Cloc : nullptr;
-      io.flips = flips; io.F = s_n_pending;
-      io.f1 = s_n_pending == 1 ? flips[0] : 0u;
-      io.sf1 = s_n_pending == 1 ? sval(sm.sb, io.f1) : 0;
-      io.alpha = alpha; io.lut = lut;
-      io.hlist = hlist; io.hcount = &ctl->hcount;
-      io.hthr = s_Psrc - 4 * (int32_t)s_n_pending - 8;
-      io.scale = ctl->c_scale;
-      io.m_lo = ctl->m_lo; io.m_hi = ctl->m_hi; io.M_lo = ctl->M_lo; io.M_hi = ctl->M_hi;
+      // ================= certified pass(es) (psl_cert.cuh).  Rows rho = i - 1
+      // (offset i) are neighbours j = start + i mod L; a window that wraps past
+      // L - 1 is scored in two passes, one per contiguous row segment.
       const CertSmem cs = cert_carve(smem_raw);
-      int accL[kCertTiles][4], accX[kCertTiles][4];
-#pragma unroll
-      for (int r = 0; r < kCertTiles; ++r)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) { accL[r][e] = 0; accX[r][e] = 0; }
-      double part[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-      double Bs[kJ] = {0.0, 0.0, 0.0, 0.0};
-      int32_t pmax = 0;
-      uint32_t nmma = 0;
       const CertLane ln = cert_lane(cs);
-      cert_build(io, cs, 0, 0, sm.sb, pmax, part);
-      __syncthreads();
-      uint32_t c = 0;
-      // phase 1: chunks holding k <= m_lo (both sides for every row: cross term)
-      for (; c < io.nchunks && 1 + c * kChunk <= io.m_lo; ++c) {
-        const uint32_t b = c & 1;
-        if (c + 1 < io.nchunks) cert_build(io, cs, c + 1, b ^ 1, sm.sb, pmax, part);
-        cert_mma_chunk<true>(io, ln, c, b, accL, accX, nmma);
-        if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, b, sm.sb, Bs);
-        __syncthreads();
-      }
-      cert_rows(accX, ctl->c_unit, cs.xrow);   // the cross term is complete
-      for (; c < io.nchunks; ++c) {
-        const uint32_t b = c & 1;
-        if (c + 1 < io.nchunks) cert_build(io, cs, c + 1, b ^ 1, sm.sb, pmax, part);
-        cert_mma_chunk<false>(io, ln, c, b, accL, accX, nmma);
-        if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, b, sm.sb, Bs);
-        __syncthreads();
-      }
-      if ((t & 31) == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&ctl->st.n_mma),
-                                   (unsigned long long)nmma);
-      const int32_t Pn = block_max(ctl, pmax);
-      // window constants: warp sums, then a fixed-order sum over warps
-      {
-        const int lane = t & 31, warp = t >> 5;
+      double mid[kJ], lo[kJ], hi[kJ];
 #pragma unroll
-        for (int i = 0; i < 5; ++i) {
-          double v = part[i];
-          for (int o = 16; o; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, o));
-          if (lane == 0) ctl->rs5[i][warp] = v;
+      for (int m = 0; m < kJ; ++m) { mid[m] = 0.0; lo[m] = 0.0; hi[m] = 0.0; }
+      const uint32_t nA = min(a.n, L - 1 - start);          // rows before the wrap
+      const int nseg = (nA > 0 && nA < a.n) ? 2 : 1;
+      for (int seg = 0; seg < nseg; ++seg) {
+        const bool wrapped = seg == 1 || nA == 0;            // rows past L - 1: j = rho - nA
+        const uint32_t r_lo = seg ? nA : 0, r_hi = (nseg == 2 && seg == 0) ? nA : a.n;
+        const int32_t j0 = wrapped ? (int32_t)start + 1 - (int32_t)L : (int32_t)start + 1;
+        if (t == 0) {
+          // zones over the segment's neighbours [jlo, jhi] (m_j = min(j, L-1-j))
+          const uint32_t jlo = (uint32_t)(j0 + (int32_t)r_lo), jhi = (uint32_t)(j0 + (int32_t)r_hi - 1);
+          const uint32_t h = (L - 1) / 2;
+          const uint32_t m0 = min(jlo, L - 1 - jlo), m1 = min(jhi, L - 1 - jhi);
+          ctl->m_lo = min(m0, m1);
+          ctl->m_hi = (jlo <= L - 1 - h && jhi >= h) ? h : max(m0, m1);
+          ctl->M_lo = L - 1 - ctl->m_hi;
+          ctl->M_hi = L - 1 - ctl->m_lo;
         }
-      }
-      double* linrow = reinterpret_cast<double*>(cs.winF);   // [1024]
-      const double* xrow = cs.xrow;
-      cert_rows(accL, ctl->c_unit, linrow);
-      if (t == 0) first_pass_state(ctl, a, w, Pn, 0.0, alpha);
-      __syncthreads();
-      if (t == 0) {
-        double sm5[5];
-        for (int i = 0; i < 5; ++i) {
-          double v = 0.0;
-          for (int x = 0; x < kThreads / 32; ++x) v = __dadd_rn(v, ctl->rs5[i][x]);
-          sm5[i] = v;
+        __syncthreads();
+        CertIO io;
+        io.L = L; io.n = a.n; io.nchunks = a.nchunks; io.j0 = j0; io.r_lo = r_lo; io.r_hi = r_hi;
+        if (seg == 0) {
+          io.Csrc = s_src_local ? Cloc : Cpiv;
+          io.Cdst = Cpiv;
+          io.Cloc = s_local_pending ? Cloc : nullptr;
+          io.F = s_n_pending;
+          io.hlist = hlist;
+        } else {   // C already folded and written by the first segment's pass
+          io.Csrc = Cpiv; io.Cdst = nullptr; io.Cloc = nullptr; io.F = 0; io.hlist = nullptr;
         }
-        const double u = 0x1p-53;
-        const double Sc = __dadd_rn(__dadd_rn(sm5[0], sm5[1]), sm5[2]);
-        ctl->c_sconst = Sc;
-        ctl->c_errconst = 2.0 * gamma_n((double)L / 256.0 + 80.0) * Sc + 8.0 * u * sm5[0] +
-                          64.0 * u * (2.0 * sm5[0] + sm5[1]) +   // sum|H4| <= S_P + S_M, sum|R4| <= S_P
-                          (ctl->c_q > 0 ? ((double)L + (double)ctl->m_lo) * ctl->c_unit : 0.0) +
-                          1024.0 * u * (double)L * ctl->c_unit;
+        io.flips = flips;
+        io.f1 = io.F == 1 ? flips[0] : 0u;
+        io.sf1 = io.F == 1 ? sval(sm.sb, io.f1) : 0;
+        io.alpha = alpha; io.lut = lut;
+        io.hcount = &ctl->hcount;
+        io.hthr = s_Psrc - 4 * (int32_t)s_n_pending - 8;
+        io.scale = ctl->c_scale;
+        io.m_lo = ctl->m_lo; io.m_hi = ctl->m_hi; io.M_lo = ctl->M_lo; io.M_hi = ctl->M_hi;
+        int accL[kCertTiles][4], accX[kCertTiles][4];
+#pragma unroll
+        for (int r = 0; r < kCertTiles; ++r)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) { accL[r][e] = 0; accX[r][e] = 0; }
+        double part[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        double Bs[kJ] = {0.0, 0.0, 0.0, 0.0};
+        int32_t pmax = 0;
+        uint32_t nmma = 0;
+        // C_k of chunk c + 2 is loaded while chunk c's MMAs run (DRAM latency off
+        // the builder's critical path)
+        int2 cpre = cert_load(io, 0);
+        cert_build(io, cs, 0, 0, sm.sb, pmax, part, cpre);
+        if (io.nchunks > 1) cpre = cert_load(io, 1);
+        __syncthreads();
+        uint32_t c = 0;
+        // phase 1: chunks holding k <= m_lo (both sides for every row: cross term)
+        for (; c < io.nchunks && 1 + c * kChunk <= io.m_lo; ++c) {
+          const uint32_t b = c & 1;
+          if (c + 1 < io.nchunks) cert_build(io, cs, c + 1, b ^ 1, sm.sb, pmax, part, cpre);
+          if (c + 2 < io.nchunks) cpre = cert_load(io, c + 2);
+          cert_mma_chunk<true>(io, ln, c, b, accL, accX, nmma);
+          if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, b, sm.sb, Bs);
+          __syncthreads();
+        }
+        cert_rows(accX, ctl->c_unit, cs.xrow);   // the cross term is complete
+        for (; c < io.nchunks; ++c) {
+          const uint32_t b = c & 1;
+          if (c + 1 < io.nchunks) cert_build(io, cs, c + 1, b ^ 1, sm.sb, pmax, part, cpre);
+          if (c + 2 < io.nchunks) cpre = cert_load(io, c + 2);
+          cert_mma_chunk<false>(io, ln, c, b, accL, accX, nmma);
+          if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, b, sm.sb, Bs);
+          __syncthreads();
+        }
+        if ((t & 31) == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&ctl->st.n_mma),
+                                     (unsigned long long)nmma);
+        if (seg == 0) {
+          const int32_t Pn = block_max(ctl, pmax);
+          if (t == 0) first_pass_state(ctl, a, w, Pn, 0.0, alpha);
+        }
+        // window constants: warp sums, then a fixed-order sum over warps
+        {
+          const int lane = t & 31, warp = t >> 5;
+#pragma unroll
+          for (int i = 0; i < 5; ++i) {
+            double v = part[i];
+            for (int o = 16; o; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, o));
+            if (lane == 0) ctl->rs5[i][warp] = v;
+          }
+        }
+        double* linrow = reinterpret_cast<double*>(cs.winF);   // [1024]
+        const double* xrow = cs.xrow;
+        cert_rows(accL, ctl->c_unit, linrow);
+        __syncthreads();
+        if (t == 0) {
+          double sm5[5];
+          for (int i = 0; i < 5; ++i) {
+            double v = 0.0;
+            for (int x = 0; x < kThreads / 32; ++x) v = __dadd_rn(v, ctl->rs5[i][x]);
+            sm5[i] = v;
+          }
+          const double u = 0x1p-53;
+          const double Sc = __dadd_rn(__dadd_rn(sm5[0], sm5[1]), sm5[2]);
+          ctl->c_sconst = Sc;
+          ctl->c_errconst = 2.0 * gamma_n((double)L / 256.0 + 80.0) * Sc + 8.0 * u * sm5[0] +
+                            64.0 * u * (2.0 * sm5[0] + sm5[1]) +   // sum|H4| <= S_P + S_M, sum|R4| <= S_P
+                            (ctl->c_q > 0 ? ((double)L + (double)ctl->m_lo) * ctl->c_unit : 0.0) +
+                            1024.0 * u * (double)L * ctl->c_unit;
+        }
+        __syncthreads();
+        // per-row intervals [lo, hi] that provably hold the serial double V(j)
+        {
+          const double u = 0x1p-53;
+          const double gL = gamma_n((double)L), gB = gamma_n(2100.0), g8 = gamma_n(8.0);
+          const double Sc = ctl->c_sconst, E0 = ctl->c_errconst;
+#pragma unroll
+          for (int m = 0; m < kJ; ++m) {
+            const uint32_t rho = kJ * t + m;
+            if (rho < r_lo || rho >= r_hi) continue;
+            const uint32_t j = (uint32_t)(j0 + (int32_t)rho);
+            const double lin = linrow[rho], xv = xrow[rho];
+            const double B4 = __dmul_rn(4.0, Bs[m]);
+            const int sj = sval(sm.sb, j);
+            const double T4 = __dadd_rn(__dadd_rn(__dadd_rn(Sc, B4), sj > 0 ? lin : -lin), xv);
+            const double Abs = Sc + B4 + fabs(lin) + fabs(xv);
+            const double Err = E0 + 2.0 * gB * B4 + 2.0 * g8 * Abs + u * (fabs(lin) + fabs(xv)) +
+                               a.cert_slack * Abs;
+            mid[m] = 0.25 * T4;
+            lo[m] = fmax(0.0, 0.25 * (T4 - Err)) * (1.0 - gL) * (1.0 - 8.0 * u);
+            hi[m] = 0.25 * (T4 + Err) * (1.0 + gL) * (1.0 + 8.0 * u);
+            if (!isfinite(hi[m])) mid[m] = __longlong_as_double(0x7ff8000000000000ll);   // -> bad
+          }
+        }
+        __syncthreads();
       }
       filter_hlist(ctl, sm, hlist);
       __syncthreads();
-      // per-row intervals [lo, hi] that provably hold the serial double V(j)
       {
-        const double u = 0x1p-53;
-        const double gL = gamma_n((double)L), gB = gamma_n(2100.0), g8 = gamma_n(8.0);
-        const double Sc = ctl->c_sconst, E0 = ctl->c_errconst;
         bool active[kJ];
         uint32_t jj[kJ];
-        double mid[kJ], lo[kJ], hi[kJ];
         const uint32_t ibase = kJ * t;
 #pragma unroll
         for (int m = 0; m < kJ; ++m) {
           const uint32_t rho = kJ * t + m;
           active[m] = rho < a.n;
-          jj[m] = start + 1 + rho;
-          const double lin = linrow[rho], xv = xrow[rho];
-          const double B4 = __dmul_rn(4.0, Bs[m]);
-          const int sj = active[m] ? sval(sm.sb, jj[m]) : 1;
-          const double T4 = __dadd_rn(__dadd_rn(__dadd_rn(Sc, B4), sj > 0 ? lin : -lin), xv);
-          const double Abs = Sc + B4 + fabs(lin) + fabs(xv);
-          const double Err = E0 + 2.0 * gB * B4 + 2.0 * g8 * Abs + u * (fabs(lin) + fabs(xv)) +
-                             a.cert_slack * Abs;
-          mid[m] = 0.25 * T4;
-          lo[m] = fmax(0.0, 0.25 * (T4 - Err)) * (1.0 - gL) * (1.0 - 8.0 * u);
-          hi[m] = 0.25 * (T4 + Err) * (1.0 + gL) * (1.0 + 8.0 * u);
-          if (!isfinite(hi[m])) mid[m] = __longlong_as_double(0x7ff8000000000000ll);   // -> bad
+          uint32_t j = start + 1 + rho;
+          if (j >= L) j -= L;
+          jj[m] = j;
         }
         reduce_group(ctl, sm, hlist, active, jj, mid, ibase, L);
         const uint32_t bi = ctl->best_i;

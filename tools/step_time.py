@@ -15,12 +15,15 @@ def timed(ctx, mode, p, walks, steps):
     torch.cuda.synchronize()
     s = torch.cuda.Stream()
     ctx.set_stream(s.cuda_stream)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(s)
-    w.step(steps)
-    e1.record(s)
-    e1.synchronize()
-    ms = e0.elapsed_time(e1)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    ev[0].record(s)
+    for i in range(steps):           # one launch per step: per-step times
+        w.step(1)
+        ev[i + 1].record(s)
+    ev[-1].synchronize()
+    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+    print("per-step ms:", " ".join(f"{x:.2f}" for x in per), file=sys.stderr)
+    ms = sum(per)
     before = ctx.scan_stats()
     w.records()
     after = ctx.scan_stats()
