@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "libpslb200.so")
+SO_PATH = os.environ.get("PSLB200_LIB") or os.path.join(HERE, "libpslb200.so")  # override: profiling builds
 
 PSL_OK, PSL_ERR_CONFIG, PSL_ERR_OVERFLOW, PSL_ERR_CUDA, PSL_ERR_CAPACITY = 0, 1, 2, 3, 4
 

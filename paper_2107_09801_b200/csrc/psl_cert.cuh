@@ -37,8 +37,15 @@ constexpr size_t kLimbBuf = 8ull * kLimbStride;          // one table, one buffe
 constexpr size_t kWinBuf = 4ull * kWinBytes;             // one direction (4 copies), one buffer
 constexpr size_t kCertRecBuf = (size_t)kChunk * sizeof(int32_t);
 constexpr size_t kCertRowBytes = (size_t)kGroup * sizeof(double);
-// [limbH 2][limbR 2][win_f 2][win_r 2][rec 2][xrow]
-constexpr size_t kCertBytes = 4 * kLimbBuf + 4 * kWinBuf + 2 * kCertRecBuf + kCertRowBytes;
+constexpr size_t kCertCBuf = (size_t)kChunk * sizeof(int32_t);     // C_k prefetch ring slot
+// [digits 2][win_f 2][win_r 2][rec 2][xrow][C ring 3]
+constexpr size_t kCertBytes = 2 * kLimbBuf + 4 * kWinBuf + 2 * kCertRecBuf + kCertRowBytes + 3 * kCertCBuf;
+// fixed-point digits per shift: H4 (the correlation coefficient) in digit
+// columns 0..4 (40 bits), R4 (the cross coefficient) in columns 5..7 (24 bits),
+// each with its own power-of-two unit; the MMA accumulates both into one
+// m16n8 tile (B of the linear MMAs carries zeros in 5..7, the cross MMA's in 0..4)
+constexpr int kDigH = 5, kDigR = 3;
+constexpr long long kMaxH = 0x7F7F7F7F7Fll, kMaxR = 0x7F7F7Fll;
 constexpr uint32_t kCertMinL = 2048;
 
 struct CertIO {
@@ -57,27 +64,28 @@ struct CertIO {
   int2* hlist;
   uint32_t* hcount;
   int32_t hthr;
-  double scale;                               // 2^-q
+  double scaleH, scaleR;                      // 2^-qH, 2^-qR
   uint32_t m_lo, m_hi, M_lo, M_hi;            // zone bounds (see above)
 };
 
 struct CertSmem {
-  unsigned char* limbH;   // [2][8][kLimbStride]
-  unsigned char* limbR;
+  unsigned char* limbH;   // [2][8][kLimbStride] digit rows (H4: 0-4, R4: 5-7)
   unsigned char* winF;    // [2][4][kWinBytes]  F[x] = s_{j0+kb+x}
   unsigned char* winV;    // [2][4][kWinBytes]  V[y] = s_{j0-kb+kY0-y}
   int32_t* rec;           // [2][kChunk]        C_k (band chunks only)
   double* xrow;           // [1024]             cross-term sums per row
+  int32_t* cring;         // [3][kChunk]        C_k of chunks c+1, c+2 in flight (cp.async)
 };
 
 __device__ __forceinline__ CertSmem cert_carve(unsigned char* base) {
   CertSmem m;
   m.limbH = base;
-  m.limbR = base + 2 * kLimbBuf;
-  m.winF = base + 4 * kLimbBuf;
-  m.winV = base + 4 * kLimbBuf + 2 * kWinBuf;
-  m.rec = reinterpret_cast<int32_t*>(base + 4 * kLimbBuf + 4 * kWinBuf);
-  m.xrow = reinterpret_cast<double*>(base + 4 * kLimbBuf + 4 * kWinBuf + 2 * kCertRecBuf);
+  m.winF = base + 2 * kLimbBuf;
+  m.winV = base + 2 * kLimbBuf + 2 * kWinBuf;
+  m.rec = reinterpret_cast<int32_t*>(base + 2 * kLimbBuf + 4 * kWinBuf);
+  m.xrow = reinterpret_cast<double*>(base + 2 * kLimbBuf + 4 * kWinBuf + 2 * kCertRecBuf);
+  m.cring = reinterpret_cast<int32_t*>(base + 2 * kLimbBuf + 4 * kWinBuf + 2 * kCertRecBuf +
+                                       kCertRowBytes);
   return m;
 }
 
@@ -100,10 +108,25 @@ __device__ __forceinline__ uint32_t sbyte(const uint32_t* sb, long long p, uint3
   return ((sb[(p >> 5) + 1] >> (p & 31)) & 1u) ? 0xFFu : 0x01u;
 }
 
-// C_k of this thread's two shifts of chunk c (prefetched one chunk ahead)
-__device__ __forceinline__ int2 cert_load(const CertIO& io, uint32_t c) {
+// C_k of this thread's two shifts of chunk c -> ring slot c % 3, asynchronously
+// (cp.async, zero-filled past L); the thread itself consumes them in cert_build
+__device__ __forceinline__ void cert_prefetch(const CertIO& io, const CertSmem& cs, uint32_t c) {
   const uint32_t k = 1 + c * kChunk + 2 * threadIdx.x;
-  return make_int2(k < io.L ? io.Csrc[k] : 0, k + 1 < io.L ? io.Csrc[k + 1] : 0);
+  int32_t* dst = cs.cring + (size_t)(c % 3) * kChunk + 2 * threadIdx.x;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const bool in = k + i < io.L;
+    const int32_t* src = io.Csrc + (in ? k + i : 0);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst + i)), "l"(src),
+                 "r"(in ? 4 : 0) : "memory");
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ int2 cert_take(const CertSmem& cs, uint32_t c, bool newest_pending) {
+  if (newest_pending) asm volatile("cp.async.wait_group 1;" ::: "memory");
+  else asm volatile("cp.async.wait_group 0;" ::: "memory");
+  const int32_t* p = cs.cring + (size_t)(c % 3) * kChunk + 2 * threadIdx.x;
+  return make_int2(p[0], p[1]);
 }
 
 // Builder for chunk c into buffer b: fold pending flips into C, write C back,
@@ -112,12 +135,12 @@ __device__ __forceinline__ int2 cert_load(const CertIO& io, uint32_t c) {
 // sequence windows the MMAs read.
 __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs, uint32_t c,
                                            uint32_t b, const uint32_t* sb, int32_t& pmax,
-                                           double (&part)[5], int2 cpre) {
+                                           double (&part)[5], int2 cpre, bool& ovf) {
   const uint32_t t = threadIdx.x;
   const uint32_t kb = 1 + c * kChunk;
   const bool band = cert_band_chunk(io, c);
   int32_t* rec = cs.rec + (size_t)b * kChunk;
-  uint64_t VH[2], VR[2];
+  uint64_t VD[2];
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     const uint32_t r = 2 * t + i;
@@ -173,31 +196,31 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
         part[2] = __dadd_rn(part[2], __dmul_rn(4.0, e2));
       }
     }
-    // fixed point (|V| < 2^62) -> 8 balanced base-256 digits, as bytes
-    const long long hv = __double2ll_rn(__dmul_rn(H, io.scale));
-    const long long rv = __double2ll_rn(__dmul_rn(R, io.scale));
-    VH[i] = ((unsigned long long)hv + 0x8080808080808080ull) ^ 0x8080808080808080ull;
-    VR[i] = ((unsigned long long)rv + 0x8080808080808080ull) ^ 0x8080808080808080ull;
+    // fixed point -> balanced base-256 digits: H4 in bytes 0..4, R4 in 5..7
+    const long long hv = __double2ll_rn(__dmul_rn(H, io.scaleH));
+    const long long rv = __double2ll_rn(__dmul_rn(R, io.scaleR));
+    ovf |= hv > kMaxH || hv < -kMaxH || rv > kMaxR || rv < -kMaxR;
+    const unsigned long long dh = ((unsigned long long)hv + 0x8080808080ull) ^ 0x8080808080ull;
+    const unsigned long long dr = ((unsigned long long)rv + 0x808080ull) ^ 0x808080ull;
+    VD[i] = (dh & 0xFFFFFFFFFFull) | ((dr & 0xFFFFFFull) << 40);
     if (band) rec[r] = cv;
   }
   // digit d of the two k's -> one u16 per digit row (PRMT gathers byte d of each)
   unsigned char* lh = cs.limbH + (size_t)b * kLimbBuf + 2 * t;
-  unsigned char* lr = cs.limbR + (size_t)b * kLimbBuf + 2 * t;
-  const uint32_t h0l = (uint32_t)VH[0], h0h = (uint32_t)(VH[0] >> 32);
-  const uint32_t h1l = (uint32_t)VH[1], h1h = (uint32_t)(VH[1] >> 32);
-  const uint32_t r0l = (uint32_t)VR[0], r0h = (uint32_t)(VR[0] >> 32);
-  const uint32_t r1l = (uint32_t)VR[1], r1h = (uint32_t)(VR[1] >> 32);
+  const uint32_t h0l = (uint32_t)VD[0], h0h = (uint32_t)(VD[0] >> 32);
+  const uint32_t h1l = (uint32_t)VD[1], h1h = (uint32_t)(VD[1] >> 32);
 #pragma unroll
   for (int d = 0; d < 8; ++d) {
     const uint32_t sel = (uint32_t)(d & 3) | ((uint32_t)(4 + (d & 3)) << 4);
     const uint32_t h = __byte_perm(d < 4 ? h0l : h0h, d < 4 ? h1l : h1h, sel);
-    const uint32_t r = __byte_perm(d < 4 ? r0l : r0h, d < 4 ? r1l : r1h, sel);
     *reinterpret_cast<uint16_t*>(lh + d * kLimbStride) = (uint16_t)h;
-    *reinterpret_cast<uint16_t*>(lr + d * kLimbStride) = (uint16_t)r;
   }
   // sequence windows: 4 copies x 392 words per direction, only for chunks with
   // MMA work and only the directions some row still has in range
   if (!cert_mma_work(io, kb)) return;
+#ifdef PSL_ABLATE_STAGE
+  return;
+#endif
   const int L = (int)io.L, j0 = io.j0;
   const bool nf = j0 + (int)io.r_lo + (int)kb < L, nv = (int)kb <= j0 + (int)io.r_hi - 1;
   constexpr int kW = kWinBytes / 4;
@@ -255,7 +278,8 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
 //   reversed word m' (past base_v = kY0 - 128w - g + 4t) = s_{j-k} for
 //     m' = 4c - 2r + {0: a0, -1: a1, 2: a2, 1: a3}
 struct CertLane {
-  uint32_t f, v, bh, br;
+  uint32_t f, v, bd;
+  bool dh;                    // this lane's B column (= g) is an H4 digit (g < 5)
 };
 __device__ __forceinline__ CertLane cert_lane(const CertSmem& cs) {
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -265,56 +289,112 @@ __device__ __forceinline__ CertLane cert_lane(const CertSmem& cs) {
   CertLane l;
   l.f = smem_u32(cs.winF) + af * kWinBytes + (base_f - af);
   l.v = smem_u32(cs.winV) + av * kWinBytes + (base_v - av);
-  l.bh = smem_u32(cs.limbH) + gid * kLimbStride + 4 * tig;
-  l.br = smem_u32(cs.limbR) + gid * kLimbStride + 4 * tig;
+  l.bd = smem_u32(cs.limbH) + gid * kLimbStride + 4 * tig;
+  l.dh = gid < (uint32_t)kDigH;
   return l;
 }
 
-// ncols consecutive 32-k columns with one warp-uniform mode
-template <bool FWD, bool REV, bool CRS>
-__device__ __forceinline__ void cert_cols(uint32_t f, uint32_t v, uint32_t bh, uint32_t br, int ncols,
-                                          int (&accL)[kCertTiles][4], int (&accX)[kCertTiles][4]) {
-#pragma unroll 1
-  for (int cc = 0; cc < ncols; ++cc, f += 32, v += 32, bh += 32, br += 32) {
-    uint32_t b0 = 0, b1 = 0, r0 = 0, r1 = 0;
-    if (FWD || REV) { b0 = lds32<0>(bh); b1 = lds32<16>(bh); }
-    if (CRS) { r0 = lds32<0>(br); r1 = lds32<16>(br); }
-#pragma unroll
-    for (int r = 0; r < kCertTiles; ++r) {
-      uint32_t f0 = 0, f1 = 0, f2 = 0, f3 = 0, v0 = 0, v1 = 0, v2 = 0, v3 = 0;
-      switch (r) {   // immediate offsets: 16r + {0,8,16,24} / -16r + {0,-8,16,8}
-#define CERT_LOADS(R)                                                                    \
-  case R:                                                                                \
-    if (FWD || CRS) {                                                                    \
-      f0 = lds32<16 * R>(f); f1 = lds32<16 * R + 8>(f);                                  \
-      f2 = lds32<16 * R + 16>(f); f3 = lds32<16 * R + 24>(f);                            \
-    }                                                                                    \
-    if (REV || CRS) {                                                                    \
-      v0 = lds32<-16 * R>(v); v1 = lds32<-16 * R - 8>(v);                                \
-      v2 = lds32<-16 * R + 16>(v); v3 = lds32<-16 * R + 8>(v);                           \
-    }                                                                                    \
-    break;
-        CERT_LOADS(0) CERT_LOADS(1) CERT_LOADS(2) CERT_LOADS(3)
-        CERT_LOADS(4) CERT_LOADS(5) CERT_LOADS(6) CERT_LOADS(7)
-#undef CERT_LOADS
-      }
-      if (FWD) imma_s8(accL[r], f0, f1, f2, f3, b0, b1);
-      if (CRS) imma_s8(accX[r], uv_bytes(f0, v0), uv_bytes(f1, v1), uv_bytes(f2, v2), uv_bytes(f3, v3), r0, r1);
-      if (REV) imma_s8(accL[r], v0, v1, v2, v3, b0, b1);
-    }
-  }
+struct Quad {
+  uint32_t x, y, z, w;
+};
+// tile-quads of the sliding windows (see cert_run): forward E/O at e, reversed E/O at e
+template <int E>
+__device__ __forceinline__ Quad qfe(uint32_t f) {
+  return {lds32<32 * E>(f), lds32<32 * E + 8>(f), lds32<32 * E + 16>(f), lds32<32 * E + 24>(f)};
+}
+template <int E>
+__device__ __forceinline__ Quad qfo(uint32_t f) {
+  return {lds32<32 * E + 16>(f), lds32<32 * E + 24>(f), lds32<32 * E + 32>(f), lds32<32 * E + 40>(f)};
+}
+template <int E>
+__device__ __forceinline__ Quad qve(uint32_t v) {
+  return {lds32<32 * E>(v), lds32<32 * E - 8>(v), lds32<32 * E + 16>(v), lds32<32 * E + 8>(v)};
+}
+template <int E>
+__device__ __forceinline__ Quad qvo(uint32_t v) {
+  return {lds32<32 * E - 16>(v), lds32<32 * E - 24>(v), lds32<32 * E>(v), lds32<32 * E - 8>(v)};
+}
+__device__ __forceinline__ void imma_q(int (&d)[4], const Quad& a, uint32_t b0, uint32_t b1) {
+  imma_s8(d, a.x, a.y, a.z, a.w, b0, b1);
+}
+__device__ __forceinline__ Quad uv_q(const Quad& f, const Quad& v) {
+  return {uv_bytes(f.x, v.x), uv_bytes(f.y, v.y), uv_bytes(f.z, v.z), uv_bytes(f.w, v.w)};
 }
 
-// The tensor-core part of chunk c (buffer b) for this warp's 128 rows:
-// accL += digits of H4 x (s_{j+k} + s_{j-k}), accX += digits of R4 x s_{j+k} s_{j-k}.
-// Columns are grouped into runs of one mode (zones and row ranges are
-// monotone in k, so a chunk has at most a few runs).
+// n consecutive 32-k columns of one warp-uniform mode.  Tile r = 2i (+1) of
+// relative column c reads the forward quad E (O) at e = c + i and the reversed
+// quad E (O) at e = c - i: each column loads one new quad per window (ring of
+// four, slot = e mod 4, resolved at compile time) instead of all eight.
+template <bool FWD, bool REV, bool CRS>
+__device__ __forceinline__ void cert_run(uint32_t f, uint32_t v, uint32_t bd, bool dh, int n,
+                                         int (&acc)[kCertTiles][4]) {
+  constexpr bool F = FWD || CRS, V = REV || CRS;
+  Quad fe[4], fo[4], ve[4], vo[4];
+  if (F) { fe[0] = qfe<0>(f); fo[0] = qfo<0>(f); fe[1] = qfe<1>(f); fo[1] = qfo<1>(f);
+           fe[2] = qfe<2>(f); fo[2] = qfo<2>(f); fe[3] = qfe<3>(f); fo[3] = qfo<3>(f); }
+  // reversed quads e = 0, -1, -2, -3 -> slots 0, 3, 2, 1
+  if (V) { ve[0] = qve<0>(v); vo[0] = qvo<0>(v); ve[3] = qve<-1>(v); vo[3] = qvo<-1>(v);
+           ve[2] = qve<-2>(v); vo[2] = qvo<-2>(v); ve[1] = qve<-3>(v); vo[1] = qvo<-3>(v); }
+  auto column = [&](auto U) {
+    constexpr int u = decltype(U)::value;       // relative column mod 4
+    uint32_t bl0 = 0, bl1 = 0, bx0 = 0, bx1 = 0;
+    {
+      const uint32_t b0 = lds32<0>(bd), b1 = lds32<16>(bd);
+      if (FWD || REV) { bl0 = dh ? b0 : 0u; bl1 = dh ? b1 : 0u; }
+      if (CRS) { bx0 = dh ? 0u : b0; bx1 = dh ? 0u : b1; }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (FWD) {
+        imma_q(acc[2 * i], fe[(u + i) & 3], bl0, bl1);
+        imma_q(acc[2 * i + 1], fo[(u + i) & 3], bl0, bl1);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (REV) {
+        imma_q(acc[2 * i], ve[(u - i + 8) & 3], bl0, bl1);
+        imma_q(acc[2 * i + 1], vo[(u - i + 8) & 3], bl0, bl1);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (CRS) {
+        imma_q(acc[2 * i], uv_q(fe[(u + i) & 3], ve[(u - i + 8) & 3]), bx0, bx1);
+        imma_q(acc[2 * i + 1], uv_q(fo[(u + i) & 3], vo[(u - i + 8) & 3]), bx0, bx1);
+      }
+    }
+    // advance: forward e = c + 4 -> slot u; reversed e = c + 1 -> slot u + 1
+    f += 32; v += 32; bd += 32;
+    if (F) { fe[u] = qfe<3>(f); fo[u] = qfo<3>(f); }
+    if (V) { ve[(u + 1) & 3] = qve<0>(v); vo[(u + 1) & 3] = qvo<0>(v); }
+  };
+  int c = 0;
+#pragma unroll 1
+  for (; c + 4 <= n; c += 4) {
+    column(std::integral_constant<int, 0>{});
+    column(std::integral_constant<int, 1>{});
+    column(std::integral_constant<int, 2>{});
+    column(std::integral_constant<int, 3>{});
+  }
+  if (c < n) column(std::integral_constant<int, 0>{});
+  if (c + 1 < n) column(std::integral_constant<int, 1>{});
+  if (c + 2 < n) column(std::integral_constant<int, 2>{});
+}
+
+// The tensor-core part of chunk c (buffer b) for this warp's 128 rows: the
+// accumulator's digit columns 0..4 collect H4 x (s_{j+k} + s_{j-k}), columns
+// 5..7 collect R4 x s_{j+k} s_{j-k}.  Columns are grouped into runs of one
+// mode (zones and row ranges are monotone in k: a chunk has few runs).
 template <bool kCross>
 __device__ __forceinline__ void cert_mma_chunk(const CertIO& io, const CertLane& ln, uint32_t c,
-                                               uint32_t b, int (&accL)[kCertTiles][4],
-                                               int (&accX)[kCertTiles][4], uint32_t& nmma) {
+                                               uint32_t b, int (&acc)[kCertTiles][4],
+                                               uint32_t& nmma) {
   const uint32_t kb = 1 + c * kChunk;
   if (!cert_mma_work(io, kb)) return;
+#ifdef PSL_ABLATE_MMA
+  return;
+#endif
   const uint32_t w = threadIdx.x >> 5;
   // this warp's active rows (none: no MMAs)
   const int rw_lo = max(128 * (int)w, (int)io.r_lo), rw_hi = min(128 * (int)w + 127, (int)io.r_hi - 1);
@@ -340,36 +420,49 @@ __device__ __forceinline__ void cert_mma_chunk(const CertIO& io, const CertLane&
     starts &= starts - 1;
     const int ce = starts ? __ffs(starts) - 1 : kCertCols;
     const int md = __shfl_sync(FULL, my, cc);
-    const uint32_t f = ln.f + fo + 32 * cc, v = ln.v + fo + 32 * cc;
-    const uint32_t bh = ln.bh + bo + 32 * cc, br = ln.br + bo + 32 * cc;
+    const uint32_t f = ln.f + fo + 32 * cc, v = ln.v + fo + 32 * cc, bd = ln.bd + bo + 32 * cc;
     const int n = ce - cc;
-    nmma += (uint32_t)(n * kCertTiles) * (uint32_t)(((md & 1) && true) + ((md >> 1) & 1) + (kCross ? (md >> 2) & 1 : 0));
+    nmma += (uint32_t)(n * kCertTiles) * (uint32_t)((md & 1) + ((md >> 1) & 1) + ((md >> 2) & 1));
     switch (md) {
-      case 1: cert_cols<true, false, false>(f, v, bh, br, n, accL, accX); break;
-      case 2: cert_cols<false, true, false>(f, v, bh, br, n, accL, accX); break;
-      case 3: cert_cols<true, true, false>(f, v, bh, br, n, accL, accX); break;
-      case 7: if (kCross) cert_cols<true, true, true>(f, v, bh, br, n, accL, accX); break;
-      case 5: if (kCross) cert_cols<true, false, true>(f, v, bh, br, n, accL, accX); break;
-      case 6: if (kCross) cert_cols<false, true, true>(f, v, bh, br, n, accL, accX); break;
-      case 4: if (kCross) cert_cols<false, false, true>(f, v, bh, br, n, accL, accX); break;
+      case 1: cert_run<true, false, false>(f, v, bd, ln.dh, n, acc); break;
+      case 2: cert_run<false, true, false>(f, v, bd, ln.dh, n, acc); break;
+      case 3: cert_run<true, true, false>(f, v, bd, ln.dh, n, acc); break;
+      case 7: if (kCross) cert_run<true, true, true>(f, v, bd, ln.dh, n, acc); break;
+      case 5: if (kCross) cert_run<true, false, true>(f, v, bd, ln.dh, n, acc); break;
+      case 6: if (kCross) cert_run<false, true, true>(f, v, bd, ln.dh, n, acc); break;
+      case 4: if (kCross) cert_run<false, false, true>(f, v, bd, ln.dh, n, acc); break;
       default: break;
     }
   }
 }
 
-// Accumulator digits -> per-row doubles (rows 128w + 16r + g (+8)); the quad
-// holds digits 2 tig, 2 tig + 1 (weights 256^d), times the unit 2^q.
-__device__ __forceinline__ void cert_rows(const int (&acc)[kCertTiles][4], double unit, double* row) {
+// Accumulator digits -> per-row doubles (rows 128w + 16r + g (+8)).  The quad
+// holds digit columns 2 tig, 2 tig + 1: columns 0..4 are H4 digits (weight
+// 256^d x 2^qH), 5..7 R4 digits (256^(d-5) x 2^qR).
+__device__ __forceinline__ void cert_rows(const int (&acc)[kCertTiles][4], double unitH,
+                                          double unitR, double* lrow, double* xrow) {
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gid = lane >> 2, tig = lane & 3;
-  const double w0 = ldexp(1.0, 16 * tig), w1 = ldexp(1.0, 16 * tig + 8);
+  const int d0 = 2 * tig, d1 = 2 * tig + 1;
+  const double w0 = d0 < kDigH ? ldexp(unitH, 8 * d0) : ldexp(unitR, 8 * (d0 - kDigH));
+  const double w1 = d1 < kDigH ? ldexp(unitH, 8 * d1) : ldexp(unitR, 8 * (d1 - kDigH));
+  const bool h0 = d0 < kDigH, h1 = d1 < kDigH;
 #pragma unroll
   for (int r = 0; r < kCertTiles; ++r) {
 #pragma unroll
     for (int hh = 0; hh < 2; ++hh) {
-      double p = __dadd_rn(__dmul_rn((double)acc[r][2 * hh], w0), __dmul_rn((double)acc[r][2 * hh + 1], w1));
-      p = __dadd_rn(p, __shfl_xor_sync(FULL, p, 1));
-      p = __dadd_rn(p, __shfl_xor_sync(FULL, p, 2));
-      if (tig == 0) row[128 * warp + 16 * r + gid + 8 * hh] = __dmul_rn(p, unit);
+      const double x0 = __dmul_rn((double)acc[r][2 * hh], w0);
+      const double x1 = __dmul_rn((double)acc[r][2 * hh + 1], w1);
+      double pl = __dadd_rn(h0 ? x0 : 0.0, h1 ? x1 : 0.0);
+      double px = __dadd_rn(h0 ? 0.0 : x0, h1 ? 0.0 : x1);
+      pl = __dadd_rn(pl, __shfl_xor_sync(FULL, pl, 1));
+      px = __dadd_rn(px, __shfl_xor_sync(FULL, px, 1));
+      pl = __dadd_rn(pl, __shfl_xor_sync(FULL, pl, 2));
+      px = __dadd_rn(px, __shfl_xor_sync(FULL, px, 2));
+      if (tig == 0) {
+        const uint32_t rho = 128 * warp + 16 * r + gid + 8 * hh;
+        lrow[rho] = pl;
+        xrow[rho] = px;
+      }
     }
   }
 }
@@ -383,6 +476,9 @@ __device__ __forceinline__ void cert_band_cells(const CertIO& io, const CertSmem
   const uint32_t ke = min(kb + kChunk - 1, io.L - 1);
   const int32_t* rec = cs.rec + (size_t)b * kChunk;
   const uint32_t L = io.L;
+#ifdef PSL_ABLATE_BAND
+  return;
+#endif
   const double* __restrict__ lut = io.lut;
 #pragma unroll 1
   for (int band = 0; band < 2; ++band) {

@@ -24,6 +24,7 @@
 //    |C_k| >= PSL(pivot) - 8 can hold a neighbour's peak, and those are
 //    collected while streaming.
 #include <algorithm>
+#include <type_traits>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -156,9 +157,9 @@ struct Ctl {
   int32_t P_new;
   long long energy;
   // certified scan (psl_cert.cuh)
-  int32_t cert, need_exact, need_vl, cmp, cv_exact, c_q;
+  int32_t cert, need_exact, need_vl, cmp, cv_exact, c_qH, c_qR, c_ovf;
   double cv_lo, cv_hi;
-  double c_scale, c_unit, c_sconst, c_errconst;
+  double c_scaleH, c_unitH, c_scaleR, c_unitR, c_sconst, c_errconst;
   uint32_t m_lo, m_hi, M_lo, M_hi;
   double rs5[5][8];
 };
@@ -169,7 +170,7 @@ constexpr size_t kHfBytes = (size_t)kHCap * sizeof(int2);
 constexpr size_t kCtlBytes = (sizeof(Ctl) + 15) & ~size_t(15);
 // the exact sweep's records and the certified scan's buffers share one region
 // (psl_cert.cuh: 4 digit rows + 4 window copies + 2 record buffers)
-constexpr size_t kCertRegion = 4ull * 8 * (kChunk + 16) + 4ull * 4 * 1568 + 2ull * kChunk * 4 + 8ull * kGroup;
+constexpr size_t kCertRegion = 2ull * 8 * (kChunk + 16) + 4ull * 4 * 1568 + 2ull * kChunk * 4 + 8ull * kGroup + 3ull * kChunk * 4;
 constexpr size_t kMainBytes = (kTabBytes + kTailBytes) > kCertRegion ? (kTabBytes + kTailBytes) : kCertRegion;
 
 struct Smem {
@@ -925,10 +926,18 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
         const double amax = (double)Psrc + 4.0 * S.n_pending + 4.0;
         const double fa = pow_int_dev(amax, alpha);
         if (isfinite(fa) && fa * 8.0 * (double)L < 1e300) {
-          const int q = fa > 0.0 ? max(0, ilogb(2.0 * fa) - 61) : 0;
-          ctl->c_scale = ldexp(1.0, -q);
-          ctl->c_unit = ldexp(1.0, q);
-          ctl->c_q = q;
+          // digit units: |H4| <= 8 alpha Amax^(alpha-1), |R4| <= 16 alpha (alpha-1)
+          // Amax^(alpha-2) (mean-value bounds; x4 margin for rounding; a digit
+          // overflow is detected in the builder and sends the step to the exact sweep)
+          const double bh = 4.0 * fmin(2.0 * fa, 8.0 * alpha * pow(amax, (double)alpha - 1.0));
+          const double br = 4.0 * (alpha >= 2 ? fmin(2.0 * fa, 16.0 * alpha * (alpha - 1.0) *
+                                                             pow(amax, (double)alpha - 2.0))
+                                              : 2.0 * amax);
+          const int qh = bh > 0.0 ? max(0, ilogb(bh) + 1 - 38) : 0;
+          const int qr = br > 0.0 ? max(0, ilogb(br) + 1 - 22) : 0;
+          ctl->c_scaleH = ldexp(1.0, -qh); ctl->c_unitH = ldexp(1.0, qh); ctl->c_qH = qh;
+          ctl->c_scaleR = ldexp(1.0, -qr); ctl->c_unitR = ldexp(1.0, qr); ctl->c_qR = qr;
+          ctl->c_ovf = 0;
           ctl->cert = 1;
         }
       }
@@ -987,44 +996,47 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
         io.alpha = alpha; io.lut = lut;
         io.hcount = &ctl->hcount;
         io.hthr = s_Psrc - 4 * (int32_t)s_n_pending - 8;
-        io.scale = ctl->c_scale;
+        io.scaleH = ctl->c_scaleH; io.scaleR = ctl->c_scaleR;
         io.m_lo = ctl->m_lo; io.m_hi = ctl->m_hi; io.M_lo = ctl->M_lo; io.M_hi = ctl->M_hi;
-        int accL[kCertTiles][4], accX[kCertTiles][4];
+        int acc[kCertTiles][4];
 #pragma unroll
         for (int r = 0; r < kCertTiles; ++r)
 #pragma unroll
-          for (int e = 0; e < 4; ++e) { accL[r][e] = 0; accX[r][e] = 0; }
+          for (int e = 0; e < 4; ++e) acc[r][e] = 0;
+        bool ovf = false;
         double part[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         double Bs[kJ] = {0.0, 0.0, 0.0, 0.0};
         int32_t pmax = 0;
         uint32_t nmma = 0;
-        // C_k of chunk c + 2 is loaded while chunk c's MMAs run (DRAM latency off
-        // the builder's critical path)
-        int2 cpre = cert_load(io, 0);
-        cert_build(io, cs, 0, 0, sm.sb, pmax, part, cpre);
-        if (io.nchunks > 1) cpre = cert_load(io, 1);
+        // C_k of chunks c + 1 and c + 2 stream into shared memory (cp.async) while
+        // chunk c's MMAs run: DRAM latency off the builder's critical path
+        cert_prefetch(io, cs, 0);
+        if (io.nchunks > 1) cert_prefetch(io, cs, 1);
+        cert_build(io, cs, 0, 0, sm.sb, pmax, part, cert_take(cs, 0, io.nchunks > 1), ovf);
         __syncthreads();
         uint32_t c = 0;
         // phase 1: chunks holding k <= m_lo (both sides for every row: cross term)
         for (; c < io.nchunks && 1 + c * kChunk <= io.m_lo; ++c) {
           const uint32_t b = c & 1;
-          if (c + 1 < io.nchunks) cert_build(io, cs, c + 1, b ^ 1, sm.sb, pmax, part, cpre);
-          if (c + 2 < io.nchunks) cpre = cert_load(io, c + 2);
-          cert_mma_chunk<true>(io, ln, c, b, accL, accX, nmma);
+          if (c + 2 < io.nchunks) cert_prefetch(io, cs, c + 2);
+          if (c + 1 < io.nchunks)
+            cert_build(io, cs, c + 1, b ^ 1, sm.sb, pmax, part, cert_take(cs, c + 1, c + 2 < io.nchunks), ovf);
+          cert_mma_chunk<true>(io, ln, c, b, acc, nmma);
           if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, b, sm.sb, Bs);
           __syncthreads();
         }
-        cert_rows(accX, ctl->c_unit, cs.xrow);   // the cross term is complete
         for (; c < io.nchunks; ++c) {
           const uint32_t b = c & 1;
-          if (c + 1 < io.nchunks) cert_build(io, cs, c + 1, b ^ 1, sm.sb, pmax, part, cpre);
-          if (c + 2 < io.nchunks) cpre = cert_load(io, c + 2);
-          cert_mma_chunk<false>(io, ln, c, b, accL, accX, nmma);
+          if (c + 2 < io.nchunks) cert_prefetch(io, cs, c + 2);
+          if (c + 1 < io.nchunks)
+            cert_build(io, cs, c + 1, b ^ 1, sm.sb, pmax, part, cert_take(cs, c + 1, c + 2 < io.nchunks), ovf);
+          cert_mma_chunk<false>(io, ln, c, b, acc, nmma);
           if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, b, sm.sb, Bs);
           __syncthreads();
         }
         if ((t & 31) == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&ctl->st.n_mma),
                                      (unsigned long long)nmma);
+        if (ovf) atomicOr(&ctl->c_ovf, 1);
         if (seg == 0) {
           const int32_t Pn = block_max(ctl, pmax);
           if (t == 0) first_pass_state(ctl, a, w, Pn, 0.0, alpha);
@@ -1041,7 +1053,7 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
         }
         double* linrow = reinterpret_cast<double*>(cs.winF);   // [1024]
         const double* xrow = cs.xrow;
-        cert_rows(accL, ctl->c_unit, linrow);
+        cert_rows(acc, ctl->c_unitH, ctl->c_unitR, linrow, cs.xrow);
         __syncthreads();
         if (t == 0) {
           double sm5[5];
@@ -1055,8 +1067,9 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
           ctl->c_sconst = Sc;
           ctl->c_errconst = 2.0 * gamma_n((double)L / 256.0 + 80.0) * Sc + 8.0 * u * sm5[0] +
                             64.0 * u * (2.0 * sm5[0] + sm5[1]) +   // sum|H4| <= S_P + S_M, sum|R4| <= S_P
-                            (ctl->c_q > 0 ? ((double)L + (double)ctl->m_lo) * ctl->c_unit : 0.0) +
-                            1024.0 * u * (double)L * ctl->c_unit;
+                            (ctl->c_qH > 0 ? (double)L * ctl->c_unitH : 0.0) +
+                            (ctl->c_qR > 0 ? (double)ctl->m_lo * ctl->c_unitR : 0.0) +
+                            1024.0 * u * (double)L * (ctl->c_unitH + ctl->c_unitR);
         }
         __syncthreads();
         // per-row intervals [lo, hi] that provably hold the serial double V(j)
@@ -1114,7 +1127,7 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
           ctl->cp = ctl->best_psl; ctl->cpi = ctl->best_pi; ctl->cbad = ctl->bad;
           ctl->cv_exact = 0;
           const WalkState& S = ctl->st;
-          int need = amb || ctl->bad;
+          int need = amb || ctl->bad || ctl->c_ovf;
           if (!need) {
             ctl->cmp = compare_local(S, ctl->cv_lo, ctl->cv_hi, false, ctl->cv);
             need = ctl->cmp == 2;
