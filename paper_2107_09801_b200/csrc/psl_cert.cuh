@@ -38,8 +38,10 @@ constexpr size_t kWinBuf = 4ull * kWinBytes;             // one direction (4 cop
 constexpr size_t kCertRecBuf = (size_t)kChunk * sizeof(int32_t);
 constexpr size_t kCertRowBytes = (size_t)kGroup * sizeof(double);
 constexpr size_t kCertCBuf = (size_t)kChunk * sizeof(int32_t);     // C_k prefetch ring slot
-// [digits 2][win_f 2][win_r 2][rec 2][xrow][C ring 3]
-constexpr size_t kCertBytes = 2 * kLimbBuf + 4 * kWinBuf + 2 * kCertRecBuf + kCertRowBytes + 3 * kCertCBuf;
+constexpr size_t kCertB2 = (size_t)kGroup * sizeof(double);        // band-2 constants
+// [digits 2][win_f 2][win_r 2][rec 2][xrow][C ring 3][band2 M, E]
+constexpr size_t kCertBytes = 2 * kLimbBuf + 4 * kWinBuf + 2 * kCertRecBuf + kCertRowBytes +
+                              3 * kCertCBuf + 2 * kCertB2;
 // fixed-point digits per shift: H4 (the correlation coefficient) in digit
 // columns 0..4 (40 bits), R4 (the cross coefficient) in columns 5..7 (24 bits),
 // each with its own power-of-two unit; the MMA accumulates both into one
@@ -75,6 +77,8 @@ struct CertSmem {
   int32_t* rec;           // [2][kChunk]        C_k (band chunks only)
   double* xrow;           // [1024]             cross-term sums per row
   int32_t* cring;         // [3][kChunk]        C_k of chunks c+1, c+2 in flight (cp.async)
+  double* b2M;            // [1024] 4M_k = 2(e3+e1), k = M_lo+1+i (band 2: one side or none)
+  double* b2E;            // [1024] 4 e2_k
 };
 
 __device__ __forceinline__ CertSmem cert_carve(unsigned char* base) {
@@ -86,17 +90,20 @@ __device__ __forceinline__ CertSmem cert_carve(unsigned char* base) {
   m.xrow = reinterpret_cast<double*>(base + 2 * kLimbBuf + 4 * kWinBuf + 2 * kCertRecBuf);
   m.cring = reinterpret_cast<int32_t*>(base + 2 * kLimbBuf + 4 * kWinBuf + 2 * kCertRecBuf +
                                        kCertRowBytes);
+  m.b2M = reinterpret_cast<double*>(base + 2 * kLimbBuf + 4 * kWinBuf + 2 * kCertRecBuf +
+                                    kCertRowBytes + 3 * kCertCBuf);
+  m.b2E = m.b2M + kGroup;
   return m;
 }
 
 __device__ __forceinline__ bool cert_band_chunk(const CertIO& io, uint32_t c) {
   const uint32_t kb = 1 + c * kChunk, ke = kb + kChunk - 1;
-  return (kb <= io.m_hi && ke > io.m_lo) || (kb <= io.M_hi && ke > io.M_lo);
+  return kb <= io.m_hi && ke > io.m_lo;      // band 1 (band 2 is linear: MMA + prefix sums)
 }
 
-// any k column with nonzero H4 / R4 (zones Z1, Z3) in the chunk starting at kb
+// any k column with nonzero H4 / R4 (Z1, Z3, band 2) in the chunk starting at kb
 __device__ __forceinline__ bool cert_mma_work(const CertIO& io, uint32_t kb) {
-  return kb <= io.m_lo || (kb + kChunk - 1 > io.m_hi && kb <= io.M_lo);
+  return kb <= io.m_lo || (kb + kChunk - 1 > io.m_hi && kb <= io.M_hi);
 }
 
 // +-1 / 0 bytes of the staged windows
@@ -145,7 +152,6 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
   for (int i = 0; i < 2; ++i) {
     const uint32_t r = 2 * t + i;
     const uint32_t k = kb + r;
-    double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0, e4 = 0.0;
     bool want = false;
     int32_t cv = 0;
     if (k < io.L) {
@@ -165,11 +171,6 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
       const int32_t a = abs(cv);
       pmax = max(pmax, a);
       want = io.hlist != nullptr && a >= io.hthr;
-      e2 = __ldg(io.lut + a);
-      e4 = __ldg(io.lut + abs(cv - 4));
-      e3 = __ldg(io.lut + abs(cv - 2));
-      e1 = __ldg(io.lut + abs(cv + 2));
-      e0 = __ldg(io.lut + abs(cv + 4));
     }
     if (io.hlist) {
       const uint32_t m = __ballot_sync(FULL, want);
@@ -181,19 +182,28 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
         if (want) io.hlist[base + __popc(m & ((1u << lane) - 1))] = make_int2((int)k, cv);
       }
     }
+    // per zone only the terms it needs (PowerTable lookups, e_x = E_k(x))
     double H = 0.0, R = 0.0;
     if (k < io.L) {
       if (k <= io.m_lo) {                               // Z1: both sides for every row
+        const double e4 = __ldg(io.lut + abs(cv - 4)), e0 = __ldg(io.lut + abs(cv + 4));
+        const double e2 = __ldg(io.lut + abs(cv));
         H = __dsub_rn(e4, e0);
         R = __dsub_rn(__dadd_rn(e4, e0), __dmul_rn(2.0, e2));
         part[0] = __dadd_rn(part[0], __dadd_rn(__dadd_rn(e4, e0), __dmul_rn(2.0, e2)));
       } else if (k <= io.m_hi) {                        // band 1: exact terms per row
-      } else if (k <= io.M_lo) {                        // Z3: one side for every row
+      } else if (k <= io.M_hi) {                        // Z3 / band 2: one side or none
+        const double e3 = __ldg(io.lut + abs(cv - 2)), e1 = __ldg(io.lut + abs(cv + 2));
         H = __dmul_rn(2.0, __dsub_rn(e3, e1));
-        part[1] = __dadd_rn(part[1], __dmul_rn(2.0, __dadd_rn(e3, e1)));
-      } else if (k <= io.M_hi) {                        // band 2
+        const double m4 = __dmul_rn(2.0, __dadd_rn(e3, e1));
+        if (k <= io.M_lo) {
+          part[1] = __dadd_rn(part[1], m4);
+        } else {                                        // band 2: per-row prefix sums
+          cs.b2M[k - io.M_lo - 1] = m4;
+          cs.b2E[k - io.M_lo - 1] = __dmul_rn(4.0, __ldg(io.lut + abs(cv)));
+        }
       } else {                                          // Z5: no side for any row
-        part[2] = __dadd_rn(part[2], __dmul_rn(4.0, e2));
+        part[2] = __dadd_rn(part[2], __dmul_rn(4.0, __ldg(io.lut + abs(cv))));
       }
     }
     // fixed point -> balanced base-256 digits: H4 in bytes 0..4, R4 in 5..7
@@ -205,6 +215,7 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
     VD[i] = (dh & 0xFFFFFFFFFFull) | ((dr & 0xFFFFFFull) << 40);
     if (band) rec[r] = cv;
   }
+  if (!cert_mma_work(io, kb)) return;   // no MMA reads this chunk's digits / windows
   // digit d of the two k's -> one u16 per digit row (PRMT gathers byte d of each)
   unsigned char* lh = cs.limbH + (size_t)b * kLimbBuf + 2 * t;
   const uint32_t h0l = (uint32_t)VD[0], h0h = (uint32_t)(VD[0] >> 32);
@@ -215,9 +226,8 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
     const uint32_t h = __byte_perm(d < 4 ? h0l : h0h, d < 4 ? h1l : h1h, sel);
     *reinterpret_cast<uint16_t*>(lh + d * kLimbStride) = (uint16_t)h;
   }
-  // sequence windows: 4 copies x 392 words per direction, only for chunks with
-  // MMA work and only the directions some row still has in range
-  if (!cert_mma_work(io, kb)) return;
+  // sequence windows: 4 copies x 392 words per direction, only the directions
+  // some row still has in range
 #ifdef PSL_ABLATE_STAGE
   return;
 #endif
@@ -404,7 +414,7 @@ __device__ __forceinline__ void cert_mma_chunk(const CertIO& io, const CertLane&
   auto mode = [&](int cc) -> int {
     const uint32_t k0 = kb + 32 * cc, k1 = k0 + 31;
     if (k0 >= io.L) return 0;
-    const bool lin = k0 <= io.m_lo || (k1 > io.m_hi && k0 <= io.M_lo);
+    const bool lin = k0 <= io.m_lo || (k1 > io.m_hi && k0 <= io.M_hi);
     const bool fwd = lin && jw_lo + k0 < (long long)io.L;
     const bool rev = lin && (long long)k0 <= jw_hi;
     const bool crs = kCross && k0 <= io.m_lo;
@@ -467,7 +477,7 @@ __device__ __forceinline__ void cert_rows(const int (&acc)[kCertTiles][4], doubl
   }
 }
 
-// Exact band terms of chunk c for this thread's rows rho = 4t + m: per cell
+// Exact band-1 terms of chunk c for this thread's rows rho = 4t + m: per cell
 // pow_int(|C_k - 2x|, alpha), x = s_j (s_{j-k} [k <= j] + s_{j+k} [j+k < L]).
 __device__ __forceinline__ void cert_band_cells(const CertIO& io, const CertSmem& cs, uint32_t c,
                                                 uint32_t b, const uint32_t* __restrict__ sb,
@@ -480,11 +490,10 @@ __device__ __forceinline__ void cert_band_cells(const CertIO& io, const CertSmem
   return;
 #endif
   const double* __restrict__ lut = io.lut;
-#pragma unroll 1
-  for (int band = 0; band < 2; ++band) {
-    const uint32_t blo = max(kb, (band ? io.M_lo : io.m_lo) + 1);
-    const uint32_t bhi = min(ke, band ? io.M_hi : io.m_hi);
-    if (blo > bhi) continue;
+  {
+    const uint32_t blo = max(kb, io.m_lo + 1);
+    const uint32_t bhi = min(ke, io.m_hi);
+    if (blo > bhi) return;
 #pragma unroll
     for (int m = 0; m < kJ; ++m) {
       const uint32_t rho = 4 * threadIdx.x + m;
@@ -511,6 +520,32 @@ __device__ __forceinline__ void cert_band_cells(const CertIO& io, const CertSmem
       Bs[m] = s;
     }
   }
+}
+
+// Band 2 (k in (M_lo, M_hi]): row j's constant is sum_{k <= M_j} 4M_k +
+// sum_{k > M_j} 4 e2_k.  Warp 0 turns b2M into inclusive prefix sums and b2E
+// into inclusive suffix sums (32 serial terms per lane + a shuffle scan).
+__device__ __forceinline__ void cert_band2_scan(const CertSmem& cs, uint32_t nb2) {
+  if (threadIdx.x >= 32) return;
+  const uint32_t lane = threadIdx.x;
+  const uint32_t per = (nb2 + 31) / 32, lo = lane * per, hi = min(nb2, lo + per);
+  double sm = 0.0, se = 0.0;
+  for (uint32_t i = lo; i < hi; ++i) { sm = __dadd_rn(sm, cs.b2M[i]); cs.b2M[i] = sm; }
+  for (uint32_t i = hi; i-- > lo;) { se = __dadd_rn(se, cs.b2E[i]); cs.b2E[i] = se; }
+  double pm = sm, ps = se;   // inclusive scans over lanes (prefix for M, suffix for E)
+  for (int o = 1; o < 32; o <<= 1) {
+    const double a = __shfl_up_sync(FULL, pm, o), bb = __shfl_down_sync(FULL, ps, o);
+    if ((int)lane >= o) pm = __dadd_rn(pm, a);
+    if ((int)lane + o < 32) ps = __dadd_rn(ps, bb);
+  }
+  const double offm = __dsub_rn(pm, sm), offe = __dsub_rn(ps, se);   // exclusive carries
+  for (uint32_t i = lo; i < hi; ++i) {
+    cs.b2M[i] = __dadd_rn(cs.b2M[i], offm);
+    cs.b2E[i] = __dadd_rn(cs.b2E[i], offe);
+  }
+}
+__device__ __forceinline__ double cert_band2_const(const CertSmem& cs, uint32_t nb2, uint32_t i) {
+  return __dadd_rn(i > 0 ? cs.b2M[i - 1] : 0.0, i < nb2 ? cs.b2E[i] : 0.0);
 }
 
 // gamma_n = n u / (1 - n u), u = 2^-53 (Higham)

@@ -170,7 +170,7 @@ constexpr size_t kHfBytes = (size_t)kHCap * sizeof(int2);
 constexpr size_t kCtlBytes = (sizeof(Ctl) + 15) & ~size_t(15);
 // the exact sweep's records and the certified scan's buffers share one region
 // (psl_cert.cuh: 4 digit rows + 4 window copies + 2 record buffers)
-constexpr size_t kCertRegion = 2ull * 8 * (kChunk + 16) + 4ull * 4 * 1568 + 2ull * kChunk * 4 + 8ull * kGroup + 3ull * kChunk * 4;
+constexpr size_t kCertRegion = 2ull * 8 * (kChunk + 16) + 4ull * 4 * 1568 + 2ull * kChunk * 4 + 8ull * kGroup + 3ull * kChunk * 4 + 16ull * kGroup;
 constexpr size_t kMainBytes = (kTabBytes + kTailBytes) > kCertRegion ? (kTabBytes + kTailBytes) : kCertRegion;
 
 struct Smem {
@@ -1072,6 +1072,14 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
                             1024.0 * u * (double)L * (ctl->c_unitH + ctl->c_unitR);
         }
         __syncthreads();
+        if (ctl->M_hi > ctl->M_lo) cert_band2_scan(cs, ctl->M_hi - ctl->M_lo);
+        __syncthreads();
+        if (t == 0 && ctl->M_hi > ctl->M_lo) {
+          // scan rounding, absolute: relative to the band-2 totals
+          const uint32_t nb2 = ctl->M_hi - ctl->M_lo;
+          ctl->c_errconst += 4.0 * gamma_n(128.0) * (cs.b2M[nb2 - 1] + cs.b2E[0]);
+        }
+        __syncthreads();
         // per-row intervals [lo, hi] that provably hold the serial double V(j)
         {
           const double u = 0x1p-53;
@@ -1083,7 +1091,9 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
             if (rho < r_lo || rho >= r_hi) continue;
             const uint32_t j = (uint32_t)(j0 + (int32_t)rho);
             const double lin = linrow[rho], xv = xrow[rho];
-            const double B4 = __dmul_rn(4.0, Bs[m]);
+            const uint32_t Mj = max(j, L - 1 - j);
+            const double B4 = __dadd_rn(__dmul_rn(4.0, Bs[m]),
+                                        cert_band2_const(cs, ctl->M_hi - ctl->M_lo, Mj - ctl->M_lo));
             const int sj = sval(sm.sb, j);
             const double T4 = __dadd_rn(__dadd_rn(__dadd_rn(Sc, B4), sj > 0 ? lin : -lin), xv);
             const double Abs = Sc + B4 + fabs(lin) + fabs(xv);
