@@ -39,9 +39,8 @@ constexpr size_t kCertRecBuf = (size_t)kChunk * sizeof(int32_t);
 constexpr size_t kCertRowBytes = (size_t)kGroup * sizeof(double);
 constexpr size_t kCertCBuf = (size_t)kChunk * sizeof(int32_t);     // C_k prefetch ring slot
 constexpr size_t kCertB2 = (size_t)kGroup * sizeof(double);        // band-2 constants
-// [digits B][win_f B][win_r B][rec B][xrow][C ring 3][band2 M, E], B = kCertBufs
-constexpr int kCertBufs = 4;                                        // chunk pipeline depth
-constexpr size_t kCertBytes = kCertBufs * (kLimbBuf + 2 * kWinBuf + kCertRecBuf) + kCertRowBytes +
+// [digits 2][win_f 2][win_r 2][rec 2][xrow][C ring 3][band2 M, E]
+constexpr size_t kCertBytes = 2 * kLimbBuf + 4 * kWinBuf + 2 * kCertRecBuf + kCertRowBytes +
                               3 * kCertCBuf + 2 * kCertB2;
 // fixed-point digits per shift: H4 (the correlation coefficient) in digit
 // columns 0..4 (40 bits), R4 (the cross coefficient) in columns 5..7 (24 bits),
@@ -85,26 +84,17 @@ struct CertSmem {
 __device__ __forceinline__ CertSmem cert_carve(unsigned char* base) {
   CertSmem m;
   m.limbH = base;
-  m.winF = base + kCertBufs * kLimbBuf;
-  m.winV = m.winF + kCertBufs * kWinBuf;
-  m.rec = reinterpret_cast<int32_t*>(m.winV + kCertBufs * kWinBuf);
-  unsigned char* p = reinterpret_cast<unsigned char*>(m.rec) + kCertBufs * kCertRecBuf;
-  m.xrow = reinterpret_cast<double*>(p);
-  m.cring = reinterpret_cast<int32_t*>(p + kCertRowBytes);
-  m.b2M = reinterpret_cast<double*>(p + kCertRowBytes + 3 * kCertCBuf);
+  m.winF = base + 2 * kLimbBuf;
+  m.winV = base + 2 * kLimbBuf + 2 * kWinBuf;
+  m.rec = reinterpret_cast<int32_t*>(base + 2 * kLimbBuf + 4 * kWinBuf);
+  m.xrow = reinterpret_cast<double*>(base + 2 * kLimbBuf + 4 * kWinBuf + 2 * kCertRecBuf);
+  m.cring = reinterpret_cast<int32_t*>(base + 2 * kLimbBuf + 4 * kWinBuf + 2 * kCertRecBuf +
+                                       kCertRowBytes);
+  m.b2M = reinterpret_cast<double*>(base + 2 * kLimbBuf + 4 * kWinBuf + 2 * kCertRecBuf +
+                                    kCertRowBytes + 3 * kCertCBuf);
   m.b2E = m.b2M + kGroup;
   return m;
 }
-
-// named barriers of the chunk pipeline (0 is __syncthreads): chunk buffer b
-// full (main -> tensor group) / empty (tensor -> main), and the main group alone
-__device__ __forceinline__ void nb_sync(uint32_t id, uint32_t n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void nb_arrive(uint32_t id, uint32_t n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-constexpr uint32_t kBarFull = 1, kBarEmpty = 1 + kCertBufs, kBarMain = 1 + 2 * kCertBufs;
 
 __device__ __forceinline__ bool cert_band_chunk(const CertIO& io, uint32_t c) {
   const uint32_t kb = 1 + c * kChunk, ke = kb + kChunk - 1;
@@ -139,9 +129,8 @@ __device__ __forceinline__ void cert_prefetch(const CertIO& io, const CertSmem& 
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
-__device__ __forceinline__ int2 cert_take(const CertSmem& cs, uint32_t c, int pending) {
-  if (pending >= 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
-  else if (pending == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
+__device__ __forceinline__ int2 cert_take(const CertSmem& cs, uint32_t c, bool newest_pending) {
+  if (newest_pending) asm volatile("cp.async.wait_group 1;" ::: "memory");
   else asm volatile("cp.async.wait_group 0;" ::: "memory");
   const int32_t* p = cs.cring + (size_t)(c % 3) * kChunk + 2 * threadIdx.x;
   return make_int2(p[0], p[1]);
@@ -154,9 +143,6 @@ __device__ __forceinline__ int2 cert_take(const CertSmem& cs, uint32_t c, int pe
 __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs, uint32_t c,
                                            uint32_t b, const uint32_t* sb, int32_t& pmax,
                                            double (&part)[5], int2 cpre, bool& ovf) {
-#ifdef PSL_ABLATE_BUILD
-  return;
-#endif
   const uint32_t t = threadIdx.x;
   const uint32_t kb = 1 + c * kChunk;
   const bool band = cert_band_chunk(io, c);
@@ -305,10 +291,8 @@ struct CertLane {
   uint32_t f, v, bd;
   bool dh;                    // this lane's B column (= g) is an H4 digit (g < 5)
 };
-__device__ __forceinline__ uint32_t mma_tid() { return threadIdx.x - kThreads; }   // tensor-core group
-
 __device__ __forceinline__ CertLane cert_lane(const CertSmem& cs) {
-  const uint32_t lane = mma_tid() & 31, w = mma_tid() >> 5;
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t gid = lane >> 2, tig = lane & 3;
   const uint32_t base_f = 128 * w + gid + 4 * tig, af = gid & 3;
   const uint32_t base_v = kY0 - 128 * w - gid + 4 * tig, av = base_v & 3;
@@ -421,7 +405,7 @@ __device__ __forceinline__ void cert_mma_chunk(const CertIO& io, const CertLane&
 #ifdef PSL_ABLATE_MMA
   return;
 #endif
-  const uint32_t w = mma_tid() >> 5;
+  const uint32_t w = threadIdx.x >> 5;
   // this warp's active rows (none: no MMAs)
   const int rw_lo = max(128 * (int)w, (int)io.r_lo), rw_hi = min(128 * (int)w + 127, (int)io.r_hi - 1);
   if (rw_lo > rw_hi) return;
@@ -467,7 +451,7 @@ __device__ __forceinline__ void cert_mma_chunk(const CertIO& io, const CertLane&
 // 256^d x 2^qH), 5..7 R4 digits (256^(d-5) x 2^qR).
 __device__ __forceinline__ void cert_rows(const int (&acc)[kCertTiles][4], double unitH,
                                           double unitR, double* lrow, double* xrow) {
-  const uint32_t lane = mma_tid() & 31, warp = mma_tid() >> 5, gid = lane >> 2, tig = lane & 3;
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5, gid = lane >> 2, tig = lane & 3;
   const int d0 = 2 * tig, d1 = 2 * tig + 1;
   const double w0 = d0 < kDigH ? ldexp(unitH, 8 * d0) : ldexp(unitR, 8 * (d0 - kDigH));
   const double w1 = d1 < kDigH ? ldexp(unitH, 8 * d1) : ldexp(unitR, 8 * (d1 - kDigH));

@@ -161,7 +161,7 @@ struct Ctl {
   double cv_lo, cv_hi;
   double c_scaleH, c_unitH, c_scaleR, c_unitR, c_sconst, c_errconst;
   uint32_t m_lo, m_hi, M_lo, M_hi;
-  double rs5[5][16];
+  double rs5[5][8];
 };
 
 constexpr size_t kTabBytes = 2ull * kChunk * kRecDoubles * sizeof(double);
@@ -170,8 +170,8 @@ constexpr size_t kHfBytes = (size_t)kHCap * sizeof(int2);
 constexpr size_t kCtlBytes = (sizeof(Ctl) + 15) & ~size_t(15);
 // the exact sweep's records and the certified scan's buffers share one region
 // (psl_cert.cuh: 4 digit rows + 4 window copies + 2 record buffers)
-constexpr size_t kCertRegion = 4ull * (8 * (kChunk + 16) + 2 * 4 * 1568 + kChunk * 4) + 8ull * kGroup + 3ull * kChunk * 4 + 16ull * kGroup;
-constexpr size_t kExactMain = kTabBytes + kTailBytes;
+constexpr size_t kCertRegion = 2ull * 8 * (kChunk + 16) + 4ull * 4 * 1568 + 2ull * kChunk * 4 + 8ull * kGroup + 3ull * kChunk * 4 + 16ull * kGroup;
+constexpr size_t kMainBytes = (kTabBytes + kTailBytes) > kCertRegion ? (kTabBytes + kTailBytes) : kCertRegion;
 
 struct Smem {
   double* tab;     // [2][kChunk][8]
@@ -182,16 +182,12 @@ struct Smem {
                        // sb[0] zero pad, word i at sb[i+1], zero pads after
 };
 
-template <bool kCert = false>
 __device__ __forceinline__ Smem carve(unsigned char* base) {
-  // the exact sweep's records and (certified kernel) the certified scan's
-  // buffers share the first region
-  constexpr size_t main_bytes = kCert ? (kExactMain > kCertRegion ? kExactMain : kCertRegion) : kExactMain;
   Smem m;
   m.tab = reinterpret_cast<double*>(base);
   m.tail = reinterpret_cast<double*>(base + kTabBytes);
-  m.hf = reinterpret_cast<int2*>(base + main_bytes);
-  m.ctl = reinterpret_cast<Ctl*>(base + main_bytes + kHfBytes);
+  m.hf = reinterpret_cast<int2*>(base + kMainBytes);
+  m.ctl = reinterpret_cast<Ctl*>(base + kMainBytes + kHfBytes);
   m.sb = nullptr;
   return m;
 }
@@ -250,7 +246,7 @@ __device__ __forceinline__ double term(const SweepIO& io, int32_t a) {
 __device__ __forceinline__ void build_chunk(const SweepIO& io, uint32_t c, double* tab,
                                             double* tail, const uint32_t* sb, int32_t& pmax) {
 #pragma unroll 1
-  for (uint32_t r = threadIdx.x; r < (uint32_t)kChunk; r += blockDim.x) {
+  for (uint32_t r = threadIdx.x; r < (uint32_t)kChunk; r += kThreads) {
     const uint32_t k = 1 + c * kChunk + r;
     double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0, e4 = 0.0;
     bool want = false;
@@ -789,7 +785,7 @@ __global__ void __launch_bounds__(256) build_tables_kernel(const uint32_t* bits,
 }
 
 #include "psl_cert.cuh"
-static_assert(kCertBytes <= kCertRegion, "certified buffers exceed the shared region");
+static_assert(kCertBytes <= kMainBytes, "certified buffers exceed the shared region");
 
 // Neighbour PSL + thread-local reduce_scan over this thread's kJ neighbours
 // (ascending offset) + the block-wide lexicographic minima (ctl->best_*).
@@ -851,7 +847,7 @@ __device__ __forceinline__ void first_pass_state(Ctl* ctl, const RunArgs& a, uin
 __device__ __forceinline__ void filter_hlist(Ctl* ctl, const Smem& sm, const int2* hlist) {
   const int32_t thr = ctl->P_new - 8;
   const uint32_t hc = ctl->hcount;
-  for (uint32_t e = threadIdx.x; e < hc; e += blockDim.x) {
+  for (uint32_t e = threadIdx.x; e < hc; e += kThreads) {
     const int2 kc = hlist[e];
     if (abs(kc.y) >= thr) {
       const uint32_t slot = atomicAdd(&ctl->hf_count, 1u);
@@ -875,13 +871,10 @@ __device__ __forceinline__ int compare_local(const WalkState& S, double lo, doub
 // kCert: steps may be decided by the certified scan (psl_cert.cuh); any step
 // it cannot decide is re-scored by the exact sweep, so every decision (and
 // the RunRecord) is the reference's.
-// kCert runs 512 threads (one walk per SM): warps 0-7 are the main group
-// (control, builder, bands, exact fallback), warps 8-15 the tensor-core group
-// of the certified scan; the exact kernel runs the main group alone.
 template <bool kCert>
-__global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2) run_kernel(RunArgs a) {
+__global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  Smem sm = carve<kCert>(smem_raw);
+  Smem sm = carve(smem_raw);
   Ctl* ctl = sm.ctl;
   const uint32_t w = blockIdx.x, t = threadIdx.x;
   const uint32_t L = a.L, nw = a.nwords;
@@ -1015,40 +1008,32 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         double Bs[kJ] = {0.0, 0.0, 0.0, 0.0};
         int32_t pmax = 0;
         uint32_t nmma = 0;
-        // roles: the main group (t < 256) builds chunk c into buffer c % kCertBufs
-        // (C_k streamed into shared memory by cp.async two chunks ahead) and sums
-        // its band cells; the tensor-core group runs the MMAs of chunk c once the
-        // buffer is full.  Named barriers let the builder run up to kCertBufs
-        // chunks ahead.
-        if (t < (uint32_t)kThreads) {
-          const uint32_t n = io.nchunks;
-          cert_prefetch(io, cs, 0);
-          if (n > 1) cert_prefetch(io, cs, 1);
-          for (uint32_t c = 0; c < n; ++c) {
-            const uint32_t b = c % kCertBufs;
-            if (c >= (uint32_t)kCertBufs) nb_sync(kBarEmpty + b, 2 * kThreads);
-            if (c + 2 < n) cert_prefetch(io, cs, c + 2);
-            const int pending = (int)min(2u, n - 1 - c);
-            cert_build(io, cs, c, b, sm.sb, pmax, part, cert_take(cs, c, pending), ovf);
-            nb_arrive(kBarFull + b, 2 * kThreads);
-            if (cert_band_chunk(io, c)) {
-              nb_sync(kBarMain, kThreads);            // all of chunk c's records written
-              cert_band_cells(io, cs, c, b, sm.sb, Bs);
-            }
-          }
-          // consume the tensor group's last releases (keeps the barriers balanced)
-          for (uint32_t c = n > (uint32_t)kCertBufs ? n - kCertBufs : 0; c < n; ++c)
-            nb_sync(kBarEmpty + c % kCertBufs, 2 * kThreads);
-        } else {
-          for (uint32_t c = 0; c < io.nchunks; ++c) {
-            const uint32_t b = c % kCertBufs;
-            nb_sync(kBarFull + b, 2 * kThreads);
-            if (1 + c * kChunk <= io.m_lo) cert_mma_chunk<true>(io, ln, c, b, acc, nmma);
-            else cert_mma_chunk<false>(io, ln, c, b, acc, nmma);
-            nb_arrive(kBarEmpty + b, 2 * kThreads);
-          }
-        }
+        // C_k of chunks c + 1 and c + 2 stream into shared memory (cp.async) while
+        // chunk c's MMAs run: DRAM latency off the builder's critical path
+        cert_prefetch(io, cs, 0);
+        if (io.nchunks > 1) cert_prefetch(io, cs, 1);
+        cert_build(io, cs, 0, 0, sm.sb, pmax, part, cert_take(cs, 0, io.nchunks > 1), ovf);
         __syncthreads();
+        uint32_t c = 0;
+        // phase 1: chunks holding k <= m_lo (both sides for every row: cross term)
+        for (; c < io.nchunks && 1 + c * kChunk <= io.m_lo; ++c) {
+          const uint32_t b = c & 1;
+          if (c + 2 < io.nchunks) cert_prefetch(io, cs, c + 2);
+          if (c + 1 < io.nchunks)
+            cert_build(io, cs, c + 1, b ^ 1, sm.sb, pmax, part, cert_take(cs, c + 1, c + 2 < io.nchunks), ovf);
+          cert_mma_chunk<true>(io, ln, c, b, acc, nmma);
+          if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, b, sm.sb, Bs);
+          __syncthreads();
+        }
+        for (; c < io.nchunks; ++c) {
+          const uint32_t b = c & 1;
+          if (c + 2 < io.nchunks) cert_prefetch(io, cs, c + 2);
+          if (c + 1 < io.nchunks)
+            cert_build(io, cs, c + 1, b ^ 1, sm.sb, pmax, part, cert_take(cs, c + 1, c + 2 < io.nchunks), ovf);
+          cert_mma_chunk<false>(io, ln, c, b, acc, nmma);
+          if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, b, sm.sb, Bs);
+          __syncthreads();
+        }
         if ((t & 31) == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&ctl->st.n_mma),
                                      (unsigned long long)nmma);
         if (ovf) atomicOr(&ctl->c_ovf, 1);
@@ -1068,13 +1053,13 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         }
         double* linrow = reinterpret_cast<double*>(cs.winF);   // [1024]
         const double* xrow = cs.xrow;
-        if (t >= (uint32_t)kThreads) cert_rows(acc, ctl->c_unitH, ctl->c_unitR, linrow, cs.xrow);
+        cert_rows(acc, ctl->c_unitH, ctl->c_unitR, linrow, cs.xrow);
         __syncthreads();
         if (t == 0) {
           double sm5[5];
           for (int i = 0; i < 5; ++i) {
             double v = 0.0;
-            for (int x = 0; x < (int)(blockDim.x >> 5); ++x) v = __dadd_rn(v, ctl->rs5[i][x]);
+            for (int x = 0; x < kThreads / 32; ++x) v = __dadd_rn(v, ctl->rs5[i][x]);
             sm5[i] = v;
           }
           const double u = 0x1p-53;
@@ -1353,7 +1338,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
     if (ctl->imp) {
       // best_seq = pivot with the best-PSL neighbour's flip (:385-387)
       const uint32_t pp = ctl->ppos;
-      for (uint32_t i = t; i < nw; i += blockDim.x) {
+      for (uint32_t i = t; i < nw; i += kThreads) {
         uint32_t v = bits_piv[i + 1];
         if (i == (pp >> 5)) v ^= 1u << (pp & 31);
         bits_best[i + 1] = v;
@@ -1365,7 +1350,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
     if (ctl->restart) {
       // back to the phase-local best (:405-406): bits from the snapshot, C via
       // the next pass (src_local); then flip_random_distinct (:407, :131-148)
-      for (uint32_t i = t; i < nw; i += blockDim.x) bits_piv[i + 1] = bits_loc[i + 1];
+      for (uint32_t i = t; i < nw; i += kThreads) bits_piv[i + 1] = bits_loc[i + 1];
       __syncthreads();
       if (t == 0) {
         WalkState& S = ctl->st;
@@ -1393,7 +1378,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
     }
     __syncthreads();
     if (ctl->improve) {
-      for (uint32_t i = t; i < nw; i += blockDim.x) bits_loc[i + 1] = bits_piv[i + 1];
+      for (uint32_t i = t; i < nw; i += kThreads) bits_loc[i + 1] = bits_piv[i + 1];
     }
     __syncthreads();
   }
@@ -1474,10 +1459,7 @@ __global__ void power_tables_kernel(double* lut, uint32_t n, uint32_t alpha1, ui
 
 }  // namespace
 
-size_t run_smem_bytes(bool cert) {
-  const size_t main_bytes = cert ? (kExactMain > kCertRegion ? kExactMain : kCertRegion) : kExactMain;
-  return main_bytes + kHfBytes + kCtlBytes;
-}
+size_t run_smem_bytes(uint32_t) { return kMainBytes + kHfBytes + kCtlBytes; }
 
 int launch_init_walks(const RunArgs& a, uint32_t n_walks, const uint64_t* d_seeds,
                       const int8_t* d_inits, uint32_t* d_bad, cudaStream_t s) {
@@ -1502,26 +1484,27 @@ int launch_table_only(const uint32_t* d_bits, int32_t* d_C, uint32_t L, uint32_t
 }
 
 int launch_run(const RunArgs& a, uint32_t n_walks, cudaStream_t s) {
+  const size_t smem = run_smem_bytes(a.nwords);
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(run_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)run_smem_bytes(true)) != cudaSuccess ||
+                             (int)run_smem_bytes((1u << 20) / 32 + 1)) != cudaSuccess ||
         cudaFuncSetAttribute(run_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)run_smem_bytes(false)) != cudaSuccess)
+                             (int)run_smem_bytes((1u << 20) / 32 + 1)) != cudaSuccess)
       return -1;
     attr = true;
   }
-  if (a.cert) run_kernel<true><<<n_walks, 2 * kThreads, run_smem_bytes(true), s>>>(a);
-  else run_kernel<false><<<n_walks, kThreads, run_smem_bytes(false), s>>>(a);
+  if (a.cert) run_kernel<true><<<n_walks, kThreads, smem, s>>>(a);
+  else run_kernel<false><<<n_walks, kThreads, smem, s>>>(a);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
 int launch_scan(const ScanArgs& a, cudaStream_t s) {
-  const size_t smem = run_smem_bytes(false);
+  const size_t smem = run_smem_bytes(a.nwords);
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)run_smem_bytes(false)) != cudaSuccess)
+                             (int)run_smem_bytes((1u << 20) / 32 + 1)) != cudaSuccess)
       return -1;
     attr = true;
   }
