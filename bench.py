@@ -262,12 +262,12 @@ def main():
     achieved = mma_ops / (ms * 1e-3)
     peak = mma_per_s * 16 * 8 * 32 * 2.0
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "r01_run_kernel.json")
+    prof = os.path.join(ROOT, "profiles", "r01_cert_kernel.json")
     if os.path.exists(prof) and L == L_DEFAULT and n == 1024:
         try:
             pj = json.load(open(prof))
             # ncu --set full capture of run_kernel on this workload, scaled to one
-            # step of this run's walk count (profiles/r01_run_kernel.txt)
+            # step of this run's walk count (profiles/r01_cert_kernel.txt)
             traffic = pj["dram_bytes_per_launch"] / pj.get("steps_per_launch", 1) \
                 * n_walks / float(pj.get("launch__grid_size", n_walks))
         except Exception:
@@ -277,7 +277,7 @@ def main():
         "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TOP/s (int8)",
         "frac": achieved / peak if peak else None,
         "traffic": traffic,
-        "traffic_unit": "DRAM bytes per step (ncu capture, profiles/r01_run_kernel.json)",
+        "traffic_unit": "DRAM bytes per step (ncu capture, profiles/r01_cert_kernel.json)",
         "algorithmic_bytes_per_step": n_walks * 8.0 * L,
         "peak_source": "measured live: mma.sync m16n8k32 s8 issue rate of this GPU "
                        "(psl_probe_imma); the kernel's MMAs are counted on the device",
