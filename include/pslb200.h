@@ -159,9 +159,10 @@ int psl_ctx_set_scan_mode(psl_ctx* ctx, int mode);
 int psl_ctx_scan_mode(psl_ctx* ctx);
 /* Totals over the walks whose records were read on this context: steps decided
  * by the certified scan alone, certified steps re-scored exactly, exact
- * value_local chains, and tensor-core mma.sync (m16n8k32 s8) instructions. */
+ * value_local chains, mma.sync (m16n8k32 s8) instructions per warp and
+ * tcgen05.mma (M128 N64 K32, kind::i8) instructions. */
 int psl_ctx_scan_stats(psl_ctx* ctx, uint64_t* certified, uint64_t* refined, uint64_t* chains,
-                       uint64_t* mma);
+                       uint64_t* mma, uint64_t* umma);
 /* Measurement helper: mma.sync m16n8k32 s8 instructions per second (all SMs). */
 int psl_probe_imma(psl_ctx* ctx, double* mma_per_s, char* err, size_t errlen);
 /* Measurement helper for the roofline (bench.py): FP64-add pipe throughput

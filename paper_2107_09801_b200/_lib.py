@@ -75,7 +75,8 @@ SIGNATURES = {
     "psl_ctx_set_scan_mode": (C.c_int, [C.c_void_p, C.c_int]),
     "psl_ctx_scan_mode": (C.c_int, [C.c_void_p]),
     "psl_ctx_scan_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
-                                     C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+                                     C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                     C.POINTER(C.c_uint64)]),
     "psl_probe_imma": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_char_p, C.c_size_t]),
     "psl_probe_peaks": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                   C.POINTER(C.c_double), C.c_char_p, C.c_size_t]),

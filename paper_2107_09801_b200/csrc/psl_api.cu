@@ -29,7 +29,7 @@ struct psl_ctx {
   cudaStream_t stream = nullptr;
   uint32_t launches = 0;
   int scan_mode = PSL_SCAN_AUTO;
-  uint64_t stats[4] = {0, 0, 0, 0};
+  uint64_t stats[5] = {0, 0, 0, 0, 0};
 };
 
 struct psl_walks {
@@ -51,7 +51,8 @@ struct psl_walks {
   uint32_t* bad = nullptr;      // [first bad flat index + 1, value]
   int8_t* sol = nullptr;        // unpack scratch for solutions
   double* lut = nullptr;        // [2][lut_n] power tables
-  uint64_t stats_read[4] = {0, 0, 0, 0};   // scan statistics already added to ctx->stats
+  double* b2 = nullptr;         // certified-scan band-2 scratch
+  uint64_t stats_read[5] = {0, 0, 0, 0, 0};   // scan statistics already added to ctx->stats
 };
 
 namespace {
@@ -189,8 +190,9 @@ int psl_ctx_set_scan_mode(psl_ctx* ctx, int mode) {
 int psl_ctx_scan_mode(psl_ctx* ctx) { return ctx ? ctx->scan_mode : -1; }
 
 int psl_ctx_scan_stats(psl_ctx* ctx, uint64_t* certified, uint64_t* refined, uint64_t* chains,
-                       uint64_t* mma) {
+                       uint64_t* mma, uint64_t* umma) {
   if (!ctx) return PSL_ERR_CONFIG;
+  if (umma) *umma = ctx->stats[4];
   if (certified) *certified = ctx->stats[0];
   if (refined) *refined = ctx->stats[1];
   if (chains) *chains = ctx->stats[2];
@@ -534,7 +536,7 @@ void psl_walks_destroy(psl_walks* w) {
   cudaStream_t s = w->ctx->stream;
   for (void* p : {(void*)w->st, (void*)w->Cpiv, (void*)w->Cloc, (void*)w->bits, (void*)w->hlist,
                   (void*)w->flips, (void*)w->events, (void*)w->traces, (void*)w->seeds,
-                  (void*)w->inits, (void*)w->bad, (void*)w->sol, (void*)w->lut})
+                  (void*)w->inits, (void*)w->bad, (void*)w->sol, (void*)w->lut, (void*)w->b2})
     if (p) cudaFreeAsync(p, s);
   delete w;
 }
@@ -601,6 +603,8 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
   a.lut_n = L + 8;
   AL(W->lut, 2ull * a.lut_n * sizeof(double));
   a.lut1 = W->lut; a.lut2 = W->lut + a.lut_n;
+  AL(W->b2, 2ull * kGroup * sizeof(double) * n_walks);
+  a.b2 = W->b2;
   a.st = W->st; a.Cpiv = W->Cpiv; a.Cloc = W->Cloc;
   a.bits_piv = W->bits;
   a.bits_loc = W->bits + a.w_stride * n_walks;
@@ -717,11 +721,12 @@ int psl_walks_records(psl_walks* w, psl_walk_record* records, int8_t* solutions,
     r.switches = S.switches;
     r.steps = S.steps;
   }
-  uint64_t tot[4] = {0, 0, 0, 0};
+  uint64_t tot[5] = {0, 0, 0, 0, 0};
   for (const WalkState& S : st) {
     tot[0] += S.n_cert; tot[1] += S.n_refine; tot[2] += S.n_vlchain; tot[3] += S.n_mma;
+    tot[4] += S.n_umma;
   }
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < 5; ++i) {
     w->ctx->stats[i] += tot[i] - w->stats_read[i];
     w->stats_read[i] = tot[i];
   }

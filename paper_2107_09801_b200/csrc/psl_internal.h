@@ -54,6 +54,7 @@ struct WalkState {
   uint64_t n_refine;    // certified steps that needed the exact sweep
   uint64_t n_vlchain;   // exact value_local chains over the local snapshot
   uint64_t n_mma;       // tensor-core mma.sync m16n8k32 instructions (per warp) issued
+  uint64_t n_umma;      // tcgen05.mma M128 N64 K32 (kind::i8) instructions issued
 };
 
 struct RunArgs {
@@ -83,6 +84,7 @@ struct RunArgs {
   size_t f_stride;
   psl_event* events;
   psl_trace* traces;
+  double* b2;           // certified scan scratch: [walk][2][1024] band-2 constants
   const double* lut1;   // PowerTable(L, alpha1) / (L, alpha2) on the device (sequence.hpp:72-84)
   const double* lut2;
   uint32_t lut_n;       // entries per table (> max |C_k| + 4)

@@ -162,6 +162,8 @@ struct Ctl {
   double c_scaleH, c_unitH, c_scaleR, c_unitR, c_sconst, c_errconst;
   uint32_t m_lo, m_hi, M_lo, M_hi;
   double rs5[5][8];
+  uint64_t mbar[2];          // tcgen05 commit barriers (iteration parity)
+  uint32_t tmem;             // TMEM base of this CTA's accumulators (kTmemCols columns)
 };
 
 constexpr size_t kTabBytes = 2ull * kChunk * kRecDoubles * sizeof(double);
@@ -170,7 +172,8 @@ constexpr size_t kHfBytes = (size_t)kHCap * sizeof(int2);
 constexpr size_t kCtlBytes = (sizeof(Ctl) + 15) & ~size_t(15);
 // the exact sweep's records and the certified scan's buffers share one region
 // (psl_cert.cuh: 4 digit rows + 4 window copies + 2 record buffers)
-constexpr size_t kCertRegion = 2ull * 8 * (kChunk + 16) + 4ull * 4 * 1568 + 2ull * kChunk * 4 + 8ull * kGroup + 3ull * kChunk * 4 + 16ull * kGroup;
+constexpr size_t kCertRegion = 2ull * 128 * 128 + 2ull * (2 * 50 * 128) + 2ull * 8 * (256 + 16) +
+                                 4ull * 4 * 1312 + 2ull * 256 * 4 + 3ull * 256 * 4;
 constexpr size_t kMainBytes = (kTabBytes + kTailBytes) > kCertRegion ? (kTabBytes + kTailBytes) : kCertRegion;
 
 struct Smem {
@@ -897,6 +900,22 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
   sm.sb = bits_piv;   // padded: word i at bits_piv[i + 1]
   __syncthreads();
   if (ctl->st.done || ctl->st.status != PSL_OK) return;
+  uint32_t mb_par[2] = {0u, 0u};   // next phase parity to wait for on ctl->mbar[0/1]
+  if (kCert) {
+    if (t < 32) {   // the certified scan's tcgen05 accumulators live in TMEM
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       smem_u32(&ctl->tmem)), "r"(kTmemCols) : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (t == 0) {
+      for (int i = 0; i < 2; ++i)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&ctl->mbar[i])) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
 
   const uint32_t ngroups = (a.n + kGroup - 1) / kGroup;
   for (;;) {
@@ -933,8 +952,8 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
           const double br = 4.0 * (alpha >= 2 ? fmin(2.0 * fa, 16.0 * alpha * (alpha - 1.0) *
                                                              pow(amax, (double)alpha - 2.0))
                                               : 2.0 * amax);
-          const int qh = bh > 0.0 ? max(0, ilogb(bh) + 1 - 38) : 0;
-          const int qr = br > 0.0 ? max(0, ilogb(br) + 1 - 22) : 0;
+          const int qh = bh > 0.0 ? max(0, ilogb(bh) + 1 - 62) : 0;
+          const int qr = br > 0.0 ? max(0, ilogb(br) + 1 - 62) : 0;
           ctl->c_scaleH = ldexp(1.0, -qh); ctl->c_unitH = ldexp(1.0, qh); ctl->c_qH = qh;
           ctl->c_scaleR = ldexp(1.0, -qr); ctl->c_unitR = ldexp(1.0, qr); ctl->c_qR = qr;
           ctl->c_ovf = 0;
@@ -980,7 +999,8 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
         }
         __syncthreads();
         CertIO io;
-        io.L = L; io.n = a.n; io.nchunks = a.nchunks; io.j0 = j0; io.r_lo = r_lo; io.r_hi = r_hi;
+        io.L = L; io.n = a.n; io.nchunks = (L - 1 + kCC - 1) / kCC;
+        io.j0 = j0; io.r_lo = r_lo; io.r_hi = r_hi; io.JT = j0 + (int32_t)r_lo;
         if (seg == 0) {
           io.Csrc = s_src_local ? Cloc : Cpiv;
           io.Cdst = Cpiv;
@@ -998,6 +1018,8 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
         io.hthr = s_Psrc - 4 * (int32_t)s_n_pending - 8;
         io.scaleH = ctl->c_scaleH; io.scaleR = ctl->c_scaleR;
         io.m_lo = ctl->m_lo; io.m_hi = ctl->m_hi; io.M_lo = ctl->M_lo; io.M_hi = ctl->M_hi;
+        io.b2M = a.b2 + (size_t)w * 2 * kGroup;
+        io.b2E = io.b2M + kGroup;
         int acc[kCertTiles][4];
 #pragma unroll
         for (int r = 0; r < kCertTiles; ++r)
@@ -1007,35 +1029,59 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
         double part[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         double Bs[kJ] = {0.0, 0.0, 0.0, 0.0};
         int32_t pmax = 0;
-        uint32_t nmma = 0;
-        // C_k of chunks c + 1 and c + 2 stream into shared memory (cp.async) while
-        // chunk c's MMAs run: DRAM latency off the builder's critical path
+        uint32_t nmma = 0, numma = 0, started = 0;
+        const uint32_t tmem = ctl->tmem;
+        // digit cores of shifts <= 0 (read by the first chunks' shifted N-groups) are zero
+        for (int32_t cz = -(int32_t)kLag; cz < 0; ++cz) cert_zero_digits(cs, cz);
+        // C_k streams into shared memory by cp.async two chunks ahead
+        const uint32_t nch = io.nchunks;
         cert_prefetch(io, cs, 0);
-        if (io.nchunks > 1) cert_prefetch(io, cs, 1);
-        cert_build(io, cs, 0, 0, sm.sb, pmax, part, cert_take(cs, 0, io.nchunks > 1), ovf);
-        __syncthreads();
-        uint32_t c = 0;
-        // phase 1: chunks holding k <= m_lo (both sides for every row: cross term)
-        for (; c < io.nchunks && 1 + c * kChunk <= io.m_lo; ++c) {
-          const uint32_t b = c & 1;
-          if (c + 2 < io.nchunks) cert_prefetch(io, cs, c + 2);
-          if (c + 1 < io.nchunks)
-            cert_build(io, cs, c + 1, b ^ 1, sm.sb, pmax, part, cert_take(cs, c + 1, c + 2 < io.nchunks), ovf);
-          cert_mma_chunk<true>(io, ln, c, b, acc, nmma);
-          if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, b, sm.sb, Bs);
+        if (nch > 1) cert_prefetch(io, cs, 1);
+        uint32_t issued = 0;        // bit (c & 1): iteration c committed MMAs not yet waited for
+        // iteration c: build chunk c, stage the sequence cores of forward kappa-chunk c and
+        // reversed kappa'-chunk c - kLag, issue their tcgen05 MMAs (one thread, async),
+        // then the zone-1 cross MMAs (mma.sync) and band-1 cells of chunk c
+        for (uint32_t c = 0; c < nch + kLag; ++c) {
+          if (issued & (1u << (c & 1))) {      // MMAs of iteration c - 2 read this buffer
+            mbar_wait(&ctl->mbar[c & 1], mb_par[c & 1]);
+            mb_par[c & 1] ^= 1u;
+            issued &= ~(1u << (c & 1));
+          }
+          if (c < nch) {
+            if (c + 2 < nch) cert_prefetch(io, cs, c + 2);
+            const int pending = (int)min(2u, nch - 1 - c);
+            cert_build(io, cs, c, sm.sb, pmax, part, cert_take(cs, c, pending), ovf);
+          } else {
+            cert_zero_digits(cs, c);
+          }
+          const uint32_t kb = cert_kb(c);
+          const bool fw = io.JT + (long long)kb < (long long)L &&
+                          cert_lin_in(io, (long long)kb - 896, (long long)kb + kCC - 1);
+          const long long kbr = (long long)(int32_t)cert_kb((int32_t)c - (int32_t)kLag);
+          const bool rv = (long long)io.JT + 127 - kbr >= 0 && cert_lin_in(io, kbr, kbr + kCC - 1 + 896);
+          cert_cores(io, cs, (int32_t)c, sm.sb, fw, rv);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncthreads();
+          if ((fw || rv)) {
+            if (t == 0) {
+              cert_issue(cs, tmem, (int32_t)c, fw, rv, started);
+              umma_commit(&ctl->mbar[c & 1]);
+            }
+            started |= (fw ? 1u : 0u) | (rv ? 2u : 0u);   // uniform copy of the issuer's flags
+            numma += (fw ? kCCols : 0) + (rv ? kCCols : 0);
+            issued |= 1u << (c & 1);
+          }
+          if (c < nch) {
+            cert_cross_chunk(io, ln, c, acc, nmma);
+            if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, sm.sb, Bs);
+          }
         }
-        for (; c < io.nchunks; ++c) {
-          const uint32_t b = c & 1;
-          if (c + 2 < io.nchunks) cert_prefetch(io, cs, c + 2);
-          if (c + 1 < io.nchunks)
-            cert_build(io, cs, c + 1, b ^ 1, sm.sb, pmax, part, cert_take(cs, c + 1, c + 2 < io.nchunks), ovf);
-          cert_mma_chunk<false>(io, ln, c, b, acc, nmma);
-          if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, b, sm.sb, Bs);
-          __syncthreads();
-        }
+        for (uint32_t bb = 0; bb < 2; ++bb)
+          if (issued & (1u << bb)) { mbar_wait(&ctl->mbar[bb], mb_par[bb]); mb_par[bb] ^= 1u; }
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if ((t & 31) == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&ctl->st.n_mma),
                                      (unsigned long long)nmma);
+        if (t == 0) ctl->st.n_umma += numma;
         if (ovf) atomicOr(&ctl->c_ovf, 1);
         if (seg == 0) {
           const int32_t Pn = block_max(ctl, pmax);
@@ -1051,9 +1097,13 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
             if (lane == 0) ctl->rs5[i][warp] = v;
           }
         }
-        double* linrow = reinterpret_cast<double*>(cs.winF);   // [1024]
+        __syncthreads();                       // windows / cores are free: row arrays alias them
+        double* linrow = cs.linrow;
         const double* xrow = cs.xrow;
-        cert_rows(acc, ctl->c_unitH, ctl->c_unitR, linrow, cs.xrow);
+        cert_cross_rows(acc, ctl->c_unitR, cs.xrow);
+        cert_lin_rows(tmem, false, started, ctl->c_unitH, io, linrow);
+        __syncthreads();
+        cert_lin_rows(tmem, true, started, ctl->c_unitH, io, linrow);
         __syncthreads();
         if (t == 0) {
           double sm5[5];
@@ -1072,12 +1122,12 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
                             1024.0 * u * (double)L * (ctl->c_unitH + ctl->c_unitR);
         }
         __syncthreads();
-        if (ctl->M_hi > ctl->M_lo) cert_band2_scan(cs, ctl->M_hi - ctl->M_lo);
+        if (ctl->M_hi > ctl->M_lo) cert_band2_scan(io, ctl->M_hi - ctl->M_lo);
         __syncthreads();
         if (t == 0 && ctl->M_hi > ctl->M_lo) {
           // scan rounding, absolute: relative to the band-2 totals
           const uint32_t nb2 = ctl->M_hi - ctl->M_lo;
-          ctl->c_errconst += 4.0 * gamma_n(128.0) * (cs.b2M[nb2 - 1] + cs.b2E[0]);
+          ctl->c_errconst += 4.0 * gamma_n(128.0) * (io.b2M[nb2 - 1] + io.b2E[0]);
         }
         __syncthreads();
         // per-row intervals [lo, hi] that provably hold the serial double V(j)
@@ -1093,7 +1143,7 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
             const double lin = linrow[rho], xv = xrow[rho];
             const uint32_t Mj = max(j, L - 1 - j);
             const double B4 = __dadd_rn(__dmul_rn(4.0, Bs[m]),
-                                        cert_band2_const(cs, ctl->M_hi - ctl->M_lo, Mj - ctl->M_lo));
+                                        cert_band2_const(io, ctl->M_hi - ctl->M_lo, Mj - ctl->M_lo));
             const int sj = sval(sm.sb, j);
             const double T4 = __dadd_rn(__dadd_rn(__dadd_rn(Sc, B4), sj > 0 ? lin : -lin), xv);
             const double Abs = Sc + B4 + fabs(lin) + fabs(xv);
@@ -1388,6 +1438,10 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
   if (t == 0) {
     if (ctl->st.status != PSL_OK) ctl->st.end_ns = globaltimer();
     *gst = ctl->st;
+  }
+  if (kCert && t < 32) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(ctl->tmem), "r"(kTmemCols) : "memory");
   }
 }
 

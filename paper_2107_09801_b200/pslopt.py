@@ -104,9 +104,11 @@ class Context:
     def scan_stats(self) -> dict:
         """Totals over records read on this context: certified steps, certified
         steps re-scored by the exact sweep, exact value_local chains."""
-        a, b, c, d = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
-        B.lib().psl_ctx_scan_stats(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d))
-        return {"certified": a.value, "refined": b.value, "chains": c.value, "mma": d.value}
+        a, b, c, d, e = C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64(), C.c_uint64()
+        B.lib().psl_ctx_scan_stats(self._h, C.byref(a), C.byref(b), C.byref(c), C.byref(d),
+                                   C.byref(e))
+        return {"certified": a.value, "refined": b.value, "chains": c.value, "mma": d.value,
+                "umma": e.value}
 
     def probe_imma(self) -> float:
         """mma.sync m16n8k32 s8 instructions per second on this GPU (all SMs)."""
