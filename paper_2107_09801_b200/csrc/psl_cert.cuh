@@ -301,21 +301,49 @@ __device__ __forceinline__ void cert_zero_digits(const CertSmem& cs, long long c
   }
 }
 
+// 20 sequence bytes for positions p0 + dir * x, x = 0..19, as 5 words (0 outside [0, L))
+__device__ __forceinline__ void seq20(const uint32_t* sb, int32_t p0, int dir, int32_t L, uint32_t (&w)[5]) {
+  const int32_t lo = dir > 0 ? p0 : p0 - 19, hi = lo + 19;
+  if (lo >= 0 && hi < L) {
+    uint32_t x = __funnelshift_r(sb[(lo >> 5) + 1], sb[(lo >> 5) + 2], (uint32_t)lo & 31) & 0xFFFFFu;
+    if (dir < 0) x = __brev(x) >> 12;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) w[q] = nib_bytes((x >> (4 * q)) & 0xFu);
+  } else {
+#pragma unroll
+    for (int q = 0; q < 5; ++q) w[q] = 0u;
+    if (hi >= 0 && lo < L)
+      for (int i = 0; i < 20; ++i) w[i >> 2] |= sbyte(sb, p0 + dir * i, (uint32_t)L) << (8 * (i & 3));
+  }
+}
+
 // Sequence cores of iteration c (buffer c & 1): forward kappa-chunk c
 // (core m row i = s[JT + kb + 8m + i + x]) and reversed kappa'-chunk c - kLag
-// (core m row i = s[JT + 127 - kb' - 8m - i - x]).
+// (core m row i = s[JT + 127 - kb' - 8m - i - x]).  Core row (m, i) is the 16
+// bytes at position offset r = 8m + i (address 16 r); a thread expands 20 bytes
+// once and emits the four rows r0..r0+3 by byte shifts.
 __device__ __forceinline__ void cert_cores(const CertIO& io, const CertSmem& cs, int32_t c,
                                            const uint32_t* sb, bool fwd, bool rev) {
   unsigned char* base = cs.acore + (size_t)(c & 1) * kABuf;
-  for (uint32_t idx = threadIdx.x; idx < 2 * kACores * 8; idx += kThreads) {
-    const uint32_t dir = idx >= kACores * 8 ? 1 : 0;
-    if (dir ? !rev : !fwd) continue;
-    const uint32_t rem = idx - dir * kACores * 8, m = rem >> 3, i = rem & 7;
-    const long long p0 = dir == 0 ? (long long)io.JT + cert_kb(c) + 8 * m + i
-                                  : (long long)io.JT + 127 - (long long)(int32_t)cert_kb(c - (int32_t)kLag) - 8 * m - i;
-    const uint4 v = seq16(sb, p0, dir == 0 ? 1 : -1, io.L);
-    *reinterpret_cast<uint4*>(base + (size_t)dir * kACores * 128 + m * 128 + i * 16) = v;
-  }
+  constexpr uint32_t kQuads = kACores * 2;    // 100 groups of 4 rows per direction
+  const uint32_t t = threadIdx.x;
+  uint32_t dir, g;
+  if (t < kQuads) { dir = 0; g = t; }
+  else if (t < 2 * kQuads) { dir = 1; g = t - kQuads; }
+  else return;
+  if (dir == 0 ? !fwd : !rev) return;
+  const int32_t p0 = dir == 0 ? io.JT + (int32_t)cert_kb(c) + 4 * (int32_t)g
+                              : io.JT + 127 - (int32_t)cert_kb(c - (int32_t)kLag) - 4 * (int32_t)g;
+  uint32_t w[5];
+  seq20(sb, p0, dir == 0 ? 1 : -1, (int32_t)io.L, w);
+  uint4* dst = reinterpret_cast<uint4*>(base + (size_t)dir * kACores * 128 + 64 * g);
+  dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+  dst[1] = make_uint4(__funnelshift_r(w[0], w[1], 8), __funnelshift_r(w[1], w[2], 8),
+                      __funnelshift_r(w[2], w[3], 8), __funnelshift_r(w[3], w[4], 8));
+  dst[2] = make_uint4(__funnelshift_r(w[0], w[1], 16), __funnelshift_r(w[1], w[2], 16),
+                      __funnelshift_r(w[2], w[3], 16), __funnelshift_r(w[3], w[4], 16));
+  dst[3] = make_uint4(__funnelshift_r(w[0], w[1], 24), __funnelshift_r(w[1], w[2], 24),
+                      __funnelshift_r(w[2], w[3], 24), __funnelshift_r(w[3], w[4], 24));
 }
 
 // ---- tcgen05 plumbing
@@ -347,7 +375,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
 }
 
 // The tensor-core MMAs of iteration c (one thread): forward kappa-chunk c and
-// reversed kappa'-chunk c - kLag, 8 K-steps of 32 shifts each.
+// reversed kappa'-chunk c - kLag, 8 K-steps of 32 shifts each.  Descriptors
+// advance by constants per K-step: A by 4 cores (512 B), B by 2 digit cores
+// (256 B; the double-mapped ring keeps every span contiguous).
 __device__ __forceinline__ void cert_issue(const CertSmem& cs, uint32_t tmem, int32_t c, bool fwd,
                                            bool rev, uint32_t& started) {
   const uint32_t abuf = smem_u32(cs.acore) + (uint32_t)(c & 1) * (uint32_t)kABuf;
@@ -355,24 +385,29 @@ __device__ __forceinline__ void cert_issue(const CertSmem& cs, uint32_t tmem, in
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (fwd) {
     // B core of K-step s, N-group g (sigma = 7 - g): k = kappa - 128 sigma -> q = 16c - 56 + 2s + h + 8g
+    const long long q0 = 16ll * c - 56;
+    uint64_t da = umma_desc(abuf, 256, 128);
+    uint64_t db = umma_desc(ring + (uint32_t)((((q0 % kRing) + kRing) % kRing) * 128), 128, 1024);
+#pragma unroll
     for (int s = 0; s < kCCols; ++s) {
-      const long long q0 = 16ll * c - 56 + 2 * s;
-      const uint32_t qa = ring + (uint32_t)((((q0 % kRing) + kRing) % kRing) * 128);
-      umma_i8(tmem, umma_desc(abuf + 128u * (4 * s), 256, 128), umma_desc(qa, 128, 1024),
-              (started & 1u) ? 1u : 0u);
-      started |= 1u;
+      umma_i8(tmem, da, db, (s > 0 || (started & 1u)) ? 1u : 0u);
+      da += 512 >> 4;
+      db += 256 >> 4;
     }
+    started |= 1u;
   }
   if (rev) {
-    const int32_t cr = c - (int32_t)kLag;
     // N-group g = sigma: k = kappa' + 128 sigma -> q = 16 cr + 2s + h + 8g
+    const long long q0 = 16ll * (c - (int32_t)kLag);
+    uint64_t da = umma_desc(abuf + (uint32_t)(kACores * 128), 256, 128);
+    uint64_t db = umma_desc(ring + (uint32_t)((((q0 % kRing) + kRing) % kRing) * 128), 128, 1024);
+#pragma unroll
     for (int s = 0; s < kCCols; ++s) {
-      const long long q0 = 16ll * cr + 2 * s;
-      const uint32_t qa = ring + (uint32_t)((((q0 % kRing) + kRing) % kRing) * 128);
-      umma_i8(tmem + 64, umma_desc(abuf + (uint32_t)(kACores * 128) + 128u * (4 * s), 256, 128),
-              umma_desc(qa, 128, 1024), (started & 2u) ? 1u : 0u);
-      started |= 2u;
+      umma_i8(tmem + 64, da, db, (s > 0 || (started & 2u)) ? 1u : 0u);
+      da += 512 >> 4;
+      db += 256 >> 4;
     }
+    started |= 2u;
   }
 }
 
