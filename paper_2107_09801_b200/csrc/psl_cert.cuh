@@ -234,18 +234,34 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
   // fixed point -> 8 balanced base-256 digits
   const long long hv = __double2ll_rn(__dmul_rn(H, io.scaleH));
   const long long rv = __double2ll_rn(__dmul_rn(R, io.scaleR));
-  ovf |= hv > kMaxD || hv < -kMaxD || rv > kMaxD || rv < -kMaxD;
+  // |v| < 2^61 (the units leave a 4x margin under 2^62 < kMaxD): top 3 bits all equal
+  ovf |= (((unsigned long long)hv + (1ull << 61)) >> 62) != 0 ||
+         (((unsigned long long)rv + (1ull << 61)) >> 62) != 0;
   const unsigned long long dh = ((unsigned long long)hv + 0x8080808080808080ull) ^ 0x8080808080808080ull;
-  // H4 digit core: core q = 16 c + t / 16, byte (d, t % 16); both ring mappings
+  // H4 digit core: core q = 16 c + t / 16 holds rows d (16 shifts each).  Lane
+  // x of a 4-lane group assembles row (x & 3) / row 4 + (x & 3) of the group's
+  // 4 shifts from the group's digit words (shuffles + byte permutes): two word
+  // stores per mapping instead of eight byte stores.
   {
-    unsigned char* p0 = dcore(cs, 16ll * c + (t >> 4)) + (t & 15);
-    unsigned char* p1 = p0 + kRing * 128;
+    const uint32_t lane = t & 31, x = lane & 3, gbase = lane & ~3u;
+    const uint32_t lo = (uint32_t)dh, hi = (uint32_t)(dh >> 32);
+    uint32_t L4[4], H4[4];
 #pragma unroll
-    for (int d = 0; d < 8; ++d) {
-      const unsigned char v = (unsigned char)(dh >> (8 * d));
-      p0[16 * d] = v;
-      p1[16 * d] = v;
+    for (int i = 0; i < 4; ++i) {
+      L4[i] = __shfl_sync(FULL, lo, gbase + i);
+      H4[i] = __shfl_sync(FULL, hi, gbase + i);
     }
+    // byte x of each of the 4 words -> one word (shift i's byte at position i)
+    const uint32_t sel = x | ((4 + x) << 4);
+    const uint32_t wl = __byte_perm(__byte_perm(L4[0], L4[1], sel), __byte_perm(L4[2], L4[3], sel), 0x5410);
+    const uint32_t wh = __byte_perm(__byte_perm(H4[0], H4[1], sel), __byte_perm(H4[2], H4[3], sel), 0x5410);
+    const uint32_t col = (t & 15) & ~3u;                 // first of the group's 4 shifts in the core
+    unsigned char* p0 = dcore(cs, 16ll * c + (t >> 4)) + col;
+    unsigned char* p1 = p0 + kRing * 128;
+    *reinterpret_cast<uint32_t*>(p0 + 16 * x) = wl;
+    *reinterpret_cast<uint32_t*>(p0 + 16 * (4 + x)) = wh;
+    *reinterpret_cast<uint32_t*>(p1 + 16 * x) = wl;
+    *reinterpret_cast<uint32_t*>(p1 + 16 * (4 + x)) = wh;
   }
   if (cert_band_chunk(io, c)) cs.rec[b * kCC + t] = cv;
   if (kb > io.m_lo) return;

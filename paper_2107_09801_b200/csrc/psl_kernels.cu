@@ -1063,8 +1063,9 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncthreads();
           if ((fw || rv)) {
-            if (t == 0) {
-              cert_issue(cs, tmem, (int32_t)c, fw, rv, started);
+            if (t == (uint32_t)kThreads - 32) {        // warp 7 stages no cores: it issues
+              uint32_t st = started;
+              cert_issue(cs, tmem, (int32_t)c, fw, rv, st);
               umma_commit(&ctl->mbar[c & 1]);
             }
             started |= (fw ? 1u : 0u) | (rv ? 2u : 0u);   // uniform copy of the issuer's flags
