@@ -208,6 +208,7 @@ def main():
     P._lib.lib().psl_probe_peaks(ctx.handle, ctypes.byref(dadd), ctypes.byref(lds),
                                  ctypes.byref(mhz), err, 256)
     mma_per_s = ctx.probe_imma()
+    umma_per_s = ctx.probe_umma()
 
     # setup: pivots (random_sequence), O(L^2) tables -- untimed, like the reference
     t_setup = time.perf_counter()
@@ -251,16 +252,17 @@ def main():
     walks.close()
 
     # dominant kernel: run_kernel, one launch for the K timed steps.  Steps are
-    # scored by the certified scan (int8 mma.sync correlations)
-    # and fall back to the exact DADD sweep where the intervals cannot decide;
-    # the bound is the legacy tensor pipe: achieved = int8 ops of the mma.sync
-    # instructions the kernel issued (device counter) / time, peak = the same
-    # instruction's measured throughput on this GPU.
+    # scored by the certified scan: the correlation on tcgen05
+    # (kind::i8 M128 N64 K32, accumulators in TMEM), the zone-1 cross term on
+    # mma.sync m16n8k32, the exact DADD sweep only where intervals cannot decide.
+    # achieved = int8 ops of the MMAs the kernel issued (device counters) / time;
+    # peak = the tcgen05 kind::i8 instruction's measured issue rate on this GPU.
     cells_per_step = n_walks * n * (L - 1)
     per_step_s = (ms * 1e-3) / args.steps
-    mma_ops = scan["mma"] * 16 * 8 * 32 * 2.0          # m16n8k32: 4096 MACs
-    achieved = mma_ops / (ms * 1e-3)
-    peak = mma_per_s * 16 * 8 * 32 * 2.0
+    umma_ops = scan["umma"] * 128 * 64 * 32 * 2.0
+    mma_ops = scan["mma"] * 16 * 8 * 32 * 2.0
+    achieved = (umma_ops + mma_ops) / (ms * 1e-3)
+    peak = umma_per_s * 128 * 64 * 32 * 2.0
     traffic = None
     prof = os.path.join(ROOT, "profiles", "r01_cert_kernel.json")
     if os.path.exists(prof) and L == L_DEFAULT and n == 1024:
@@ -279,8 +281,12 @@ def main():
         "traffic": traffic,
         "traffic_unit": "DRAM bytes per step (ncu capture, profiles/r01_cert_kernel.json)",
         "algorithmic_bytes_per_step": n_walks * 8.0 * L,
-        "peak_source": "measured live: mma.sync m16n8k32 s8 issue rate of this GPU "
-                       "(psl_probe_imma); the kernel's MMAs are counted on the device",
+        "peak_source": "measured live: tcgen05.mma kind::i8 M128 N64 K32 issue rate of this GPU "
+                       "(psl_probe_umma); the kernel's MMAs are counted on the device",
+        "tcgen05_tops": umma_ops / (ms * 1e-3) / 1e12,
+        "mma_sync_tops": mma_ops / (ms * 1e-3) / 1e12,
+        "mma_sync_peak_tops": mma_per_s * 16 * 8 * 32 * 2.0 / 1e12,
+        "umma_per_step": scan["umma"] / args.steps,
         "mma_per_step": scan["mma"] / args.steps,
         "cells_per_s": cells_per_step / per_step_s,
         "fp64_dadd_peak_gcell_s": dadd.value / 1e9,

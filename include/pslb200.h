@@ -163,8 +163,10 @@ int psl_ctx_scan_mode(psl_ctx* ctx);
  * tcgen05.mma (M128 N64 K32, kind::i8) instructions. */
 int psl_ctx_scan_stats(psl_ctx* ctx, uint64_t* certified, uint64_t* refined, uint64_t* chains,
                        uint64_t* mma, uint64_t* umma);
-/* Measurement helper: mma.sync m16n8k32 s8 instructions per second (all SMs). */
+/* Measurement helpers: mma.sync m16n8k32 s8 instructions per second and
+ * tcgen05.mma kind::i8 M128 N64 K32 instructions per second (all SMs). */
 int psl_probe_imma(psl_ctx* ctx, double* mma_per_s, char* err, size_t errlen);
+int psl_probe_umma(psl_ctx* ctx, double* mma_per_s, char* err, size_t errlen);
 /* Measurement helper for the roofline (bench.py): FP64-add pipe throughput
  * (cells/s at one DADD per cell), the divergent-LDS.64+DADD loop rate, and the
  * SM clock seen by the probe. */

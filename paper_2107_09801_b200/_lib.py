@@ -78,6 +78,7 @@ SIGNATURES = {
                                      C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                      C.POINTER(C.c_uint64)]),
     "psl_probe_imma": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_char_p, C.c_size_t]),
+    "psl_probe_umma": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_char_p, C.c_size_t]),
     "psl_probe_peaks": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                   C.POINTER(C.c_double), C.c_char_p, C.c_size_t]),
     "psl_default_alpha2": (C.c_uint32, [C.c_uint32]),

@@ -200,6 +200,17 @@ int psl_ctx_scan_stats(psl_ctx* ctx, uint64_t* certified, uint64_t* refined, uin
   return PSL_OK;
 }
 
+int psl_probe_umma(psl_ctx* ctx, double* mma_per_s, char* err, size_t errlen) {
+  int rc = device_ready(ctx, err, errlen);
+  if (rc) return rc;
+  int nsm = 0;
+  CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
+  const int n = probe_umma(nsm, ctx->stream, mma_per_s);
+  if (n < 0) return cuda_fail(err, errlen, cudaGetLastError(), "probe_umma");
+  ctx->launches += (uint32_t)n;
+  return PSL_OK;
+}
+
 int psl_probe_imma(psl_ctx* ctx, double* mma_per_s, char* err, size_t errlen) {
   int rc = device_ready(ctx, err, errlen);
   if (rc) return rc;

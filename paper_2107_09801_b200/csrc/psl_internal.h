@@ -122,5 +122,6 @@ int launch_power_tables(double* lut, uint32_t lut_n, uint32_t alpha1, uint32_t a
 int launch_apply_flip(uint32_t* d_bits, int32_t* d_C, uint32_t L, uint32_t j, cudaStream_t s);
 int probe_peaks(int nsm, cudaStream_t s, double* dadd_cps, double* lds_cps, double* mhz);
 int probe_imma(int nsm, cudaStream_t s, double* mma_per_s);
+int probe_umma(int nsm, cudaStream_t s, double* mma_per_s);
 
 }  // namespace pslb

@@ -1446,6 +1446,45 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
   }
 }
 
+// tcgen05.mma kind::i8 M128 N64 K32 issue rate (the certified scan's MMA shape):
+// one CTA per SM, one thread issues `per` MMAs back to back per commit.
+__global__ void __launch_bounds__(128) probe_umma_kernel(int reps, int per, int* out) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  __shared__ uint32_t tmem_base;
+  __shared__ __align__(8) uint64_t mbar;
+  for (int i = threadIdx.x; i < 8192 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem_raw)[i] = make_uint4(0x01010101u * (i & 3), 0u, 0x02020202u, 0u);
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_base)),
+                 "r"(64) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&mbar)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t base = smem_u32(smem_raw);
+  uint32_t par = 0;
+  for (int r = 0; r < reps; ++r) {
+    if (threadIdx.x == 0) {
+      const uint64_t da = umma_desc(base, 256, 128), db = umma_desc(base + 4096, 128, 1024);
+      for (int i = 0; i < per; ++i) umma_i8(tmem_base, da, db, i > 0 ? 1u : 0u);
+      umma_commit(&mbar);
+    }
+    mbar_wait(&mbar, par);
+    par ^= 1u;
+  }
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (threadIdx.x < 32)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(64) : "memory");
+  if (threadIdx.x == 0 && reps < 0) out[0] = 1;
+}
+
 // ScanJob / neighborhood_scan: neighbours of one given pivot, kGroup per CTA,
 // terms from the caller's PowerTable.
 __global__ void __launch_bounds__(kThreads, 2) scan_kernel(ScanArgs a) {
@@ -1643,6 +1682,29 @@ __global__ void __launch_bounds__(256) probe_imma_kernel(int reps, int* out) {
   int s = 0;
   for (int q = 0; q < 8; ++q) s += d[q][0] + d[q][1] + d[q][2] + d[q][3];
   if (s == 0x7fffffff) out[0] = s;
+}
+
+int probe_umma(int nsm, cudaStream_t s, double* mma_per_s) {
+  int* out = nullptr;
+  if (cudaMalloc(&out, 64) != cudaSuccess) return -1;
+  if (cudaFuncSetAttribute(probe_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384) != cudaSuccess)
+    return -1;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  const int reps = 400, per = 256;
+  probe_umma_kernel<<<nsm, 128, 16384, s>>>(4, per, out);
+  cudaEventRecord(a, s);
+  probe_umma_kernel<<<nsm, 128, 16384, s>>>(reps, per, out);
+  cudaEventRecord(b, s);
+  cudaEventSynchronize(b);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, a, b);
+  *mma_per_s = (double)nsm * reps * per / (ms * 1e-3);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(out);
+  return cudaGetLastError() == cudaSuccess ? 2 : -1;
 }
 
 int probe_imma(int nsm, cudaStream_t s, double* mma_per_s) {

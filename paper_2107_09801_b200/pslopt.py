@@ -110,6 +110,15 @@ class Context:
         return {"certified": a.value, "refined": b.value, "chains": c.value, "mma": d.value,
                 "umma": e.value}
 
+    def probe_umma(self) -> float:
+        """tcgen05.mma kind::i8 M128 N64 K32 instructions per second (all SMs)."""
+        v = C.c_double()
+        err = _err()
+        rc = B.lib().psl_probe_umma(self._h, C.byref(v), err, len(err))
+        if rc:
+            _raise(rc, err)
+        return v.value
+
     def probe_imma(self) -> float:
         """mma.sync m16n8k32 s8 instructions per second on this GPU (all SMs)."""
         v = C.c_double()
