@@ -193,7 +193,7 @@ def main():
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     nsm = torch.cuda.get_device_properties(local_rank).multi_processor_count
-    n_walks = args.walks or 2 * nsm   # two walk CTAs per SM (82 KB smem, 8 warps each)
+    n_walks = args.walks or nsm   # one walk CTA per SM (512 threads, ~160 KB smem)
     L, n = args.length, args.n_lmt
     total_steps = args.warmup + args.steps + 4
     params = P.SearchParams(length=L, seed=args.seed, alpha1=4, alpha2=P.default_alpha2(L),
@@ -344,7 +344,7 @@ def main():
             "dtype": "f64", "data": "synthetic",
             "config": {
                 "workload": f"m20 two-phase search: L={L}, {n_walks} independent walks per GPU "
-                            f"(two walk CTAs per SM), alpha1=4, alpha2={P.default_alpha2(L)}, "
+                            f"(one walk CTA per SM), alpha1=4, alpha2={P.default_alpha2(L)}, "
                             f"ls_lmt=2000, flip_lmt=10, n_lmt={n}",
                 "L": L, "walks_per_gpu": n_walks, "n_lmt": n, "parallelism": f"walks x{world}",
                 "l2": "inputs larger than L2: each step streams every walk's 4 MB C_k table "

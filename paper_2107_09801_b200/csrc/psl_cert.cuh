@@ -35,14 +35,15 @@
 // separable (s_{j+k} s_{j-k}) and stays on mma.sync (zone 1 only).
 #pragma once
 
-constexpr uint32_t kCC = 256;                 // shifts per certified chunk
+constexpr uint32_t kCC = 512;                 // shifts per certified chunk (one per thread)
+constexpr uint32_t kCertThreads = 2 * kThreads;   // the certified kernel's CTA (one walk per SM)
 constexpr int kCCols = kCC / 32;              // 32-shift columns per chunk
 constexpr int kCertTiles = 8;                 // mma.sync m16 row tiles per warp (128 rows)
-constexpr uint32_t kLag = 4;                  // reversed MMAs trail the builder by 4 chunks
-constexpr uint32_t kRing = 128;               // digit-core ring (x2 mapped), cores of 16 shifts
+constexpr uint32_t kLag = 3;                  // reversed MMAs trail the builder by 3 chunks
+constexpr uint32_t kRing = 256;               // digit-core ring (x2 mapped), cores of 16 shifts
 constexpr uint32_t kACores = (128 + kCC) / 8 + 2;   // sequence cores per direction per chunk
 constexpr int kLimbStride = kCC + 16;         // bytes per R digit row (bank spread)
-constexpr int kWinBytes = 1312;               // staged bytes per copy (328 words, = 8 mod 32)
+constexpr int kWinBytes = 1568;               // staged bytes per copy (392 words, = 8 mod 32)
 constexpr int kY0 = 1031;                     // origin of the reversed window
 constexpr size_t kLimbBuf = 8ull * kLimbStride;
 constexpr size_t kWinBuf = 4ull * kWinBytes;
@@ -256,7 +257,7 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
     const uint32_t wl = __byte_perm(__byte_perm(L4[0], L4[1], sel), __byte_perm(L4[2], L4[3], sel), 0x5410);
     const uint32_t wh = __byte_perm(__byte_perm(H4[0], H4[1], sel), __byte_perm(H4[2], H4[3], sel), 0x5410);
     const uint32_t col = (t & 15) & ~3u;                 // first of the group's 4 shifts in the core
-    unsigned char* p0 = dcore(cs, 16ll * c + (t >> 4)) + col;
+    unsigned char* p0 = dcore(cs, (long long)(kCC / 16) * c + (t >> 4)) + col;
     unsigned char* p1 = p0 + kRing * 128;
     *reinterpret_cast<uint32_t*>(p0 + 16 * x) = wl;
     *reinterpret_cast<uint32_t*>(p0 + 16 * (4 + x)) = wh;
@@ -279,7 +280,7 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
   constexpr int kW = kWinBytes / 4;
   // thread -> base word q of one direction: bytes 4q..4q+7 of the base copy
   // from one bit window, copy a word q = base bytes 4q+a..4q+a+3
-  for (int idx = (int)t; idx < 2 * kW; idx += kThreads) {
+  for (int idx = (int)t; idx < 2 * kW; idx += (int)blockDim.x) {
     const int dir = idx >= kW ? 1 : 0;
     const int q = dir ? idx - kW : idx;
     // fwd: byte i <-> position p0 + i; rev: byte i <-> position p0 - i (i = 0..7)
@@ -309,11 +310,11 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
 
 // Zero digit cores for chunk c (ring slots of chunks past the end / before the start)
 __device__ __forceinline__ void cert_zero_digits(const CertSmem& cs, long long c) {
-  const uint32_t t = threadIdx.x;   // 256 threads x 16 bytes = 16 cores
-  uint4* p0 = reinterpret_cast<uint4*>(dcore(cs, 16ll * c + (t >> 4)) + 16 * (t & 7));
-  if ((t & 15) < 8) {
-    *p0 = make_uint4(0u, 0u, 0u, 0u);
-    *reinterpret_cast<uint4*>(reinterpret_cast<unsigned char*>(p0) + kRing * 128) = make_uint4(0u, 0u, 0u, 0u);
+  constexpr uint32_t kCores = kCC / 16, kParts = kCores * 8;   // 16-byte parts per mapping
+  for (uint32_t i = threadIdx.x; i < 2 * kParts; i += blockDim.x) {
+    const uint32_t part = i % kParts, map = i / kParts;
+    unsigned char* p = dcore(cs, (long long)kCores * c + part / 8) + 16 * (part & 7) + map * kRing * 128;
+    *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u);
   }
 }
 
@@ -401,7 +402,7 @@ __device__ __forceinline__ void cert_issue(const CertSmem& cs, uint32_t tmem, in
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (fwd) {
     // B core of K-step s, N-group g (sigma = 7 - g): k = kappa - 128 sigma -> q = 16c - 56 + 2s + h + 8g
-    const long long q0 = 16ll * c - 56;
+    const long long q0 = (long long)(kCC / 16) * c - 56;
     uint64_t da = umma_desc(abuf, 256, 128);
     uint64_t db = umma_desc(ring + (uint32_t)((((q0 % kRing) + kRing) % kRing) * 128), 128, 1024);
 #pragma unroll
@@ -414,7 +415,7 @@ __device__ __forceinline__ void cert_issue(const CertSmem& cs, uint32_t tmem, in
   }
   if (rev) {
     // N-group g = sigma: k = kappa' + 128 sigma -> q = 16 cr + 2s + h + 8g
-    const long long q0 = 16ll * (c - (int32_t)kLag);
+    const long long q0 = (long long)(kCC / 16) * (c - (int32_t)kLag);
     uint64_t da = umma_desc(abuf + (uint32_t)(kACores * 128), 256, 128);
     uint64_t db = umma_desc(ring + (uint32_t)((((q0 % kRing) + kRing) % kRing) * 128), 128, 1024);
 #pragma unroll
@@ -598,7 +599,8 @@ __device__ __forceinline__ void cert_lin_rows(uint32_t tmem, bool rev, uint32_t 
 // Exact band-1 terms of chunk c for this thread's rows rho = 4t + m: per cell
 // pow_int(|C_k - 2x|, alpha), x = s_j (s_{j-k} [k <= j] + s_{j+k} [j+k < L]).
 __device__ __forceinline__ void cert_band_cells(const CertIO& io, const CertSmem& cs, uint32_t c,
-                                                const uint32_t* __restrict__ sb, double (&Bs)[kJ]) {
+                                                const uint32_t* __restrict__ sb, double (&Bs)[kJ],
+                                                uint32_t owner) {
   const uint32_t kb = cert_kb(c);
   const uint32_t ke = min(kb + kCC - 1, io.L - 1);
   const int32_t* rec = cs.rec + (size_t)(c & 1) * kCC;
@@ -612,7 +614,7 @@ __device__ __forceinline__ void cert_band_cells(const CertIO& io, const CertSmem
   if (blo > bhi) return;
 #pragma unroll
   for (int m = 0; m < kJ; ++m) {
-    const uint32_t rho = 4 * threadIdx.x + m;
+    const uint32_t rho = 4 * owner + m;
     if (rho < io.r_lo || rho >= io.r_hi) continue;
     const uint32_t j = (uint32_t)(io.j0 + (int32_t)rho);
     const uint32_t sjb = (sb[(j >> 5) + 1] >> (j & 31)) & 1u;

@@ -102,7 +102,7 @@ struct ScanArgs {
   int32_t* psls;        // [n+1]
 };
 
-size_t run_smem_bytes(uint32_t nwords);
+size_t run_smem_bytes(bool cert);
 
 // Launchers (return the number of kernels launched, or -1 on launch error).
 int launch_init_walks(const RunArgs& a, uint32_t n_walks, const uint64_t* d_seeds,

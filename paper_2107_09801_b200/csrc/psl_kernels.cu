@@ -161,7 +161,7 @@ struct Ctl {
   double cv_lo, cv_hi;
   double c_scaleH, c_unitH, c_scaleR, c_unitR, c_sconst, c_errconst;
   uint32_t m_lo, m_hi, M_lo, M_hi;
-  double rs5[5][8];
+  double rs5[5][16];
   uint64_t mbar[2];          // tcgen05 commit barriers (iteration parity)
   uint32_t tmem;             // TMEM base of this CTA's accumulators (kTmemCols columns)
 };
@@ -172,9 +172,9 @@ constexpr size_t kHfBytes = (size_t)kHCap * sizeof(int2);
 constexpr size_t kCtlBytes = (sizeof(Ctl) + 15) & ~size_t(15);
 // the exact sweep's records and the certified scan's buffers share one region
 // (psl_cert.cuh: 4 digit rows + 4 window copies + 2 record buffers)
-constexpr size_t kCertRegion = 2ull * 128 * 128 + 2ull * (2 * 50 * 128) + 2ull * 8 * (256 + 16) +
-                                 4ull * 4 * 1312 + 2ull * 256 * 4 + 3ull * 256 * 4;
-constexpr size_t kMainBytes = (kTabBytes + kTailBytes) > kCertRegion ? (kTabBytes + kTailBytes) : kCertRegion;
+constexpr size_t kCertRegion = 2ull * 256 * 128 + 2ull * (2 * 82 * 128) + 2ull * 8 * (512 + 16) +
+                                 4ull * 4 * 1568 + 2ull * 512 * 4 + 3ull * 512 * 4;
+constexpr size_t kExactMain = kTabBytes + kTailBytes;
 
 struct Smem {
   double* tab;     // [2][kChunk][8]
@@ -185,12 +185,16 @@ struct Smem {
                        // sb[0] zero pad, word i at sb[i+1], zero pads after
 };
 
+template <bool kCert = false>
 __device__ __forceinline__ Smem carve(unsigned char* base) {
+  // the exact sweep's records and (certified kernel) the certified scan's
+  // buffers share the first region
+  constexpr size_t main_bytes = kCert ? (kExactMain > kCertRegion ? kExactMain : kCertRegion) : kExactMain;
   Smem m;
   m.tab = reinterpret_cast<double*>(base);
   m.tail = reinterpret_cast<double*>(base + kTabBytes);
-  m.hf = reinterpret_cast<int2*>(base + kMainBytes);
-  m.ctl = reinterpret_cast<Ctl*>(base + kMainBytes + kHfBytes);
+  m.hf = reinterpret_cast<int2*>(base + main_bytes);
+  m.ctl = reinterpret_cast<Ctl*>(base + main_bytes + kHfBytes);
   m.sb = nullptr;
   return m;
 }
@@ -249,7 +253,7 @@ __device__ __forceinline__ double term(const SweepIO& io, int32_t a) {
 __device__ __forceinline__ void build_chunk(const SweepIO& io, uint32_t c, double* tab,
                                             double* tail, const uint32_t* sb, int32_t& pmax) {
 #pragma unroll 1
-  for (uint32_t r = threadIdx.x; r < (uint32_t)kChunk; r += kThreads) {
+  for (uint32_t r = threadIdx.x; r < (uint32_t)kChunk; r += blockDim.x) {
     const uint32_t k = 1 + c * kChunk + r;
     double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0, e4 = 0.0;
     bool want = false;
@@ -788,7 +792,7 @@ __global__ void __launch_bounds__(256) build_tables_kernel(const uint32_t* bits,
 }
 
 #include "psl_cert.cuh"
-static_assert(kCertBytes <= kMainBytes, "certified buffers exceed the shared region");
+static_assert(kCertBytes <= kCertRegion, "certified buffers exceed the shared region");
 
 // Neighbour PSL + thread-local reduce_scan over this thread's kJ neighbours
 // (ascending offset) + the block-wide lexicographic minima (ctl->best_*).
@@ -850,7 +854,7 @@ __device__ __forceinline__ void first_pass_state(Ctl* ctl, const RunArgs& a, uin
 __device__ __forceinline__ void filter_hlist(Ctl* ctl, const Smem& sm, const int2* hlist) {
   const int32_t thr = ctl->P_new - 8;
   const uint32_t hc = ctl->hcount;
-  for (uint32_t e = threadIdx.x; e < hc; e += kThreads) {
+  for (uint32_t e = threadIdx.x; e < hc; e += blockDim.x) {
     const int2 kc = hlist[e];
     if (abs(kc.y) >= thr) {
       const uint32_t slot = atomicAdd(&ctl->hf_count, 1u);
@@ -874,10 +878,13 @@ __device__ __forceinline__ int compare_local(const WalkState& S, double lo, doub
 // kCert: steps may be decided by the certified scan (psl_cert.cuh); any step
 // it cannot decide is re-scored by the exact sweep, so every decision (and
 // the RunRecord) is the reference's.
+// kCert: 512 threads, one walk per SM (the certified scan's digit ring and
+// chunk buffers need the shared memory); the exact kernel: 256 threads, two per
+// SM.  The exact sweep in the 512-thread kernel leaves threads >= 256 inactive.
 template <bool kCert>
-__global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
+__global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2) run_kernel(RunArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  Smem sm = carve(smem_raw);
+  Smem sm = carve<kCert>(smem_raw);
   Ctl* ctl = sm.ctl;
   const uint32_t w = blockIdx.x, t = threadIdx.x;
   const uint32_t L = a.L, nw = a.nwords;
@@ -1063,7 +1070,7 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncthreads();
           if ((fw || rv)) {
-            if (t == (uint32_t)kThreads - 32) {        // warp 7 stages no cores: it issues
+            if (t == kCertThreads - 32) {              // warp 15 stages no cores: it issues
               uint32_t st = started;
               cert_issue(cs, tmem, (int32_t)c, fw, rv, st);
               umma_commit(&ctl->mbar[c & 1]);
@@ -1072,9 +1079,9 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
             numma += (fw ? kCCols : 0) + (rv ? kCCols : 0);
             issued |= 1u << (c & 1);
           }
-          if (c < nch) {
-            cert_cross_chunk(io, ln, c, acc, nmma);
-            if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, sm.sb, Bs);
+          if (c < nch) {   // warps 0-7: zone-1 cross MMAs; warps 8-15: band-1 cells
+            if (t < (uint32_t)kThreads) cert_cross_chunk(io, ln, c, acc, nmma);
+            else if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, sm.sb, Bs, t - kThreads);
           }
         }
         for (uint32_t bb = 0; bb < 2; ++bb)
@@ -1101,7 +1108,7 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
         __syncthreads();                       // windows / cores are free: row arrays alias them
         double* linrow = cs.linrow;
         const double* xrow = cs.xrow;
-        cert_cross_rows(acc, ctl->c_unitR, cs.xrow);
+        if (t < (uint32_t)kThreads) cert_cross_rows(acc, ctl->c_unitR, cs.xrow);
         cert_lin_rows(tmem, false, started, ctl->c_unitH, io, linrow);
         __syncthreads();
         cert_lin_rows(tmem, true, started, ctl->c_unitH, io, linrow);
@@ -1110,7 +1117,7 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
           double sm5[5];
           for (int i = 0; i < 5; ++i) {
             double v = 0.0;
-            for (int x = 0; x < kThreads / 32; ++x) v = __dadd_rn(v, ctl->rs5[i][x]);
+            for (int x = 0; x < (int)(blockDim.x >> 5); ++x) v = __dadd_rn(v, ctl->rs5[i][x]);
             sm5[i] = v;
           }
           const double u = 0x1p-53;
@@ -1138,7 +1145,8 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
           const double Sc = ctl->c_sconst, E0 = ctl->c_errconst;
 #pragma unroll
           for (int m = 0; m < kJ; ++m) {
-            const uint32_t rho = kJ * t + m;
+            if (t < (uint32_t)kThreads) break;              // row owners: threads 256..511
+            const uint32_t rho = kJ * (t - kThreads) + m;
             if (rho < r_lo || rho >= r_hi) continue;
             const uint32_t j = (uint32_t)(j0 + (int32_t)rho);
             const double lin = linrow[rho], xv = xrow[rho];
@@ -1163,11 +1171,12 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
       {
         bool active[kJ];
         uint32_t jj[kJ];
-        const uint32_t ibase = kJ * t;
+        const uint32_t owner = t >= (uint32_t)kThreads ? t - kThreads : 0u;
+        const uint32_t ibase = kJ * owner;
 #pragma unroll
         for (int m = 0; m < kJ; ++m) {
-          const uint32_t rho = kJ * t + m;
-          active[m] = rho < a.n;
+          const uint32_t rho = kJ * owner + m;
+          active[m] = t >= (uint32_t)kThreads && rho < a.n;
           uint32_t j = start + 1 + rho;
           if (j >= L) j -= L;
           jj[m] = j;
@@ -1389,7 +1398,7 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
     if (ctl->imp) {
       // best_seq = pivot with the best-PSL neighbour's flip (:385-387)
       const uint32_t pp = ctl->ppos;
-      for (uint32_t i = t; i < nw; i += kThreads) {
+      for (uint32_t i = t; i < nw; i += blockDim.x) {
         uint32_t v = bits_piv[i + 1];
         if (i == (pp >> 5)) v ^= 1u << (pp & 31);
         bits_best[i + 1] = v;
@@ -1401,7 +1410,7 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
     if (ctl->restart) {
       // back to the phase-local best (:405-406): bits from the snapshot, C via
       // the next pass (src_local); then flip_random_distinct (:407, :131-148)
-      for (uint32_t i = t; i < nw; i += kThreads) bits_piv[i + 1] = bits_loc[i + 1];
+      for (uint32_t i = t; i < nw; i += blockDim.x) bits_piv[i + 1] = bits_loc[i + 1];
       __syncthreads();
       if (t == 0) {
         WalkState& S = ctl->st;
@@ -1429,7 +1438,7 @@ __global__ void __launch_bounds__(kThreads, 2) run_kernel(RunArgs a) {
     }
     __syncthreads();
     if (ctl->improve) {
-      for (uint32_t i = t; i < nw; i += kThreads) bits_loc[i + 1] = bits_piv[i + 1];
+      for (uint32_t i = t; i < nw; i += blockDim.x) bits_loc[i + 1] = bits_piv[i + 1];
     }
     __syncthreads();
   }
@@ -1489,7 +1498,7 @@ __global__ void __launch_bounds__(128) probe_umma_kernel(int reps, int per, int*
 // terms from the caller's PowerTable.
 __global__ void __launch_bounds__(kThreads, 2) scan_kernel(ScanArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  Smem sm = carve(smem_raw);
+  Smem sm = carve<false>(smem_raw);
   const uint32_t t = threadIdx.x;
   const uint32_t nw = a.nwords;
   sm.sb = a.bits;     // padded: word i at a.bits[i + 1]
@@ -1553,7 +1562,10 @@ __global__ void power_tables_kernel(double* lut, uint32_t n, uint32_t alpha1, ui
 
 }  // namespace
 
-size_t run_smem_bytes(uint32_t) { return kMainBytes + kHfBytes + kCtlBytes; }
+size_t run_smem_bytes(bool cert) {
+  const size_t main_bytes = cert ? (kExactMain > kCertRegion ? kExactMain : kCertRegion) : kExactMain;
+  return main_bytes + kHfBytes + kCtlBytes;
+}
 
 int launch_init_walks(const RunArgs& a, uint32_t n_walks, const uint64_t* d_seeds,
                       const int8_t* d_inits, uint32_t* d_bad, cudaStream_t s) {
@@ -1578,27 +1590,26 @@ int launch_table_only(const uint32_t* d_bits, int32_t* d_C, uint32_t L, uint32_t
 }
 
 int launch_run(const RunArgs& a, uint32_t n_walks, cudaStream_t s) {
-  const size_t smem = run_smem_bytes(a.nwords);
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(run_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)run_smem_bytes((1u << 20) / 32 + 1)) != cudaSuccess ||
+                             (int)run_smem_bytes(true)) != cudaSuccess ||
         cudaFuncSetAttribute(run_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)run_smem_bytes((1u << 20) / 32 + 1)) != cudaSuccess)
+                             (int)run_smem_bytes(false)) != cudaSuccess)
       return -1;
     attr = true;
   }
-  if (a.cert) run_kernel<true><<<n_walks, kThreads, smem, s>>>(a);
-  else run_kernel<false><<<n_walks, kThreads, smem, s>>>(a);
+  if (a.cert) run_kernel<true><<<n_walks, 2 * kThreads, run_smem_bytes(true), s>>>(a);
+  else run_kernel<false><<<n_walks, kThreads, run_smem_bytes(false), s>>>(a);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 
 int launch_scan(const ScanArgs& a, cudaStream_t s) {
-  const size_t smem = run_smem_bytes(a.nwords);
+  const size_t smem = run_smem_bytes(false);
   static bool attr = false;
   if (!attr) {
     if (cudaFuncSetAttribute(scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)run_smem_bytes((1u << 20) / 32 + 1)) != cudaSuccess)
+                             (int)run_smem_bytes(false)) != cudaSuccess)
       return -1;
     attr = true;
   }
