@@ -38,7 +38,7 @@
 constexpr uint32_t kCC = 512;                 // shifts per certified chunk (one per thread)
 constexpr uint32_t kCertThreads = 2 * kThreads;   // the certified kernel's CTA (one walk per SM)
 constexpr int kCCols = kCC / 32;              // 32-shift columns per chunk
-constexpr int kCertTiles = 8;                 // mma.sync m16 row tiles per warp (128 rows)
+constexpr int kCertTiles = 4;                 // mma.sync m16 row tiles per warp (64 rows, 16 warps)
 constexpr uint32_t kLag = 3;                  // reversed MMAs trail the builder by 3 chunks
 constexpr uint32_t kRing = 256;               // digit-core ring (x2 mapped), cores of 16 shifts
 constexpr uint32_t kACores = (128 + kCC) / 8 + 2;   // sequence cores per direction per chunk
@@ -446,10 +446,10 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
 }
 
 // Per-lane shared addresses (buffer 0) of this warp's cross-MMA operands.  Row
-// rho = 128 w + 16 r + g (+8 for a1/a3), fragment layout of mma.m16n8k32:
-//   forward word m (bytes 8m..8m+3 past base_f = 128w + g + 4t) = s_{j+k} for
+// rho = 64 w + 16 r + g (+8 for a1/a3), fragment layout of mma.m16n8k32:
+//   forward word m (bytes 8m..8m+3 past base_f = 64w + g + 4t) = s_{j+k} for
 //     m = 2r + 4c + {0: a0, 1: a1, 2: a2, 3: a3}
-//   reversed word m' (past base_v = kY0 - 128w - g + 4t) = s_{j-k} for
+//   reversed word m' (past base_v = kY0 - 64w - g + 4t) = s_{j-k} for
 //     m' = 4c - 2r + {0: a0, -1: a1, 2: a2, 1: a3}
 struct CertLane {
   uint32_t f, v, bd;
@@ -457,8 +457,8 @@ struct CertLane {
 __device__ __forceinline__ CertLane cert_lane(const CertSmem& cs) {
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t gid = lane >> 2, tig = lane & 3;
-  const uint32_t base_f = 128 * w + gid + 4 * tig, af = gid & 3;
-  const uint32_t base_v = kY0 - 128 * w - gid + 4 * tig, av = base_v & 3;
+  const uint32_t base_f = 64 * w + gid + 4 * tig, af = gid & 3;
+  const uint32_t base_v = kY0 - 64 * w - gid + 4 * tig, av = base_v & 3;
   CertLane l;
   l.f = smem_u32(cs.winF) + af * kWinBytes + (base_f - af);
   l.v = smem_u32(cs.winV) + av * kWinBytes + (base_v - av);
@@ -494,40 +494,34 @@ __device__ __forceinline__ Quad uv_q(const Quad& f, const Quad& v) {
 
 // n consecutive 32-k columns of cross MMAs.  Tile r = 2i (+1) of relative
 // column c reads the forward quad E (O) at e = c + i and the reversed quad E (O)
-// at e = c - i: each column loads one new quad per window (ring of four, slot =
-// e mod 4, resolved at compile time) instead of all eight.
+// at e = c - i (i = 0, 1): each column loads one new quad per window (rings of
+// two, slot = e mod 2, resolved at compile time).
 __device__ __forceinline__ void cert_cross_run(uint32_t f, uint32_t v, uint32_t bd, int n,
                                                int (&acc)[kCertTiles][4]) {
-  Quad fe[4], fo[4], ve[4], vo[4];
+  Quad fe[2], fo[2], ve[2], vo[2];
   fe[0] = qfe<0>(f); fo[0] = qfo<0>(f); fe[1] = qfe<1>(f); fo[1] = qfo<1>(f);
-  fe[2] = qfe<2>(f); fo[2] = qfo<2>(f); fe[3] = qfe<3>(f); fo[3] = qfo<3>(f);
-  // reversed quads e = 0, -1, -2, -3 -> slots 0, 3, 2, 1
-  ve[0] = qve<0>(v); vo[0] = qvo<0>(v); ve[3] = qve<-1>(v); vo[3] = qvo<-1>(v);
-  ve[2] = qve<-2>(v); vo[2] = qvo<-2>(v); ve[1] = qve<-3>(v); vo[1] = qvo<-3>(v);
+  // reversed quads e = 0, -1 -> slots 0, 1
+  ve[0] = qve<0>(v); vo[0] = qvo<0>(v); ve[1] = qve<-1>(v); vo[1] = qvo<-1>(v);
   auto column = [&](auto U) {
-    constexpr int u = decltype(U)::value;       // relative column mod 4
+    constexpr int u = decltype(U)::value;       // relative column mod 2
     const uint32_t b0 = lds32<0>(bd), b1 = lds32<16>(bd);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      imma_q(acc[2 * i], uv_q(fe[(u + i) & 3], ve[(u - i + 8) & 3]), b0, b1);
-      imma_q(acc[2 * i + 1], uv_q(fo[(u + i) & 3], vo[(u - i + 8) & 3]), b0, b1);
+    for (int i = 0; i < 2; ++i) {
+      imma_q(acc[2 * i], uv_q(fe[(u + i) & 1], ve[(u - i + 2) & 1]), b0, b1);
+      imma_q(acc[2 * i + 1], uv_q(fo[(u + i) & 1], vo[(u - i + 2) & 1]), b0, b1);
     }
-    // advance: forward e = c + 4 -> slot u; reversed e = c + 1 -> slot u + 1
+    // advance: forward e = c + 2 -> slot u; reversed e = c + 1 -> slot u + 1
     f += 32; v += 32; bd += 32;
-    fe[u] = qfe<3>(f); fo[u] = qfo<3>(f);
-    ve[(u + 1) & 3] = qve<0>(v); vo[(u + 1) & 3] = qvo<0>(v);
+    fe[u] = qfe<1>(f); fo[u] = qfo<1>(f);
+    ve[(u + 1) & 1] = qve<0>(v); vo[(u + 1) & 1] = qvo<0>(v);
   };
   int c = 0;
 #pragma unroll 1
-  for (; c + 4 <= n; c += 4) {
+  for (; c + 2 <= n; c += 2) {
     column(std::integral_constant<int, 0>{});
     column(std::integral_constant<int, 1>{});
-    column(std::integral_constant<int, 2>{});
-    column(std::integral_constant<int, 3>{});
   }
   if (c < n) column(std::integral_constant<int, 0>{});
-  if (c + 1 < n) column(std::integral_constant<int, 1>{});
-  if (c + 2 < n) column(std::integral_constant<int, 2>{});
 }
 
 // The cross MMAs of zone-1 chunk c (buffer c & 1) for this warp's 128 rows.
@@ -539,7 +533,7 @@ __device__ __forceinline__ void cert_cross_chunk(const CertIO& io, const CertLan
   return;
 #endif
   const uint32_t w = threadIdx.x >> 5;
-  const int rw_lo = max(128 * (int)w, (int)io.r_lo), rw_hi = min(128 * (int)w + 127, (int)io.r_hi - 1);
+  const int rw_lo = max(64 * (int)w, (int)io.r_lo), rw_hi = min(64 * (int)w + 63, (int)io.r_hi - 1);
   if (rw_lo > rw_hi) return;
   // columns whose first shift is still in zone 1 (the rest of the chunk has R4 = 0)
   const int n = (int)min((uint32_t)kCCols, (io.m_lo - kb) / 32 + 1);
@@ -549,7 +543,7 @@ __device__ __forceinline__ void cert_cross_chunk(const CertIO& io, const CertLan
                  ln.bd + b * (uint32_t)kLimbBuf, n, acc);
 }
 
-// Cross accumulator digits -> per-row doubles (rows 128w + 16r + g (+8)); the
+// Cross accumulator digits -> per-row doubles (rows 64w + 16r + g (+8)); the
 // quad holds digit columns 2 tig, 2 tig + 1 (weights 256^d x 2^qR).
 __device__ __forceinline__ void cert_cross_rows(const int (&acc)[kCertTiles][4], double unitR,
                                                 double* xrow) {
@@ -562,7 +556,7 @@ __device__ __forceinline__ void cert_cross_rows(const int (&acc)[kCertTiles][4],
       double p = __dadd_rn(__dmul_rn((double)acc[r][2 * hh], w0), __dmul_rn((double)acc[r][2 * hh + 1], w1));
       p = __dadd_rn(p, __shfl_xor_sync(FULL, p, 1));
       p = __dadd_rn(p, __shfl_xor_sync(FULL, p, 2));
-      if (tig == 0) xrow[128 * warp + 16 * r + gid + 8 * hh] = p;
+      if (tig == 0) xrow[64 * warp + 16 * r + gid + 8 * hh] = p;
     }
   }
 }

@@ -1079,9 +1079,9 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
             numma += (fw ? kCCols : 0) + (rv ? kCCols : 0);
             issued |= 1u << (c & 1);
           }
-          if (c < nch) {   // warps 0-7: zone-1 cross MMAs; warps 8-15: band-1 cells
-            if (t < (uint32_t)kThreads) cert_cross_chunk(io, ln, c, acc, nmma);
-            else if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, sm.sb, Bs, t - kThreads);
+          if (c < nch) {   // zone-1 cross MMAs (all warps); band-1 cells (warps 8-15)
+            cert_cross_chunk(io, ln, c, acc, nmma);          // all 16 warps, 64 rows each
+            if (t >= (uint32_t)kThreads && cert_band_chunk(io, c)) cert_band_cells(io, cs, c, sm.sb, Bs, t - kThreads);
           }
         }
         for (uint32_t bb = 0; bb < 2; ++bb)
@@ -1108,7 +1108,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         __syncthreads();                       // windows / cores are free: row arrays alias them
         double* linrow = cs.linrow;
         const double* xrow = cs.xrow;
-        if (t < (uint32_t)kThreads) cert_cross_rows(acc, ctl->c_unitR, cs.xrow);
+        cert_cross_rows(acc, ctl->c_unitR, cs.xrow);
         cert_lin_rows(tmem, false, started, ctl->c_unitH, io, linrow);
         __syncthreads();
         cert_lin_rows(tmem, true, started, ctl->c_unitH, io, linrow);
