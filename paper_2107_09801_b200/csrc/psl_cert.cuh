@@ -35,11 +35,16 @@
 // separable (s_{j+k} s_{j-k}) and stays on mma.sync (zone 1 only).
 #pragma once
 
-constexpr uint32_t kCC = 512;                 // shifts per certified chunk (one per thread)
-constexpr uint32_t kCertThreads = 2 * kThreads;   // the certified kernel's CTA (one walk per SM)
+// The certified kernel's CTA (one walk per SM) is 16 warps: warps 0-14 build
+// one shift each per chunk, warp 15 issues the chunk's tcgen05 MMAs (its issue
+// blocks while the tensor pipe drains them, so it builds nothing); all 16
+// warps run the cross MMAs.
+constexpr uint32_t kCertThreads = 2 * kThreads;
+constexpr uint32_t kCC = kCertThreads - 32;   // shifts per certified chunk (one per builder thread)
 constexpr int kCCols = kCC / 32;              // 32-shift columns per chunk
 constexpr int kCertTiles = 4;                 // mma.sync m16 row tiles per warp (64 rows, 16 warps)
-constexpr uint32_t kLag = 3;                  // reversed MMAs trail the builder by 3 chunks
+constexpr uint32_t kLag = 2;                  // reversed MMAs trail the builder by 2 chunks (>= 896 shifts)
+static_assert(kLag * kCC >= 896 && kCC % 32 == 0, "chunk geometry");
 constexpr uint32_t kRing = 256;               // digit-core ring (x2 mapped), cores of 16 shifts
 constexpr uint32_t kACores = (128 + kCC) / 8 + 2;   // sequence cores per direction per chunk
 constexpr int kLimbStride = kCC + 16;         // bytes per R digit row (bank spread)
@@ -56,7 +61,8 @@ constexpr size_t kCertBytes = kDRing + 2 * kABuf + 2 * kLimbBuf + 4 * kWinBuf +
                               2 * kCertRecBuf + 3 * kCertCBuf;
 constexpr long long kMaxD = 0x7F7F7F7F7F7F7F7Fll;      // 8 balanced base-256 digits
 constexpr uint32_t kCertMinL = 2048;
-constexpr uint32_t kTmemCols = 128;           // fwd accumulator cols 0-63, rev 64-127
+constexpr uint32_t kTmemCols = 128;
+constexpr uint32_t kLutS = 6144;             // PowerTable entries staged in shared memory           // fwd accumulator cols 0-63, rev 64-127
 
 struct CertIO {
   uint32_t L, n, nchunks;
@@ -71,7 +77,8 @@ struct CertIO {
   uint32_t f1;                                // flips[0] and s_{f1} (after) when F == 1
   int sf1;
   uint32_t alpha;
-  const double* lut;                          // PowerTable of the phase (covers |C_k| + 4)
+  const double* lut;                          // PowerTable of the phase (covers |C_k| + 4): its
+                                              // head staged in shared memory when it fits (generic loads)
   int2* hlist;
   uint32_t* hcount;
   int32_t hthr;
@@ -172,9 +179,18 @@ __device__ __forceinline__ unsigned char* dcore(const CertSmem& cs, long long q)
 // sidelobes, window constants, band records, the H4 digit cores (ring) and,
 // in zone-1 chunks, the R4 digit rows + sequence windows of the cross MMAs.
 // One shift per thread.
+// The single move's fold words of chunk c (s_{f-k}, s_{f+k} for this thread's
+// k), loaded one iteration ahead so the global latency overlaps a chunk.
+// Positions past either end index the zero pads (the fold masks them out).
+__device__ __forceinline__ uint2 cert_fold_words(const CertIO& io, uint32_t c, const uint32_t* sb) {
+  const int32_t k = (int32_t)cert_kb(c) + (int32_t)threadIdx.x;
+  const int32_t f = (int32_t)io.f1;
+  return make_uint2(sb[((f - k) >> 5) + 1], sb[((f + k) >> 5) + 1]);
+}
+
 __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs, uint32_t c,
                                            const uint32_t* sb, int32_t& pmax, double (&part)[5],
-                                           int32_t cpre, bool& ovf) {
+                                           int32_t cpre, uint2 fw, bool& ovf) {
   const uint32_t t = threadIdx.x;
   const uint32_t kb = cert_kb(c), k = kb + t;
   const uint32_t b = c & 1;
@@ -182,16 +198,19 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
   int32_t cv = 0;
   if (k < io.L) {
     cv = cpre;
+#ifndef PSL_ABLATE_FOLD
     if (io.F == 1) {
       // the common single move: C_k += 2 s_f (s_{f-k} + s_{f+k}), s_f after the flip
       const uint32_t f = io.f1;
-      const int acc = (k <= f ? sval(sb, f - k) : 0) + (f + k < io.L ? sval(sb, f + k) : 0);
+      const int bA = (int)((fw.x >> ((f - k) & 31)) & 1u), bB = (int)((fw.y >> ((f + k) & 31)) & 1u);
+      const int acc = (k <= f ? 1 - 2 * bA : 0) + (f + k < io.L ? 1 - 2 * bB : 0);
       cv += 2 * io.sf1 * acc;
     } else if (io.F) {
       SweepIO fio;
       fio.L = io.L; fio.flips = io.flips; fio.F = io.F;
       cv = fold_flips(cv, k, fio, sb);
     }
+#endif
     if (io.Cdst) io.Cdst[k] = cv;
     if (io.Cloc) io.Cloc[k] = cv;
     const int32_t a = abs(cv);
@@ -212,24 +231,24 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
   double H = 0.0, R = 0.0;
   if (k < io.L) {
     if (k <= io.m_lo) {                               // Z1: both sides for every row
-      const double e4 = __ldg(io.lut + abs(cv - 4)), e0 = __ldg(io.lut + abs(cv + 4));
-      const double e2 = __ldg(io.lut + abs(cv));
+      const double e4 = io.lut[abs(cv - 4)], e0 = io.lut[abs(cv + 4)];
+      const double e2 = io.lut[abs(cv)];
       H = __dsub_rn(e4, e0);
       R = __dsub_rn(__dadd_rn(e4, e0), __dmul_rn(2.0, e2));
       part[0] = __dadd_rn(part[0], __dadd_rn(__dadd_rn(e4, e0), __dmul_rn(2.0, e2)));
     } else if (k <= io.m_hi) {                        // band 1: exact terms per row
     } else if (k <= io.M_hi) {                        // Z3 / band 2: one side or none
-      const double e3 = __ldg(io.lut + abs(cv - 2)), e1 = __ldg(io.lut + abs(cv + 2));
+      const double e3 = io.lut[abs(cv - 2)], e1 = io.lut[abs(cv + 2)];
       H = __dmul_rn(2.0, __dsub_rn(e3, e1));
       const double m4 = __dmul_rn(2.0, __dadd_rn(e3, e1));
       if (k <= io.M_lo) {
         part[1] = __dadd_rn(part[1], m4);
       } else {                                        // band 2: per-row prefix sums
         io.b2M[k - io.M_lo - 1] = m4;
-        io.b2E[k - io.M_lo - 1] = __dmul_rn(4.0, __ldg(io.lut + abs(cv)));
+        io.b2E[k - io.M_lo - 1] = __dmul_rn(4.0, io.lut[abs(cv)]);
       }
     } else {                                          // Z5: no side for any row
-      part[2] = __dadd_rn(part[2], __dmul_rn(4.0, __ldg(io.lut + abs(cv))));
+      part[2] = __dadd_rn(part[2], __dmul_rn(4.0, io.lut[abs(cv)]));
     }
   }
   // fixed point -> 8 balanced base-256 digits
@@ -243,6 +262,7 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
   // x of a 4-lane group assembles row (x & 3) / row 4 + (x & 3) of the group's
   // 4 shifts from the group's digit words (shuffles + byte permutes): two word
   // stores per mapping instead of eight byte stores.
+#ifndef PSL_ABLATE_DIGITS
   {
     const uint32_t lane = t & 31, x = lane & 3, gbase = lane & ~3u;
     const uint32_t lo = (uint32_t)dh, hi = (uint32_t)(dh >> 32);
@@ -264,6 +284,7 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
     *reinterpret_cast<uint32_t*>(p1 + 16 * x) = wl;
     *reinterpret_cast<uint32_t*>(p1 + 16 * (4 + x)) = wh;
   }
+#endif
   if (cert_band_chunk(io, c)) cs.rec[b * kCC + t] = cv;
   if (kb > io.m_lo) return;
   // zone-1 chunk: R4 digit rows and the sequence windows of the cross MMAs
@@ -280,7 +301,7 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
   constexpr int kW = kWinBytes / 4;
   // thread -> base word q of one direction: bytes 4q..4q+7 of the base copy
   // from one bit window, copy a word q = base bytes 4q+a..4q+a+3
-  for (int idx = (int)t; idx < 2 * kW; idx += (int)blockDim.x) {
+  for (int idx = (int)t; idx < 2 * kW; idx += (int)kCC) {
     const int dir = idx >= kW ? 1 : 0;
     const int q = dir ? idx - kW : idx;
     // fwd: byte i <-> position p0 + i; rev: byte i <-> position p0 - i (i = 0..7)
@@ -349,18 +370,22 @@ __device__ __forceinline__ void cert_cores(const CertIO& io, const CertSmem& cs,
   else if (t < 2 * kQuads) { dir = 1; g = t - kQuads; }
   else return;
   if (dir == 0 ? !fwd : !rev) return;
+#ifdef PSL_ABLATE_CORES
+  return;
+#endif
   const int32_t p0 = dir == 0 ? io.JT + (int32_t)cert_kb(c) + 4 * (int32_t)g
                               : io.JT + 127 - (int32_t)cert_kb(c - (int32_t)kLag) - 4 * (int32_t)g;
   uint32_t w[5];
   seq20(sb, p0, dir == 0 ? 1 : -1, (int32_t)io.L, w);
   uint4* dst = reinterpret_cast<uint4*>(base + (size_t)dir * kACores * 128 + 64 * g);
-  dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-  dst[1] = make_uint4(__funnelshift_r(w[0], w[1], 8), __funnelshift_r(w[1], w[2], 8),
-                      __funnelshift_r(w[2], w[3], 8), __funnelshift_r(w[3], w[4], 8));
-  dst[2] = make_uint4(__funnelshift_r(w[0], w[1], 16), __funnelshift_r(w[1], w[2], 16),
-                      __funnelshift_r(w[2], w[3], 16), __funnelshift_r(w[3], w[4], 16));
-  dst[3] = make_uint4(__funnelshift_r(w[0], w[1], 24), __funnelshift_r(w[1], w[2], 24),
-                      __funnelshift_r(w[2], w[3], 24), __funnelshift_r(w[3], w[4], 24));
+  // row r of the quad = the 16 bytes from byte r; rows in a lane-rotated order
+  // (r = i + g/2 mod 4) so each quarter-warp store covers 8 distinct 16-byte bank groups
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t r = (uint32_t)(i + (g >> 1)) & 3u, sh = 8u * r;
+    dst[r] = make_uint4(__funnelshift_r(w[0], w[1], sh), __funnelshift_r(w[1], w[2], sh),
+                        __funnelshift_r(w[2], w[3], sh), __funnelshift_r(w[3], w[4], sh));
+  }
 }
 
 // ---- tcgen05 plumbing
@@ -492,36 +517,45 @@ __device__ __forceinline__ Quad uv_q(const Quad& f, const Quad& v) {
   return {uv_bytes(f.x, v.x), uv_bytes(f.y, v.y), uv_bytes(f.z, v.z), uv_bytes(f.w, v.w)};
 }
 
-// n consecutive 32-k columns of cross MMAs.  Tile r = 2i (+1) of relative
-// column c reads the forward quad E (O) at e = c + i and the reversed quad E (O)
-// at e = c - i (i = 0, 1): each column loads one new quad per window (rings of
-// two, slot = e mod 2, resolved at compile time).
+// n consecutive 32-k columns of cross MMAs.  Tile r = 2i (+1) of column c
+// reads the forward quad E (O) at e = c + i and the reversed quad E (O) at
+// e = c - i (i = 0, 1).  The odd quads are halves of neighbouring even quads
+// (fo(e) = {F(e).z, F(e).w, F(e+1).x, F(e+1).y}, vo(e) = {V(e-1).z, V(e-1).w,
+// V(e).x, V(e).y}), so each column loads one new even quad per window: rings
+// of three (slot = e mod 3, resolved at compile time).
 __device__ __forceinline__ void cert_cross_run(uint32_t f, uint32_t v, uint32_t bd, int n,
                                                int (&acc)[kCertTiles][4]) {
-  Quad fe[2], fo[2], ve[2], vo[2];
-  fe[0] = qfe<0>(f); fo[0] = qfo<0>(f); fe[1] = qfe<1>(f); fo[1] = qfo<1>(f);
-  // reversed quads e = 0, -1 -> slots 0, 1
-  ve[0] = qve<0>(v); vo[0] = qvo<0>(v); ve[1] = qve<-1>(v); vo[1] = qvo<-1>(v);
-  auto column = [&](auto U) {
-    constexpr int u = decltype(U)::value;       // relative column mod 2
+  Quad F[3], V[3];
+  F[0] = qfe<0>(f); F[1] = qfe<1>(f); F[2] = qfe<2>(f);
+  V[0] = qve<0>(v); V[2] = qve<-1>(v);                      // V(-1) -> slot 2
+  V[1] = {0u, 0u, lds32<-48>(v), lds32<-56>(v)};            // V(-2): only z, w are used
+  auto column = [&](auto U_) {
+    constexpr int U = decltype(U_)::value;                  // column mod 3
     const uint32_t b0 = lds32<0>(bd), b1 = lds32<16>(bd);
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      imma_q(acc[2 * i], uv_q(fe[(u + i) & 1], ve[(u - i + 2) & 1]), b0, b1);
-      imma_q(acc[2 * i + 1], uv_q(fo[(u + i) & 1], vo[(u - i + 2) & 1]), b0, b1);
-    }
-    // advance: forward e = c + 2 -> slot u; reversed e = c + 1 -> slot u + 1
+    const Quad& f0 = F[U];
+    const Quad& f1 = F[(U + 1) % 3];
+    const Quad& f2 = F[(U + 2) % 3];
+    const Quad& v0 = V[U];
+    const Quad& v1 = V[(U + 2) % 3];
+    const Quad& v2 = V[(U + 1) % 3];
+    imma_q(acc[0], uv_q(f0, v0), b0, b1);
+    imma_q(acc[1], uv_q(Quad{f0.z, f0.w, f1.x, f1.y}, Quad{v1.z, v1.w, v0.x, v0.y}), b0, b1);
+    imma_q(acc[2], uv_q(f1, v1), b0, b1);
+    imma_q(acc[3], uv_q(Quad{f1.z, f1.w, f2.x, f2.y}, Quad{v2.z, v2.w, v1.x, v1.y}), b0, b1);
+    // advance: F(c + 3) -> slot U, V(c + 1) -> slot U + 1
     f += 32; v += 32; bd += 32;
-    fe[u] = qfe<1>(f); fo[u] = qfo<1>(f);
-    ve[(u + 1) & 1] = qve<0>(v); vo[(u + 1) & 1] = qvo<0>(v);
+    F[U] = qfe<2>(f);
+    V[(U + 1) % 3] = qve<0>(v);
   };
   int c = 0;
 #pragma unroll 1
-  for (; c + 2 <= n; c += 2) {
+  for (; c + 3 <= n; c += 3) {
     column(std::integral_constant<int, 0>{});
     column(std::integral_constant<int, 1>{});
+    column(std::integral_constant<int, 2>{});
   }
   if (c < n) column(std::integral_constant<int, 0>{});
+  if (c + 1 < n) column(std::integral_constant<int, 1>{});
 }
 
 // The cross MMAs of zone-1 chunk c (buffer c & 1) for this warp's 128 rows.
@@ -626,7 +660,7 @@ __device__ __forceinline__ void cert_band_cells(const CertIO& io, const CertSmem
         const int u = ((Bw >> q) & 1u) == sjb ? 1 : -1;
         const int v = ((Aw >> q) & 1u) == sjb ? 1 : -1;
         const int x = (k <= j ? v : 0) + (j + k < L ? u : 0);
-        s = __dadd_rn(s, __ldg(lut + abs(rec[k - kb] - 2 * x)));
+        s = __dadd_rn(s, lut[abs(rec[k - kb] - 2 * x)]);
       }
     }
     Bs[m] = s;

@@ -162,6 +162,7 @@ struct Ctl {
   double c_scaleH, c_unitH, c_scaleR, c_unitR, c_sconst, c_errconst;
   uint32_t m_lo, m_hi, M_lo, M_hi;
   double rs5[5][16];
+  uint32_t cfw[72], crv[72]; // per-chunk tcgen05 flags of the pass segment (bit c: fwd / rev MMAs)
   uint64_t mbar[2];          // tcgen05 commit barriers (iteration parity)
   uint32_t tmem;             // TMEM base of this CTA's accumulators (kTmemCols columns)
 };
@@ -793,6 +794,7 @@ __global__ void __launch_bounds__(256) build_tables_kernel(const uint32_t* bits,
 
 #include "psl_cert.cuh"
 static_assert(kCertBytes <= kCertRegion, "certified buffers exceed the shared region");
+static_assert(((1u << 20) - 1 + kCC - 1) / kCC + kLag <= 72 * 32, "per-chunk flag words");
 
 // Neighbour PSL + thread-local reduce_scan over this thread's kJ neighbours
 // (ascending offset) + the block-wide lexicographic minima (ctl->best_*).
@@ -881,12 +883,38 @@ __device__ __forceinline__ int compare_local(const WalkState& S, double lo, doub
 // kCert: 512 threads, one walk per SM (the certified scan's digit ring and
 // chunk buffers need the shared memory); the exact kernel: 256 threads, two per
 // SM.  The exact sweep in the 512-thread kernel leaves threads >= 256 inactive.
+// Timing-only instrumentation (-DPSL_PHASE_TIMING, tools/ablate.sh): per-warp
+// cycles per phase of the certified chunk loop, printed by CTA 0 at exit.
+#ifdef PSL_PHASE_TIMING
+}  // namespace
+}  // namespace pslb
+#include <cstdio>
+namespace pslb {
+namespace {
+constexpr int kPT = 9;   // loop top, build, cores, barrier, issue, cross, band, outside the loop, mbar wait
+#define PT_MARK(i)                                                   \
+  do {                                                               \
+    const long long _n = clock64();                                  \
+    if ((t & 31) == 0) pt_acc[t >> 5][i] += _n - pt_last;            \
+    pt_last = _n;                                                    \
+  } while (0)
+#else
+#define PT_MARK(i) do {} while (0)
+#endif
+
 template <bool kCert>
 __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2) run_kernel(RunArgs a) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   Smem sm = carve<kCert>(smem_raw);
   Ctl* ctl = sm.ctl;
   const uint32_t w = blockIdx.x, t = threadIdx.x;
+#ifdef PSL_PHASE_TIMING
+  __shared__ long long pt_acc[16][kPT];
+  if (t < 16 * kPT) pt_acc[t / kPT][t % kPT] = 0;
+  __syncthreads();
+  long long pt_last = clock64();
+  const long long pt_t0 = pt_last;
+#endif
   const uint32_t L = a.L, nw = a.nwords;
   WalkState* gst = a.st + w;
   uint32_t* bits_piv = a.bits_piv + (size_t)w * a.w_stride + a.w_front;
@@ -988,6 +1016,17 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
       double mid[kJ], lo[kJ], hi[kJ];
 #pragma unroll
       for (int m = 0; m < kJ; ++m) { mid[m] = 0.0; lo[m] = 0.0; hi[m] = 0.0; }
+      // the phase's PowerTable head (indices <= Psrc + 4F + 4 cover every lookup
+      // of the pass) in shared memory when it fits
+      const double* lut_c = lut;
+      {
+        const uint32_t nlut = (uint32_t)s_Psrc + 4u * s_n_pending + 5u;
+        if (nlut <= kLutS) {
+          double* lut_s = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(ctl) + kCtlBytes);
+          for (uint32_t i = t; i < nlut; i += blockDim.x) lut_s[i] = __ldg(lut + i);
+          lut_c = lut_s;
+        }
+      }
       const uint32_t nA = min(a.n, L - 1 - start);          // rows before the wrap
       const int nseg = (nA > 0 && nA < a.n) ? 2 : 1;
       for (int seg = 0; seg < nseg; ++seg) {
@@ -1020,7 +1059,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         io.flips = flips;
         io.f1 = io.F == 1 ? flips[0] : 0u;
         io.sf1 = io.F == 1 ? sval(sm.sb, io.f1) : 0;
-        io.alpha = alpha; io.lut = lut;
+        io.alpha = alpha; io.lut = lut_c;
         io.hcount = &ctl->hcount;
         io.hthr = s_Psrc - 4 * (int32_t)s_n_pending - 8;
         io.scaleH = ctl->c_scaleH; io.scaleR = ctl->c_scaleR;
@@ -1042,34 +1081,62 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         for (int32_t cz = -(int32_t)kLag; cz < 0; ++cz) cert_zero_digits(cs, cz);
         // C_k streams into shared memory by cp.async two chunks ahead
         const uint32_t nch = io.nchunks;
-        cert_prefetch(io, cs, 0);
-        if (nch > 1) cert_prefetch(io, cs, 1);
+        const bool builder = t < kCC;   // warp 15 issues the tcgen05 MMAs instead
+        if (builder) {
+          cert_prefetch(io, cs, 0);
+          if (nch > 1) cert_prefetch(io, cs, 1);
+        }
+        // which iterations issue forward (kappa-chunk c) / reversed (c - kLag) MMAs
+        for (uint32_t c = t; c < (nch + kLag + 31) / 32 * 32; c += blockDim.x) {
+          bool fw = false, rv = false;
+          if (c < nch + kLag) {
+            const long long kb = (long long)cert_kb(c);
+            fw = io.JT + kb < (long long)L && cert_lin_in(io, kb - 896, kb + kCC - 1);
+            const long long kbr = (long long)(int32_t)cert_kb((int32_t)c - (int32_t)kLag);
+            rv = (long long)io.JT + 127 - kbr >= 0 && cert_lin_in(io, kbr, kbr + kCC - 1 + 896);
+          }
+          const uint32_t mf = __ballot_sync(FULL, fw), mr = __ballot_sync(FULL, rv);
+          if ((t & 31) == 0) { ctl->cfw[c >> 5] = mf; ctl->crv[c >> 5] = mr; }
+        }
+        __syncthreads();
+        uint2 fwords = (builder && io.F == 1) ? cert_fold_words(io, 0, sm.sb) : make_uint2(0u, 0u);
         uint32_t issued = 0;        // bit (c & 1): iteration c committed MMAs not yet waited for
         // iteration c: build chunk c, stage the sequence cores of forward kappa-chunk c and
         // reversed kappa'-chunk c - kLag, issue their tcgen05 MMAs (one thread, async),
         // then the zone-1 cross MMAs (mma.sync) and band-1 cells of chunk c
+        PT_MARK(7);
         for (uint32_t c = 0; c < nch + kLag; ++c) {
           if (issued & (1u << (c & 1))) {      // MMAs of iteration c - 2 read this buffer
+            PT_MARK(0);
             mbar_wait(&ctl->mbar[c & 1], mb_par[c & 1]);
+            PT_MARK(8);
             mb_par[c & 1] ^= 1u;
             issued &= ~(1u << (c & 1));
           }
+          PT_MARK(0);
+          const bool fw = (ctl->cfw[c >> 5] >> (c & 31)) & 1u, rv = (ctl->crv[c >> 5] >> (c & 31)) & 1u;
           if (c < nch) {
-            if (c + 2 < nch) cert_prefetch(io, cs, c + 2);
-            const int pending = (int)min(2u, nch - 1 - c);
-            cert_build(io, cs, c, sm.sb, pmax, part, cert_take(cs, c, pending), ovf);
+            if (builder) {
+              if (c + 2 < nch) cert_prefetch(io, cs, c + 2);
+              const uint2 fnext = (io.F == 1 && c + 1 < nch) ? cert_fold_words(io, c + 1, sm.sb) : fwords;
+              const int pending = (int)min(2u, nch - 1 - c);
+              cert_build(io, cs, c, sm.sb, pmax, part, cert_take(cs, c, pending), fwords, ovf);
+              fwords = fnext;
+            }
           } else {
             cert_zero_digits(cs, c);
           }
-          const uint32_t kb = cert_kb(c);
-          const bool fw = io.JT + (long long)kb < (long long)L &&
-                          cert_lin_in(io, (long long)kb - 896, (long long)kb + kCC - 1);
-          const long long kbr = (long long)(int32_t)cert_kb((int32_t)c - (int32_t)kLag);
-          const bool rv = (long long)io.JT + 127 - kbr >= 0 && cert_lin_in(io, kbr, kbr + kCC - 1 + 896);
+          PT_MARK(1);
           cert_cores(io, cs, (int32_t)c, sm.sb, fw, rv);
+          PT_MARK(2);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           __syncthreads();
+          PT_MARK(3);
+#ifdef PSL_ABLATE_ISSUE
+          if (false) {
+#else
           if ((fw || rv)) {
+#endif
             if (t == kCertThreads - 32) {              // warp 15 stages no cores: it issues
               uint32_t st = started;
               cert_issue(cs, tmem, (int32_t)c, fw, rv, st);
@@ -1079,11 +1146,15 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
             numma += (fw ? kCCols : 0) + (rv ? kCCols : 0);
             issued |= 1u << (c & 1);
           }
+          PT_MARK(4);
           if (c < nch) {   // zone-1 cross MMAs (all warps); band-1 cells (warps 8-15)
             cert_cross_chunk(io, ln, c, acc, nmma);          // all 16 warps, 64 rows each
+            PT_MARK(5);
             if (t >= (uint32_t)kThreads && cert_band_chunk(io, c)) cert_band_cells(io, cs, c, sm.sb, Bs, t - kThreads);
+            PT_MARK(6);
           }
         }
+        PT_MARK(0);
         for (uint32_t bb = 0; bb < 2; ++bb)
           if (issued & (1u << bb)) { mbar_wait(&ctl->mbar[bb], mb_par[bb]); mb_par[bb] ^= 1u; }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -1444,7 +1515,16 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
   }
 
   // ---- persist
+  PT_MARK(7);
   __syncthreads();
+#ifdef PSL_PHASE_TIMING
+  if (kCert && t == 0) printf("PTCTA %u %lld\n", w, clock64() - pt_t0);
+  if (kCert && w == 0 && t < 16) {
+    const long long* q = pt_acc[t];
+    printf("PT warp %2u top %lld build %lld cores %lld bar %lld issue %lld cross %lld band %lld other %lld mbarwait %lld\n", t,
+           q[0], q[1], q[2], q[3], q[4], q[5], q[6], q[7], q[8]);
+  }
+#endif
   if (t == 0) {
     if (ctl->st.status != PSL_OK) ctl->st.end_ns = globaltimer();
     *gst = ctl->st;
@@ -1564,7 +1644,7 @@ __global__ void power_tables_kernel(double* lut, uint32_t n, uint32_t alpha1, ui
 
 size_t run_smem_bytes(bool cert) {
   const size_t main_bytes = cert ? (kExactMain > kCertRegion ? kExactMain : kCertRegion) : kExactMain;
-  return main_bytes + kHfBytes + kCtlBytes;
+  return main_bytes + kHfBytes + kCtlBytes + (cert ? (size_t)kLutS * sizeof(double) : 0);
 }
 
 int launch_init_walks(const RunArgs& a, uint32_t n_walks, const uint64_t* d_seeds,
