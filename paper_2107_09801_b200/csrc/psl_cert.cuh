@@ -35,12 +35,15 @@
 // separable (s_{j+k} s_{j-k}) and stays on mma.sync (zone 1 only).
 #pragma once
 
-// The certified kernel's CTA (one walk per SM) is 16 warps: warps 0-14 build
-// one shift each per chunk, warp 15 issues the chunk's tcgen05 MMAs (its issue
-// blocks while the tensor pipe drains them, so it builds nothing); all 16
-// warps run the cross MMAs.
+// The certified kernel's CTA (one walk per SM) is 16 warps: every thread
+// builds one shift per chunk (kCC = 512) and lane 0 of warp 15 also issues the
+// chunk's tcgen05 MMAs; all 16 warps run the cross MMAs.  (-DPSL_CC=480 makes
+// warp 15 a dedicated issuer that builds nothing: measured 1 % slower.)
 constexpr uint32_t kCertThreads = 2 * kThreads;
-constexpr uint32_t kCC = kCertThreads - 32;   // shifts per certified chunk (one per builder thread)
+#ifndef PSL_CC
+#define PSL_CC kCertThreads
+#endif
+constexpr uint32_t kCC = PSL_CC;              // shifts per certified chunk (one per builder thread)
 constexpr int kCCols = kCC / 32;              // 32-shift columns per chunk
 constexpr int kCertTiles = 4;                 // mma.sync m16 row tiles per warp (64 rows, 16 warps)
 constexpr uint32_t kLag = 2;                  // reversed MMAs trail the builder by 2 chunks (>= 896 shifts)
@@ -86,6 +89,7 @@ struct CertIO {
   uint32_t m_lo, m_hi, M_lo, M_hi;            // zone bounds (see above)
   double* b2M;                                // [1024] global scratch: band-2 4M_k, 4 e2_k
   double* b2E;
+  bool chain;                                 // also the serial fitness() of the folded table
 };
 
 struct CertSmem {
@@ -285,7 +289,7 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
     *reinterpret_cast<uint32_t*>(p1 + 16 * (4 + x)) = wh;
   }
 #endif
-  if (cert_band_chunk(io, c)) cs.rec[b * kCC + t] = cv;
+  if (io.chain || cert_band_chunk(io, c)) cs.rec[b * kCC + t] = cv;
   if (kb > io.m_lo) return;
   // zone-1 chunk: R4 digit rows and the sequence windows of the cross MMAs
   {
@@ -665,6 +669,16 @@ __device__ __forceinline__ void cert_band_cells(const CertIO& io, const CertSmem
     }
     Bs[m] = s;
   }
+}
+
+// fitness() of the folded table (sequence.cpp:131-141): one thread adds the
+// chunk's terms lut[|C_k|] in ascending k to the serial double chain.
+__device__ __forceinline__ void cert_chain_chunk(const CertIO& io, const CertSmem& cs, uint32_t c,
+                                                 double& chain) {
+  const uint32_t kb = cert_kb(c);
+  const uint32_t nk = min(kCC, io.L - kb);
+  const int32_t* rec = cs.rec + (size_t)(c & 1) * kCC;
+  for (uint32_t i = 0; i < nk; ++i) chain = __dadd_rn(chain, io.lut[abs(rec[i])]);
 }
 
 // Band 2 (k in (M_lo, M_hi]): row j's constant is sum_{k <= M_j} 4M_k +

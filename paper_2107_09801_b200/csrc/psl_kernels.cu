@@ -972,7 +972,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
       ctl->cert = 0;
       ctl->need_exact = 0;
       ctl->need_vl = 0;
-      if (kCert && a.cert && ctl->do_scan && !S.fitness_pending && a.n <= (uint32_t)kGroup &&
+      if (kCert && a.cert && ctl->do_scan && a.n <= (uint32_t)kGroup &&
           L >= kCertMinL) {
         // fixed-point scale: every |H4|, |R4| <= 2 pow(Amax, alpha) < 2^(62+q)
         const uint32_t alpha = S.phase == 1 ? a.alpha1 : a.alpha2;
@@ -1066,6 +1066,10 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         io.m_lo = ctl->m_lo; io.m_hi = ctl->m_hi; io.M_lo = ctl->M_lo; io.M_hi = ctl->M_hi;
         io.b2M = a.b2 + (size_t)w * 2 * kGroup;
         io.b2E = io.b2M + kGroup;
+        // first step / restart: fitness() of the folded table, serially, by one
+        // thread of warp 14 behind the builder (search.cpp:348, :409)
+        io.chain = seg == 0 && s_fitness_pending != 0;
+        double chain = 0.0;
         int acc[kCertTiles][4];
 #pragma unroll
         for (int r = 0; r < kCertTiles; ++r)
@@ -1150,6 +1154,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           if (c < nch) {   // zone-1 cross MMAs (all warps); band-1 cells (warps 8-15)
             cert_cross_chunk(io, ln, c, acc, nmma);          // all 16 warps, 64 rows each
             PT_MARK(5);
+            if (io.chain && t == kCertThreads - 64) cert_chain_chunk(io, cs, c, chain);
             if (t >= (uint32_t)kThreads && cert_band_chunk(io, c)) cert_band_cells(io, cs, c, sm.sb, Bs, t - kThreads);
             PT_MARK(6);
           }
@@ -1163,8 +1168,9 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         if (t == 0) ctl->st.n_umma += numma;
         if (ovf) atomicOr(&ctl->c_ovf, 1);
         if (seg == 0) {
-          const int32_t Pn = block_max(ctl, pmax);
-          if (t == 0) first_pass_state(ctl, a, w, Pn, 0.0, alpha);
+          if (io.chain && t == kCertThreads - 64) ctl->fit = chain;
+          const int32_t Pn = block_max(ctl, pmax);   // (its barrier publishes ctl->fit)
+          if (t == 0) first_pass_state(ctl, a, w, Pn, ctl->fit, alpha);
         }
         // window constants: warp sums, then a fixed-order sum over warps
         {

@@ -569,9 +569,20 @@ class Walks:
         if rc:
             _raise(rc, err)
 
-    def records(self, solutions: bool = False) -> list[WalkRecord]:
+    def records(self, solutions: bool = False, out: np.ndarray | None = None) -> list[WalkRecord]:
+        """Per-walk records; with solutions=True also each walk's best sequence
+        (int8 +-1), written into `out` (n_walks x L int8, C-contiguous; e.g. a
+        pinned buffer the caller reuses) when given."""
         recs = (B.psl_walk_record * self.n_walks)()
-        sol = np.zeros((self.n_walks, self.params.length), np.int8) if solutions else None
+        sol = None
+        if solutions:
+            if out is not None:
+                if (out.dtype != np.int8 or out.shape != (self.n_walks, self.params.length)
+                        or not out.flags.c_contiguous):
+                    raise ValueError("out must be a C-contiguous int8 array of shape (n_walks, length)")
+                sol = out
+            else:
+                sol = np.zeros((self.n_walks, self.params.length), np.int8)
         err = _err()
         rc = B.lib().psl_walks_records(self._h, recs, sol.ctypes.data if sol is not None else None,
                                        err, len(err))
@@ -594,10 +605,11 @@ class Walks:
 
 
 def run_walks(params: SearchParams, n_walks: int, seeds=None, inits=None,
-              ctx: Context | None = None, solutions: bool = True) -> list[WalkRecord]:
+              ctx: Context | None = None, solutions: bool = True,
+              out: np.ndarray | None = None) -> list[WalkRecord]:
     w = Walks(params, n_walks, seeds, inits, ctx)
     try:
         w.run()
-        return w.records(solutions)
+        return w.records(solutions, out)
     finally:
         w.close()
