@@ -683,13 +683,34 @@ __global__ void __launch_bounds__(256) init_walks_kernel(RunArgs a, const uint64
     // warm starts: validate (BinarySequence ctor, sequence.cpp:20-35) and pack;
     // bad[0] = first offending flat index + 1, bad[1] = its value
     const int8_t* src = inits + (size_t)w * a.L;
+    const size_t base = (size_t)w * a.L;
     for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) {
       uint32_t word = 0;
       const uint32_t nb = min(32u, a.L - i * 32);
+      if (nb == 32) {
+        // 8 byte quads (aligned loads + funnel shifts): -1 bytes -> bits, any
+        // byte not in {+1, -1} flagged
+        const uintptr_t pa = reinterpret_cast<uintptr_t>(src + (size_t)i * 32);
+        const uint32_t* q = reinterpret_cast<const uint32_t*>(pa & ~uintptr_t(3));
+        const uint32_t sh = 8u * (uint32_t)(pa & 3);
+        uint32_t qw[9];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) qw[r] = __ldg(q + r);
+        qw[8] = sh ? __ldg(q + 8) : 0u;
+        uint32_t badm = 0;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const uint32_t v = __funnelshift_r(qw[r], qw[r + 1], sh);
+          badm |= (~(__vcmpeq4(v, 0x01010101u) | __vcmpeq4(v, 0xFFFFFFFFu)) != 0u) << r;
+          word |= ((((v >> 7) & 0x01010101u) * 0x01020408u) >> 24) << (4 * r);
+        }
+        if (!badm) { bp[i + 1] = word; continue; }
+        word = 0;
+      }
       for (uint32_t b = 0; b < nb; ++b) {
         const int8_t v = src[i * 32 + b];
         if (v != 1 && v != -1) {
-          const uint32_t flat = (uint32_t)((size_t)w * a.L + i * 32 + b) + 1;
+          const uint32_t flat = (uint32_t)(base + i * 32 + b) + 1;
           if (atomicMin(&bad[0], flat) > flat) bad[1] = (uint32_t)(int32_t)v;
         }
         word |= (uint32_t)(v < 0) << b;

@@ -2,12 +2,24 @@
 // exact number-theoretic transform.
 //
 // C_k = sum_i s_i s_{i+k} is the correlation of the +-1 sequence with itself:
-// C_k = (s * rev(s))[L-1-k].  Over Z_p with p = 998244353 = 119 * 2^23 + 1
-// (3 is a primitive root) the cyclic convolution of length N = 2^ceil(log2(2L))
-// is exact, and |C_k| <= L < p/2 recovers the signed value.  O(L log L) per
-// walk instead of the O(L^2) popcount kernel (which stays for small L and the
-// single-table C-ABI call).  Forward DIF (natural -> bit-reversed), pointwise
-// product, inverse DIT (bit-reversed -> natural): no permutation pass.
+// C_k = (x * y)[L-1-k] with y_i = x_{L-1-i}.  Over Z_p with p = 998244353 =
+// 119 * 2^23 + 1 (3 is a primitive root) the cyclic convolution of length
+// N = 2^ceil(log2(2L)) is exact, and |C_k| <= L < p/2 recovers the signed value.
+// O(L log L) per walk instead of the O(L^2) popcount kernel (which stays for
+// small L and the single-table C-ABI call).
+//
+// Only x is transformed: Y(k) = sum_m x_m w^{(L-1-m)k} = w^{(L-1)k} X(-k), so
+// the spectrum of the correlation is X(k) X(N-k) w^{(L-1)k}.
+//
+// Layout: each walk's N values as R rows x C columns (i = m C + col, R C = N).
+// Forward DIF (natural -> bit-reversed):  stages with span h >= C pair
+// elements of one column (column pass: a CTA holds 8 adjacent columns in
+// shared memory, generated straight from the packed bits), stages h < C pair
+// elements of one row (row pass: a CTA holds a row).  Pointwise product on the
+// bit-reversed spectrum.  Inverse DIT (bit-reversed -> natural): row pass,
+// then the column pass, which also scales by N^-1, writes C_k (pivot and local
+// tables) and reduces the walk's PSL and energy.  Four passes over HBM instead
+// of one per radix-2 stage.
 #include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -19,6 +31,10 @@ namespace {
 
 constexpr uint32_t kP = 998244353u;
 constexpr uint32_t kPinv = 998244351u;   // -p^{-1} mod 2^32 (Montgomery)
+constexpr uint32_t kOne = 301989884u;    // 2^32 mod p (Montgomery 1)
+constexpr int kCols = 8;                 // columns per column-pass CTA (one 32 B sector per row)
+constexpr int kMaxRows = 1024;           // R <= 1024, C <= 2048 (N <= 2^21)
+constexpr int kMaxRowLen = 2048;
 
 // Montgomery product: returns a*b*2^-32 mod p for a, b < p.
 __device__ __forceinline__ uint32_t mmul(uint32_t a, uint32_t b) {
@@ -34,74 +50,141 @@ __device__ __forceinline__ uint32_t madd(uint32_t a, uint32_t b) {
 __device__ __forceinline__ uint32_t msub(uint32_t a, uint32_t b) {
   return a >= b ? a - b : a + kP - b;
 }
+// w^e for any e (mod N) from the half table tw[j] = w^j, j < N/2 (w^{N/2} = -1)
+__device__ __forceinline__ uint32_t wpow(const uint32_t* tw, uint32_t e, uint32_t N) {
+  e &= N - 1;
+  const uint32_t h = N >> 1;
+  return e < h ? tw[e] : (kP - tw[e - h]) % kP;
+}
 
-// +-1 -> Montgomery form of +1 / -1; x natural order, y reversed.
-__global__ void ntt_load_kernel(const uint32_t* bits, size_t w_stride, uint32_t L, uint32_t N,
-                                uint32_t* x, uint32_t* y) {
-  const uint32_t walk = blockIdx.y;
+// Forward column pass: stages h = N/2 .. C (rows span R/2 .. 1), DIF.  The
+// inputs are generated from the packed bits (x_i = +-1 for i < L, 0 past L).
+__global__ void __launch_bounds__(256) ntt_col_fwd_kernel(const uint32_t* bits, size_t w_stride,
+                                                          uint32_t L, uint32_t R, uint32_t C,
+                                                          const uint32_t* tw, uint32_t* x) {
+  __shared__ uint32_t s[kMaxRows * kCols];
+  const uint32_t walk = blockIdx.y, col0 = blockIdx.x * kCols;
+  const uint32_t N = R * C;
   const uint32_t* S = bits + (size_t)walk * w_stride;
+  for (uint32_t e = threadIdx.x; e < R * kCols; e += blockDim.x) {
+    const uint32_t m = e / kCols, c = e % kCols, i = m * C + col0 + c;
+    uint32_t v = 0;
+    if (i < L) v = ((S[i >> 5] >> (i & 31)) & 1u) ? kP - kOne : kOne;
+    s[e] = v;
+  }
+  __syncthreads();
+  for (uint32_t hr = R >> 1; hr >= 1; hr >>= 1) {
+    const uint32_t h = hr * C, tstride = N / (2 * h);
+    for (uint32_t b = threadIdx.x; b < (R / 2) * kCols; b += blockDim.x) {
+      const uint32_t c = b % kCols, q = b / kCols;          // q-th butterfly row pair
+      const uint32_t jr = q & (hr - 1), m1 = ((q - jr) << 1) + jr, m2 = m1 + hr;
+      const uint32_t j = jr * C + col0 + c;                   // position within the 2h block
+      const uint32_t w = tw[j * tstride];
+      const uint32_t u = s[m1 * kCols + c], v = s[m2 * kCols + c];
+      s[m1 * kCols + c] = madd(u, v);
+      s[m2 * kCols + c] = mmul(msub(u, v), w);
+    }
+    __syncthreads();
+  }
   uint32_t* X = x + (size_t)walk * N;
-  uint32_t* Y = y + (size_t)walk * N;
-  const uint32_t one = 301989884u;            // 2^32 mod p  (Montgomery 1)
-  const uint32_t mone = kP - one;             // Montgomery -1
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
-    uint32_t vx = 0, vy = 0;
-    if (i < L) {
-      vx = ((S[i >> 5] >> (i & 31)) & 1u) ? mone : one;
-      const uint32_t r = L - 1 - i;
-      vy = ((S[r >> 5] >> (r & 31)) & 1u) ? mone : one;
-    }
-    X[i] = vx;
-    Y[i] = vy;
+  for (uint32_t e = threadIdx.x; e < R * kCols; e += blockDim.x) {
+    const uint32_t m = e / kCols, c = e % kCols;
+    X[m * C + col0 + c] = s[e];
   }
 }
 
-// One radix-2 stage over all walks.  tw[j] = w_N^j (Montgomery), j < N/2.
+// Row pass over the rows of every walk: forward DIF stages h = C/2 .. 1 or
+// inverse DIT stages h = 1 .. C/2.  Twiddles of the row stages (the same for
+// every row) staged in shared memory: stage h uses tw[j N / 2h], j < h.
 template <bool kForward>
-__global__ void ntt_stage_kernel(uint32_t* a, uint32_t N, uint32_t h, const uint32_t* tw,
-                                 uint32_t walks_per_arr) {
-  const uint32_t arr = blockIdx.y;
-  uint32_t* A = a + (size_t)arr * N;
-  const uint32_t stride = N / (2 * h);
-  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < N / 2; t += gridDim.x * blockDim.x) {
-    const uint32_t j = t & (h - 1);
-    const uint32_t i1 = ((t - j) << 1) + j;
-    const uint32_t i2 = i1 + h;
-    const uint32_t w = tw[j * stride];
-    const uint32_t u = A[i1], v = A[i2];
-    if (kForward) {            // DIF: (u+v, (u-v) w)
-      A[i1] = madd(u, v);
-      A[i2] = mmul(msub(u, v), w);
-    } else {                   // DIT: (u + v w, u - v w)
-      const uint32_t vw = mmul(v, w);
-      A[i1] = madd(u, vw);
-      A[i2] = msub(u, vw);
+__global__ void __launch_bounds__(256) ntt_row_kernel(uint32_t* x, uint32_t R, uint32_t C,
+                                                      const uint32_t* tw) {
+  __shared__ uint32_t s[kMaxRowLen];
+  __shared__ uint32_t ts[kMaxRowLen];                         // ts[h + j] = stage-h twiddle j
+  const uint32_t N = R * C;
+  for (uint32_t h = 1; h < C; h <<= 1)
+    for (uint32_t j = threadIdx.x; j < h; j += blockDim.x) ts[h + j] = tw[j * (N / (2 * h))];
+  uint32_t* X = x + (size_t)blockIdx.y * N + (size_t)blockIdx.x * C;
+  for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) s[i] = X[i];
+  __syncthreads();
+  for (uint32_t it = 0, h = kForward ? C >> 1 : 1; h >= 1 && h < C; ++it, h = kForward ? h >> 1 : h << 1) {
+    for (uint32_t b = threadIdx.x; b < C / 2; b += blockDim.x) {
+      const uint32_t j = b & (h - 1), i1 = ((b - j) << 1) + j, i2 = i1 + h;
+      const uint32_t w = ts[h + j], u = s[i1], v = s[i2];
+      if (kForward) {
+        s[i1] = madd(u, v);
+        s[i2] = mmul(msub(u, v), w);
+      } else {
+        const uint32_t vw = mmul(v, w);
+        s[i1] = madd(u, vw);
+        s[i2] = msub(u, vw);
+      }
     }
+    __syncthreads();
   }
-  (void)walks_per_arr;
+  for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) X[i] = s[i];
 }
 
-__global__ void ntt_pointwise_kernel(uint32_t* x, const uint32_t* y, size_t total) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
-       i += (size_t)gridDim.x * blockDim.x)
-    x[i] = mmul(x[i], y[i]);
+// Spectrum of the correlation at bit-reversed position p (k = brev(p)):
+// Z(k) = X(k) X(N-k) w^{(L-1)k}.  Pairs (p, p') are updated by the lower of the two.
+__global__ void ntt_pointwise_kernel(uint32_t* x, uint32_t logN, uint32_t L, const uint32_t* tw) {
+  const uint32_t N = 1u << logN;
+  uint32_t* X = x + (size_t)blockIdx.y * N;
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < N; p += gridDim.x * blockDim.x) {
+    const uint32_t k = __brev(p) >> (32 - logN);
+    const uint32_t kn = (N - k) & (N - 1);
+    const uint32_t p2 = __brev(kn) >> (32 - logN);
+    if (p2 < p) continue;                                    // done by the partner
+    const uint32_t a = X[p], b = X[p2];
+    const uint32_t ab = mmul(a, b);
+    const uint32_t e1 = (uint32_t)(((uint64_t)(L - 1) * k) & (N - 1));
+    const uint32_t e2 = (uint32_t)(((uint64_t)(L - 1) * kn) & (N - 1));
+    X[p] = mmul(ab, wpow(tw, e1, N));
+    if (p2 != p) X[p2] = mmul(ab, wpow(tw, e2, N));
+  }
 }
 
-// z = INTT output (times N, Montgomery): C_k = z[L-1-k] * N^-1, signed.
-__global__ void ntt_extract_kernel(const uint32_t* z, uint32_t N, uint32_t ninv_m, uint32_t L,
-                                   int32_t* C, int32_t* Cloc, size_t c_stride, WalkState* st) {
-  const uint32_t walk = blockIdx.y;
-  const uint32_t* Z = z + (size_t)walk * N;
-  int32_t* Cw = C + (size_t)walk * c_stride;
-  int32_t* Cl = Cloc ? Cloc + (size_t)walk * c_stride : nullptr;
+// Inverse column pass: DIT stages h = C .. N/2 (rows span 1 .. R/2), then
+// C_{L-1-i} = z_i N^-1 (signed) into the pivot / local tables, PSL and energy.
+__global__ void __launch_bounds__(256) ntt_col_inv_kernel(const uint32_t* x, uint32_t R, uint32_t C,
+                                                          const uint32_t* twi, uint32_t ninv_m,
+                                                          uint32_t L, int32_t* Cp, int32_t* Cl,
+                                                          size_t c_stride, WalkState* st) {
+  __shared__ uint32_t s[kMaxRows * kCols];
+  const uint32_t walk = blockIdx.y, col0 = blockIdx.x * kCols;
+  const uint32_t N = R * C;
+  const uint32_t* X = x + (size_t)walk * N;
+  for (uint32_t e = threadIdx.x; e < R * kCols; e += blockDim.x) {
+    const uint32_t m = e / kCols, c = e % kCols;
+    s[e] = X[m * C + col0 + c];
+  }
+  __syncthreads();
+  for (uint32_t hr = 1; hr < R; hr <<= 1) {
+    const uint32_t h = hr * C, tstride = N / (2 * h);
+    for (uint32_t b = threadIdx.x; b < (R / 2) * kCols; b += blockDim.x) {
+      const uint32_t c = b % kCols, q = b / kCols;
+      const uint32_t jr = q & (hr - 1), m1 = ((q - jr) << 1) + jr, m2 = m1 + hr;
+      const uint32_t j = jr * C + col0 + c;
+      const uint32_t w = twi[j * tstride];
+      const uint32_t u = s[m1 * kCols + c], vw = mmul(s[m2 * kCols + c], w);
+      s[m1 * kCols + c] = madd(u, vw);
+      s[m2 * kCols + c] = msub(u, vw);
+    }
+    __syncthreads();
+  }
+  int32_t* Cw = Cp + (size_t)walk * c_stride;
+  int32_t* Cw2 = Cl ? Cl + (size_t)walk * c_stride : nullptr;
   int32_t pm = 0;
   long long en = 0;
-  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < L; k += gridDim.x * blockDim.x) {
-    // mmul(v, ninv_m) with ninv_m = N^-1 * 2^64 mod p... see host: result in normal form
-    uint32_t v = mmul(mmul(Z[L - 1 - k], ninv_m), 1u);
+  for (uint32_t e = threadIdx.x; e < R * kCols; e += blockDim.x) {
+    const uint32_t m = e / kCols, c = e % kCols, i = m * C + col0 + c;
+    if (i >= L) continue;
+    // z holds N c R (Montgomery); mmul(., N^-1 R) = c R; mmul(., 1) = c
+    const uint32_t v = mmul(mmul(s[e], ninv_m), 1u);
     const int32_t cv = v > kP / 2 ? (int32_t)v - (int32_t)kP : (int32_t)v;
+    const uint32_t k = L - 1 - i;
     Cw[k] = cv;
-    if (Cl) Cl[k] = cv;
+    if (Cw2) Cw2[k] = cv;
     if (k > 0) {
       pm = max(pm, abs(cv));
       en += (long long)cv * cv;
@@ -118,10 +201,9 @@ __global__ void ntt_extract_kernel(const uint32_t* z, uint32_t N, uint32_t ninv_
 }
 
 __global__ void ntt_twiddle_kernel(uint32_t* tw, uint32_t half, uint32_t root_m) {
-  // tw[j] = root^j, computed per block by powering (each thread: square-and-multiply)
+  // tw[j] = root^j (Montgomery), each thread by square-and-multiply
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < half; j += gridDim.x * blockDim.x) {
-    const uint32_t one = 301989884u;
-    uint32_t r = one, b = root_m, e = j;
+    uint32_t r = kOne, b = root_m, e = j;
     while (e) {
       if (e & 1u) r = mmul(r, b);
       b = mmul(b, b);
@@ -146,47 +228,34 @@ uint32_t to_mont(uint32_t x) { return (uint32_t)(((uint64_t)x << 32) % kP); }
 }  // namespace
 
 // Builds C for n_walks walks (bits padded as in RunArgs, word i at bits[i+1]).
-// Scratch: 2 * n_walks * N uint32 + N/2 twiddles.  Returns launches or -1.
+// Scratch: n_walks * N uint32 + 2 * N/2 twiddles.  Returns launches or -1.
 int launch_build_tables_ntt(const RunArgs& a, uint32_t n_walks, cudaStream_t s) {
   const uint32_t L = a.L;
-  uint32_t N = 1;
-  while (N < 2 * L) N <<= 1;
-  uint32_t *x = nullptr, *y = nullptr, *tw = nullptr, *twi = nullptr;
-  const size_t total = (size_t)n_walks * N;
-  if (cudaMallocAsync(&x, 2 * total * 4, s) != cudaSuccess) return -1;
-  y = x + total;                              // [x arrays | y arrays]
-  if (cudaMallocAsync(&tw, (size_t)N / 2 * 4, s) != cudaSuccess) return -1;
-  if (cudaMallocAsync(&twi, (size_t)N / 2 * 4, s) != cudaSuccess) return -1;
+  uint32_t logN = 1;
+  while ((1u << logN) < 2 * L) ++logN;
+  const uint32_t N = 1u << logN;
+  const uint32_t logR = logN / 2, R = 1u << logR, C = N >> logR;   // R <= C <= 2R
+  if (R > (uint32_t)kMaxRows || C > (uint32_t)kMaxRowLen || C < (uint32_t)kCols) return -1;
+  uint32_t *x = nullptr, *tw = nullptr;
+  if (cudaMallocAsync(&x, (size_t)n_walks * N * 4, s) != cudaSuccess) return -1;
+  if (cudaMallocAsync(&tw, (size_t)N * 4, s) != cudaSuccess) return -1;
+  uint32_t* twi = tw + N / 2;
   int launches = 0;
   const uint32_t root = host_pow(3, (kP - 1) / N);          // primitive N-th root
   const uint32_t iroot = host_pow(root, kP - 2);
   ntt_twiddle_kernel<<<(N / 2 + 255) / 256, 256, 0, s>>>(tw, N / 2, to_mont(root));
   ntt_twiddle_kernel<<<(N / 2 + 255) / 256, 256, 0, s>>>(twi, N / 2, to_mont(iroot));
-  launches += 2;
-  const dim3 gl(std::min<uint32_t>((N + 255) / 256, 256), n_walks);
-  ntt_load_kernel<<<gl, 256, 0, s>>>(a.bits_piv + a.w_front + 1, a.w_stride, L, N, x, y);
-  launches += 1;
-  const uint32_t bx = std::min<uint32_t>((N / 2 + 255) / 256, 1024);
-  for (uint32_t h = N / 2; h >= 1; h >>= 1) {
-    ntt_stage_kernel<true><<<dim3(bx, 2 * n_walks), 256, 0, s>>>(x, N, h, tw, n_walks);
-    launches += 1;
-    if (h == 1) break;
-  }
-  ntt_pointwise_kernel<<<4096, 256, 0, s>>>(x, y, total);
-  launches += 1;
-  for (uint32_t h = 1; h <= N / 2; h <<= 1) {
-    ntt_stage_kernel<false><<<dim3(bx, n_walks), 256, 0, s>>>(x, N, h, twi, n_walks);
-    launches += 1;
-  }
-  // N^-1 in Montgomery-domain factor: z holds N*c (Montgomery form, i.e. N*c*R).
-  // mmul(zM, ninvM) = N*c*R * Ninv*R / R = c*R ; mmul(., 1) = c.
+  const dim3 gcol(C / kCols, n_walks), grow(R, n_walks);
+  ntt_col_fwd_kernel<<<gcol, 256, 0, s>>>(a.bits_piv + a.w_front + 1, a.w_stride, L, R, C, tw, x);
+  ntt_row_kernel<true><<<grow, 256, 0, s>>>(x, R, C, tw);
+  ntt_pointwise_kernel<<<dim3(std::min<uint32_t>(N / 256, 1024), n_walks), 256, 0, s>>>(x, logN, L, tw);
+  ntt_row_kernel<false><<<grow, 256, 0, s>>>(x, R, C, twi);
   const uint32_t ninv = host_pow(N, kP - 2);
-  ntt_extract_kernel<<<dim3(std::min<uint32_t>((L + 255) / 256, 256), n_walks), 256, 0, s>>>(
-      x, N, to_mont(ninv), L, a.Cpiv, a.Cloc, a.c_stride, a.st);
-  launches += 1;
+  ntt_col_inv_kernel<<<gcol, 256, 0, s>>>(x, R, C, twi, to_mont(ninv), L, a.Cpiv, a.Cloc, a.c_stride,
+                                           a.st);
+  launches += 7;
   cudaFreeAsync(x, s);
   cudaFreeAsync(tw, s);
-  cudaFreeAsync(twi, s);
   return cudaGetLastError() == cudaSuccess ? launches : -1;
 }
 

@@ -339,6 +339,28 @@ def test_walks_warm_starts(engine):
         engine.run_walks(p, 3, inits=bad)
 
 
+def test_walks_warm_starts_unaligned(engine):
+    """Odd L: walks start at every byte alignment of the packed-int8 upload
+    (the device validates / packs 32-byte groups with aligned loads + funnel
+    shifts); first offending element wins."""
+    L, nw = 301, 6
+    rng = np.random.default_rng(9)
+    inits = np.where(rng.integers(0, 2, (nw, L)) == 1, -1, 1).astype(np.int8)
+    p = _params(engine, L, 11, 4, 13, 6, 10, 64, 1 + 8 * 64)
+    recs = engine.run_walks(p, nw, inits=inits)
+    for w, r in enumerate(recs):
+        rc, orec, osol, _, _ = O.run_search(L, 11 + w, 4, 13, 6, 10, 64, 1 + 8 * 64, init=inits[w])
+        assert (r.nse, r.psl_best) == (orec.nse, orec.psl_best)
+        assert np.array_equal(r.solution_best, osol)
+    for (w, i, v) in ((3, 40, 2), (5, 300, 0), (1, 63, -3)):
+        bad = inits.copy()
+        bad[w, i] = v
+        if i + 100 < L:
+            bad[w, i + 100] = 7            # a later offender in the same walk is not reported
+        with pytest.raises(engine.ConfigError, match=f"position {i} is {v};"):
+            engine.run_walks(p, nw, inits=bad)
+
+
 def test_drain_and_resume(engine, golden, monkeypatch):
     """Tiny device event/trace buffers: run_search drains and relaunches many
     times; hooks must still see the reference's exact event/trace stream."""
