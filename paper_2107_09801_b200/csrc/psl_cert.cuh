@@ -457,6 +457,48 @@ __device__ __forceinline__ void cert_issue(const CertSmem& cs, uint32_t tmem, in
   }
 }
 
+// The same MMAs issued by a whole warp (warp-uniform descriptors, one lane
+// elected inside the asm; no per-MMA waterfall over a divergent thread), then
+// committed to the iteration's barrier by the elected lane.
+__device__ __forceinline__ void umma_i8_elect(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
+}
+__device__ __forceinline__ void cert_issue_warp(const CertSmem& cs, uint32_t tmem, int32_t c, bool fwd,
+                                                bool rev, uint32_t started, uint64_t* mbar) {
+  const uint32_t abuf = smem_u32(cs.acore) + (uint32_t)(c & 1) * (uint32_t)kABuf;
+  const uint32_t ring = smem_u32(cs.dring);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (fwd) {
+    const long long q0 = (long long)(kCC / 16) * c - 56;
+    uint64_t da = umma_desc(abuf, 256, 128);
+    uint64_t db = umma_desc(ring + (uint32_t)((((q0 % kRing) + kRing) % kRing) * 128), 128, 1024);
+#pragma unroll
+    for (int s = 0; s < kCCols; ++s) {
+      umma_i8_elect(tmem, da, db, (s > 0 || (started & 1u)) ? 1u : 0u);
+      da += 512 >> 4;
+      db += 256 >> 4;
+    }
+  }
+  if (rev) {
+    const long long q0 = (long long)(kCC / 16) * (c - (int32_t)kLag);
+    uint64_t da = umma_desc(abuf + (uint32_t)(kACores * 128), 256, 128);
+    uint64_t db = umma_desc(ring + (uint32_t)((((q0 % kRing) + kRing) % kRing) * 128), 128, 1024);
+#pragma unroll
+    for (int s = 0; s < kCCols; ++s) {
+      umma_i8_elect(tmem + 64, da, db, (s > 0 || (started & 2u)) ? 1u : 0u);
+      da += 512 >> 4;
+      db += 256 >> 4;
+    }
+  }
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+          smem_u32(mbar)) : "memory");
+}
+
 // ---- the cross term on mma.sync (zone-1 chunks)
 __device__ __forceinline__ void imma_s8(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                         uint32_t a3, uint32_t b0, uint32_t b1) {

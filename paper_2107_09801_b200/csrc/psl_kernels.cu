@@ -164,6 +164,8 @@ struct Ctl {
   double rs5[5][16];
   uint32_t cfw[72], crv[72]; // per-chunk tcgen05 flags of the pass segment (bit c: fwd / rev MMAs)
   uint64_t mbar[2];          // tcgen05 commit barriers (iteration parity)
+  uint64_t mbar_f[2];        // decoupled issuer: chunk staged (builder warps arrive)
+  uint64_t mbar_e[2];        // decoupled issuer: warp 15 done reading the chunk's buffers
   uint32_t tmem;             // TMEM base of this CTA's accumulators (kTmemCols columns)
 };
 
@@ -957,6 +959,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
   __syncthreads();
   if (ctl->st.done || ctl->st.status != PSL_OK) return;
   uint32_t mb_par[2] = {0u, 0u};   // next phase parity to wait for on ctl->mbar[0/1]
+  uint32_t mf_par[2] = {0u, 0u}, me_par[2] = {0u, 0u};   // ... on ctl->mbar_f / mbar_e
   if (kCert) {
     if (t < 32) {   // the certified scan's tcgen05 accumulators live in TMEM
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -964,8 +967,12 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     if (t == 0) {
-      for (int i = 0; i < 2; ++i)
+      for (int i = 0; i < 2; ++i) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&ctl->mbar[i])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&ctl->mbar_f[i])),
+                     "r"(kCC / 32) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&ctl->mbar_e[i])) : "memory");
+      }
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1130,6 +1137,75 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         // reversed kappa'-chunk c - kLag, issue their tcgen05 MMAs (one thread, async),
         // then the zone-1 cross MMAs (mma.sync) and band-1 cells of chunk c
         PT_MARK(7);
+        if (kCC < kCertThreads) {
+          // ---- decoupled issuer (kCC = 480): warps 0-14 build / stage / cross and
+          // sync among themselves (named barrier 1); warp 15 waits for each staged
+          // chunk on an mbarrier, issues its tcgen05 MMAs (blocking while the
+          // tensor pipe drains them), runs its own cross rows and band cells and
+          // releases the chunk's buffers on a second mbarrier.
+          if (builder) {
+            uint32_t used = 0;
+            for (uint32_t c = 0; c < nch + kLag; ++c) {
+              const uint32_t b = c & 1;
+              if (used & (1u << b)) {       // iteration c - 2 used buffer b
+                if (issued & (1u << b)) { mbar_wait(&ctl->mbar[b], mb_par[b]); mb_par[b] ^= 1u; }
+                mbar_wait(&ctl->mbar_e[b], me_par[b]);
+                me_par[b] ^= 1u;
+                issued &= ~(1u << b);
+              }
+              used |= 1u << b;
+              const bool fw = (ctl->cfw[c >> 5] >> (c & 31)) & 1u, rv = (ctl->crv[c >> 5] >> (c & 31)) & 1u;
+              if (c < nch) {
+                if (c + 2 < nch) cert_prefetch(io, cs, c + 2);
+                const uint2 fnext = (io.F == 1 && c + 1 < nch) ? cert_fold_words(io, c + 1, sm.sb) : fwords;
+                const int pending = (int)min(2u, nch - 1 - c);
+                cert_build(io, cs, c, sm.sb, pmax, part, cert_take(cs, c, pending), fwords, ovf);
+                fwords = fnext;
+              } else {
+                cert_zero_digits(cs, c);
+              }
+              cert_cores(io, cs, (int32_t)c, sm.sb, fw, rv);
+              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+              asm volatile("bar.sync 1, %0;" ::"n"(kCC) : "memory");
+              if ((t & 31) == 0)
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&ctl->mbar_f[b])) : "memory");
+              if (fw || rv) {
+                started |= (fw ? 1u : 0u) | (rv ? 2u : 0u);
+                numma += (fw ? kCCols : 0) + (rv ? kCCols : 0);
+                issued |= 1u << b;
+              }
+              if (c < nch) {
+                cert_cross_chunk(io, ln, c, acc, nmma);
+                if (io.chain && t == kCertThreads - 64) cert_chain_chunk(io, cs, c, chain);
+                if (t >= (uint32_t)kThreads && cert_band_chunk(io, c)) cert_band_cells(io, cs, c, sm.sb, Bs, t - kThreads);
+              }
+            }
+            for (uint32_t bb = 0; bb < 2; ++bb) {
+              if (issued & (1u << bb)) { mbar_wait(&ctl->mbar[bb], mb_par[bb]); mb_par[bb] ^= 1u; }
+              if (used & (1u << bb)) { mbar_wait(&ctl->mbar_e[bb], me_par[bb]); me_par[bb] ^= 1u; }
+            }
+            issued = 0;
+          } else {
+            for (uint32_t c = 0; c < nch + kLag; ++c) {
+              const uint32_t b = c & 1;
+              mbar_wait(&ctl->mbar_f[b], mf_par[b]);
+              mf_par[b] ^= 1u;
+              const bool fw = (ctl->cfw[c >> 5] >> (c & 31)) & 1u, rv = (ctl->crv[c >> 5] >> (c & 31)) & 1u;
+              if (fw || rv) {
+                cert_issue_warp(cs, tmem, (int32_t)c, fw, rv, started, &ctl->mbar[b]);
+                started |= (fw ? 1u : 0u) | (rv ? 2u : 0u);
+                numma += (fw ? kCCols : 0) + (rv ? kCCols : 0);
+              }
+              if (c < nch) {
+                cert_cross_chunk(io, ln, c, acc, nmma);
+                if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, sm.sb, Bs, t - kThreads);
+              }
+              __syncwarp();
+              if ((t & 31) == 0)
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&ctl->mbar_e[b])) : "memory");
+            }
+          }
+        } else
         for (uint32_t c = 0; c < nch + kLag; ++c) {
           if (issued & (1u << (c & 1))) {      // MMAs of iteration c - 2 read this buffer
             PT_MARK(0);

@@ -10,7 +10,7 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
   return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
 }
-__global__ void __launch_bounds__(128) k(int n, int R, int ldsw, long long* out, int nis) {
+__global__ void __launch_bounds__(128) k(int n, int R, int ldsw, long long* out, int nis, int mode) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint32_t tmem_base;
   __shared__ __align__(8) uint64_t mbar;
@@ -32,7 +32,28 @@ __global__ void __launch_bounds__(128) k(int n, int R, int ldsw, long long* out,
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(smem);
   const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
   long long t0 = 0, t1 = 0, t2 = 0;
-  if ((t & 31) == 0 && (t >> 5) < nis) {
+  if (mode == 1 && t < 32) {
+    // whole warp, uniform descriptors, one lane elected inside the asm
+    uint64_t da = sdesc(base, 256, 128), db = sdesc(base + 40960, 128, 1024);
+    t0 = clock64();
+#pragma unroll 1
+    for (int r = 0; r < R; ++r) {
+      asm volatile("{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+                   "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_base),
+                   "l"(da), "l"(db), "r"(idesc), "r"(r));
+      da += 512 >> 4; db += 256 >> 4;
+      if ((r & 15) == 15) { da -= (16 * 512) >> 4; db -= (16 * 256) >> 4; }
+    }
+    t1 = clock64();
+    if (t == 0)
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       (uint32_t)__cvta_generic_to_shared(&mbar)) : "memory");
+    uint32_t done = 0;
+    for (int it = 0; !done && it < 2000000; ++it)
+      asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                   "selp.u32 %0, 1, 0, p;\n\t}\n" : "=r"(done) : "r"((uint32_t)__cvta_generic_to_shared(&mbar)), "r"(0) : "memory");
+    t2 = clock64();
+  } else if (mode == 0 && (t & 31) == 0 && (t >> 5) < nis) {
     uint64_t da = sdesc(base, 256, 128), db = sdesc(base + 40960, 128, 1024);
     t0 = clock64();
     for (int r = 0; r < R / nis; ++r) {
@@ -72,14 +93,15 @@ int main(int argc, char** argv) {
   long long h[2];
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
   int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-  for (int nis : {1, 2, 4}) if (!only_nis || nis == only_nis)
+  for (int mode : {0, 1})
+  for (int nis : {1}) if (!only_nis || nis == only_nis)
   for (int ldsw : {0})
-    for (int n : {16, 64, 128, 256})
-      for (int R : {8, 32, 64}) {
-        k<<<nsm, 128, 96 * 1024>>>(n, R, ldsw, d, nis);
-        k<<<nsm, 128, 96 * 1024>>>(n, R, ldsw, d, nis);
+    for (int n : {64})
+      for (int R : {1, 2, 4, 8, 16, 32}) {
+        k<<<nsm, 128, 96 * 1024>>>(n, R, ldsw, d, nis, mode);
+        k<<<nsm, 128, 96 * 1024>>>(n, R, ldsw, d, nis, mode);
         cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
-        printf("issuers=%d lds=%d N=%2d R=%2d issue %6lld cyc  complete %6lld cyc  (%.1f cyc/mma)  %s\n", nis, ldsw, n, R, h[0], h[1],
+        printf("mode=%d issuers=%d lds=%d N=%2d R=%2d issue %6lld cyc  complete %6lld cyc  (%.1f cyc/mma)  %s\n", mode, nis, ldsw, n, R, h[0], h[1],
                (double)h[1] / R, cudaGetErrorString(cudaGetLastError()));
       }
   return 0;
