@@ -257,10 +257,8 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
   }
   // fixed point -> 8 balanced base-256 digits
   const long long hv = __double2ll_rn(__dmul_rn(H, io.scaleH));
-  const long long rv = __double2ll_rn(__dmul_rn(R, io.scaleR));
   // |v| < 2^61 (the units leave a 4x margin under 2^62 < kMaxD): top 3 bits all equal
-  ovf |= (((unsigned long long)hv + (1ull << 61)) >> 62) != 0 ||
-         (((unsigned long long)rv + (1ull << 61)) >> 62) != 0;
+  ovf |= (((unsigned long long)hv + (1ull << 61)) >> 62) != 0;
   const unsigned long long dh = ((unsigned long long)hv + 0x8080808080808080ull) ^ 0x8080808080808080ull;
   // H4 digit core: core q = 16 c + t / 16 holds rows d (16 shifts each).  Lane
   // x of a 4-lane group assembles row (x & 3) / row 4 + (x & 3) of the group's
@@ -293,6 +291,8 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
   if (kb > io.m_lo) return;
   // zone-1 chunk: R4 digit rows and the sequence windows of the cross MMAs
   {
+    const long long rv = __double2ll_rn(__dmul_rn(R, io.scaleR));
+    ovf |= (((unsigned long long)rv + (1ull << 61)) >> 62) != 0;
     const unsigned long long dr = ((unsigned long long)rv + 0x8080808080808080ull) ^ 0x8080808080808080ull;
     unsigned char* lr = cs.limbR + (size_t)b * kLimbBuf + t;
 #pragma unroll
@@ -420,46 +420,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
   }
 }
 
-// The tensor-core MMAs of iteration c (one thread): forward kappa-chunk c and
-// reversed kappa'-chunk c - kLag, 8 K-steps of 32 shifts each.  Descriptors
-// advance by constants per K-step: A by 4 cores (512 B), B by 2 digit cores
-// (256 B; the double-mapped ring keeps every span contiguous).
-__device__ __forceinline__ void cert_issue(const CertSmem& cs, uint32_t tmem, int32_t c, bool fwd,
-                                           bool rev, uint32_t& started) {
-  const uint32_t abuf = smem_u32(cs.acore) + (uint32_t)(c & 1) * (uint32_t)kABuf;
-  const uint32_t ring = smem_u32(cs.dring);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (fwd) {
-    // B core of K-step s, N-group g (sigma = 7 - g): k = kappa - 128 sigma -> q = 16c - 56 + 2s + h + 8g
-    const long long q0 = (long long)(kCC / 16) * c - 56;
-    uint64_t da = umma_desc(abuf, 256, 128);
-    uint64_t db = umma_desc(ring + (uint32_t)((((q0 % kRing) + kRing) % kRing) * 128), 128, 1024);
-#pragma unroll
-    for (int s = 0; s < kCCols; ++s) {
-      umma_i8(tmem, da, db, (s > 0 || (started & 1u)) ? 1u : 0u);
-      da += 512 >> 4;
-      db += 256 >> 4;
-    }
-    started |= 1u;
-  }
-  if (rev) {
-    // N-group g = sigma: k = kappa' + 128 sigma -> q = 16 cr + 2s + h + 8g
-    const long long q0 = (long long)(kCC / 16) * (c - (int32_t)kLag);
-    uint64_t da = umma_desc(abuf + (uint32_t)(kACores * 128), 256, 128);
-    uint64_t db = umma_desc(ring + (uint32_t)((((q0 % kRing) + kRing) % kRing) * 128), 128, 1024);
-#pragma unroll
-    for (int s = 0; s < kCCols; ++s) {
-      umma_i8(tmem + 64, da, db, (s > 0 || (started & 2u)) ? 1u : 0u);
-      da += 512 >> 4;
-      db += 256 >> 4;
-    }
-    started |= 2u;
-  }
-}
-
-// The same MMAs issued by a whole warp (warp-uniform descriptors, one lane
-// elected inside the asm; no per-MMA waterfall over a divergent thread), then
-// committed to the iteration's barrier by the elected lane.
+// The tensor-core MMAs of iteration c, issued by a whole warp (warp-uniform
+// descriptors, one lane elected inside the asm: no per-MMA waterfall over a
+// divergent thread): forward kappa-chunk c and reversed kappa'-chunk c - kLag,
+// kCCols K-steps of 32 shifts each.  Descriptors advance by constants per
+// K-step: A by 4 cores (512 B), B by 2 digit cores (256 B; the double-mapped
+// ring keeps every span contiguous).  Then committed to the iteration's
+// barrier by the elected lane.
 __device__ __forceinline__ void umma_i8_elect(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"

@@ -1238,11 +1238,8 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
 #else
           if ((fw || rv)) {
 #endif
-            if (t == kCertThreads - 32) {              // warp 15 stages no cores: it issues
-              uint32_t st = started;
-              cert_issue(cs, tmem, (int32_t)c, fw, rv, st);
-              umma_commit(&ctl->mbar[c & 1]);
-            }
+            // warp 15 (stages no cores) issues, one lane elected per MMA
+            if ((t >> 5) == 15) cert_issue_warp(cs, tmem, (int32_t)c, fw, rv, started, &ctl->mbar[c & 1]);
             started |= (fw ? 1u : 0u) | (rv ? 2u : 0u);   // uniform copy of the issuer's flags
             numma += (fw ? kCCols : 0) + (rv ? kCCols : 0);
             issued |= 1u << (c & 1);
