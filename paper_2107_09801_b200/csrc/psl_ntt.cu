@@ -57,15 +57,38 @@ __device__ __forceinline__ uint32_t wpow(const uint32_t* tw, uint32_t e, uint32_
   return e < h ? tw[e] : (kP - tw[e - h]) % kP;
 }
 
+// Twiddle factors of the column stages for the CTA's 8 columns: stage st
+// (hr = R/2 >> st, span h = hr C) needs w^{(jr C + col) N / 2h}
+// = w^{jr N / 2hr} * w^{col N / 2h}: rf[hr + jr] and cf[st][c] (Montgomery;
+// the product costs one extra mmul per butterfly instead of a scattered load).
+__device__ __forceinline__ void col_twiddles(const uint32_t* tw, uint32_t R, uint32_t C, uint32_t col0,
+                                             uint32_t* rf, uint32_t* cf) {
+  const uint32_t N = R * C;
+  for (uint32_t hr = 1; hr < R; hr <<= 1)
+    for (uint32_t jr = threadIdx.x; jr < hr; jr += blockDim.x) rf[hr + jr] = tw[jr * (N / (2 * hr))];
+  uint32_t st = 0;
+  for (uint32_t hr = R >> 1; hr >= 1; hr >>= 1, ++st)
+    if (threadIdx.x < (uint32_t)kCols) {
+      const uint32_t col = col0 + threadIdx.x;
+      // col N / 2h = col R / 2hr * (N / (R C)) ... as an index into tw: col * (N / (2 hr C))
+      const uint32_t e = col * (N / (2 * hr * C));
+      cf[st * kCols + threadIdx.x] = (N / (2 * hr * C)) ? tw[e] : 0u;
+    }
+  __syncthreads();
+}
+
 // Forward column pass: stages h = N/2 .. C (rows span R/2 .. 1), DIF.  The
 // inputs are generated from the packed bits (x_i = +-1 for i < L, 0 past L).
 __global__ void __launch_bounds__(256) ntt_col_fwd_kernel(const uint32_t* bits, size_t w_stride,
                                                           uint32_t L, uint32_t R, uint32_t C,
                                                           const uint32_t* tw, uint32_t* x) {
   __shared__ uint32_t s[kMaxRows * kCols];
+  __shared__ uint32_t rf[kMaxRows];                          // rf[hr + jr] = w^{jr N / 2hr}
+  __shared__ uint32_t cf[11 * kCols];                        // cf[stage][c] = w^{col N / (2 hr C)}
   const uint32_t walk = blockIdx.y, col0 = blockIdx.x * kCols;
   const uint32_t N = R * C;
   const uint32_t* S = bits + (size_t)walk * w_stride;
+  col_twiddles(tw, R, C, col0, rf, cf);
   for (uint32_t e = threadIdx.x; e < R * kCols; e += blockDim.x) {
     const uint32_t m = e / kCols, c = e % kCols, i = m * C + col0 + c;
     uint32_t v = 0;
@@ -73,13 +96,12 @@ __global__ void __launch_bounds__(256) ntt_col_fwd_kernel(const uint32_t* bits, 
     s[e] = v;
   }
   __syncthreads();
-  for (uint32_t hr = R >> 1; hr >= 1; hr >>= 1) {
-    const uint32_t h = hr * C, tstride = N / (2 * h);
+  for (uint32_t hr = R >> 1, st = 0; hr >= 1; hr >>= 1, ++st) {
     for (uint32_t b = threadIdx.x; b < (R / 2) * kCols; b += blockDim.x) {
       const uint32_t c = b % kCols, q = b / kCols;          // q-th butterfly row pair
       const uint32_t jr = q & (hr - 1), m1 = ((q - jr) << 1) + jr, m2 = m1 + hr;
-      const uint32_t j = jr * C + col0 + c;                   // position within the 2h block
-      const uint32_t w = tw[j * tstride];
+      // position j = jr C + col within the 2h block: w^{j N / 2h} = rf * cf
+      const uint32_t w = mmul(rf[hr + jr], cf[st * kCols + c]);
       const uint32_t u = s[m1 * kCols + c], v = s[m2 * kCols + c];
       s[m1 * kCols + c] = madd(u, v);
       s[m2 * kCols + c] = mmul(msub(u, v), w);
@@ -151,21 +173,25 @@ __global__ void __launch_bounds__(256) ntt_col_inv_kernel(const uint32_t* x, uin
                                                           uint32_t L, int32_t* Cp, int32_t* Cl,
                                                           size_t c_stride, WalkState* st) {
   __shared__ uint32_t s[kMaxRows * kCols];
+  __shared__ uint32_t rf[kMaxRows];
+  __shared__ uint32_t cf[11 * kCols];
   const uint32_t walk = blockIdx.y, col0 = blockIdx.x * kCols;
   const uint32_t N = R * C;
   const uint32_t* X = x + (size_t)walk * N;
+  col_twiddles(twi, R, C, col0, rf, cf);
   for (uint32_t e = threadIdx.x; e < R * kCols; e += blockDim.x) {
     const uint32_t m = e / kCols, c = e % kCols;
     s[e] = X[m * C + col0 + c];
   }
   __syncthreads();
+  uint32_t sg = 0;
+  for (uint32_t hr = R >> 1; hr >= 1; hr >>= 1) ++sg;       // stage index of hr = 1 in col_twiddles order
   for (uint32_t hr = 1; hr < R; hr <<= 1) {
-    const uint32_t h = hr * C, tstride = N / (2 * h);
+    --sg;
     for (uint32_t b = threadIdx.x; b < (R / 2) * kCols; b += blockDim.x) {
       const uint32_t c = b % kCols, q = b / kCols;
       const uint32_t jr = q & (hr - 1), m1 = ((q - jr) << 1) + jr, m2 = m1 + hr;
-      const uint32_t j = jr * C + col0 + c;
-      const uint32_t w = twi[j * tstride];
+      const uint32_t w = mmul(rf[hr + jr], cf[sg * kCols + c]);
       const uint32_t u = s[m1 * kCols + c], vw = mmul(s[m2 * kCols + c], w);
       s[m1 * kCols + c] = madd(u, vw);
       s[m2 * kCols + c] = msub(u, vw);
