@@ -158,7 +158,7 @@ struct Ctl {
   long long energy;
   // certified scan (psl_cert.cuh)
   int32_t cert, need_exact, need_vl, cmp, cv_exact, c_qH, c_qR, c_ovf;
-  double cv_lo, cv_hi;
+  double cv_lo, cv_hi, gv_lo, gv_hi;
   double c_scaleH, c_unitH, c_scaleR, c_unitR, c_sconst, c_errconst;
   uint32_t m_lo, m_hi, M_lo, M_hi;
   double rs5[5][16];
@@ -1000,7 +1000,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
       ctl->cert = 0;
       ctl->need_exact = 0;
       ctl->need_vl = 0;
-      if (kCert && a.cert && ctl->do_scan && a.n <= (uint32_t)kGroup &&
+      if (kCert && a.cert && ctl->do_scan &&
           L >= kCertMinL) {
         // fixed-point scale: every |H4|, |R4| <= 2 pow(Amax, alpha) < 2^(62+q)
         const uint32_t alpha = S.phase == 1 ? a.alpha1 : a.alpha2;
@@ -1055,12 +1055,23 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           lut_c = lut_s;
         }
       }
-      const uint32_t nA = min(a.n, L - 1 - start);          // rows before the wrap
-      const int nseg = (nA > 0 && nA < a.n) ? 2 : 1;
+      // n_lmt > 1024: groups of 1024 rows, one certified pass each (the first one
+      // folds the move into C, collects the high sidelobes and the fitness chain);
+      // group results combine in ascending offset order like the exact sweep's
+      const uint32_t ngrp = (a.n + kGroup - 1) / kGroup;
+      double* lo_all = a.lo_buf + (size_t)w * a.n;           // per-row lower bounds (ngrp > 1)
+      for (uint32_t g = 0; g < ngrp; ++g) {
+      const bool first = g == 0;
+      const uint32_t gn = min((uint32_t)kGroup, a.n - g * kGroup);
+      const uint32_t gs = (uint32_t)(((uint64_t)start + (uint64_t)g * kGroup) % L);   // rows j = gs + 1 + rho
+#pragma unroll
+      for (int m = 0; m < kJ; ++m) { mid[m] = 0.0; lo[m] = 0.0; hi[m] = 0.0; }
+      const uint32_t nA = min(gn, L - 1 - gs);               // rows before the wrap
+      const int nseg = (nA > 0 && nA < gn) ? 2 : 1;
       for (int seg = 0; seg < nseg; ++seg) {
         const bool wrapped = seg == 1 || nA == 0;            // rows past L - 1: j = rho - nA
-        const uint32_t r_lo = seg ? nA : 0, r_hi = (nseg == 2 && seg == 0) ? nA : a.n;
-        const int32_t j0 = wrapped ? (int32_t)start + 1 - (int32_t)L : (int32_t)start + 1;
+        const uint32_t r_lo = seg ? nA : 0, r_hi = (nseg == 2 && seg == 0) ? nA : gn;
+        const int32_t j0 = wrapped ? (int32_t)gs + 1 - (int32_t)L : (int32_t)gs + 1;
         if (t == 0) {
           // zones over the segment's neighbours [jlo, jhi] (m_j = min(j, L-1-j))
           const uint32_t jlo = (uint32_t)(j0 + (int32_t)r_lo), jhi = (uint32_t)(j0 + (int32_t)r_hi - 1);
@@ -1073,15 +1084,15 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         }
         __syncthreads();
         CertIO io;
-        io.L = L; io.n = a.n; io.nchunks = (L - 1 + kCC - 1) / kCC;
+        io.L = L; io.n = gn; io.nchunks = (L - 1 + kCC - 1) / kCC;
         io.j0 = j0; io.r_lo = r_lo; io.r_hi = r_hi; io.JT = j0 + (int32_t)r_lo;
-        if (seg == 0) {
+        if (first && seg == 0) {
           io.Csrc = s_src_local ? Cloc : Cpiv;
           io.Cdst = Cpiv;
           io.Cloc = s_local_pending ? Cloc : nullptr;
           io.F = s_n_pending;
           io.hlist = hlist;
-        } else {   // C already folded and written by the first segment's pass
+        } else {   // C already folded and written by the first pass
           io.Csrc = Cpiv; io.Cdst = nullptr; io.Cloc = nullptr; io.F = 0; io.hlist = nullptr;
         }
         io.flips = flips;
@@ -1096,7 +1107,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         io.b2E = io.b2M + kGroup;
         // first step / restart: fitness() of the folded table, serially, by one
         // thread of warp 14 behind the builder (search.cpp:348, :409)
-        io.chain = seg == 0 && s_fitness_pending != 0;
+        io.chain = first && seg == 0 && s_fitness_pending != 0;
         double chain = 0.0;
         int acc[kCertTiles][4];
 #pragma unroll
@@ -1261,7 +1272,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
                                      (unsigned long long)nmma);
         if (t == 0) ctl->st.n_umma += numma;
         if (ovf) atomicOr(&ctl->c_ovf, 1);
-        if (seg == 0) {
+        if (first && seg == 0) {
           if (io.chain && t == kCertThreads - 64) ctl->fit = chain;
           const int32_t Pn = block_max(ctl, pmax);   // (its barrier publishes ctl->fit)
           if (t == 0) first_pass_state(ctl, a, w, Pn, ctl->fit, alpha);
@@ -1337,75 +1348,103 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         }
         __syncthreads();
       }
-      filter_hlist(ctl, sm, hlist);
-      __syncthreads();
+      if (first) {
+        filter_hlist(ctl, sm, hlist);
+        __syncthreads();
+      }
       {
         bool active[kJ];
         uint32_t jj[kJ];
         const uint32_t owner = t >= (uint32_t)kThreads ? t - kThreads : 0u;
-        const uint32_t ibase = kJ * owner;
+        const uint32_t ibase = g * kGroup + kJ * owner;
 #pragma unroll
         for (int m = 0; m < kJ; ++m) {
           const uint32_t rho = kJ * owner + m;
-          active[m] = t >= (uint32_t)kThreads && rho < a.n;
-          uint32_t j = start + 1 + rho;
+          active[m] = t >= (uint32_t)kThreads && rho < gn;
+          uint32_t j = gs + 1 + rho;
           if (j >= L) j -= L;
           jj[m] = j;
         }
         reduce_group(ctl, sm, hlist, active, jj, mid, ibase, L);
         const uint32_t bi = ctl->best_i;
 #pragma unroll
-        for (int m = 0; m < kJ; ++m)
-          if (active[m] && ibase + m + 1 == bi) { ctl->cv_lo = lo[m]; ctl->cv_hi = hi[m]; }
-        __syncthreads();
-        const double hs = ctl->cv_hi;
-        int amb = 0;
-#pragma unroll
-        for (int m = 0; m < kJ; ++m) amb |= active[m] && ibase + m + 1 != bi && lo[m] <= hs;
-        amb = __syncthreads_or(amb);
-        if (t == 0) {
-          ctl->cv = ctl->best_v; ctl->ci = ctl->best_i;
-          ctl->cp = ctl->best_psl; ctl->cpi = ctl->best_pi; ctl->cbad = ctl->bad;
-          ctl->cv_exact = 0;
-          const WalkState& S = ctl->st;
-          int need = amb || ctl->bad || ctl->c_ovf;
-          if (!need) {
-            ctl->cmp = compare_local(S, ctl->cv_lo, ctl->cv_hi, false, ctl->cv);
-            need = ctl->cmp == 2;
-          }
-          ctl->need_exact = need;
-          ctl->st.n_cert += need ? 0 : 1;
-          ctl->st.n_refine += need ? 1 : 0;
-        }
-        __syncthreads();
-      }
-      if (ctl->need_exact) {
-        // exact re-score of the same pivot (flips already folded into Cpiv)
-        const uint32_t ibase = (t >> 5) * (32 * kJ) + (t & 31) * kJ;
-        bool active[kJ];
-        uint32_t jj[kJ];
-#pragma unroll
         for (int m = 0; m < kJ; ++m) {
-          const uint32_t i = ibase + m + 1;
-          active[m] = i <= a.n;
-          uint32_t j = 0;
-          if (active[m]) { j = start + i; if (j >= L) j -= L; }
-          jj[m] = j;
+          if (active[m] && ibase + m + 1 == bi) { ctl->gv_lo = lo[m]; ctl->gv_hi = hi[m]; }
+          if (active[m] && ngrp > 1) lo_all[ibase + m] = lo[m];
         }
-        SweepIO sio;
-        sio.L = L; sio.nwords = nw; sio.nchunks = a.nchunks;
-        sio.alpha = alpha; sio.lut = lut; sio.lut_size = a.lut_n;
-        sio.scan = true; sio.hcount = &ctl->hcount;
-        sio.Csrc = Cpiv; sio.Cdst = nullptr; sio.Cloc = nullptr;
-        sio.flips = flips; sio.F = 0; sio.hlist = nullptr; sio.hthr = 0; sio.chain = false;
-        int32_t pm = 0;
-        double chain = 0.0;
-        double val[kJ];
-        sweep(sio, sm, active, jj, val, pm, chain);
-        reduce_group(ctl, sm, hlist, active, jj, val, ibase, L);
+        __syncthreads();
+        if (t == 0) {   // combine groups in ascending offset order (strict <: smallest offset wins)
+          if (first || ctl->best_v < ctl->cv) {
+            ctl->cv = ctl->best_v; ctl->ci = ctl->best_i; ctl->cv_lo = ctl->gv_lo; ctl->cv_hi = ctl->gv_hi;
+          }
+          if (first || ctl->best_psl < ctl->cp) { ctl->cp = ctl->best_psl; ctl->cpi = ctl->best_pi; }
+          ctl->cbad = first ? ctl->bad : (ctl->cbad | ctl->bad);
+        }
+        __syncthreads();
+        if (g + 1 == ngrp) {
+          // certified argmin: no other row's interval reaches below the best's upper bound
+          const double hs = ctl->cv_hi;
+          const uint32_t ci = ctl->ci;
+          int amb = 0;
+          if (ngrp == 1) {
+#pragma unroll
+            for (int m = 0; m < kJ; ++m) amb |= active[m] && ibase + m + 1 != ci && lo[m] <= hs;
+          } else {
+            for (uint32_t i = t; i < a.n; i += blockDim.x) amb |= i + 1 != ci && lo_all[i] <= hs;
+          }
+          amb = __syncthreads_or(amb);
+          if (t == 0) {
+            ctl->cv_exact = 0;
+            const WalkState& S = ctl->st;
+            int need = amb || ctl->cbad || ctl->c_ovf;
+            if (!need) {
+              ctl->cmp = compare_local(S, ctl->cv_lo, ctl->cv_hi, false, ctl->cv);
+              need = ctl->cmp == 2;
+            }
+            ctl->need_exact = need;
+            ctl->st.n_cert += need ? 0 : 1;
+            ctl->st.n_refine += need ? 1 : 0;
+          }
+          __syncthreads();
+        }
+      }
+      }   // groups
+      if (ctl->need_exact) {
+        // exact re-score of the same pivot (flips already folded into Cpiv), in
+        // groups of kJ * blockDim.x rows combined in ascending offset order
+        const uint32_t rows_per = kJ * blockDim.x;
+        const uint32_t ng2 = (a.n + rows_per - 1) / rows_per;
+        for (uint32_t g2 = 0; g2 < ng2; ++g2) {
+          const uint32_t ibase = g2 * rows_per + (t >> 5) * (32 * kJ) + (t & 31) * kJ;
+          bool active[kJ];
+          uint32_t jj[kJ];
+#pragma unroll
+          for (int m = 0; m < kJ; ++m) {
+            const uint32_t i = ibase + m + 1;
+            active[m] = i <= a.n;
+            uint32_t j = 0;
+            if (active[m]) { j = (uint32_t)(((uint64_t)start + i) % L); }
+            jj[m] = j;
+          }
+          SweepIO sio;
+          sio.L = L; sio.nwords = nw; sio.nchunks = a.nchunks;
+          sio.alpha = alpha; sio.lut = lut; sio.lut_size = a.lut_n;
+          sio.scan = true; sio.hcount = &ctl->hcount;
+          sio.Csrc = Cpiv; sio.Cdst = nullptr; sio.Cloc = nullptr;
+          sio.flips = flips; sio.F = 0; sio.hlist = nullptr; sio.hthr = 0; sio.chain = false;
+          int32_t pm = 0;
+          double chain = 0.0;
+          double val[kJ];
+          sweep(sio, sm, active, jj, val, pm, chain);
+          reduce_group(ctl, sm, hlist, active, jj, val, ibase, L);
+          if (t == 0) {
+            if (g2 == 0 || ctl->best_v < ctl->cv) { ctl->cv = ctl->best_v; ctl->ci = ctl->best_i; }
+            if (g2 == 0 || ctl->best_psl < ctl->cp) { ctl->cp = ctl->best_psl; ctl->cpi = ctl->best_pi; }
+            ctl->cbad = g2 == 0 ? ctl->bad : (ctl->cbad | ctl->bad);
+          }
+          __syncthreads();
+        }
         if (t == 0) {
-          ctl->cv = ctl->best_v; ctl->ci = ctl->best_i;
-          ctl->cp = ctl->best_psl; ctl->cpi = ctl->best_pi; ctl->cbad = ctl->bad;
           ctl->cv_exact = 1; ctl->cv_lo = ctl->cv; ctl->cv_hi = ctl->cv;
           ctl->cmp = compare_local(ctl->st, ctl->cv, ctl->cv, true, ctl->cv);
           ctl->need_vl = !ctl->cbad && ctl->cmp == 2;

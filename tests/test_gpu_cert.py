@@ -85,6 +85,30 @@ def test_certified_vs_oracle_with_phase_switches(engine, L, n, a2, ls):
     assert st["certified"] > 0
 
 
+@pytest.mark.parametrize("L,n,ls,slack", [(5000, 3000, 3, None), (4097, 4097, 2, None),
+                                           (9000, 2049, 4, "1e-5"), (6000, 6000, 3, "1e-4")])
+def test_certified_row_groups_vs_oracle(engine, monkeypatch, L, n, ls, slack):
+    """n_lmt > 1024 (the paper's N_lmt = 6912 style): one certified pass per
+    group of 1024 rows, groups combined in offset order, wrapped windows inside
+    groups; with widened intervals the multi-group exact re-score and value_local
+    chains run too."""
+    if slack:
+        monkeypatch.setenv("PSLB200_CERT_SLACK", slack)
+    max_nse = 1 + 25 * n
+    rc, rec, sol, ev, _ = O.run_search(L, 3, 4, 13, ls, 10, n, max_nse, traces_cap=0)
+    assert rc == 0
+    ctx = engine.default_context()
+    before = ctx.scan_stats()
+    r = engine.run_search(_params(engine, L, 3, 4, 13, ls, 10, n, max_nse))
+    st = _stats_delta(ctx, before)
+    assert (r.nse, r.psl_best, to_pm(r.solution_best)) == (rec.nse, rec.psl_best, to_pm(sol))
+    assert hx(r.merit_factor) == hx(rec.merit_factor)
+    assert [(e.nse, e.psl_best, e.phase_index, int(e.kind)) for e in r.events] == ev
+    assert st["certified"] + st["refined"] > 0
+    if slack:
+        assert st["refined"] > 0
+
+
 @pytest.mark.parametrize("L,ls,slack", [(16383, 5, None), (65535, 3, None), (16383, 4, "1e-6")])
 def test_walks_auto_equals_exact(engine, monkeypatch, L, ls, slack):
     if slack:

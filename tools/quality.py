@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Best PSL at fixed wall time (BASELINE.json metric part 2, configs 4-5).
 
-For each m, runs W independent walks (seed0 + w, one CTA each, two per SM) of
+For each m, runs W independent walks (seed0 + w, one CTA each) of
 the two-phase search for T seconds on one B200 (max_seconds stop, device
 clock), and optionally the single-exponent ablations (alpha1 = alpha2 = 4 and
 alpha1 = alpha2 = default alpha2, reference main.cpp:145-151).  Prints one JSON
@@ -37,7 +37,7 @@ def main():
     ctx = P.Context(0)
     import torch
     nsm = torch.cuda.get_device_properties(0).multi_processor_count
-    walks = args.walks or 2 * nsm
+    walks = args.walks or nsm          # one walk CTA per SM (the certified kernel)
     for m in args.m:
         L = (1 << m) - 1
         a2 = P.default_alpha2(L)

@@ -10,7 +10,7 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
   return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
 }
-__global__ void __launch_bounds__(128) k(int n, int R, int ldsw, long long* out, int nis, int mode) {
+__global__ void __launch_bounds__(512) k(int n, int R, int ldsw, long long* out, int nis, int mode) {
   extern __shared__ __align__(1024) unsigned char smem[];
   __shared__ uint32_t tmem_base;
   __shared__ __align__(8) uint64_t mbar;
@@ -71,13 +71,14 @@ __global__ void __launch_bounds__(128) k(int n, int R, int ldsw, long long* out,
       asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
                    "selp.u32 %0, 1, 0, p;\n\t}\n" : "=r"(done) : "r"((uint32_t)__cvta_generic_to_shared(&mbar)), "r"(0) : "memory");
     t2 = clock64();
-  } else if (ldsw && t >= 32 * nis) {
-    // other warps hammer shared memory (LDS.32, conflict-free) meanwhile
-    uint32_t acc = 0, a = base + 4 * t;
+  }
+  if (ldsw && t >= 32) {
+    // other warps hammer shared memory (LDS.128, conflict-free) meanwhile
+    uint32_t acc = 0, a = base + 16 * (t & 31) + 512 * ((t >> 5) & 7);
     for (int i = 0; i < ldsw; ++i) {
-      uint32_t v;
-      asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a + ((i * 128) & 32767)));
-      acc += v;
+      uint4 v;
+      asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a + ((i * 4096) & 32767)));
+      acc += v.x ^ v.y ^ v.z ^ v.w;
     }
     if (acc == 0x12345) out[1023] = acc;
   }
@@ -93,15 +94,16 @@ int main(int argc, char** argv) {
   long long h[2];
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
   int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
-  for (int mode : {0, 1})
+  for (int mode : {1})
   for (int nis : {1}) if (!only_nis || nis == only_nis)
-  for (int ldsw : {0})
+  for (int thr : {128, 512})
+  for (int ldsw : {0, 20000})
     for (int n : {64})
-      for (int R : {1, 2, 4, 8, 16, 32}) {
-        k<<<nsm, 128, 96 * 1024>>>(n, R, ldsw, d, nis, mode);
-        k<<<nsm, 128, 96 * 1024>>>(n, R, ldsw, d, nis, mode);
+      for (int R : {32, 64}) {
+        k<<<nsm, thr, 96 * 1024>>>(n, R, ldsw, d, nis, mode);
+        k<<<nsm, thr, 96 * 1024>>>(n, R, ldsw, d, nis, mode);
         cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
-        printf("mode=%d issuers=%d lds=%d N=%2d R=%2d issue %6lld cyc  complete %6lld cyc  (%.1f cyc/mma)  %s\n", mode, nis, ldsw, n, R, h[0], h[1],
+        printf("thr=%d mode=%d issuers=%d lds=%d N=%2d R=%2d issue %6lld cyc  complete %6lld cyc  (%.1f cyc/mma)  %s\n", thr, mode, nis, ldsw, n, R, h[0], h[1],
                (double)h[1] / R, cudaGetErrorString(cudaGetLastError()));
       }
   return 0;
