@@ -53,7 +53,19 @@ psl_params to_c(const SearchParams& p) {
   c.max_nse = p.stop.max_nse.value_or(0);
   c.has_max_seconds = p.stop.max_seconds.has_value();
   c.max_seconds = p.stop.max_seconds.value_or(0.0);
-  c.init = p.init ? p.init->data() : nullptr;
+  c.init = nullptr;
+  if (p.init) {
+    if (p.init->size() != p.length) {
+      // the C ABI reads `length` elements: the checks that precede this one
+      // first (search.cpp:40-71), then the reference's message (:72-76)
+      char err[512] = {0};
+      const int rc = psl_validate_params(&c, nullptr, nullptr, 0, err, sizeof err);
+      if (rc != PSL_OK) raise(rc, err);
+      throw ConfigError("warm-start sequence has length " + std::to_string(p.init->size()) +
+                        ", expected " + std::to_string(p.length));
+    }
+    c.init = p.init->data();
+  }
   return c;
 }
 

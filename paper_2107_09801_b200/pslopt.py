@@ -193,7 +193,15 @@ def _to_c(p: SearchParams):
     c.max_seconds = float(p.stop.max_seconds or 0.0)
     keep = None
     if p.init is not None:
-        keep = np.ascontiguousarray(p.init, np.int8)
+        keep = np.ascontiguousarray(p.init, np.int8).reshape(-1)
+        if keep.size != p.length:
+            # the C ABI reads `length` elements: report the checks that precede
+            # this one first (search.cpp:40-71), then the reference's message (:72-76)
+            err = _err()
+            rc = B.lib().psl_validate_params(C.byref(c), None, None, 0, err, len(err))
+            if rc:
+                _raise(rc, err)
+            raise ConfigError(f"warm-start sequence has length {keep.size}, expected {p.length}")
         c.init = keep.ctypes.data
     return c, keep
 

@@ -74,8 +74,16 @@ def test_validate_rejects_bad_configurations():
     with pytest.raises(P.ConfigError):
         P.validate_params(p)
     p = _ok(init=np.ones(63, np.int8))
-    with pytest.raises(P.ConfigError):
+    with pytest.raises(P.ConfigError, match="warm-start sequence has length 63, expected 64"):
         P.validate_params(p)
+    # search.cpp:40-76 order: a bad exponent is reported before the init length
+    p = _ok(init=np.ones(63, np.int8))
+    p.alpha1 = 0
+    with pytest.raises(P.ConfigError, match="alpha1"):
+        P.validate_params(p)
+    # every entry that takes params checks the length before the C ABI reads `length` bytes
+    with pytest.raises(P.ConfigError, match="has length 65, expected 64"):
+        P.run_search(_ok(init=np.ones(65, np.int8)))
     p = _ok(init=np.array([1, 2] * 32, np.int8))
     with pytest.raises(P.ConfigError, match="must be \\+1 or -1"):
         P.validate_params(p)
