@@ -109,6 +109,27 @@ def test_certified_row_groups_vs_oracle(engine, monkeypatch, L, n, ls, slack):
         assert st["refined"] > 0
 
 
+def test_certified_high_psl_warm_start_vs_oracle(engine):
+    """A warm start with a huge peak sidelobe (PSL > 6139): the PowerTable head
+    does not fit in shared memory and the certified pass reads the global table."""
+    L, n = 16383, 1024
+    rng = np.random.default_rng(21)
+    init = np.ones(L, np.int8)
+    init[rng.choice(L, 2000, replace=False)] = -1        # C_1 ~ L - 4000: PSL ~ 12000
+    max_nse = 1 + 20 * n
+    rc, rec, sol, ev, _ = O.run_search(L, 7, 4, 13, 3, 10, n, max_nse, init=init, traces_cap=0)
+    assert rc == 0
+    ctx = engine.default_context()
+    before = ctx.scan_stats()
+    r = engine.run_search(_params(engine, L, 7, 4, 13, 3, 10, n, max_nse, init=init))
+    st = _stats_delta(ctx, before)
+    assert (r.nse, r.psl_best, to_pm(r.solution_best)) == (rec.nse, rec.psl_best, to_pm(sol))
+    assert hx(r.merit_factor) == hx(rec.merit_factor)
+    assert [(e.nse, e.psl_best, e.phase_index, int(e.kind)) for e in r.events] == ev
+    assert st["certified"] > 0
+    assert r.psl_best > 6139
+
+
 @pytest.mark.parametrize("L,ls,slack", [(16383, 5, None), (65535, 3, None), (16383, 4, "1e-6")])
 def test_walks_auto_equals_exact(engine, monkeypatch, L, ls, slack):
     if slack:
