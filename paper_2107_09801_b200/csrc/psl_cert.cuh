@@ -91,6 +91,8 @@ struct CertIO {
   double* b2M;                                // [1024] global scratch: band-2 4M_k, 4 e2_k
   double* b2E;
   bool chain;                                 // also the serial fitness() of the folded table
+  bool fsum;                                  // the initial fitness() as a certified interval:
+                                              // builders add lut[|C_k|] into part[3]
 };
 
 struct CertSmem {
@@ -216,6 +218,7 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
       cv = fold_flips(cv, k, fio, sb);
     }
 #endif
+    if (io.fsum) part[3] = __dadd_rn(part[3], io.lut[abs(cv)]);
     if (io.Cdst) io.Cdst[k] = cv;
     if (io.Cloc) io.Cloc[k] = cv;
     const int32_t a = abs(cv);

@@ -1107,7 +1107,14 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         io.b2E = io.b2M + kGroup;
         // first step / restart: fitness() of the folded table, serially, by one
         // thread of warp 14 behind the builder (search.cpp:348, :409)
-        io.chain = first && seg == 0 && s_fitness_pending != 0;
+        // the first step's value_local (search.cpp:348) as an interval from a
+        // parallel sum: it is only compared with (and, if undecided, recomputed
+        // exactly as fitness() of) the local snapshot = the initial table.  After a
+        // restart (:409) value_local belongs to the kicked pivot, not to the
+        // snapshot, so there the exact serial chain runs (one thread behind the builder).
+        const bool initial = ctl->st.nse == 1;
+        io.fsum = first && seg == 0 && s_fitness_pending != 0 && initial;
+        io.chain = first && seg == 0 && s_fitness_pending != 0 && !initial;
         double chain = 0.0;
         int acc[kCertTiles][4];
 #pragma unroll
@@ -1274,8 +1281,36 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         if (ovf) atomicOr(&ctl->c_ovf, 1);
         if (first && seg == 0) {
           if (io.chain && t == kCertThreads - 64) ctl->fit = chain;
-          const int32_t Pn = block_max(ctl, pmax);   // (its barrier publishes ctl->fit)
-          if (t == 0) first_pass_state(ctl, a, w, Pn, ctl->fit, alpha);
+          if (io.fsum) {
+            double v = part[3];
+            for (int o = 16; o; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(FULL, v, o));
+            if ((t & 31) == 0) ctl->rs5[3][t >> 5] = v;
+          }
+          const int32_t Pn = block_max(ctl, pmax);   // (its barriers publish ctl->fit, rs5)
+          if (t == 0) {
+            if (io.fsum) {
+              double S = 0.0;
+              for (int x = 0; x < (int)(blockDim.x >> 5); ++x) S = __dadd_rn(S, ctl->rs5[3][x]);
+              if (isfinite(S) && S < 0x1p1020) {
+                // serial fitness in [S_exact (1 -+ g_L)], S_exact in S / (1 +- g_p): the
+                // parallel sum's depth is L/kCC per thread + 5 + 16
+                const double gL = gamma_n((double)L), gp = gamma_n((double)L / kCC + 24.0);
+                const double u = 0x1p-53;
+                first_pass_state(ctl, a, w, Pn, S, alpha);
+                WalkState& St = ctl->st;
+                St.vl_exact = 0;
+                St.vl_lo = S * (1.0 - gL) / (1.0 + gp) * (1.0 - 8.0 * u);
+                St.vl_hi = S * (1.0 + gL) / (1.0 - gp) * (1.0 + 8.0 * u);
+              } else {
+                // near or past DBL_MAX: the exact serial chain decides OverflowError
+                double ch = 0.0;
+                for (uint32_t k = 1; k < L; ++k) ch = __dadd_rn(ch, io.lut[abs(Cpiv[k])]);
+                first_pass_state(ctl, a, w, Pn, ch, alpha);
+              }
+            } else {
+              first_pass_state(ctl, a, w, Pn, ctl->fit, alpha);
+            }
+          }
         }
         // window constants: warp sums, then a fixed-order sum over warps
         {

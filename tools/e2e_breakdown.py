@@ -3,7 +3,7 @@ import os, sys, time
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2107_09801_b200 as P  # noqa: E402
-L, nw, steps = 1048575, 148, int(sys.argv[1]) if len(sys.argv) > 1 else 10
+L, nw, steps = 1048575, int(os.environ.get("NW", 148)), int(sys.argv[1]) if len(sys.argv) > 1 else 10
 ctx = P.Context(0)
 p = P.SearchParams(length=L, seed=1, alpha1=4, alpha2=P.default_alpha2(L), ls_lmt=2000, flip_lmt=10,
                    n_lmt=1024, stop=P.StopCondition(max_nse=1 + steps * 1024))
