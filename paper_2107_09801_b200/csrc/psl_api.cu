@@ -27,6 +27,7 @@ struct psl_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy = nullptr;   // warm-start uploads overlapped with the table builds
   uint32_t launches = 0;
   int scan_mode = PSL_SCAN_AUTO;
   uint64_t stats[5] = {0, 0, 0, 0, 0};
@@ -169,6 +170,7 @@ void psl_ctx_destroy(psl_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->own) cudaStreamDestroy(ctx->own);
+  if (ctx->copy) cudaStreamDestroy(ctx->copy);
   delete ctx;
 }
 
@@ -634,10 +636,22 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
   AL(W->bad, 8);
   if ((e = cudaMemsetAsync(W->bad, 0xff, 4, s)) != cudaSuccess) return fail(e, "bad flag");
   if ((e = cudaMemsetAsync(W->bad + 1, 0, 4, s)) != cudaSuccess) return fail(e, "bad flag");
+  // per-walk warm starts of many long walks: uploaded in batches on a copy
+  // stream, each batch validated / packed and its tables built while the next
+  // batch is in flight
+  const uint32_t nbatch = (inits && L >= 8192 && n_walks >= 32) ? 4u : 1u;
   if (inits || p.init) {
     const size_t bytes = (size_t)n_walks * L;
     AL(W->inits, bytes);
-    if (inits) {
+    if (inits && nbatch > 1) {
+      if (!ctx->copy && (e = cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking)) != cudaSuccess)
+        return fail(e, "copy stream");
+      cudaEvent_t ready;
+      if ((e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming)) != cudaSuccess) return fail(e, "event");
+      cudaEventRecord(ready, s);                    // the allocation is stream-ordered on s
+      cudaStreamWaitEvent(ctx->copy, ready, 0);
+      cudaEventDestroy(ready);
+    } else if (inits) {
       if ((e = cudaMemcpyAsync(W->inits, inits, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess)
         return fail(e, "inits");
     } else {
@@ -647,16 +661,32 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
     }
   }
 #undef AL
-  if (launch_init_walks(a, n_walks, W->seeds, W->inits, W->bad, s) < 0)
-    return fail(cudaGetLastError(), "init_walks_kernel");
   if (launch_power_tables(W->lut, a.lut_n, p.alpha1, p.alpha2, s) < 0)
     return fail(cudaGetLastError(), "power_tables_kernel");
   ctx->launches += 1;
-  // SidelobeTable::build: exact NTT correlation for long sequences (O(L log L)),
-  // bit-parallel popcount kernel (O(L^2/32)) for short ones
-  const int nb = L >= 8192 ? launch_build_tables_ntt(a, n_walks, s) : launch_build_tables(a, n_walks, s);
-  if (nb < 0) return fail(cudaGetLastError(), "build_tables");
-  ctx->launches += 1 + (uint32_t)nb;
+  for (uint32_t bi = 0; bi < nbatch; ++bi) {
+    const uint32_t w0 = (uint32_t)((uint64_t)n_walks * bi / nbatch);
+    const uint32_t cnt = (uint32_t)((uint64_t)n_walks * (bi + 1) / nbatch) - w0;
+    int8_t* dinit = W->inits ? W->inits + (size_t)w0 * L : nullptr;
+    if (nbatch > 1) {
+      cudaEvent_t done;
+      if ((e = cudaMemcpyAsync(dinit, inits + (size_t)w0 * L, (size_t)cnt * L, cudaMemcpyHostToDevice,
+                               ctx->copy)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming)) != cudaSuccess)
+        return fail(e, "inits");
+      cudaEventRecord(done, ctx->copy);
+      cudaStreamWaitEvent(s, done, 0);
+      cudaEventDestroy(done);
+    }
+    const RunArgs ab = walk_offset(a, w0);
+    if (launch_init_walks(ab, cnt, W->seeds + w0, dinit, W->bad, s, w0) < 0)
+      return fail(cudaGetLastError(), "init_walks_kernel");
+    // SidelobeTable::build: exact NTT correlation for long sequences (O(L log L)),
+    // bit-parallel popcount kernel (O(L^2/32)) for short ones
+    const int nb = L >= 8192 ? launch_build_tables_ntt(ab, cnt, s) : launch_build_tables(ab, cnt, s);
+    if (nb < 0) return fail(cudaGetLastError(), "build_tables");
+    ctx->launches += 1 + (uint32_t)nb;
+  }
   if (W->inits) {
     uint32_t bad[2];
     if ((e = cudaMemcpyAsync(bad, W->bad, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||

@@ -107,7 +107,9 @@ size_t run_smem_bytes(bool cert);
 
 // Launchers (return the number of kernels launched, or -1 on launch error).
 int launch_init_walks(const RunArgs& a, uint32_t n_walks, const uint64_t* d_seeds,
-                      const int8_t* d_inits, uint32_t* d_bad, cudaStream_t s);
+                      const int8_t* d_inits, uint32_t* d_bad, cudaStream_t s, uint32_t walk0 = 0);
+// RunArgs whose per-walk arrays start at walk w0 (batched setup)
+RunArgs walk_offset(const RunArgs& a, uint32_t w0);
 int launch_verify(const int32_t* C, uint32_t L, int32_t* psl, unsigned long long* energy,
                   unsigned long long* hist, cudaStream_t s);
 int launch_unpack(const uint32_t* bits, size_t w_stride, uint32_t L, uint32_t n_walks, int8_t* out,

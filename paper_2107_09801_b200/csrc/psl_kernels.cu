@@ -654,7 +654,8 @@ __device__ long long energy_sweep(Ctl* ctl, const int32_t* C, uint32_t L, const 
 // Walk setup: RNG, pivot (random_sequence, search.cpp:120-129, or warm start),
 // snapshot copies.  One CTA per walk.
 __global__ void __launch_bounds__(256) init_walks_kernel(RunArgs a, const uint64_t* seeds,
-                                                         const int8_t* inits, uint32_t* bad) {
+                                                         const int8_t* inits, uint32_t* bad,
+                                                         uint32_t walk0) {
   const uint32_t w = blockIdx.x;
   WalkState* S = a.st + w;
   uint32_t* bp = a.bits_piv + (size_t)w * a.w_stride + a.w_front;
@@ -685,7 +686,7 @@ __global__ void __launch_bounds__(256) init_walks_kernel(RunArgs a, const uint64
     // warm starts: validate (BinarySequence ctor, sequence.cpp:20-35) and pack;
     // bad[0] = first offending flat index + 1, bad[1] = its value
     const int8_t* src = inits + (size_t)w * a.L;
-    const size_t base = (size_t)w * a.L;
+    const size_t base = (size_t)(walk0 + w) * a.L;   // flat index over all walks (first offender)
     for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) {
       uint32_t word = 0;
       const uint32_t nb = min(32u, a.L - i * 32);
@@ -1821,9 +1822,23 @@ size_t run_smem_bytes(bool cert) {
   return main_bytes + kHfBytes + kCtlBytes + (cert ? (size_t)kLutS * sizeof(double) : 0);
 }
 
+RunArgs walk_offset(const RunArgs& a, uint32_t w0) {
+  RunArgs b = a;
+  b.st += w0;
+  b.Cpiv += (size_t)w0 * a.c_stride;
+  b.Cloc += (size_t)w0 * a.c_stride;
+  b.bits_piv += (size_t)w0 * a.w_stride;
+  b.bits_loc += (size_t)w0 * a.w_stride;
+  b.bits_best += (size_t)w0 * a.w_stride;
+  b.used += (size_t)w0 * a.w_stride;
+  b.hlist += (size_t)w0 * a.h_stride;
+  b.flips += (size_t)w0 * a.f_stride;
+  return b;
+}
+
 int launch_init_walks(const RunArgs& a, uint32_t n_walks, const uint64_t* d_seeds,
-                      const int8_t* d_inits, uint32_t* d_bad, cudaStream_t s) {
-  init_walks_kernel<<<n_walks, 256, 0, s>>>(a, d_seeds, d_inits, d_bad);
+                      const int8_t* d_inits, uint32_t* d_bad, cudaStream_t s, uint32_t walk0) {
+  init_walks_kernel<<<n_walks, 256, 0, s>>>(a, d_seeds, d_inits, d_bad, walk0);
   return cudaGetLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -361,6 +361,25 @@ def test_walks_warm_starts_unaligned(engine):
             engine.run_walks(p, nw, inits=bad)
 
 
+def test_walks_warm_starts_batched_upload(engine):
+    """Many long warm-started walks: uploaded in four batches on a copy stream,
+    each batch packed and its NTT tables built while the next one is in flight."""
+    L, nw = 9001, 40
+    rng = np.random.default_rng(12)
+    inits = np.where(rng.integers(0, 2, (nw, L)) == 1, -1, 1).astype(np.int8)
+    p = _params(engine, L, 30, 4, 13, 3, 10, 256, 1 + 4 * 256)
+    recs = engine.run_walks(p, nw, inits=inits)
+    for w in (0, 9, 10, 19, 20, 30, 39):          # first / last walk of each batch
+        rc, orec, osol, _, _ = O.run_search(L, 30 + w, 4, 13, 3, 10, 256, 1 + 4 * 256, init=inits[w])
+        assert (recs[w].nse, recs[w].psl_best) == (orec.nse, orec.psl_best)
+        assert np.array_equal(recs[w].solution_best, osol)
+    bad = inits.copy()
+    bad[37, 4000] = 3
+    bad[38, 5] = 0                                 # a later walk: not the first offender
+    with pytest.raises(engine.ConfigError, match="position 4000 is 3;"):
+        engine.run_walks(p, nw, inits=bad)
+
+
 def test_drain_and_resume(engine, golden, monkeypatch):
     """Tiny device event/trace buffers: run_search drains and relaunches many
     times; hooks must still see the reference's exact event/trace stream."""
