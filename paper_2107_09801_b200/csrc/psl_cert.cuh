@@ -470,6 +470,34 @@ __device__ __forceinline__ void cert_issue_warp(const CertSmem& cs, uint32_t tme
           smem_u32(mbar)) : "memory");
 }
 
+// One direction's MMAs of iteration c (dir 0: forward kappa-chunk c, 1:
+// reversed kappa'-chunk c - kLag), issued by a whole warp, then committed.  The
+// commit also arrives when the warp issued nothing (two issuing warps, one
+// barrier arrival each per iteration).
+__device__ __forceinline__ void cert_issue_dir(const CertSmem& cs, uint32_t tmem, int32_t c, int dir,
+                                               bool active, uint32_t started, uint64_t* mbar) {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (active) {
+    const uint32_t abuf = smem_u32(cs.acore) + (uint32_t)(c & 1) * (uint32_t)kABuf +
+                          (dir ? (uint32_t)(kACores * 128) : 0u);
+    const uint32_t ring = smem_u32(cs.dring);
+    const long long q0 = dir ? (long long)(kCC / 16) * (c - (int32_t)kLag) : (long long)(kCC / 16) * c - 56;
+    uint64_t da = umma_desc(abuf, 256, 128);
+    uint64_t db = umma_desc(ring + (uint32_t)((((q0 % kRing) + kRing) % kRing) * 128), 128, 1024);
+    const uint32_t bit = dir ? 2u : 1u;
+#pragma unroll
+    for (int s = 0; s < kCCols; ++s) {
+      umma_i8_elect(tmem + (dir ? 64u : 0u), da, db, (s > 0 || (started & bit)) ? 1u : 0u);
+      da += 512 >> 4;
+      db += 256 >> 4;
+    }
+  }
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+          smem_u32(mbar)) : "memory");
+}
+
 // ---- the cross term on mma.sync (zone-1 chunks)
 __device__ __forceinline__ void imma_s8(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                         uint32_t a3, uint32_t b0, uint32_t b1) {

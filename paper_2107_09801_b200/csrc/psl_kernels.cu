@@ -969,7 +969,10 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
     }
     if (t == 0) {
       for (int i = 0; i < 2; ++i) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&ctl->mbar[i])) : "memory");
+        // two committing warps per iteration (forward: warp 15, reversed: warp 14);
+        // the decoupled variant commits once
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&ctl->mbar[i])),
+                     "r"(kCC < kCertThreads ? 1 : 2) : "memory");
         asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&ctl->mbar_f[i])),
                      "r"(kCC / 32) : "memory");
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&ctl->mbar_e[i])) : "memory");
@@ -1224,8 +1227,18 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
                 asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&ctl->mbar_e[b])) : "memory");
             }
           }
-        } else
+        } else {
+        // warp 15 issues the forward MMAs of chunk c right after its barrier,
+        // warp 14 the reversed ones at the top of the next iteration (after the
+        // forward ones drained): the tensor-pipe wait is split over two warps
+        int32_t pend_c = -1;
+        bool pend_rv = false;
+        uint32_t pend_started = 0;
         for (uint32_t c = 0; c < nch + kLag; ++c) {
+          if (pend_c >= 0) {
+            if ((t >> 5) == 14) cert_issue_dir(cs, tmem, pend_c, 1, pend_rv, pend_started, &ctl->mbar[pend_c & 1]);
+            pend_c = -1;
+          }
           if (issued & (1u << (c & 1))) {      // MMAs of iteration c - 2 read this buffer
             PT_MARK(0);
             mbar_wait(&ctl->mbar[c & 1], mb_par[c & 1]);
@@ -1258,7 +1271,8 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           if ((fw || rv)) {
 #endif
             // warp 15 (stages no cores) issues, one lane elected per MMA
-            if ((t >> 5) == 15) cert_issue_warp(cs, tmem, (int32_t)c, fw, rv, started, &ctl->mbar[c & 1]);
+            if ((t >> 5) == 15) cert_issue_dir(cs, tmem, (int32_t)c, 0, fw, started, &ctl->mbar[c & 1]);
+            pend_c = (int32_t)c; pend_rv = rv; pend_started = started;
             started |= (fw ? 1u : 0u) | (rv ? 2u : 0u);   // uniform copy of the issuer's flags
             numma += (fw ? kCCols : 0) + (rv ? kCCols : 0);
             issued |= 1u << (c & 1);
@@ -1271,6 +1285,8 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
             if (t >= (uint32_t)kThreads && cert_band_chunk(io, c)) cert_band_cells(io, cs, c, sm.sb, Bs, t - kThreads);
             PT_MARK(6);
           }
+        }
+        if (pend_c >= 0 && (t >> 5) == 14) cert_issue_dir(cs, tmem, pend_c, 1, pend_rv, pend_started, &ctl->mbar[pend_c & 1]);
         }
         PT_MARK(0);
         for (uint32_t bb = 0; bb < 2; ++bb)
