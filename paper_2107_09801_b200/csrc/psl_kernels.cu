@@ -907,6 +907,13 @@ __device__ __forceinline__ int compare_local(const WalkState& S, double lo, doub
 // kCert: 512 threads, one walk per SM (the certified scan's digit ring and
 // chunk buffers need the shared memory); the exact kernel: 256 threads, two per
 // SM.  The exact sweep in the 512-thread kernel leaves threads >= 256 inactive.
+#ifndef PSL_FWD_WARP
+#define PSL_FWD_WARP 15
+#endif
+#ifndef PSL_REV_WARP
+#define PSL_REV_WARP 14
+#endif
+
 // Timing-only instrumentation (-DPSL_PHASE_TIMING, tools/ablate.sh): per-warp
 // cycles per phase of the certified chunk loop, printed by CTA 0 at exit.
 #ifdef PSL_PHASE_TIMING
@@ -1236,7 +1243,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         uint32_t pend_started = 0;
         for (uint32_t c = 0; c < nch + kLag; ++c) {
           if (pend_c >= 0) {
-            if ((t >> 5) == 14) cert_issue_dir(cs, tmem, pend_c, 1, pend_rv, pend_started, &ctl->mbar[pend_c & 1]);
+            if ((t >> 5) == PSL_REV_WARP) cert_issue_dir(cs, tmem, pend_c, 1, pend_rv, pend_started, &ctl->mbar[pend_c & 1]);
             pend_c = -1;
           }
           if (issued & (1u << (c & 1))) {      // MMAs of iteration c - 2 read this buffer
@@ -1271,7 +1278,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           if ((fw || rv)) {
 #endif
             // warp 15 (stages no cores) issues, one lane elected per MMA
-            if ((t >> 5) == 15) cert_issue_dir(cs, tmem, (int32_t)c, 0, fw, started, &ctl->mbar[c & 1]);
+            if ((t >> 5) == PSL_FWD_WARP) cert_issue_dir(cs, tmem, (int32_t)c, 0, fw, started, &ctl->mbar[c & 1]);
             pend_c = (int32_t)c; pend_rv = rv; pend_started = started;
             started |= (fw ? 1u : 0u) | (rv ? 2u : 0u);   // uniform copy of the issuer's flags
             numma += (fw ? kCCols : 0) + (rv ? kCCols : 0);
@@ -1286,7 +1293,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
             PT_MARK(6);
           }
         }
-        if (pend_c >= 0 && (t >> 5) == 14) cert_issue_dir(cs, tmem, pend_c, 1, pend_rv, pend_started, &ctl->mbar[pend_c & 1]);
+        if (pend_c >= 0 && (t >> 5) == PSL_REV_WARP) cert_issue_dir(cs, tmem, pend_c, 1, pend_rv, pend_started, &ctl->mbar[pend_c & 1]);
         }
         PT_MARK(0);
         for (uint32_t bb = 0; bb < 2; ++bb)
