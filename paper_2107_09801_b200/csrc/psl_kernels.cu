@@ -922,7 +922,7 @@ __device__ __forceinline__ int compare_local(const WalkState& S, double lo, doub
 #include <cstdio>
 namespace pslb {
 namespace {
-constexpr int kPT = 9;   // loop top, build, cores, barrier, issue, cross, band, outside the loop, mbar wait
+constexpr int kPT = 10;  // loop top, build, cores, barrier, issue, cross, band, outside the loop, mbar wait, fence
 #define PT_MARK(i)                                                   \
   do {                                                               \
     const long long _n = clock64();                                  \
@@ -1270,6 +1270,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           cert_cores(io, cs, (int32_t)c, sm.sb, fw, rv);
           PT_MARK(2);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          PT_MARK(9);
           __syncthreads();
           PT_MARK(3);
 #ifdef PSL_ABLATE_ISSUE
@@ -1719,8 +1720,8 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
   if (kCert && t == 0) printf("PTCTA %u %lld\n", w, clock64() - pt_t0);
   if (kCert && w == 0 && t < 16) {
     const long long* q = pt_acc[t];
-    printf("PT warp %2u top %lld build %lld cores %lld bar %lld issue %lld cross %lld band %lld other %lld mbarwait %lld\n", t,
-           q[0], q[1], q[2], q[3], q[4], q[5], q[6], q[7], q[8]);
+    printf("PT warp %2u top %lld build %lld cores %lld bar %lld issue %lld cross %lld band %lld other %lld mbarwait %lld fence %lld\n", t,
+           q[0], q[1], q[2], q[3], q[4], q[5], q[6], q[7], q[8], q[9]);
   }
 #endif
   if (t == 0) {
