@@ -54,6 +54,7 @@ struct psl_walks {
   double* lut = nullptr;        // [2][lut_n] power tables
   double* b2 = nullptr;         // certified-scan band-2 scratch
   double* lo_buf = nullptr;     // certified-scan per-row lower bounds (n_lmt > 1024)
+  double* iv_buf = nullptr;     // certified-scan row intervals of a group
   uint64_t stats_read[5] = {0, 0, 0, 0, 0};   // scan statistics already added to ctx->stats
 };
 
@@ -551,7 +552,7 @@ void psl_walks_destroy(psl_walks* w) {
   for (void* p : {(void*)w->st, (void*)w->Cpiv, (void*)w->Cloc, (void*)w->bits, (void*)w->hlist,
                   (void*)w->flips, (void*)w->events, (void*)w->traces, (void*)w->seeds,
                   (void*)w->inits, (void*)w->bad, (void*)w->sol, (void*)w->lut, (void*)w->b2,
-                  (void*)w->lo_buf})
+                  (void*)w->lo_buf, (void*)w->iv_buf})
     if (p) cudaFreeAsync(p, s);
   delete w;
 }
@@ -622,6 +623,8 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
   a.b2 = W->b2;
   AL(W->lo_buf, (size_t)p.n_lmt * sizeof(double) * n_walks);
   a.lo_buf = W->lo_buf;
+  AL(W->iv_buf, 3ull * kGroup * sizeof(double) * n_walks);
+  a.iv_buf = W->iv_buf;
   a.st = W->st; a.Cpiv = W->Cpiv; a.Cloc = W->Cloc;
   a.bits_piv = W->bits;
   a.bits_loc = W->bits + a.w_stride * n_walks;

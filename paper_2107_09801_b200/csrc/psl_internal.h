@@ -86,6 +86,7 @@ struct RunArgs {
   psl_trace* traces;
   double* b2;           // certified scan scratch: [walk][2][1024] band-2 constants
   double* lo_buf;       // certified scan scratch: [walk][n] per-row lower bounds (n > 1024)
+  double* iv_buf;       // certified scan scratch: [walk][3][1024] a row group's mid / lo / hi
   const double* lut1;   // PowerTable(L, alpha1) / (L, alpha2) on the device (sequence.hpp:72-84)
   const double* lut2;
   uint32_t lut_n;       // entries per table (> max |C_k| + 4)

@@ -1052,9 +1052,11 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
       // L - 1 is scored in two passes, one per contiguous row segment.
       const CertSmem cs = cert_carve(smem_raw);
       const CertLane ln = cert_lane(cs);
-      double mid[kJ], lo[kJ], hi[kJ];
-#pragma unroll
-      for (int m = 0; m < kJ; ++m) { mid[m] = 0.0; lo[m] = 0.0; hi[m] = 0.0; }
+      // row intervals [lo, hi] and midpoints of the current group, through global
+      // scratch (not registers across the chunk loop)
+      double* ivm = a.iv_buf + (size_t)w * 3 * kGroup;
+      double* ivl = ivm + kGroup;
+      double* ivh = ivl + kGroup;
       // the phase's PowerTable head (indices <= Psrc + 4F + 4 cover every lookup
       // of the pass) in shared memory when it fits
       const double* lut_c = lut;
@@ -1075,8 +1077,6 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
       const bool first = g == 0;
       const uint32_t gn = min((uint32_t)kGroup, a.n - g * kGroup);
       const uint32_t gs = (uint32_t)(((uint64_t)start + (uint64_t)g * kGroup) % L);   // rows j = gs + 1 + rho
-#pragma unroll
-      for (int m = 0; m < kJ; ++m) { mid[m] = 0.0; lo[m] = 0.0; hi[m] = 0.0; }
       const uint32_t nA = min(gn, L - 1 - gs);               // rows before the wrap
       const int nseg = (nA > 0 && nA < gn) ? 2 : 1;
       for (int seg = 0; seg < nseg; ++seg) {
@@ -1400,10 +1400,10 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
             const double Abs = Sc + B4 + fabs(lin) + fabs(xv);
             const double Err = E0 + 2.0 * gB * B4 + 2.0 * g8 * Abs + u * (fabs(lin) + fabs(xv)) +
                                a.cert_slack * Abs;
-            mid[m] = 0.25 * T4;
-            lo[m] = fmax(0.0, 0.25 * (T4 - Err)) * (1.0 - gL) * (1.0 - 8.0 * u);
-            hi[m] = 0.25 * (T4 + Err) * (1.0 + gL) * (1.0 + 8.0 * u);
-            if (!isfinite(hi[m])) mid[m] = __longlong_as_double(0x7ff8000000000000ll);   // -> bad
+            const double hv = 0.25 * (T4 + Err) * (1.0 + gL) * (1.0 + 8.0 * u);
+            ivm[rho] = isfinite(hv) ? 0.25 * T4 : __longlong_as_double(0x7ff8000000000000ll);   // -> bad
+            ivl[rho] = fmax(0.0, 0.25 * (T4 - Err)) * (1.0 - gL) * (1.0 - 8.0 * u);
+            ivh[rho] = hv;
           }
         }
         __syncthreads();
@@ -1424,6 +1424,14 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           uint32_t j = gs + 1 + rho;
           if (j >= L) j -= L;
           jj[m] = j;
+        }
+        double mid[kJ], lo[kJ], hi[kJ];
+#pragma unroll
+        for (int m = 0; m < kJ; ++m) {
+          const uint32_t rho = kJ * owner + m;
+          mid[m] = active[m] ? ivm[rho] : 0.0;
+          lo[m] = active[m] ? ivl[rho] : 0.0;
+          hi[m] = active[m] ? ivh[rho] : 0.0;
         }
         reduce_group(ctl, sm, hlist, active, jj, mid, ibase, L);
         const uint32_t bi = ctl->best_i;
