@@ -28,7 +28,7 @@ def main():
     ap.add_argument("--seed", type=int, default=1)
     args = ap.parse_args()
     import torch
-    walks = args.walks or 2 * torch.cuda.get_device_properties(0).multi_processor_count
+    walks = args.walks or torch.cuda.get_device_properties(0).multi_processor_count   # one wave
     ctx = P.Context(0)
     L = (1 << args.m) - 1
     best_seq, best_psl = None, None
