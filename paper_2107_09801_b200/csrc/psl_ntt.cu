@@ -11,15 +11,17 @@
 // Only x is transformed: Y(k) = sum_m x_m w^{(L-1-m)k} = w^{(L-1)k} X(-k), so
 // the spectrum of the correlation is X(k) X(N-k) w^{(L-1)k}.
 //
-// Layout: each walk's N values as R rows x C columns (i = m C + col, R C = N).
-// Forward DIF (natural -> bit-reversed):  stages with span h >= C pair
-// elements of one column (column pass: a CTA holds 8 adjacent columns in
-// shared memory, generated straight from the packed bits), stages h < C pair
-// elements of one row (row pass: a CTA holds a row).  Pointwise product on the
-// bit-reversed spectrum.  Inverse DIT (bit-reversed -> natural): row pass,
-// then the column pass, which also scales by N^-1, writes C_k (pivot and local
-// tables) and reduces the walk's PSL and energy.  Four passes over HBM instead
-// of one per radix-2 stage.
+// Layout: each walk's N values as R rows x C columns (i = m C + col, R C = N),
+// transformed by the four-step scheme: R-point DIF down every column (column
+// pass: a CTA holds 8 adjacent columns in shared memory, generated straight
+// from the packed bits), the twiddle w_N^{k1 col} on the way out, then C-point
+// DIF along every row (row pass: a CTA holds a row).  The result sits at the
+// full bit-reversed position of k = k1 + R k2, as a radix-2 DIF over N would
+// leave it.  Pointwise product on the bit-reversed spectrum.  Inverse
+// (bit-reversed -> natural): C-point DIT rows, the inverse twiddle, R-point DIT
+// columns, which also scale by N^-1, write C_k (pivot and local tables) and
+// reduce the walk's PSL and energy.  Four passes over HBM; inside a pass the
+// stages run three at a time in registers (radix-8 rounds).
 #include <algorithm>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -35,6 +37,7 @@ constexpr uint32_t kOne = 301989884u;    // 2^32 mod p (Montgomery 1)
 constexpr int kCols = 8;                 // columns per column-pass CTA (one 32 B sector per row)
 constexpr int kMaxRows = 1024;           // R <= 1024, C <= 2048 (N <= 2^21)
 constexpr int kMaxRowLen = 2048;
+constexpr uint32_t kRowsPerCta = 4;     // rows per row-pass CTA (amortises the twiddle copy)
 
 // Montgomery product: returns a*b*2^-32 mod p for a, b < p.
 __device__ __forceinline__ uint32_t mmul(uint32_t a, uint32_t b) {
@@ -57,94 +60,159 @@ __device__ __forceinline__ uint32_t wpow(const uint32_t* tw, uint32_t e, uint32_
   return e < h ? tw[e] : (kP - tw[e - h]) % kP;
 }
 
-// Twiddle factors of the column stages for the CTA's 8 columns: stage st
-// (hr = R/2 >> st, span h = hr C) needs w^{(jr C + col) N / 2h}
-// = w^{jr N / 2hr} * w^{col N / 2h}: rf[hr + jr] and cf[st][c] (Montgomery;
-// the product costs one extra mmul per butterfly instead of a scattered load).
-__device__ __forceinline__ void col_twiddles(const uint32_t* tw, uint32_t R, uint32_t C, uint32_t col0,
-                                             uint32_t* rf, uint32_t* cf) {
-  const uint32_t N = R * C;
-  for (uint32_t hr = 1; hr < R; hr <<= 1)
-    for (uint32_t jr = threadIdx.x; jr < hr; jr += blockDim.x) rf[hr + jr] = tw[jr * (N / (2 * hr))];
-  uint32_t st = 0;
-  for (uint32_t hr = R >> 1; hr >= 1; hr >>= 1, ++st)
-    if (threadIdx.x < (uint32_t)kCols) {
-      const uint32_t col = col0 + threadIdx.x;
-      // col N / 2h = col R / 2hr * (N / (R C)) ... as an index into tw: col * (N / (2 hr C))
-      const uint32_t e = col * (N / (2 * hr * C));
-      cf[st * kCols + threadIdx.x] = (N / (2 * hr * C)) ? tw[e] : 0u;
+// ---- radix-8 register rounds -------------------------------------------------
+// An n-point transform (n = 2^logn) of each of `cols` interleaved columns is
+// held in shared memory, element (i, c) at phys(i, c).  A round performs RB
+// consecutive radix-2 stages in registers: every work item loads the 2^RB
+// elements base + k u (k < 2^RB), runs the stages of spans u 2^q, stores them
+// back: one shared-memory round trip and one barrier per three stages instead
+// of per stage.  Stage twiddles: tws[h + j] = w_n^{j n / 2h} (j < h).
+//
+// Layouts (bank-conflict free for every round, checked by simulation):
+//   cols == 1 (row pass):  phys = i ^ (((i >> 5) & 7) << 2); the u == 1 round
+//                          moves its 8 contiguous elements as two 16-byte words
+//   cols == 8 (column pass): row i sits at row (i & ~3) | ((i + (i >> 3)) & 3)
+template <int kColsLog>
+__device__ __forceinline__ uint32_t phys(uint32_t i, uint32_t c) {
+  if (kColsLog == 0) return i ^ (((i >> 5) & 7u) << 2);
+  return ((((i & ~3u) | ((i + (i >> 3)) & 3u))) << kColsLog) + c;
+}
+
+template <int RB, bool kFwd, int kColsLog>
+__device__ __forceinline__ void ntt_round(uint32_t* __restrict__ s, uint32_t logn, uint32_t ulog,
+                                          const uint32_t* __restrict__ tws) {
+  constexpr int E = 1 << RB;
+  constexpr uint32_t cols = 1u << kColsLog;
+  const uint32_t u = 1u << ulog;
+  const uint32_t items = (1u << (logn - RB)) << kColsLog;
+  for (uint32_t it = threadIdx.x; it < items; it += blockDim.x) {
+    const uint32_t c = it & (cols - 1), g = it >> kColsLog;
+    const uint32_t off = g & (u - 1), base = ((g >> ulog) << (ulog + RB)) + off;
+    uint32_t v[E];
+    const bool vec = kColsLog == 0 && RB == 3 && ulog == 0;
+    if (vec) {
+      const uint4 a = *reinterpret_cast<const uint4*>(s + phys<kColsLog>(base, 0));
+      const uint4 b = *reinterpret_cast<const uint4*>(s + phys<kColsLog>(base + 4, 0));
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+      v[4 % E] = b.x; v[5 % E] = b.y; v[6 % E] = b.z; v[7 % E] = b.w;
+    } else {
+#pragma unroll
+      for (int k = 0; k < E; ++k) v[k] = s[phys<kColsLog>(base + k * u, c)];
     }
+#pragma unroll
+    for (int qq = 0; qq < RB; ++qq) {
+      const int q = kFwd ? RB - 1 - qq : qq;                   // DIF: wide spans first
+      const uint32_t h = u << q;
+      uint32_t w[1 << (RB - 1)];
+#pragma unroll
+      for (int k = 0; k < (1 << q); ++k) w[k] = tws[h + off + k * u];
+#pragma unroll
+      for (int k = 0; k < E; ++k) {
+        if (k & (1 << q)) continue;
+        const uint32_t a = v[k], b = v[k + (1 << q)], ww = w[k & ((1 << q) - 1)];
+        if (kFwd) {
+          v[k] = madd(a, b);
+          v[k + (1 << q)] = mmul(msub(a, b), ww);
+        } else {
+          const uint32_t bw = mmul(b, ww);
+          v[k] = madd(a, bw);
+          v[k + (1 << q)] = msub(a, bw);
+        }
+      }
+    }
+    if (vec) {
+      *reinterpret_cast<uint4*>(s + phys<kColsLog>(base, 0)) = make_uint4(v[0], v[1], v[2], v[3]);
+      *reinterpret_cast<uint4*>(s + phys<kColsLog>(base + 4, 0)) =
+          make_uint4(v[4 % E], v[5 % E], v[6 % E], v[7 % E]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < E; ++k) s[phys<kColsLog>(base + k * u, c)] = v[k];
+    }
+  }
   __syncthreads();
 }
 
-// Forward column pass: stages h = N/2 .. C (rows span R/2 .. 1), DIF.  The
-// inputs are generated from the packed bits (x_i = +-1 for i < L, 0 past L).
+// All logn stages: rounds of three from the narrow end, the remainder (1 or 2
+// stages) at the wide end.  Forward DIF runs wide -> narrow, inverse DIT the reverse.
+template <bool kFwd, int kColsLog>
+__device__ __forceinline__ void ntt_smem(uint32_t* s, uint32_t logn, const uint32_t* tws) {
+  const uint32_t top = logn % 3, nfull = logn / 3;
+  if (kFwd && top == 1) ntt_round<1, true, kColsLog>(s, logn, logn - 1, tws);
+  if (kFwd && top == 2) ntt_round<2, true, kColsLog>(s, logn, logn - 2, tws);
+  for (uint32_t r = 0; r < nfull; ++r) {
+    const uint32_t ulog = kFwd ? 3 * (nfull - 1 - r) : 3 * r;
+    ntt_round<3, kFwd, kColsLog>(s, logn, ulog, tws);
+  }
+  if (!kFwd && top == 1) ntt_round<1, false, kColsLog>(s, logn, logn - 1, tws);
+  if (!kFwd && top == 2) ntt_round<2, false, kColsLog>(s, logn, logn - 2, tws);
+}
+
+// Stage twiddles of an n-point transform, tws[h + j] = w_N^{j N / 2h}
+// (j < h < n), precomputed once per build by ntt_stage_table_kernel (the
+// strided gather tw[j N / 2h] would cost a sector per entry in every CTA);
+// each CTA copies its table with coalesced loads.
+__device__ __forceinline__ void stage_twiddles(const uint32_t* tab, uint32_t n, uint32_t* tws) {
+  for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) tws[j] = tab[j];
+}
+
+// Four-step twiddle w_N^{k1 col} with k1 < R, col < C: k1 col = q C + r,
+// w_N^{qC} = w_R^q from the R-point stage table (w_R^{R/2} = -1), w_N^r from tlo.
+__device__ __forceinline__ uint32_t four_step_tw(uint32_t k1, uint32_t col, uint32_t logC, uint32_t R,
+                                                 const uint32_t* tws, const uint32_t* tlo) {
+  const uint32_t e = k1 * col, q = e >> logC, r = e & ((1u << logC) - 1);
+  const uint32_t hi = q < R / 2 ? tws[R / 2 + q] : kP - tws[q];
+  return mmul(hi, tlo[r]);
+}
+
+// Forward column pass (four-step): R-point DIF of 8 adjacent columns in
+// shared memory, inputs generated from the packed bits (x_i = +-1 for i < L,
+// 0 past L), then the twiddle w_N^{k1 col} for the column spectrum entry
+// k1 = brev_R(row) on the way out.
 __global__ void __launch_bounds__(256) ntt_col_fwd_kernel(const uint32_t* bits, size_t w_stride,
                                                           uint32_t L, uint32_t R, uint32_t C,
-                                                          const uint32_t* tw, uint32_t* x) {
-  __shared__ uint32_t s[kMaxRows * kCols];
-  __shared__ uint32_t rf[kMaxRows];                          // rf[hr + jr] = w^{jr N / 2hr}
-  __shared__ uint32_t cf[11 * kCols];                        // cf[stage][c] = w^{col N / (2 hr C)}
+                                                          const uint32_t* tw, const uint32_t* tabR,
+                                                          uint32_t* x) {
+  __shared__ __align__(16) uint32_t s[kMaxRows * kCols];
+  __shared__ uint32_t tws[kMaxRows];
+  __shared__ uint32_t tlo[kMaxRowLen];
   const uint32_t walk = blockIdx.y, col0 = blockIdx.x * kCols;
-  const uint32_t N = R * C;
+  const uint32_t N = R * C, logR = 31 - __clz(R), logC = 31 - __clz(C);
   const uint32_t* S = bits + (size_t)walk * w_stride;
-  col_twiddles(tw, R, C, col0, rf, cf);
+  stage_twiddles(tabR, R, tws);
+  for (uint32_t j = threadIdx.x; j < C; j += blockDim.x) tlo[j] = tw[j];
   for (uint32_t e = threadIdx.x; e < R * kCols; e += blockDim.x) {
     const uint32_t m = e / kCols, c = e % kCols, i = m * C + col0 + c;
     uint32_t v = 0;
     if (i < L) v = ((S[i >> 5] >> (i & 31)) & 1u) ? kP - kOne : kOne;
-    s[e] = v;
+    s[phys<3>(m, c)] = v;
   }
   __syncthreads();
-  for (uint32_t hr = R >> 1, st = 0; hr >= 1; hr >>= 1, ++st) {
-    for (uint32_t b = threadIdx.x; b < (R / 2) * kCols; b += blockDim.x) {
-      const uint32_t c = b % kCols, q = b / kCols;          // q-th butterfly row pair
-      const uint32_t jr = q & (hr - 1), m1 = ((q - jr) << 1) + jr, m2 = m1 + hr;
-      // position j = jr C + col within the 2h block: w^{j N / 2h} = rf * cf
-      const uint32_t w = mmul(rf[hr + jr], cf[st * kCols + c]);
-      const uint32_t u = s[m1 * kCols + c], v = s[m2 * kCols + c];
-      s[m1 * kCols + c] = madd(u, v);
-      s[m2 * kCols + c] = mmul(msub(u, v), w);
-    }
-    __syncthreads();
-  }
+  ntt_smem<true, 3>(s, logR, tws);
   uint32_t* X = x + (size_t)walk * N;
   for (uint32_t e = threadIdx.x; e < R * kCols; e += blockDim.x) {
     const uint32_t m = e / kCols, c = e % kCols;
-    X[m * C + col0 + c] = s[e];
+    const uint32_t k1 = __brev(m) >> (32 - logR);
+    X[m * C + col0 + c] = mmul(s[phys<3>(m, c)], four_step_tw(k1, col0 + c, logC, R, tws, tlo));
   }
 }
 
-// Row pass over the rows of every walk: forward DIF stages h = C/2 .. 1 or
-// inverse DIT stages h = 1 .. C/2.  Twiddles of the row stages (the same for
-// every row) staged in shared memory: stage h uses tw[j N / 2h], j < h.
+// Row pass over the rows of every walk: C-point forward DIF or inverse DIT
+// (the four-step's row transforms need no cross-row twiddles).
 template <bool kForward>
 __global__ void __launch_bounds__(256) ntt_row_kernel(uint32_t* x, uint32_t R, uint32_t C,
-                                                      const uint32_t* tw) {
-  __shared__ uint32_t s[kMaxRowLen];
-  __shared__ uint32_t ts[kMaxRowLen];                         // ts[h + j] = stage-h twiddle j
-  const uint32_t N = R * C;
-  for (uint32_t h = 1; h < C; h <<= 1)
-    for (uint32_t j = threadIdx.x; j < h; j += blockDim.x) ts[h + j] = tw[j * (N / (2 * h))];
-  uint32_t* X = x + (size_t)blockIdx.y * N + (size_t)blockIdx.x * C;
-  for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) s[i] = X[i];
-  __syncthreads();
-  for (uint32_t it = 0, h = kForward ? C >> 1 : 1; h >= 1 && h < C; ++it, h = kForward ? h >> 1 : h << 1) {
-    for (uint32_t b = threadIdx.x; b < C / 2; b += blockDim.x) {
-      const uint32_t j = b & (h - 1), i1 = ((b - j) << 1) + j, i2 = i1 + h;
-      const uint32_t w = ts[h + j], u = s[i1], v = s[i2];
-      if (kForward) {
-        s[i1] = madd(u, v);
-        s[i2] = mmul(msub(u, v), w);
-      } else {
-        const uint32_t vw = mmul(v, w);
-        s[i1] = madd(u, vw);
-        s[i2] = msub(u, vw);
-      }
-    }
+                                                      const uint32_t* tabC) {
+  __shared__ __align__(16) uint32_t s[kMaxRowLen];
+  __shared__ uint32_t ts[kMaxRowLen];
+  const uint32_t N = R * C, logC = 31 - __clz(C);
+  stage_twiddles(tabC, C, ts);
+  for (uint32_t row = blockIdx.x * kRowsPerCta; row < (blockIdx.x + 1) * kRowsPerCta && row < R; ++row) {
+    uint32_t* X = x + (size_t)blockIdx.y * N + (size_t)row * C;
+    for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) s[phys<0>(i, 0)] = X[i];
+    __syncthreads();
+    ntt_smem<kForward, 0>(s, logC, ts);
+    for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) X[i] = s[phys<0>(i, 0)];
     __syncthreads();
   }
-  for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) X[i] = s[i];
 }
 
 // Spectrum of the correlation at bit-reversed position p (k = brev(p)):
@@ -166,38 +234,30 @@ __global__ void ntt_pointwise_kernel(uint32_t* x, uint32_t logN, uint32_t L, con
   }
 }
 
-// Inverse column pass: DIT stages h = C .. N/2 (rows span 1 .. R/2), then
-// C_{L-1-i} = z_i N^-1 (signed) into the pivot / local tables, PSL and energy.
+// Inverse column pass: the inverse four-step twiddle w_N^{-k1 col} on the way
+// in, R-point DIT, then C_{L-1-i} = z_i N^-1 (signed) into the pivot / local
+// tables, PSL and energy.
 __global__ void __launch_bounds__(256) ntt_col_inv_kernel(const uint32_t* x, uint32_t R, uint32_t C,
-                                                          const uint32_t* twi, uint32_t ninv_m,
+                                                          const uint32_t* twi, const uint32_t* tabR,
+                                                          uint32_t ninv_m,
                                                           uint32_t L, int32_t* Cp, int32_t* Cl,
                                                           size_t c_stride, WalkState* st) {
-  __shared__ uint32_t s[kMaxRows * kCols];
-  __shared__ uint32_t rf[kMaxRows];
-  __shared__ uint32_t cf[11 * kCols];
+  __shared__ __align__(16) uint32_t s[kMaxRows * kCols];
+  __shared__ uint32_t tws[kMaxRows];
+  __shared__ uint32_t tlo[kMaxRowLen];
   const uint32_t walk = blockIdx.y, col0 = blockIdx.x * kCols;
-  const uint32_t N = R * C;
+  const uint32_t N = R * C, logR = 31 - __clz(R), logC = 31 - __clz(C);
   const uint32_t* X = x + (size_t)walk * N;
-  col_twiddles(twi, R, C, col0, rf, cf);
+  stage_twiddles(tabR, R, tws);
+  for (uint32_t j = threadIdx.x; j < C; j += blockDim.x) tlo[j] = twi[j];
+  __syncthreads();
   for (uint32_t e = threadIdx.x; e < R * kCols; e += blockDim.x) {
     const uint32_t m = e / kCols, c = e % kCols;
-    s[e] = X[m * C + col0 + c];
+    const uint32_t k1 = __brev(m) >> (32 - logR);
+    s[phys<3>(m, c)] = mmul(X[m * C + col0 + c], four_step_tw(k1, col0 + c, logC, R, tws, tlo));
   }
   __syncthreads();
-  uint32_t sg = 0;
-  for (uint32_t hr = R >> 1; hr >= 1; hr >>= 1) ++sg;       // stage index of hr = 1 in col_twiddles order
-  for (uint32_t hr = 1; hr < R; hr <<= 1) {
-    --sg;
-    for (uint32_t b = threadIdx.x; b < (R / 2) * kCols; b += blockDim.x) {
-      const uint32_t c = b % kCols, q = b / kCols;
-      const uint32_t jr = q & (hr - 1), m1 = ((q - jr) << 1) + jr, m2 = m1 + hr;
-      const uint32_t w = mmul(rf[hr + jr], cf[sg * kCols + c]);
-      const uint32_t u = s[m1 * kCols + c], vw = mmul(s[m2 * kCols + c], w);
-      s[m1 * kCols + c] = madd(u, vw);
-      s[m2 * kCols + c] = msub(u, vw);
-    }
-    __syncthreads();
-  }
+  ntt_smem<false, 3>(s, logR, tws);
   int32_t* Cw = Cp + (size_t)walk * c_stride;
   int32_t* Cw2 = Cl ? Cl + (size_t)walk * c_stride : nullptr;
   int32_t pm = 0;
@@ -206,7 +266,7 @@ __global__ void __launch_bounds__(256) ntt_col_inv_kernel(const uint32_t* x, uin
     const uint32_t m = e / kCols, c = e % kCols, i = m * C + col0 + c;
     if (i >= L) continue;
     // z holds N c R (Montgomery); mmul(., N^-1 R) = c R; mmul(., 1) = c
-    const uint32_t v = mmul(mmul(s[e], ninv_m), 1u);
+    const uint32_t v = mmul(mmul(s[phys<3>(m, c)], ninv_m), 1u);
     const int32_t cv = v > kP / 2 ? (int32_t)v - (int32_t)kP : (int32_t)v;
     const uint32_t k = L - 1 - i;
     Cw[k] = cv;
@@ -223,6 +283,15 @@ __global__ void __launch_bounds__(256) ntt_col_inv_kernel(const uint32_t* x, uin
   if (st && (threadIdx.x & 31) == 0) {
     atomicMax(&st[walk].P, pm);
     atomicAdd(reinterpret_cast<unsigned long long*>(&st[walk].energy_best), (unsigned long long)en);
+  }
+}
+
+// tab[h + j] = tw[j N / 2h] for 1 <= h < n, j < h (tab[0] unused)
+__global__ void ntt_stage_table_kernel(const uint32_t* tw, uint32_t N, uint32_t n, uint32_t* tab) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    if (i == 0) { tab[0] = 0; continue; }
+    const uint32_t h = 1u << (31 - __clz(i)), j = i - h;
+    tab[i] = tw[j * (N / (2 * h))];
   }
 }
 
@@ -264,22 +333,27 @@ int launch_build_tables_ntt(const RunArgs& a, uint32_t n_walks, cudaStream_t s) 
   if (R > (uint32_t)kMaxRows || C > (uint32_t)kMaxRowLen || C < (uint32_t)kCols) return -1;
   uint32_t *x = nullptr, *tw = nullptr;
   if (cudaMallocAsync(&x, (size_t)n_walks * N * 4, s) != cudaSuccess) return -1;
-  if (cudaMallocAsync(&tw, (size_t)N * 4, s) != cudaSuccess) return -1;
+  if (cudaMallocAsync(&tw, (size_t)(N + 2 * R + 2 * C) * 4, s) != cudaSuccess) return -1;
   uint32_t* twi = tw + N / 2;
+  uint32_t *tabR = tw + N, *tabRi = tabR + R, *tabC = tabRi + R, *tabCi = tabC + C;
   int launches = 0;
   const uint32_t root = host_pow(3, (kP - 1) / N);          // primitive N-th root
   const uint32_t iroot = host_pow(root, kP - 2);
   ntt_twiddle_kernel<<<(N / 2 + 255) / 256, 256, 0, s>>>(tw, N / 2, to_mont(root));
   ntt_twiddle_kernel<<<(N / 2 + 255) / 256, 256, 0, s>>>(twi, N / 2, to_mont(iroot));
-  const dim3 gcol(C / kCols, n_walks), grow(R, n_walks);
-  ntt_col_fwd_kernel<<<gcol, 256, 0, s>>>(a.bits_piv + a.w_front + 1, a.w_stride, L, R, C, tw, x);
-  ntt_row_kernel<true><<<grow, 256, 0, s>>>(x, R, C, tw);
+  ntt_stage_table_kernel<<<(R + 255) / 256, 256, 0, s>>>(tw, N, R, tabR);
+  ntt_stage_table_kernel<<<(R + 255) / 256, 256, 0, s>>>(twi, N, R, tabRi);
+  ntt_stage_table_kernel<<<(C + 255) / 256, 256, 0, s>>>(tw, N, C, tabC);
+  ntt_stage_table_kernel<<<(C + 255) / 256, 256, 0, s>>>(twi, N, C, tabCi);
+  const dim3 gcol(C / kCols, n_walks), grow((R + kRowsPerCta - 1) / kRowsPerCta, n_walks);
+  ntt_col_fwd_kernel<<<gcol, 256, 0, s>>>(a.bits_piv + a.w_front + 1, a.w_stride, L, R, C, tw, tabR, x);
+  ntt_row_kernel<true><<<grow, 256, 0, s>>>(x, R, C, tabC);
   ntt_pointwise_kernel<<<dim3(std::min<uint32_t>(N / 256, 1024), n_walks), 256, 0, s>>>(x, logN, L, tw);
-  ntt_row_kernel<false><<<grow, 256, 0, s>>>(x, R, C, twi);
+  ntt_row_kernel<false><<<grow, 256, 0, s>>>(x, R, C, tabCi);
   const uint32_t ninv = host_pow(N, kP - 2);
-  ntt_col_inv_kernel<<<gcol, 256, 0, s>>>(x, R, C, twi, to_mont(ninv), L, a.Cpiv, a.Cloc, a.c_stride,
+  ntt_col_inv_kernel<<<gcol, 256, 0, s>>>(x, R, C, twi, tabRi, to_mont(ninv), L, a.Cpiv, a.Cloc, a.c_stride,
                                            a.st);
-  launches += 7;
+  launches += 11;
   cudaFreeAsync(x, s);
   cudaFreeAsync(tw, s);
   return cudaGetLastError() == cudaSuccess ? launches : -1;

@@ -380,6 +380,23 @@ def test_walks_warm_starts_batched_upload(engine):
         engine.run_walks(p, nw, inits=bad)
 
 
+@pytest.mark.parametrize("L", [8192, 8193, 16385, 40000, 131073, 262145])
+def test_ntt_table_build_lengths(engine, L):
+    """Walk tables of every four-step shape (R x C = 128x128 .. 512x1024, the
+    radix-8 rounds with a 1- or 2-stage remainder) against the oracle: the
+    first steps, the PSL and the merit factor (exact energy over all C_k)."""
+    nw = 2
+    rng = np.random.default_rng(L)
+    inits = np.where(rng.integers(0, 2, (nw, L)) == 1, -1, 1).astype(np.int8)
+    p = _params(engine, L, 50, 4, 13, 3, 10, 64, 1 + 2 * 64)
+    recs = engine.run_walks(p, nw, inits=inits)
+    for w in range(nw):
+        rc, orec, osol, _, _ = O.run_search(L, 50 + w, 4, 13, 3, 10, 64, 1 + 2 * 64, init=inits[w])
+        assert (recs[w].nse, recs[w].psl_best) == (orec.nse, orec.psl_best)
+        assert hx(recs[w].merit_factor) == hx(orec.merit_factor)
+        assert np.array_equal(recs[w].solution_best, osol)
+
+
 def test_drain_and_resume(engine, golden, monkeypatch):
     """Tiny device event/trace buffers: run_search drains and relaunches many
     times; hooks must still see the reference's exact event/trace stream."""
