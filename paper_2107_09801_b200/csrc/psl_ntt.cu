@@ -53,6 +53,15 @@ __device__ __forceinline__ uint32_t madd(uint32_t a, uint32_t b) {
 __device__ __forceinline__ uint32_t msub(uint32_t a, uint32_t b) {
   return a >= b ? a - b : a + kP - b;
 }
+// Shoup product for the butterflies (Harvey's lazy reduction): w < p in normal
+// form with wq = floor(w 2^32 / p); for any a < 2^32 returns a w mod p + {0, p}
+// (< 2p) in three integer multiplies.  Butterfly values stay below 2p (DIF) or
+// 4p (DIT) < 2^32 and are reduced only where a consumer needs it.
+__device__ __forceinline__ uint32_t shoup(uint32_t a, uint32_t w, uint32_t wq) {
+  return a * w - __umulhi(a, wq) * kP;
+}
+// Montgomery form of a stage twiddle from its Shoup pair: w 2^32 mod p = -wq p mod 2^32
+__device__ __forceinline__ uint32_t pair_mont(uint2 t) { return 0u - t.y * kP; }
 // w^e for any e (mod N) from the half table tw[j] = w^j, j < N/2 (w^{N/2} = -1)
 __device__ __forceinline__ uint32_t wpow(const uint32_t* tw, uint32_t e, uint32_t N) {
   e &= N - 1;
@@ -80,7 +89,7 @@ __device__ __forceinline__ uint32_t phys(uint32_t i, uint32_t c) {
 
 template <int RB, bool kFwd, int kColsLog>
 __device__ __forceinline__ void ntt_round(uint32_t* __restrict__ s, uint32_t logn, uint32_t ulog,
-                                          const uint32_t* __restrict__ tws) {
+                                          const uint2* __restrict__ tws) {
   constexpr int E = 1 << RB;
   constexpr uint32_t cols = 1u << kColsLog;
   const uint32_t u = 1u << ulog;
@@ -103,20 +112,23 @@ __device__ __forceinline__ void ntt_round(uint32_t* __restrict__ s, uint32_t log
     for (int qq = 0; qq < RB; ++qq) {
       const int q = kFwd ? RB - 1 - qq : qq;                   // DIF: wide spans first
       const uint32_t h = u << q;
-      uint32_t w[1 << (RB - 1)];
+      uint2 w[1 << (RB - 1)];
 #pragma unroll
       for (int k = 0; k < (1 << q); ++k) w[k] = tws[h + off + k * u];
 #pragma unroll
       for (int k = 0; k < E; ++k) {
         if (k & (1 << q)) continue;
-        const uint32_t a = v[k], b = v[k + (1 << q)], ww = w[k & ((1 << q) - 1)];
-        if (kFwd) {
-          v[k] = madd(a, b);
-          v[k + (1 << q)] = mmul(msub(a, b), ww);
-        } else {
-          const uint32_t bw = mmul(b, ww);
-          v[k] = madd(a, bw);
-          v[k + (1 << q)] = msub(a, bw);
+        const uint32_t a = v[k], b = v[k + (1 << q)];
+        const uint2 ww = w[k & ((1 << q) - 1)];
+        if (kFwd) {                                            // in, out < 2p
+          const uint32_t t = a + b;
+          v[k] = t >= 2 * kP ? t - 2 * kP : t;
+          v[k + (1 << q)] = shoup(a + 2 * kP - b, ww.x, ww.y);
+        } else {                                               // in, out < 4p
+          const uint32_t ar = a >= 2 * kP ? a - 2 * kP : a;
+          const uint32_t bw = shoup(b, ww.x, ww.y);
+          v[k] = ar + bw;
+          v[k + (1 << q)] = ar + 2 * kP - bw;
         }
       }
     }
@@ -135,7 +147,7 @@ __device__ __forceinline__ void ntt_round(uint32_t* __restrict__ s, uint32_t log
 // All logn stages: rounds of three from the narrow end, the remainder (1 or 2
 // stages) at the wide end.  Forward DIF runs wide -> narrow, inverse DIT the reverse.
 template <bool kFwd, int kColsLog>
-__device__ __forceinline__ void ntt_smem(uint32_t* s, uint32_t logn, const uint32_t* tws) {
+__device__ __forceinline__ void ntt_smem(uint32_t* s, uint32_t logn, const uint2* tws) {
   const uint32_t top = logn % 3, nfull = logn / 3;
   if (kFwd && top == 1) ntt_round<1, true, kColsLog>(s, logn, logn - 1, tws);
   if (kFwd && top == 2) ntt_round<2, true, kColsLog>(s, logn, logn - 2, tws);
@@ -151,17 +163,18 @@ __device__ __forceinline__ void ntt_smem(uint32_t* s, uint32_t logn, const uint3
 // (j < h < n), precomputed once per build by ntt_stage_table_kernel (the
 // strided gather tw[j N / 2h] would cost a sector per entry in every CTA);
 // each CTA copies its table with coalesced loads.
-__device__ __forceinline__ void stage_twiddles(const uint32_t* tab, uint32_t n, uint32_t* tws) {
+__device__ __forceinline__ void stage_twiddles(const uint2* tab, uint32_t n, uint2* tws) {
   for (uint32_t j = threadIdx.x; j < n; j += blockDim.x) tws[j] = tab[j];
 }
 
-// Four-step twiddle w_N^{k1 col} with k1 < R, col < C: k1 col = q C + r,
-// w_N^{qC} = w_R^q from the R-point stage table (w_R^{R/2} = -1), w_N^r from tlo.
+// Four-step twiddle w_N^{k1 col} (Montgomery form) with k1 < R, col < C:
+// k1 col = q C + r, w_N^{qC} = w_R^q from the R-point stage table
+// (w_R^{R/2} = -1), w_N^r from tlo (Montgomery).
 __device__ __forceinline__ uint32_t four_step_tw(uint32_t k1, uint32_t col, uint32_t logC, uint32_t R,
-                                                 const uint32_t* tws, const uint32_t* tlo) {
+                                                 const uint2* tws, const uint32_t* tlo) {
   const uint32_t e = k1 * col, q = e >> logC, r = e & ((1u << logC) - 1);
-  const uint32_t hi = q < R / 2 ? tws[R / 2 + q] : kP - tws[q];
-  return mmul(hi, tlo[r]);
+  const uint32_t hm = pair_mont(tws[q < R / 2 ? R / 2 + q : q]);
+  return mmul(q < R / 2 ? hm : kP - hm, tlo[r]);
 }
 
 // Forward column pass (four-step): R-point DIF of 8 adjacent columns in
@@ -170,10 +183,10 @@ __device__ __forceinline__ uint32_t four_step_tw(uint32_t k1, uint32_t col, uint
 // k1 = brev_R(row) on the way out.
 __global__ void __launch_bounds__(256) ntt_col_fwd_kernel(const uint32_t* bits, size_t w_stride,
                                                           uint32_t L, uint32_t R, uint32_t C,
-                                                          const uint32_t* tw, const uint32_t* tabR,
+                                                          const uint32_t* tw, const uint2* tabR,
                                                           uint32_t* x) {
   __shared__ __align__(16) uint32_t s[kMaxRows * kCols];
-  __shared__ uint32_t tws[kMaxRows];
+  __shared__ uint2 tws[kMaxRows];
   __shared__ uint32_t tlo[kMaxRowLen];
   const uint32_t walk = blockIdx.y, col0 = blockIdx.x * kCols;
   const uint32_t N = R * C, logR = 31 - __clz(R), logC = 31 - __clz(C);
@@ -183,7 +196,7 @@ __global__ void __launch_bounds__(256) ntt_col_fwd_kernel(const uint32_t* bits, 
   for (uint32_t e = threadIdx.x; e < R * kCols; e += blockDim.x) {
     const uint32_t m = e / kCols, c = e % kCols, i = m * C + col0 + c;
     uint32_t v = 0;
-    if (i < L) v = ((S[i >> 5] >> (i & 31)) & 1u) ? kP - kOne : kOne;
+    if (i < L) v = ((S[i >> 5] >> (i & 31)) & 1u) ? kP - 1u : 1u;   // normal form
     s[phys<3>(m, c)] = v;
   }
   __syncthreads();
@@ -200,9 +213,9 @@ __global__ void __launch_bounds__(256) ntt_col_fwd_kernel(const uint32_t* bits, 
 // (the four-step's row transforms need no cross-row twiddles).
 template <bool kForward>
 __global__ void __launch_bounds__(256) ntt_row_kernel(uint32_t* x, uint32_t R, uint32_t C,
-                                                      const uint32_t* tabC) {
+                                                      const uint2* tabC) {
   __shared__ __align__(16) uint32_t s[kMaxRowLen];
-  __shared__ uint32_t ts[kMaxRowLen];
+  __shared__ uint2 ts[kMaxRowLen];
   const uint32_t N = R * C, logC = 31 - __clz(C);
   stage_twiddles(tabC, C, ts);
   for (uint32_t row = blockIdx.x * kRowsPerCta; row < (blockIdx.x + 1) * kRowsPerCta && row < R; ++row) {
@@ -238,12 +251,12 @@ __global__ void ntt_pointwise_kernel(uint32_t* x, uint32_t logN, uint32_t L, con
 // in, R-point DIT, then C_{L-1-i} = z_i N^-1 (signed) into the pivot / local
 // tables, PSL and energy.
 __global__ void __launch_bounds__(256) ntt_col_inv_kernel(const uint32_t* x, uint32_t R, uint32_t C,
-                                                          const uint32_t* twi, const uint32_t* tabR,
+                                                          const uint32_t* twi, const uint2* tabR,
                                                           uint32_t ninv_m,
                                                           uint32_t L, int32_t* Cp, int32_t* Cl,
                                                           size_t c_stride, WalkState* st) {
   __shared__ __align__(16) uint32_t s[kMaxRows * kCols];
-  __shared__ uint32_t tws[kMaxRows];
+  __shared__ uint2 tws[kMaxRows];
   __shared__ uint32_t tlo[kMaxRowLen];
   const uint32_t walk = blockIdx.y, col0 = blockIdx.x * kCols;
   const uint32_t N = R * C, logR = 31 - __clz(R), logC = 31 - __clz(C);
@@ -254,7 +267,8 @@ __global__ void __launch_bounds__(256) ntt_col_inv_kernel(const uint32_t* x, uin
   for (uint32_t e = threadIdx.x; e < R * kCols; e += blockDim.x) {
     const uint32_t m = e / kCols, c = e % kCols;
     const uint32_t k1 = __brev(m) >> (32 - logR);
-    s[phys<3>(m, c)] = mmul(X[m * C + col0 + c], four_step_tw(k1, col0 + c, logC, R, tws, tlo));
+    const uint32_t xv = X[m * C + col0 + c];                  // < 4p from the DIT rows
+    s[phys<3>(m, c)] = mmul(xv >= 2 * kP ? xv - 2 * kP : xv, four_step_tw(k1, col0 + c, logC, R, tws, tlo));
   }
   __syncthreads();
   ntt_smem<false, 3>(s, logR, tws);
@@ -265,8 +279,10 @@ __global__ void __launch_bounds__(256) ntt_col_inv_kernel(const uint32_t* x, uin
   for (uint32_t e = threadIdx.x; e < R * kCols; e += blockDim.x) {
     const uint32_t m = e / kCols, c = e % kCols, i = m * C + col0 + c;
     if (i >= L) continue;
-    // z holds N c R (Montgomery); mmul(., N^-1 R) = c R; mmul(., 1) = c
-    const uint32_t v = mmul(mmul(s[phys<3>(m, c)], ninv_m), 1u);
+    // z = N c 2^-32 (the pointwise product's Montgomery factor), < 4p;
+    // ninv_m = N^-1 2^64 mod p: mmul(z, ninv_m) = c
+    const uint32_t z = s[phys<3>(m, c)];
+    const uint32_t v = mmul(z >= 2 * kP ? z - 2 * kP : z, ninv_m);
     const int32_t cv = v > kP / 2 ? (int32_t)v - (int32_t)kP : (int32_t)v;
     const uint32_t k = L - 1 - i;
     Cw[k] = cv;
@@ -286,12 +302,14 @@ __global__ void __launch_bounds__(256) ntt_col_inv_kernel(const uint32_t* x, uin
   }
 }
 
-// tab[h + j] = tw[j N / 2h] for 1 <= h < n, j < h (tab[0] unused)
-__global__ void ntt_stage_table_kernel(const uint32_t* tw, uint32_t N, uint32_t n, uint32_t* tab) {
+// tab[h + j] = (w, floor(w 2^32 / p)) with w = tw[j N / 2h] in normal form,
+// for 1 <= h < n, j < h (tab[0] unused)
+__global__ void ntt_stage_table_kernel(const uint32_t* tw, uint32_t N, uint32_t n, uint2* tab) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    if (i == 0) { tab[0] = 0; continue; }
+    if (i == 0) { tab[0] = make_uint2(0, 0); continue; }
     const uint32_t h = 1u << (31 - __clz(i)), j = i - h;
-    tab[i] = tw[j * (N / (2 * h))];
+    const uint32_t w = mmul(tw[j * (N / (2 * h))], 1u);
+    tab[i] = make_uint2(w, (uint32_t)(((uint64_t)w << 32) / kP));
   }
 }
 
@@ -333,9 +351,10 @@ int launch_build_tables_ntt(const RunArgs& a, uint32_t n_walks, cudaStream_t s) 
   if (R > (uint32_t)kMaxRows || C > (uint32_t)kMaxRowLen || C < (uint32_t)kCols) return -1;
   uint32_t *x = nullptr, *tw = nullptr;
   if (cudaMallocAsync(&x, (size_t)n_walks * N * 4, s) != cudaSuccess) return -1;
-  if (cudaMallocAsync(&tw, (size_t)(N + 2 * R + 2 * C) * 4, s) != cudaSuccess) return -1;
+  if (cudaMallocAsync(&tw, (size_t)(N + 4 * R + 4 * C) * 4, s) != cudaSuccess) return -1;
   uint32_t* twi = tw + N / 2;
-  uint32_t *tabR = tw + N, *tabRi = tabR + R, *tabC = tabRi + R, *tabCi = tabC + C;
+  uint2* tabR = reinterpret_cast<uint2*>(tw + N);
+  uint2 *tabRi = tabR + R, *tabC = tabRi + R, *tabCi = tabC + C;
   int launches = 0;
   const uint32_t root = host_pow(3, (kP - 1) / N);          // primitive N-th root
   const uint32_t iroot = host_pow(root, kP - 2);
@@ -351,7 +370,7 @@ int launch_build_tables_ntt(const RunArgs& a, uint32_t n_walks, cudaStream_t s) 
   ntt_pointwise_kernel<<<dim3(std::min<uint32_t>(N / 256, 1024), n_walks), 256, 0, s>>>(x, logN, L, tw);
   ntt_row_kernel<false><<<grow, 256, 0, s>>>(x, R, C, tabCi);
   const uint32_t ninv = host_pow(N, kP - 2);
-  ntt_col_inv_kernel<<<gcol, 256, 0, s>>>(x, R, C, twi, tabRi, to_mont(ninv), L, a.Cpiv, a.Cloc, a.c_stride,
+  ntt_col_inv_kernel<<<gcol, 256, 0, s>>>(x, R, C, twi, tabRi, to_mont(to_mont(ninv)), L, a.Cpiv, a.Cloc, a.c_stride,
                                            a.st);
   launches += 11;
   cudaFreeAsync(x, s);
