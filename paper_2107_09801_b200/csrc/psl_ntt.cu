@@ -37,7 +37,8 @@ constexpr uint32_t kOne = 301989884u;    // 2^32 mod p (Montgomery 1)
 constexpr int kCols = 8;                 // columns per column-pass CTA (one 32 B sector per row)
 constexpr int kMaxRows = 1024;           // R <= 1024, C <= 2048 (N <= 2^21)
 constexpr int kMaxRowLen = 2048;
-constexpr uint32_t kRowsPerCta = 4;     // rows per row-pass CTA (amortises the twiddle copy)
+constexpr uint32_t kRowsPerCta = 4;
+constexpr uint32_t kNttThreads = 256;       // threads per NTT CTA     // rows per row-pass CTA (amortises the twiddle copy)
 
 // Montgomery product: returns a*b*2^-32 mod p for a, b < p.
 __device__ __forceinline__ uint32_t mmul(uint32_t a, uint32_t b) {
@@ -87,19 +88,21 @@ __device__ __forceinline__ uint32_t phys(uint32_t i, uint32_t c) {
   return ((((i & ~3u) | ((i + (i >> 3)) & 3u))) << kColsLog) + c;
 }
 
-template <int RB, bool kFwd, int kColsLog>
-__device__ __forceinline__ void ntt_round(uint32_t* __restrict__ s, uint32_t logn, uint32_t ulog,
-                                          const uint2* __restrict__ tws) {
+// Sizes are template parameters so the index arithmetic folds into immediate
+// shared-memory offsets.
+template <int RB, bool kFwd, int kColsLog, int LOGN, int ULOG>
+__device__ __forceinline__ void ntt_round(uint32_t* __restrict__ s, const uint2* __restrict__ tws) {
   constexpr int E = 1 << RB;
-  constexpr uint32_t cols = 1u << kColsLog;
-  const uint32_t u = 1u << ulog;
-  const uint32_t items = (1u << (logn - RB)) << kColsLog;
-  for (uint32_t it = threadIdx.x; it < items; it += blockDim.x) {
+  constexpr uint32_t cols = 1u << kColsLog, ulog = ULOG;
+  constexpr uint32_t u = 1u << ulog;
+  constexpr uint32_t items = (1u << (LOGN - RB)) << kColsLog;
+#pragma unroll
+  for (uint32_t it = threadIdx.x; it < items; it += kNttThreads) {
     const uint32_t c = it & (cols - 1), g = it >> kColsLog;
     const uint32_t off = g & (u - 1), base = ((g >> ulog) << (ulog + RB)) + off;
     uint32_t v[E];
-    const bool vec = kColsLog == 0 && RB == 3 && ulog == 0;
-    if (vec) {
+    constexpr bool vec = kColsLog == 0 && RB == 3 && ulog == 0;
+    if constexpr (vec) {
       const uint4 a = *reinterpret_cast<const uint4*>(s + phys<kColsLog>(base, 0));
       const uint4 b = *reinterpret_cast<const uint4*>(s + phys<kColsLog>(base + 4, 0));
       v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
@@ -132,7 +135,7 @@ __device__ __forceinline__ void ntt_round(uint32_t* __restrict__ s, uint32_t log
         }
       }
     }
-    if (vec) {
+    if constexpr (vec) {
       *reinterpret_cast<uint4*>(s + phys<kColsLog>(base, 0)) = make_uint4(v[0], v[1], v[2], v[3]);
       *reinterpret_cast<uint4*>(s + phys<kColsLog>(base + 4, 0)) =
           make_uint4(v[4 % E], v[5 % E], v[6 % E], v[7 % E]);
@@ -144,19 +147,17 @@ __device__ __forceinline__ void ntt_round(uint32_t* __restrict__ s, uint32_t log
   __syncthreads();
 }
 
-// All logn stages: rounds of three from the narrow end, the remainder (1 or 2
+// All LOGN stages: rounds of three from the narrow end, the remainder (1 or 2
 // stages) at the wide end.  Forward DIF runs wide -> narrow, inverse DIT the reverse.
-template <bool kFwd, int kColsLog>
-__device__ __forceinline__ void ntt_smem(uint32_t* s, uint32_t logn, const uint2* tws) {
-  const uint32_t top = logn % 3, nfull = logn / 3;
-  if (kFwd && top == 1) ntt_round<1, true, kColsLog>(s, logn, logn - 1, tws);
-  if (kFwd && top == 2) ntt_round<2, true, kColsLog>(s, logn, logn - 2, tws);
-  for (uint32_t r = 0; r < nfull; ++r) {
-    const uint32_t ulog = kFwd ? 3 * (nfull - 1 - r) : 3 * r;
-    ntt_round<3, kFwd, kColsLog>(s, logn, ulog, tws);
-  }
-  if (!kFwd && top == 1) ntt_round<1, false, kColsLog>(s, logn, logn - 1, tws);
-  if (!kFwd && top == 2) ntt_round<2, false, kColsLog>(s, logn, logn - 2, tws);
+template <bool kFwd, int CL, int LOGN>
+__device__ __forceinline__ void ntt_smem(uint32_t* s, const uint2* tws) {
+  constexpr int top = LOGN % 3, nf = LOGN / 3;
+  static_assert(nf >= 1 && nf <= 3, "7 <= LOGN <= 11");
+  if constexpr (kFwd && top) ntt_round<top, true, CL, LOGN, LOGN - top>(s, tws);
+  ntt_round<3, kFwd, CL, LOGN, kFwd ? 3 * (nf - 1) : 0>(s, tws);
+  if constexpr (nf >= 2) ntt_round<3, kFwd, CL, LOGN, kFwd ? 3 * (nf - 2) : 3>(s, tws);
+  if constexpr (nf >= 3) ntt_round<3, kFwd, CL, LOGN, kFwd ? 3 * (nf - 3) : 6>(s, tws);
+  if constexpr (!kFwd && top) ntt_round<top, false, CL, LOGN, LOGN - top>(s, tws);
 }
 
 // Stage twiddles of an n-point transform, tws[h + j] = w_N^{j N / 2h}
@@ -181,6 +182,7 @@ __device__ __forceinline__ uint32_t four_step_tw(uint32_t k1, uint32_t col, uint
 // shared memory, inputs generated from the packed bits (x_i = +-1 for i < L,
 // 0 past L), then the twiddle w_N^{k1 col} for the column spectrum entry
 // k1 = brev_R(row) on the way out.
+template <int LOGR>
 __global__ void __launch_bounds__(256) ntt_col_fwd_kernel(const uint32_t* bits, size_t w_stride,
                                                           uint32_t L, uint32_t R, uint32_t C,
                                                           const uint32_t* tw, const uint2* tabR,
@@ -189,7 +191,7 @@ __global__ void __launch_bounds__(256) ntt_col_fwd_kernel(const uint32_t* bits, 
   __shared__ uint2 tws[kMaxRows];
   __shared__ uint32_t tlo[kMaxRowLen];
   const uint32_t walk = blockIdx.y, col0 = blockIdx.x * kCols;
-  const uint32_t N = R * C, logR = 31 - __clz(R), logC = 31 - __clz(C);
+  const uint32_t N = R * C, logR = LOGR, logC = 31 - __clz(C);
   const uint32_t* S = bits + (size_t)walk * w_stride;
   stage_twiddles(tabR, R, tws);
   for (uint32_t j = threadIdx.x; j < C; j += blockDim.x) tlo[j] = tw[j];
@@ -200,7 +202,7 @@ __global__ void __launch_bounds__(256) ntt_col_fwd_kernel(const uint32_t* bits, 
     s[phys<3>(m, c)] = v;
   }
   __syncthreads();
-  ntt_smem<true, 3>(s, logR, tws);
+  ntt_smem<true, 3, LOGR>(s, tws);
   uint32_t* X = x + (size_t)walk * N;
   for (uint32_t e = threadIdx.x; e < R * kCols; e += blockDim.x) {
     const uint32_t m = e / kCols, c = e % kCols;
@@ -211,18 +213,18 @@ __global__ void __launch_bounds__(256) ntt_col_fwd_kernel(const uint32_t* bits, 
 
 // Row pass over the rows of every walk: C-point forward DIF or inverse DIT
 // (the four-step's row transforms need no cross-row twiddles).
-template <bool kForward>
+template <bool kForward, int LOGC>
 __global__ void __launch_bounds__(256) ntt_row_kernel(uint32_t* x, uint32_t R, uint32_t C,
                                                       const uint2* tabC) {
   __shared__ __align__(16) uint32_t s[kMaxRowLen];
   __shared__ uint2 ts[kMaxRowLen];
-  const uint32_t N = R * C, logC = 31 - __clz(C);
+  const uint32_t N = R * C;
   stage_twiddles(tabC, C, ts);
   for (uint32_t row = blockIdx.x * kRowsPerCta; row < (blockIdx.x + 1) * kRowsPerCta && row < R; ++row) {
     uint32_t* X = x + (size_t)blockIdx.y * N + (size_t)row * C;
     for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) s[phys<0>(i, 0)] = X[i];
     __syncthreads();
-    ntt_smem<kForward, 0>(s, logC, ts);
+    ntt_smem<kForward, 0, LOGC>(s, ts);
     for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) X[i] = s[phys<0>(i, 0)];
     __syncthreads();
   }
@@ -250,6 +252,7 @@ __global__ void ntt_pointwise_kernel(uint32_t* x, uint32_t logN, uint32_t L, con
 // Inverse column pass: the inverse four-step twiddle w_N^{-k1 col} on the way
 // in, R-point DIT, then C_{L-1-i} = z_i N^-1 (signed) into the pivot / local
 // tables, PSL and energy.
+template <int LOGR>
 __global__ void __launch_bounds__(256) ntt_col_inv_kernel(const uint32_t* x, uint32_t R, uint32_t C,
                                                           const uint32_t* twi, const uint2* tabR,
                                                           uint32_t ninv_m,
@@ -259,7 +262,7 @@ __global__ void __launch_bounds__(256) ntt_col_inv_kernel(const uint32_t* x, uin
   __shared__ uint2 tws[kMaxRows];
   __shared__ uint32_t tlo[kMaxRowLen];
   const uint32_t walk = blockIdx.y, col0 = blockIdx.x * kCols;
-  const uint32_t N = R * C, logR = 31 - __clz(R), logC = 31 - __clz(C);
+  const uint32_t N = R * C, logR = LOGR, logC = 31 - __clz(C);
   const uint32_t* X = x + (size_t)walk * N;
   stage_twiddles(tabR, R, tws);
   for (uint32_t j = threadIdx.x; j < C; j += blockDim.x) tlo[j] = twi[j];
@@ -271,7 +274,7 @@ __global__ void __launch_bounds__(256) ntt_col_inv_kernel(const uint32_t* x, uin
     s[phys<3>(m, c)] = mmul(xv >= 2 * kP ? xv - 2 * kP : xv, four_step_tw(k1, col0 + c, logC, R, tws, tlo));
   }
   __syncthreads();
-  ntt_smem<false, 3>(s, logR, tws);
+  ntt_smem<false, 3, LOGR>(s, tws);
   int32_t* Cw = Cp + (size_t)walk * c_stride;
   int32_t* Cw2 = Cl ? Cl + (size_t)walk * c_stride : nullptr;
   int32_t pm = 0;
@@ -365,13 +368,32 @@ int launch_build_tables_ntt(const RunArgs& a, uint32_t n_walks, cudaStream_t s) 
   ntt_stage_table_kernel<<<(C + 255) / 256, 256, 0, s>>>(tw, N, C, tabC);
   ntt_stage_table_kernel<<<(C + 255) / 256, 256, 0, s>>>(twi, N, C, tabCi);
   const dim3 gcol(C / kCols, n_walks), grow((R + kRowsPerCta - 1) / kRowsPerCta, n_walks);
-  ntt_col_fwd_kernel<<<gcol, 256, 0, s>>>(a.bits_piv + a.w_front + 1, a.w_stride, L, R, C, tw, tabR, x);
-  ntt_row_kernel<true><<<grow, 256, 0, s>>>(x, R, C, tabC);
+  const uint32_t ninv = host_pow(N, kP - 2), ninv_m = to_mont(to_mont(ninv));
+  const uint32_t* bits = a.bits_piv + a.w_front + 1;
+  switch (logR) {
+#define COL_FWD(LR) case LR: ntt_col_fwd_kernel<LR><<<gcol, kNttThreads, 0, s>>>(bits, a.w_stride, L, R, C, tw, tabR, x); break;
+    COL_FWD(7) COL_FWD(8) COL_FWD(9) COL_FWD(10)
+#undef COL_FWD
+    default: return -1;
+  }
+  const uint32_t logC = logN - logR;
+  switch (logC) {
+#define ROW(LC, F, T) case LC: ntt_row_kernel<F, LC><<<grow, kNttThreads, 0, s>>>(x, R, C, T); break;
+    ROW(7, true, tabC) ROW(8, true, tabC) ROW(9, true, tabC) ROW(10, true, tabC) ROW(11, true, tabC)
+    default: return -1;
+  }
   ntt_pointwise_kernel<<<dim3(std::min<uint32_t>(N / 256, 1024), n_walks), 256, 0, s>>>(x, logN, L, tw);
-  ntt_row_kernel<false><<<grow, 256, 0, s>>>(x, R, C, tabCi);
-  const uint32_t ninv = host_pow(N, kP - 2);
-  ntt_col_inv_kernel<<<gcol, 256, 0, s>>>(x, R, C, twi, tabRi, to_mont(to_mont(ninv)), L, a.Cpiv, a.Cloc, a.c_stride,
-                                           a.st);
+  switch (logC) {
+    ROW(7, false, tabCi) ROW(8, false, tabCi) ROW(9, false, tabCi) ROW(10, false, tabCi) ROW(11, false, tabCi)
+#undef ROW
+    default: return -1;
+  }
+  switch (logR) {
+#define COL_INV(LR) case LR: ntt_col_inv_kernel<LR><<<gcol, kNttThreads, 0, s>>>(x, R, C, twi, tabRi, ninv_m, L, a.Cpiv, a.Cloc, a.c_stride, a.st); break;
+    COL_INV(7) COL_INV(8) COL_INV(9) COL_INV(10)
+#undef COL_INV
+    default: return -1;
+  }
   launches += 11;
   cudaFreeAsync(x, s);
   cudaFreeAsync(tw, s);
