@@ -195,19 +195,33 @@ __global__ void __launch_bounds__(256) ntt_col_fwd_kernel(const uint32_t* bits, 
   const uint32_t* S = bits + (size_t)walk * w_stride;
   stage_twiddles(tabR, R, tws);
   for (uint32_t j = threadIdx.x; j < C; j += blockDim.x) tlo[j] = tw[j];
-  for (uint32_t e = threadIdx.x; e < R * kCols; e += blockDim.x) {
-    const uint32_t m = e / kCols, c = e % kCols, i = m * C + col0 + c;
-    uint32_t v = 0;
-    if (i < L) v = ((S[i >> 5] >> (i & 31)) & 1u) ? kP - 1u : 1u;   // normal form
-    s[phys<3>(m, c)] = v;
+  // work items = (row, half row of 4 columns): one bit word, one 16-byte store
+  for (uint32_t e = threadIdx.x; e < 2 * R; e += blockDim.x) {
+    const uint32_t m = e >> 1, c0 = (e & 1) * 4, i0 = m * C + col0 + c0;   // 4 | i0: one word
+    const uint32_t b = i0 < L ? S[i0 >> 5] >> (i0 & 31) : 0u;          // no reads past the bits
+    uint32_t v[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      v[c] = i0 + c < L ? (((b >> c) & 1u) ? kP - 1u : 1u) : 0u;          // normal form
+    *reinterpret_cast<uint4*>(s + phys<3>(m, c0)) = make_uint4(v[0], v[1], v[2], v[3]);
   }
   __syncthreads();
   ntt_smem<true, 3, LOGR>(s, tws);
   uint32_t* X = x + (size_t)walk * N;
-  for (uint32_t e = threadIdx.x; e < R * kCols; e += blockDim.x) {
-    const uint32_t m = e / kCols, c = e % kCols;
+  // four-step twiddles w^{k1 col}, col = col0 + c0 .. +3: one lookup, then
+  // successive products with w^{k1} (tlo[k1], k1 < R <= C)
+  for (uint32_t e = threadIdx.x; e < 2 * R; e += blockDim.x) {
+    const uint32_t m = e >> 1, c0 = (e & 1) * 4;
     const uint32_t k1 = __brev(m) >> (32 - logR);
-    X[m * C + col0 + c] = mmul(s[phys<3>(m, c)], four_step_tw(k1, col0 + c, logC, R, tws, tlo));
+    uint32_t t = four_step_tw(k1, col0 + c0, logC, R, tws, tlo);
+    const uint32_t step = tlo[k1];
+    const uint4 a = *reinterpret_cast<const uint4*>(s + phys<3>(m, c0));
+    uint4 o;
+    o.x = mmul(a.x, t); t = mmul(t, step);
+    o.y = mmul(a.y, t); t = mmul(t, step);
+    o.z = mmul(a.z, t); t = mmul(t, step);
+    o.w = mmul(a.w, t);
+    *reinterpret_cast<uint4*>(X + m * C + col0 + c0) = o;
   }
 }
 
@@ -267,11 +281,19 @@ __global__ void __launch_bounds__(256) ntt_col_inv_kernel(const uint32_t* x, uin
   stage_twiddles(tabR, R, tws);
   for (uint32_t j = threadIdx.x; j < C; j += blockDim.x) tlo[j] = twi[j];
   __syncthreads();
-  for (uint32_t e = threadIdx.x; e < R * kCols; e += blockDim.x) {
-    const uint32_t m = e / kCols, c = e % kCols;
+  for (uint32_t e = threadIdx.x; e < 2 * R; e += blockDim.x) {
+    const uint32_t m = e >> 1, c0 = (e & 1) * 4;
     const uint32_t k1 = __brev(m) >> (32 - logR);
-    const uint32_t xv = X[m * C + col0 + c];                  // < 4p from the DIT rows
-    s[phys<3>(m, c)] = mmul(xv >= 2 * kP ? xv - 2 * kP : xv, four_step_tw(k1, col0 + c, logC, R, tws, tlo));
+    uint32_t t = four_step_tw(k1, col0 + c0, logC, R, tws, tlo);
+    const uint32_t step = tlo[k1];
+    const uint4 a = *reinterpret_cast<const uint4*>(X + m * C + col0 + c0);   // < 4p (DIT rows)
+    auto r2 = [](uint32_t v) { return v >= 2 * kP ? v - 2 * kP : v; };
+    uint4 o;
+    o.x = mmul(r2(a.x), t); t = mmul(t, step);
+    o.y = mmul(r2(a.y), t); t = mmul(t, step);
+    o.z = mmul(r2(a.z), t); t = mmul(t, step);
+    o.w = mmul(r2(a.w), t);
+    *reinterpret_cast<uint4*>(s + phys<3>(m, c0)) = o;
   }
   __syncthreads();
   ntt_smem<false, 3, LOGR>(s, tws);
