@@ -89,9 +89,11 @@ __device__ __forceinline__ uint32_t phys(uint32_t i, uint32_t c) {
 }
 
 // Sizes are template parameters so the index arithmetic folds into immediate
-// shared-memory offsets.
-template <int RB, bool kFwd, int kColsLog, int LOGN, int ULOG>
-__device__ __forceinline__ void ntt_round(uint32_t* __restrict__ s, const uint2* __restrict__ tws) {
+// shared-memory offsets.  GIN / GOUT: the round reads its inputs from / writes
+// its outputs to the row in global memory gm (natural order) instead of s.
+template <int RB, bool kFwd, int kColsLog, int LOGN, int ULOG, bool GIN = false, bool GOUT = false>
+__device__ __forceinline__ void ntt_round(uint32_t* __restrict__ s, const uint2* __restrict__ tws,
+                                          uint32_t* __restrict__ gm = nullptr) {
   constexpr int E = 1 << RB;
   constexpr uint32_t cols = 1u << kColsLog, ulog = ULOG;
   constexpr uint32_t u = 1u << ulog;
@@ -103,13 +105,13 @@ __device__ __forceinline__ void ntt_round(uint32_t* __restrict__ s, const uint2*
     uint32_t v[E];
     constexpr bool vec = kColsLog == 0 && RB == 3 && ulog == 0;
     if constexpr (vec) {
-      const uint4 a = *reinterpret_cast<const uint4*>(s + phys<kColsLog>(base, 0));
-      const uint4 b = *reinterpret_cast<const uint4*>(s + phys<kColsLog>(base + 4, 0));
+      const uint4 a = *reinterpret_cast<const uint4*>(GIN ? gm + base : s + phys<kColsLog>(base, 0));
+      const uint4 b = *reinterpret_cast<const uint4*>(GIN ? gm + base + 4 : s + phys<kColsLog>(base + 4, 0));
       v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
       v[4 % E] = b.x; v[5 % E] = b.y; v[6 % E] = b.z; v[7 % E] = b.w;
     } else {
 #pragma unroll
-      for (int k = 0; k < E; ++k) v[k] = s[phys<kColsLog>(base + k * u, c)];
+      for (int k = 0; k < E; ++k) v[k] = GIN ? gm[base + k * u] : s[phys<kColsLog>(base + k * u, c)];
     }
 #pragma unroll
     for (int qq = 0; qq < RB; ++qq) {
@@ -136,12 +138,15 @@ __device__ __forceinline__ void ntt_round(uint32_t* __restrict__ s, const uint2*
       }
     }
     if constexpr (vec) {
-      *reinterpret_cast<uint4*>(s + phys<kColsLog>(base, 0)) = make_uint4(v[0], v[1], v[2], v[3]);
-      *reinterpret_cast<uint4*>(s + phys<kColsLog>(base + 4, 0)) =
+      *reinterpret_cast<uint4*>(GOUT ? gm + base : s + phys<kColsLog>(base, 0)) = make_uint4(v[0], v[1], v[2], v[3]);
+      *reinterpret_cast<uint4*>(GOUT ? gm + base + 4 : s + phys<kColsLog>(base + 4, 0)) =
           make_uint4(v[4 % E], v[5 % E], v[6 % E], v[7 % E]);
     } else {
 #pragma unroll
-      for (int k = 0; k < E; ++k) s[phys<kColsLog>(base + k * u, c)] = v[k];
+      for (int k = 0; k < E; ++k) {
+        if constexpr (GOUT) gm[base + k * u] = v[k];
+        else s[phys<kColsLog>(base + k * u, c)] = v[k];
+      }
     }
   }
   __syncthreads();
@@ -158,6 +163,25 @@ __device__ __forceinline__ void ntt_smem(uint32_t* s, const uint2* tws) {
   if constexpr (nf >= 2) ntt_round<3, kFwd, CL, LOGN, kFwd ? 3 * (nf - 2) : 3>(s, tws);
   if constexpr (nf >= 3) ntt_round<3, kFwd, CL, LOGN, kFwd ? 3 * (nf - 3) : 6>(s, tws);
   if constexpr (!kFwd && top) ntt_round<top, false, CL, LOGN, LOGN - top>(s, tws);
+}
+
+// The same for one row in global memory g: the first round reads g, the last
+// writes g (two shared-memory round trips fewer per row).
+template <bool kFwd, int LOGN>
+__device__ __forceinline__ void ntt_row_g(uint32_t* s, const uint2* tws, uint32_t* g) {
+  constexpr int top = LOGN % 3, nf = LOGN / 3;
+  static_assert(top != 0 && nf >= 2 && nf <= 3, "LOGN in {7, 8, 10, 11}");
+  if constexpr (kFwd) {
+    ntt_round<top, true, 0, LOGN, LOGN - top, true, false>(s, tws, g);
+    if constexpr (nf == 3) ntt_round<3, true, 0, LOGN, 6>(s, tws);
+    ntt_round<3, true, 0, LOGN, 3>(s, tws);
+    ntt_round<3, true, 0, LOGN, 0, false, true>(s, tws, g);
+  } else {
+    ntt_round<3, false, 0, LOGN, 0, true, false>(s, tws, g);
+    ntt_round<3, false, 0, LOGN, 3>(s, tws);
+    if constexpr (nf == 3) ntt_round<3, false, 0, LOGN, 6>(s, tws);
+    ntt_round<top, false, 0, LOGN, LOGN - top, false, true>(s, tws, g);
+  }
 }
 
 // Stage twiddles of an n-point transform, tws[h + j] = w_N^{j N / 2h}
@@ -234,13 +258,18 @@ __global__ void __launch_bounds__(256) ntt_row_kernel(uint32_t* x, uint32_t R, u
   __shared__ uint2 ts[kMaxRowLen];
   const uint32_t N = R * C;
   stage_twiddles(tabC, C, ts);
+  __syncthreads();
   for (uint32_t row = blockIdx.x * kRowsPerCta; row < (blockIdx.x + 1) * kRowsPerCta && row < R; ++row) {
     uint32_t* X = x + (size_t)blockIdx.y * N + (size_t)row * C;
-    for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) s[phys<0>(i, 0)] = X[i];
-    __syncthreads();
-    ntt_smem<kForward, 0, LOGC>(s, ts);
-    for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) X[i] = s[phys<0>(i, 0)];
-    __syncthreads();
+    if constexpr (LOGC % 3 != 0) {
+      ntt_row_g<kForward, LOGC>(s, ts, X);
+    } else {
+      for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) s[phys<0>(i, 0)] = X[i];
+      __syncthreads();
+      ntt_smem<kForward, 0, LOGC>(s, ts);
+      for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) X[i] = s[phys<0>(i, 0)];
+      __syncthreads();
+    }
   }
 }
 
