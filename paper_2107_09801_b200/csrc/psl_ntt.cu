@@ -274,17 +274,31 @@ __global__ void __launch_bounds__(256) ntt_row_kernel(uint32_t* x, uint32_t R, u
 }
 
 // Spectrum of the correlation at bit-reversed position p (k = brev(p)):
-// Z(k) = X(k) X(N-k) w^{(L-1)k}.  Pairs (p, p') are updated by the lower of the two.
-__global__ void ntt_pointwise_kernel(uint32_t* x, uint32_t logN, uint32_t L, const uint32_t* tw) {
-  const uint32_t N = 1u << logN;
+// Z(k) = X(k) X(N-k) w^{(L-1)k}.  With p = m C + c (k = k1 + R k2, k1 =
+// brev_R(m), k2 = brev_C(c)) the partner of a row m != 0 is the row
+// m' = brev_R(R - k1) read backwards (c -> C-1-c), so one CTA per row pair
+// reads and writes both rows coalesced; row 0 pairs within itself.
+__global__ void __launch_bounds__(256) ntt_pointwise_kernel(uint32_t* x, uint32_t logN, uint32_t logR,
+                                                            uint32_t L, const uint32_t* tw) {
+  const uint32_t N = 1u << logN, R = 1u << logR, logC = logN - logR, C = 1u << logC;
+  const uint32_t m = blockIdx.x;
+  const uint32_t k1 = m ? __brev(m) >> (32 - logR) : 0u;
+  const uint32_t m2 = m ? __brev(R - k1) >> (32 - logR) : 0u;
+  if (m2 < m) return;                                        // the partner row's CTA
   uint32_t* X = x + (size_t)blockIdx.y * N;
-  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < N; p += gridDim.x * blockDim.x) {
-    const uint32_t k = __brev(p) >> (32 - logN);
+  for (uint32_t c = threadIdx.x; c < C; c += blockDim.x) {
+    const uint32_t k = ((__brev(c) >> (32 - logC)) << logR) + k1;
     const uint32_t kn = (N - k) & (N - 1);
-    const uint32_t p2 = __brev(kn) >> (32 - logN);
-    if (p2 < p) continue;                                    // done by the partner
-    const uint32_t a = X[p], b = X[p2];
-    const uint32_t ab = mmul(a, b);
+    uint32_t c2;
+    if (m) {
+      c2 = C - 1 - c;
+      if (m2 == m && c2 < c) continue;                       // self-paired row: lower half does it
+    } else {
+      c2 = __brev(kn >> logR) >> (32 - logC);
+      if (c2 < c) continue;
+    }
+    const uint32_t p = m * C + c, p2 = m2 * C + c2;
+    const uint32_t ab = mmul(X[p], X[p2]);
     const uint32_t e1 = (uint32_t)(((uint64_t)(L - 1) * k) & (N - 1));
     const uint32_t e2 = (uint32_t)(((uint64_t)(L - 1) * kn) & (N - 1));
     X[p] = mmul(ab, wpow(tw, e1, N));
@@ -433,7 +447,7 @@ int launch_build_tables_ntt(const RunArgs& a, uint32_t n_walks, cudaStream_t s) 
     ROW(7, true, tabC) ROW(8, true, tabC) ROW(9, true, tabC) ROW(10, true, tabC) ROW(11, true, tabC)
     default: return -1;
   }
-  ntt_pointwise_kernel<<<dim3(std::min<uint32_t>(N / 256, 1024), n_walks), 256, 0, s>>>(x, logN, L, tw);
+  ntt_pointwise_kernel<<<dim3(R, n_walks), 256, 0, s>>>(x, logN, logR, L, tw);
   switch (logC) {
     ROW(7, false, tabCi) ROW(8, false, tabCi) ROW(9, false, tabCi) ROW(10, false, tabCi) ROW(11, false, tabCi)
 #undef ROW
