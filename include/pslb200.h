@@ -230,7 +230,11 @@ int psl_walks_records(psl_walks* w, psl_walk_record* records, int8_t* solutions,
                       char* err, size_t errlen);
 void psl_walks_destroy(psl_walks* w);
 
-/* One-call form: create, run to the stop condition, copy out, destroy. */
+/* One-call form: create, run to the stop condition, copy out, destroy. When
+ * `solutions` is page-locked host memory (cudaHostAlloc / cudaHostRegister,
+ * mapped under UVA), each walk's kernel writes its best sequence straight into
+ * it as the walk stops, so the copy-out overlaps the steps of later walks;
+ * any other buffer gets one device-side unpack and a D2H copy. */
 int psl_run_walks(psl_ctx* ctx, const psl_params* params, uint32_t n_walks,
                   const uint64_t* seeds, const int8_t* inits, psl_walk_record* records,
                   int8_t* solutions, char* err, size_t errlen);

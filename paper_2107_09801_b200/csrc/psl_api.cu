@@ -51,6 +51,7 @@ struct psl_walks {
   int8_t* inits = nullptr;      // device copy of warm starts (int8 +-1)
   uint32_t* bad = nullptr;      // [first bad flat index + 1, value]
   int8_t* sol = nullptr;        // unpack scratch for solutions
+  int8_t* sol_direct = nullptr; // host buffer the run kernel wrote the solutions into (psl_run_walks)
   double* lut = nullptr;        // [2][lut_n] power tables
   double* b2 = nullptr;         // certified-scan band-2 scratch
   double* lo_buf = nullptr;     // certified-scan per-row lower bounds (n_lmt > 1024)
@@ -746,7 +747,14 @@ int psl_walks_records(psl_walks* w, psl_walk_record* records, int8_t* solutions,
   std::vector<WalkState> st(w->n_walks);
   CK(cudaMemcpyAsync(st.data(), w->st, sizeof(WalkState) * w->n_walks, cudaMemcpyDeviceToHost, s));
   const uint32_t L = w->a.L;
-  if (solutions) {
+  bool direct = false;
+  if (solutions && w->sol_direct == solutions) {
+    // written by the run kernel as each walk stopped -- valid if every walk stopped cleanly
+    CK(cudaStreamSynchronize(s));
+    direct = true;
+    for (const WalkState& S : st) direct = direct && S.done && S.status == PSL_OK;
+  }
+  if (solutions && !direct) {
     // unpack on the device, one D2H of n_walks * L int8
     if (!w->sol) CK(cudaMallocAsync(&w->sol, (size_t)w->n_walks * L, s));
     if (launch_unpack(w->a.bits_best + w->a.w_front + 1, w->a.w_stride, L, w->n_walks, w->sol, s) < 0)
@@ -787,6 +795,17 @@ int psl_run_walks(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, cons
   psl_walks* w = nullptr;
   int rc = psl_walks_create(ctx, params, n_walks, seeds, inits, &w, err, errlen);
   if (rc) return rc;
+  if (solutions) {
+    // a pinned (mapped) caller buffer: each walk's kernel writes its best
+    // sequence there when it stops, overlapping the D2H with later walks' steps
+    cudaPointerAttributes pa;
+    if (cudaPointerGetAttributes(&pa, solutions) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
+        pa.devicePointer) {
+      w->a.sol_out = static_cast<int8_t*>(pa.devicePointer);
+      w->sol_direct = solutions;
+    }
+    cudaGetLastError();
+  }
   rc = psl_walks_run(w, err, errlen);
   if (!rc) rc = psl_walks_records(w, records, solutions, err, errlen);
   psl_walks_destroy(w);

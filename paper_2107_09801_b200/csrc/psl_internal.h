@@ -90,6 +90,8 @@ struct RunArgs {
   const double* lut1;   // PowerTable(L, alpha1) / (L, alpha2) on the device (sequence.hpp:72-84)
   const double* lut2;
   uint32_t lut_n;       // entries per table (> max |C_k| + 4)
+  int8_t* sol_out;      // optional: mapped pinned host [walk][L]; a walk that stops writes its
+                        // best sequence there from the kernel (overlaps later walks' steps)
 };
 
 struct ScanArgs {

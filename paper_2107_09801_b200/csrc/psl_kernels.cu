@@ -1736,6 +1736,25 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
     if (ctl->st.status != PSL_OK) ctl->st.end_ns = globaltimer();
     *gst = ctl->st;
   }
+  if (a.sol_out && ctl->st.done && ctl->st.status == PSL_OK) {
+    // the walk's best sequence as int8 +-1 straight into the caller's pinned
+    // host buffer (unpack_kernel's encoding), 16-byte stores over PCIe
+    int8_t* o = a.sol_out + (size_t)w * L;
+    const uint32_t* bb = bits_best + 1;
+    const uint32_t head = min(L, (uint32_t)((16u - ((uintptr_t)o & 15u)) & 15u));
+    const uint32_t nvec = (L - head) >> 4;
+    for (uint32_t i = t; i < head; i += blockDim.x) o[i] = ((bb[i >> 5] >> (i & 31)) & 1u) ? (int8_t)-1 : (int8_t)1;
+    for (uint32_t v = t; v < nvec; v += blockDim.x) {
+      const uint32_t j = head + 16 * v;
+      const uint32_t b16 = __funnelshift_r(bb[j >> 5], bb[(j >> 5) + 1], j & 31) & 0xffffu;
+      uint32_t q[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) q[k] = 0x01010101u + (((b16 >> (4 * k)) & 0xfu) * 0x00204081u & 0x01010101u) * 0xfeu;
+      *reinterpret_cast<uint4*>(o + j) = make_uint4(q[0], q[1], q[2], q[3]);
+    }
+    for (uint32_t i = head + 16 * nvec + t; i < L; i += blockDim.x)
+      o[i] = ((bb[i >> 5] >> (i & 31)) & 1u) ? (int8_t)-1 : (int8_t)1;
+  }
   if (kCert && t < 32) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(ctl->tmem), "r"(kTmemCols) : "memory");

@@ -615,9 +615,31 @@ class Walks:
 def run_walks(params: SearchParams, n_walks: int, seeds=None, inits=None,
               ctx: Context | None = None, solutions: bool = True,
               out: np.ndarray | None = None) -> list[WalkRecord]:
-    w = Walks(params, n_walks, seeds, inits, ctx)
-    try:
-        w.run()
-        return w.records(solutions, out)
-    finally:
-        w.close()
+    """One psl_run_walks call: create, run every walk to its stop, records.
+    With a pinned `out` buffer each walk's kernel writes its best sequence
+    straight into it when the walk stops (the D2H overlaps later walks)."""
+    p = validate_params(params)
+    ctx = ctx or default_context()
+    c, keep = _to_c(p)
+    seeds_arr = None if seeds is None else np.ascontiguousarray(seeds, np.uint64)
+    inits_arr = None if inits is None else np.ascontiguousarray(inits, np.int8)
+    recs = (B.psl_walk_record * n_walks)()
+    sol = None
+    if solutions:
+        if out is not None:
+            if out.dtype != np.int8 or out.shape != (n_walks, p.length) or not out.flags.c_contiguous:
+                raise ValueError("out must be a C-contiguous int8 array of shape (n_walks, length)")
+            sol = out
+        else:
+            sol = np.zeros((n_walks, p.length), np.int8)
+    err = _err()
+    rc = B.lib().psl_run_walks(ctx.handle, C.byref(c), n_walks,
+                               seeds_arr.ctypes.data if seeds_arr is not None else None,
+                               inits_arr.ctypes.data if inits_arr is not None else None,
+                               recs, sol.ctypes.data if sol is not None else None, err, len(err))
+    del keep
+    if rc:
+        _raise(rc, err)
+    return [WalkRecord(r.seed, r.nse, r.elapsed_seconds, r.psl_best, r.status, r.merit_factor,
+                       r.energy, r.switches, r.steps, None if sol is None else sol[i])
+            for i, r in enumerate(recs)]

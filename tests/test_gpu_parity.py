@@ -397,6 +397,28 @@ def test_ntt_table_build_lengths(engine, L):
         assert np.array_equal(recs[w].solution_best, osol)
 
 
+def test_run_walks_pinned_solutions(engine):
+    """psl_run_walks into a pinned buffer: the run kernel writes every walk's
+    best sequence over PCIe as the walk stops (odd L: unaligned rows, head and
+    tail bytes); equal to the unpack + D2H path and to the oracle."""
+    import torch
+    for L, nw in ((9001, 5), (4097, 3), (70001, 2)):
+        p = _params(engine, L, 11, 4, 13, 3, 10, 128, 1 + 3 * 128)
+        pinned = torch.full((nw, L), 7, dtype=torch.int8).pin_memory().numpy()
+        r1 = engine.run_walks(p, nw, out=pinned)
+        r2 = engine.run_walks(p, nw)
+        w = engine.Walks(p, nw)
+        w.run()
+        r3 = w.records(solutions=True)
+        w.close()
+        for a, b, c in zip(r1, r2, r3):
+            assert (a.nse, a.psl_best, a.energy) == (b.nse, b.psl_best, b.energy) == (c.nse, c.psl_best, c.energy)
+            assert np.array_equal(a.solution_best, b.solution_best)
+            assert np.array_equal(a.solution_best, c.solution_best)
+        rc, orec, osol, _, _ = O.run_search(L, 11, 4, 13, 3, 10, 128, 1 + 3 * 128)
+        assert np.array_equal(pinned[0], osol) and r1[0].psl_best == orec.psl_best
+
+
 def test_drain_and_resume(engine, golden, monkeypatch):
     """Tiny device event/trace buffers: run_search drains and relaunches many
     times; hooks must still see the reference's exact event/trace stream."""
