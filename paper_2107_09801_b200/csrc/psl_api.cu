@@ -683,13 +683,13 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
       cudaEventDestroy(done);
     }
     const RunArgs ab = walk_offset(a, w0);
-    if (launch_init_walks(ab, cnt, W->seeds + w0, dinit, W->bad, s, w0) < 0)
-      return fail(cudaGetLastError(), "init_walks_kernel");
+    const int ni = launch_init_walks(ab, cnt, W->seeds + w0, dinit, W->bad, s, w0);
+    if (ni < 0) return fail(cudaGetLastError(), "init_walks_kernel");
     // SidelobeTable::build: exact NTT correlation for long sequences (O(L log L)),
     // bit-parallel popcount kernel (O(L^2/32)) for short ones
     const int nb = L >= 8192 ? launch_build_tables_ntt(ab, cnt, s) : launch_build_tables(ab, cnt, s);
     if (nb < 0) return fail(cudaGetLastError(), "build_tables");
-    ctx->launches += 1 + (uint32_t)nb;
+    ctx->launches += (uint32_t)ni + (uint32_t)nb;
   }
   if (W->inits) {
     uint32_t bad[2];

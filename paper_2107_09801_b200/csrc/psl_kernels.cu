@@ -65,6 +65,17 @@ __device__ __forceinline__ uint64_t rng_next(uint64_t* s) {
   return result;
 }
 
+// The state transition of rng_next alone: linear over GF(2) (xors, shifts, a rotation).
+__device__ __forceinline__ void rng_step(uint64_t* s) {
+  const uint64_t t = s[1] << 17;
+  s[2] ^= s[0];
+  s[3] ^= s[1];
+  s[1] ^= s[2];
+  s[0] ^= s[3];
+  s[2] ^= t;
+  s[3] = rotl64(s[3], 45);
+}
+
 // rng.hpp:46-52
 __device__ __forceinline__ uint64_t rng_bounded(uint64_t* s, uint64_t n) {
   const uint64_t mask = (n <= 1) ? 0ull : (~0ull >> __clzll((long long)(n - 1)));
@@ -651,6 +662,24 @@ __device__ long long energy_sweep(Ctl* ctl, const int32_t* C, uint32_t L, const 
 
 // ------------------------------------------------------------ kernels
 
+// random_sequence's L spin draws split into chunks of kSpinChunk draws: the
+// state at the start of chunk j+1 is J s_j with J = T^kSpinChunk, T the
+// xoshiro256 transition as a 256x256 GF(2) matrix; column c of J (= J e_c)
+// is g_rng_jump[c].  One warp walks the chunk starts, then one thread per
+// chunk draws its spins: the same bits and end state as L serial draws.
+constexpr uint32_t kSpinChunk = 4096;
+constexpr uint32_t kMaxSpinChunks = (1u << 20) / kSpinChunk;   // L <= 2^20
+__device__ uint64_t g_rng_jump[256][4];
+
+__global__ void __launch_bounds__(256) rng_jump_kernel() {
+  const uint32_t c = threadIdx.x;
+  uint64_t st[4] = {0, 0, 0, 0};
+  st[c >> 6] = 1ull << (c & 63);
+  for (uint32_t i = 0; i < kSpinChunk; ++i) rng_step(st);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) g_rng_jump[c][q] = st[q];
+}
+
 // Walk setup: RNG, pivot (random_sequence, search.cpp:120-129, or warm start),
 // snapshot copies.  One CTA per walk.
 __global__ void __launch_bounds__(256) init_walks_kernel(RunArgs a, const uint64_t* seeds,
@@ -671,16 +700,58 @@ __global__ void __launch_bounds__(256) init_walks_kernel(RunArgs a, const uint64
     z.phase = 1;
     z.fitness_pending = 1;
     z.psl_best = -1;           // set from P on the first pass
-    if (!inits) {
-      // L spin() draws in position order; bit = top bit of next() (1 <-> -1)
-      for (uint32_t wd = 0; wd < nw; ++wd) {
-        uint32_t word = 0;
-        const uint32_t nb = min(32u, a.L - wd * 32);
-        for (uint32_t b = 0; b < nb; ++b) word |= (uint32_t)(rng_next(z.rng) >> 63) << b;
-        bp[wd + 1] = word;
+    *S = z;
+  }
+  if (!inits) {
+    // L spin() draws in position order; bit = top bit of next() (1 <-> -1)
+    __shared__ uint64_t cs[kMaxSpinChunks][4];
+    __shared__ uint64_t jm[256][4];
+    const uint32_t nch = (a.L + kSpinChunk - 1) / kSpinChunk;
+    if (nch > 1)
+      for (uint32_t i = threadIdx.x; i < 256 * 4; i += blockDim.x) jm[i >> 2][i & 3] = g_rng_jump[i >> 2][i & 3];
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      const uint32_t l = threadIdx.x;
+      uint64_t st[4];
+      rng_seed(st, seeds[w]);
+      for (uint32_t j = 0; j < nch; ++j) {
+        if (l == 0) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) cs[j][q] = st[q];
+        }
+        if (j + 1 == nch) break;
+        // st = J st: lane l folds the columns of state bits 8l .. 8l+7
+        uint64_t acc[4] = {0, 0, 0, 0};
+        const uint64_t byte = (st[l >> 3] >> (8 * (l & 7))) & 0xffull;
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+          if ((byte >> b) & 1ull) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] ^= jm[8 * l + b][q];
+          }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+#pragma unroll
+          for (int o = 16; o; o >>= 1) acc[q] ^= __shfl_xor_sync(0xffffffffu, acc[q], o);
+          st[q] = acc[q];
+        }
       }
     }
-    *S = z;
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < nch; j += blockDim.x) {
+      uint64_t st[4] = {cs[j][0], cs[j][1], cs[j][2], cs[j][3]};
+      const uint32_t p0 = j * kSpinChunk, p1 = min(a.L, p0 + kSpinChunk);
+      for (uint32_t wd = p0 >> 5; wd < (p1 + 31) >> 5; ++wd) {
+        uint32_t word = 0;
+        const uint32_t nb = min(32u, a.L - wd * 32);
+        for (uint32_t b = 0; b < nb; ++b) word |= (uint32_t)(rng_next(st) >> 63) << b;
+        bp[wd + 1] = word;
+      }
+      if (j + 1 == nch) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) S->rng[q] = st[q];     // the state after all L draws
+      }
+    }
   }
   if (inits) {
     // warm starts: validate (BinarySequence ctor, sequence.cpp:20-35) and pack;
@@ -1889,8 +1960,10 @@ RunArgs walk_offset(const RunArgs& a, uint32_t w0) {
 
 int launch_init_walks(const RunArgs& a, uint32_t n_walks, const uint64_t* d_seeds,
                       const int8_t* d_inits, uint32_t* d_bad, cudaStream_t s, uint32_t walk0) {
+  const bool jump = !d_inits && a.L > kSpinChunk;
+  if (jump) rng_jump_kernel<<<1, 256, 0, s>>>();
   init_walks_kernel<<<n_walks, 256, 0, s>>>(a, d_seeds, d_inits, d_bad, walk0);
-  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+  return cudaGetLastError() == cudaSuccess ? (jump ? 2 : 1) : -1;
 }
 
 int launch_build_tables(const RunArgs& a, uint32_t n_walks, cudaStream_t s) {
