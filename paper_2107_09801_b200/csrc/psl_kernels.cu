@@ -128,12 +128,6 @@ __device__ __forceinline__ uint32_t sword(const uint32_t* sb, int w, int nwords)
   w = max(-1, min(w, nwords));
   return sb[w + 1];
 }
-__device__ __forceinline__ uint32_t sword_up(const uint32_t* sb, int w, int nwords) {
-  return sb[min(w, nwords) + 1];   // index only grows (B window)
-}
-__device__ __forceinline__ uint32_t sword_dn(const uint32_t* sb, int w) {
-  return sb[max(w, -1) + 1];       // index only shrinks (A window)
-}
 // (v & mask) | base as one LOP3 (the compiler would turn a disjoint OR into
 // an extra add)
 __device__ __forceinline__ uint32_t and_or(uint32_t v, uint32_t mask, uint32_t base) {
