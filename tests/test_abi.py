@@ -144,3 +144,18 @@ def _has_gpu():
 def test_no_cpu_fallback_without_gpu():
     with pytest.raises(P.DeviceError, match="no CPU fallback"):
         P.Context(0)
+
+
+@pytest.mark.skipif(_has_gpu(), reason="checks the no-GPU failure mode")
+def test_public_entry_points_fail_loudly_without_gpu():
+    """run_walks (one psl_run_walks call), Walks and run_search: every compute
+    entry raises DeviceError on a host without a B200 -- no CPU fallback."""
+    L = 64
+    p = P.SearchParams(length=L, seed=1, alpha1=4, alpha2=13, ls_lmt=3, flip_lmt=2, n_lmt=8,
+                       stop=P.StopCondition(max_nse=100))
+    with pytest.raises(P.DeviceError):
+        P.run_walks(p, 2)
+    with pytest.raises(P.DeviceError):
+        P.Walks(p, 2)
+    with pytest.raises(P.DeviceError):
+        P.run_search(p)
