@@ -104,6 +104,10 @@ __device__ __forceinline__ void ntt_round(uint32_t* __restrict__ s, const uint2*
     const uint32_t off = g & (u - 1), base = ((g >> ulog) << (ulog + RB)) + off;
     uint32_t v[E];
     constexpr bool vec = kColsLog == 0 && RB == 3 && ulog == 0;
+    // spans that are multiples of the swizzle period keep the base's swizzle:
+    // element k sits at phys(base) + k u cols (immediate offsets)
+    constexpr bool lin = kColsLog == 3 ? (u % 32 == 0) : (u % 256 == 0);
+    const uint32_t p0 = phys<kColsLog>(base, c);
     if constexpr (vec) {
       const uint4 a = *reinterpret_cast<const uint4*>(GIN ? gm + base : s + phys<kColsLog>(base, 0));
       const uint4 b = *reinterpret_cast<const uint4*>(GIN ? gm + base + 4 : s + phys<kColsLog>(base + 4, 0));
@@ -111,7 +115,8 @@ __device__ __forceinline__ void ntt_round(uint32_t* __restrict__ s, const uint2*
       v[4 % E] = b.x; v[5 % E] = b.y; v[6 % E] = b.z; v[7 % E] = b.w;
     } else {
 #pragma unroll
-      for (int k = 0; k < E; ++k) v[k] = GIN ? gm[base + k * u] : s[phys<kColsLog>(base + k * u, c)];
+      for (int k = 0; k < E; ++k)
+        v[k] = GIN ? gm[base + k * u] : s[lin ? p0 + k * u * cols : phys<kColsLog>(base + k * u, c)];
     }
 #pragma unroll
     for (int qq = 0; qq < RB; ++qq) {
@@ -145,7 +150,7 @@ __device__ __forceinline__ void ntt_round(uint32_t* __restrict__ s, const uint2*
 #pragma unroll
       for (int k = 0; k < E; ++k) {
         if constexpr (GOUT) gm[base + k * u] = v[k];
-        else s[phys<kColsLog>(base + k * u, c)] = v[k];
+        else s[lin ? p0 + k * u * cols : phys<kColsLog>(base + k * u, c)] = v[k];
       }
     }
   }
