@@ -163,6 +163,17 @@ int psl_ctx_scan_mode(psl_ctx* ctx);
  * tcgen05.mma (M128 N64 K32, kind::i8) instructions. */
 int psl_ctx_scan_stats(psl_ctx* ctx, uint64_t* certified, uint64_t* refined, uint64_t* chains,
                        uint64_t* mma, uint64_t* umma);
+/* Certificate check (test/validation hook, not a reference interface): when
+ * on, every step the certified scan scores (n_lmt <= 1024) is also re-scored
+ * by the exact serial-chain sweep; each row's serial double is tested against
+ * the row's certified interval [lo, hi] and the intervals' own decision
+ * (argmin, value_step vs value_local) against the exact one.  Decisions are
+ * then taken from the exact sweep.  Read back with psl_ctx_cert_check_stats:
+ * counts[0..4] = steps checked, rows checked, rows outside their interval,
+ * steps the intervals decided alone, of those decided differently;
+ * maxima[0] = max |V - mid| / half-width, maxima[1] = max (hi - lo) / mid. */
+int psl_ctx_set_cert_check(psl_ctx* ctx, int on);
+int psl_ctx_cert_check_stats(psl_ctx* ctx, uint64_t counts[5], double maxima[2]);
 /* Measurement helpers: mma.sync m16n8k32 s8 instructions per second and
  * tcgen05.mma kind::i8 M128 N64 K32 instructions per second (all SMs). */
 int psl_probe_imma(psl_ctx* ctx, double* mma_per_s, char* err, size_t errlen);
@@ -207,6 +218,17 @@ int psl_verify_sequence(psl_ctx* ctx, const int8_t* seq, uint32_t length, int32_
 /* apply_flip (sequence.cpp:198-224), in place on host buffers. */
 int psl_apply_flip(psl_ctx* ctx, int8_t* seq, int32_t* table, uint32_t length, uint32_t j,
                    char* err, size_t errlen);
+/* flip_deltas (sequence.cpp:154-172): out[0] = 0, out[k] = delta_k = -2 s_j
+ * (s_{j-k} [j-k >= 0] + s_{j+k} [j+k < L]) on the sequence before the flip;
+ * out has `length` entries. */
+int psl_flip_deltas(psl_ctx* ctx, const int8_t* seq, uint32_t length, uint32_t j, int32_t* out,
+                    char* err, size_t errlen);
+/* fitness(table, PowerTable) (sequence.cpp:131-141): the serial ascending-k
+ * double sum of lut[|C_k|], k = 1..length-1, on the device (bit-identical);
+ * a non-finite sum is PSL_ERR_OVERFLOW with the reference's message
+ * (sequence.cpp:11-15).  lut_size must exceed max |C_k|. */
+int psl_fitness(psl_ctx* ctx, const int32_t* table, uint32_t length, const double* lut,
+                uint32_t lut_size, uint32_t alpha, double* fitness, char* err, size_t errlen);
 
 /* ---- run entry points -------------------------------------------------- */
 /* run_search (search.cpp:327-430).  solution_best: length bytes. */
@@ -238,6 +260,24 @@ void psl_walks_destroy(psl_walks* w);
 int psl_run_walks(psl_ctx* ctx, const psl_params* params, uint32_t n_walks,
                   const uint64_t* seeds, const int8_t* inits, psl_walk_record* records,
                   int8_t* solutions, char* err, size_t errlen);
+
+/* Many independent walks over several GPUs of one node (
+ * the reference's `bench` runs its seeds one after another, tools/main.cpp:
+ * 162-176).  Walk w (seed seeds[w], or params->seed + w) runs on device
+ * devices[d] for the contiguous block n_walks * d / n_devices <= w <
+ * n_walks * (d + 1) / n_devices; one host thread per device creates its own
+ * context and runs its block with psl_run_walks, so there is no per-step
+ * communication.  The only cross-device step is this host gather: records[w]
+ * and solutions[w] (n_walks x L, may be NULL) in global walk order, and
+ * *best_walk = the walk with the smallest key (psl_best << 32) | w (the
+ * smaller walk index wins PSL ties).  device_seconds (n_devices entries, may be
+ * NULL) receives each device's wall time for its block.  A device index may
+ * repeat (two contexts on one GPU).  Errors: the first failing device's status
+ * and message, in device order. */
+int psl_run_walks_multi(const int* devices, uint32_t n_devices, const psl_params* params,
+                        uint32_t n_walks, const uint64_t* seeds, const int8_t* inits,
+                        psl_walk_record* records, int8_t* solutions, uint32_t* best_walk,
+                        double* device_seconds, char* err, size_t errlen);
 
 #ifdef __cplusplus
 }

@@ -99,6 +99,29 @@ int solve(const Args& a) {   // main.cpp:75-105
   return kExitOk;
 }
 
+int default_device() {
+  const char* dev = std::getenv("PSLB200_DEVICE");
+  return dev ? std::atoi(dev) : 0;
+}
+
+std::vector<int> devices(const Args& a) {
+  std::string list = a.get("--devices");
+  if (list.empty()) {
+    const char* env = std::getenv("PSLB200_DEVICES");
+    if (env) list = env;
+  }
+  std::vector<int> out;
+  size_t pos = 0;
+  while (pos < list.size()) {
+    size_t end = list.find(',', pos);
+    if (end == std::string::npos) end = list.size();
+    out.push_back((int)to_u64(list.substr(pos, end - pos), "--devices"));
+    pos = end + 1;
+  }
+  if (out.empty()) out.push_back(default_device());
+  return out;
+}
+
 int bench(const Args& a) {   // main.cpp:142-181
   pslopt::SearchParams params = search_params(a);
   const std::string mode = a.get("--mode", "two-phase");
@@ -118,12 +141,16 @@ int bench(const Args& a) {   // main.cpp:142-181
   c.has_max_nse = params.stop.max_nse.has_value(); c.max_nse = params.stop.max_nse.value_or(0);
   c.has_max_seconds = params.stop.max_seconds.has_value();
   c.max_seconds = params.stop.max_seconds.value_or(0.0);
-  psl_ctx* ctx = nullptr;
+  // the seeds run as concurrent walks, split over the selected GPUs
+  // (--devices 0,1,... or PSLB200_DEVICES; default PSLB200_DEVICE or 0)
+  std::vector<int> devs = devices(a);
+  if (devs.size() > runs) devs.resize(runs);
   char err[1024] = {0};
-  if (psl_ctx_create(0, &ctx, err, sizeof err) != PSL_OK) throw pslopt::Error(err);
   std::vector<psl_walk_record> recs(runs);
-  const int rc = psl_run_walks(ctx, &c, runs, nullptr, nullptr, recs.data(), nullptr, err, sizeof err);
-  psl_ctx_destroy(ctx);
+  uint32_t best = 0;
+  std::vector<double> dev_s(devs.size());
+  const int rc = psl_run_walks_multi(devs.data(), (uint32_t)devs.size(), &c, runs, nullptr, nullptr,
+                                     recs.data(), nullptr, &best, dev_s.data(), err, sizeof err);
   if (rc == PSL_ERR_OVERFLOW) throw pslopt::OverflowError(err);
   if (rc != PSL_OK) throw pslopt::ConfigError(err);
   uint64_t total_nse = 0, psl_sum = 0;
@@ -149,6 +176,9 @@ int bench(const Args& a) {   // main.cpp:142-181
   std::printf("psl mean=%.3f min=%d max=%d evals-per-sec=%.1f aggregate-evals-per-sec=%.1f\n",
               (double)psl_sum / runs, psl_min, psl_max, (double)total_nse / total_seconds,
               (double)total_nse / wall);
+  if (devs.size() > 1)
+    std::printf("devices=%zu best seed=%llu psl=%d\n", devs.size(),
+                (unsigned long long)recs[best].seed, recs[best].psl_best);
   return kExitOk;
 }
 
@@ -158,7 +188,7 @@ int verify(const Args& a) {   // main.cpp:107-124, on the device
   const pslopt::BinarySequence seq = pslopt::io::read_sequence(path);
   psl_ctx* ctx = nullptr;
   char err[1024] = {0};
-  if (psl_ctx_create(0, &ctx, err, sizeof err) != PSL_OK) throw pslopt::Error(err);
+  if (psl_ctx_create(default_device(), &ctx, err, sizeof err) != PSL_OK) throw pslopt::Error(err);
   const uint32_t L = seq.length();
   std::vector<uint64_t> hist((size_t)L + 1);
   int32_t psl = 0;
@@ -202,8 +232,11 @@ int main(int argc, char** argv) {
   } catch (const pslopt::IoError& e) {
     std::fprintf(stderr, "error: %s\n", e.what());
     return kExitIo;
-  } catch (const std::exception& e) {
+  } catch (const pslopt::Error& e) {            // main.cpp:253-255 (engine/device errors too)
     std::fprintf(stderr, "error: %s\n", e.what());
-    return kExitIo;
+    return kExitUsage;
+  } catch (const std::exception& e) {           // main.cpp:256-258
+    std::fprintf(stderr, "error: %s\n", e.what());
+    return kExitUsage;
   }
 }

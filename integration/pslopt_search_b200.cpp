@@ -2,10 +2,12 @@
 // (proj/include/pslopt/search.hpp) implemented over the B200 engine's C ABI
 // (include/pslb200.h).
 //
-// This translation unit REPLACES the reference's src/search.cpp.  Link it with
-// the reference's own sequence.cpp / oracle.cpp / io.cpp and any reference
-// caller (the CLI, tests/acceptance.cpp, user code) and every run_search /
-// neighborhood_scan call executes on the GPU; nothing else changes.
+// This translation unit REPLACES the reference's src/search.cpp (and
+// pslopt_sequence_b200.cpp replaces src/sequence.cpp).  Link them with the
+// reference's own oracle.cpp / io.cpp and any reference caller (the CLI,
+// tests/acceptance.cpp, user code) and every run_search / neighborhood_scan /
+// SidelobeTable::build / fitness / evaluate_neighbor / flip_deltas / apply_flip
+// call executes on the GPU; nothing else changes.
 // oracle/Makefile target `dropin` builds the reference's acceptance gate this
 // way (oracle/_ref/acceptance_b200); tests/test_dropin.py runs it on a B200.
 #include <cstdlib>
@@ -13,6 +15,7 @@
 #include <vector>
 
 #include "pslb200.h"
+#include "pslb200_engine.hpp"
 #include "pslopt/errors.hpp"
 #include "pslopt/search.hpp"
 #include "pslopt/version.hpp"
@@ -21,23 +24,8 @@ namespace pslopt {
 
 namespace {
 
-psl_ctx* engine() {
-  static psl_ctx* ctx = [] {
-    psl_ctx* c = nullptr;
-    char err[512] = {0};
-    const char* dev = std::getenv("PSLB200_DEVICE");
-    if (psl_ctx_create(dev ? std::atoi(dev) : 0, &c, err, sizeof err) != PSL_OK)
-      throw Error(std::string("B200 engine unavailable: ") + err);
-    return c;
-  }();
-  return ctx;
-}
-
-[[noreturn]] void raise(int rc, const char* err) {
-  if (rc == PSL_ERR_CONFIG) throw ConfigError(err);
-  if (rc == PSL_ERR_OVERFLOW) throw OverflowError(err);
-  throw Error(err);
-}
+using b200::engine;
+using b200::raise;
 
 psl_params to_c(const SearchParams& p) {
   psl_params c{};

@@ -158,6 +158,11 @@ def ref():
         R.ref_bench_eval.argtypes = [_i8p, _i32p, C.c_uint32, C.c_uint32, _f64p, C.c_uint32,
                                      C.c_uint32, C.c_uint32, C.POINTER(C.c_double)]
         R.ref_bench_eval.restype = C.c_double
+        R.ref_walks_create.argtypes = [_u64p, C.c_uint32, C.c_uint32, C.c_uint32, _i32p, _f64p]
+        R.ref_walks_create.restype = C.c_void_p
+        R.ref_walks_destroy.argtypes = [C.c_void_p]
+        R.ref_walks_step.argtypes = [C.c_void_p, C.c_uint32, C.POINTER(C.c_double), _i32p]
+        R.ref_walks_step.restype = C.c_double
         _ref = R
     return _ref
 
@@ -195,6 +200,63 @@ def build_table(s: np.ndarray, fast: bool | None = None, threads: int = 0) -> np
     else:
         (lib().orc_build_table_fast if fast else lib().orc_build_table)(s, L, c)
     return c
+
+
+def build_table_fft(s: np.ndarray) -> np.ndarray:
+    """C_k = sum_i s_i s_{i+k} (SidelobeTable::build, sequence.cpp:46-60) as a
+    float64 FFT autocorrelation rounded to integers -- O(L log L) setup for the
+    CPU baseline's per-thread pivots.  Exact: the rounding error is < 1e-6 for
+    L <= 2^20 (checked below, with the parity invariant C_k = L - k mod 2); the
+    m20 result is pinned to the reference's table hash in tests/test_oracle.py."""
+    x = np.asarray(s, np.float64)
+    L = len(x)
+    N = 1 << (2 * L - 1).bit_length()
+    X = np.fft.rfft(x, N)
+    r = np.fft.irfft(X * np.conj(X), N)[:L]
+    c = np.rint(r)
+    if L > 1 and float(np.abs(r - c).max()) > 0.05:
+        raise RuntimeError("FFT table build lost integer precision")
+    c = c.astype(np.int32)
+    c[0] = L
+    k = np.arange(L)
+    if np.any(((c[1:] - (L - k[1:])) & 1) != 0):
+        raise RuntimeError("FFT table build broke the sidelobe parity invariant")
+    return c
+
+
+class RefWalks:
+    """The reference's step loop on all host threads, one independent walk per
+    thread (ref_shim.cpp ref_walks_*): walk w = run_search(seed_w)'s pivot,
+    table from build_table_fft (setup, untimed)."""
+
+    def __init__(self, seeds, L: int, n: int, alpha: int):
+        R = ref()
+        self.seeds = np.ascontiguousarray(seeds, np.uint64)
+        W = len(self.seeds)
+        tables = np.empty((W, L), np.int32)
+        for w, sd in enumerate(self.seeds):
+            tables[w] = build_table_fft(random_sequence(int(sd), L))
+        self.lut = power_table(L, alpha)
+        self.L, self.n, self.W = L, n, W
+        self._h = R.ref_walks_create(self.seeds, W, L, n, tables, self.lut)
+
+    def step(self, steps: int = 1):
+        """(NSE/s, seconds, per-walk pivot PSL) of `steps` steps of every walk."""
+        secs = C.c_double()
+        psl = np.zeros(self.W, np.int32)
+        rate = ref().ref_walks_step(self._h, steps, C.byref(secs), psl)
+        return rate, secs.value, psl
+
+    def close(self):
+        if self._h:
+            ref().ref_walks_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def fitness(c: np.ndarray, lut: np.ndarray) -> float:

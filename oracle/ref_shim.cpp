@@ -8,6 +8,7 @@
 // reference's naive trajectory oracle (tests/reference_search.hpp).  Used to
 // pin oracle/psl_oracle.c, to generate tests/golden/ fixtures, and as the CPU
 // baseline ("kind": "reference") in bench.py.
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdint>
@@ -247,6 +248,86 @@ double ref_bench_eval(const int8_t* seqs, const int32_t* tables, uint32_t L, uin
   for (auto& t : th) t.join();
   *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   return static_cast<double>(evals.load()) / *seconds;
+}
+
+
+// ---- CPU baseline: one independent walk per host thread (BASELINE.md's CPU
+// plan).  Walk w starts like run_search(seed_w): Rng(seed_w), the
+// pivot = random_sequence(L, rng) (search.cpp:333-334, its L spin draws); its
+// table comes from the caller (the reference's O(L^2) build is excluded from
+// the timed region, search.cpp:335 vs :342).  Each step is the body of the
+// run_search loop (search.cpp:371-392): start = rng.bounded(L), the n one-flip
+// neighbours scored by detail::eval_flip (scan_chunk, :166-175), reduce_scan's
+// first-minimum argmin (:271-292) and apply_flip of the winner (:392).  The
+// phase bookkeeping (O(L) copies at most) is left out.
+struct RefWalks {
+  uint32_t L = 0, n = 0;
+  const double* lut = nullptr;
+  std::vector<Rng> rng;
+  std::vector<std::vector<int8_t>> s;
+  std::vector<std::vector<int32_t>> c;
+  std::vector<uint64_t> evals;
+};
+
+void* ref_walks_create(const uint64_t* seeds, uint32_t walks, uint32_t L, uint32_t n,
+                       const int32_t* tables, const double* lut) {
+  auto* h = new RefWalks;
+  h->L = L; h->n = n; h->lut = lut;
+  for (uint32_t w = 0; w < walks; ++w) {
+    Rng r(seeds[w]);
+    const BinarySequence seq = random_sequence(L, r);
+    h->rng.push_back(r);
+    h->s.emplace_back(seq.data(), seq.data() + L);
+    h->c.emplace_back(tables + (size_t)w * L, tables + (size_t)(w + 1) * L);
+  }
+  h->evals.assign(walks, 0);
+  return h;
+}
+
+void ref_walks_destroy(void* handle) { delete static_cast<RefWalks*>(handle); }
+
+// Advances every walk by `steps` steps, one host thread per walk; returns the
+// aggregate one-flip evaluations per second (NSE/s) of this call.
+double ref_walks_step(void* handle, uint32_t steps, double* seconds, int32_t* psl_out) {
+  auto* h = static_cast<RefWalks*>(handle);
+  const uint32_t W = (uint32_t)h->s.size(), L = h->L, n = h->n;
+  const auto t0 = std::chrono::steady_clock::now();
+  std::vector<std::thread> th;
+  for (uint32_t w = 0; w < W; ++w) {
+    th.emplace_back([h, w, L, n, steps] {
+      int8_t* s = h->s[w].data();
+      int32_t* c = h->c[w].data();
+      for (uint32_t st = 0; st < steps; ++st) {
+        const uint32_t start = static_cast<uint32_t>(h->rng[w].bounded(L));
+        uint32_t best = 1;
+        double bv = 0.0;
+        for (uint32_t i = 1; i <= n; ++i) {
+          const NeighborEval e = detail::eval_flip(s, c, L, (start + i) % L, h->lut);
+          if (i == 1 || e.fitness < bv) { bv = e.fitness; best = i; }
+        }
+        h->evals[w] += n;
+        // apply_flip(seq, table, j) (sequence.cpp:198-224)
+        const uint32_t j = (start + best) % L;
+        const int32_t sj2 = -2 * static_cast<int32_t>(s[j]);
+        for (uint32_t k = 1; k < L; ++k) {
+          int32_t touched = 0;
+          if (j >= k) touched += s[j - k];
+          if (j + k < L) touched += s[j + k];
+          c[k] += sj2 * touched;
+        }
+        s[j] = static_cast<int8_t>(-s[j]);
+      }
+    });
+  }
+  for (auto& t : th) t.join();
+  *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  if (psl_out)
+    for (uint32_t w = 0; w < W; ++w) {
+      int32_t p = 0;
+      for (uint32_t k = 1; k < L; ++k) p = std::max(p, std::abs(h->c[w][k]));
+      psl_out[w] = p;
+    }
+  return (double)W * n * steps / *seconds;
 }
 
 }  // extern "C"

@@ -11,7 +11,7 @@ from .pslopt import (  # noqa: F401
     IoError, NeighborEval, OverflowError, ParseError, PowerTable, RunRecord, ScanResult,
     ScanTrace, SearchHooks, SearchParams, StopCondition, WalkRecord, Walks, apply_flip,
     build_table, default_alpha2, default_context, default_flip_lmt, default_n_lmt, default_params,
-    evaluate_neighbor, fitness, kVersion, merit_factor, neighborhood_scan, pow_int, psl,
-    run_search, run_walks, scan_values, validate_params, verify_sequence, SequenceReport)
+    evaluate_neighbor, fitness, flip_deltas, kVersion, merit_factor, neighborhood_scan, pow_int, psl,
+    run_search, run_walks, run_walks_multi, scan_values, validate_params, verify_sequence, SequenceReport)
 
 __version__ = kVersion

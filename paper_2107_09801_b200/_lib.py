@@ -77,6 +77,13 @@ SIGNATURES = {
     "psl_ctx_scan_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                      C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                      C.POINTER(C.c_uint64)]),
+    "psl_flip_deltas": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p,
+                                  C.c_char_p, C.c_size_t]),
+    "psl_fitness": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_void_p, C.c_uint32,
+                              C.c_uint32, C.POINTER(C.c_double), C.c_char_p, C.c_size_t]),
+    "psl_ctx_set_cert_check": (C.c_int, [C.c_void_p, C.c_int]),
+    "psl_ctx_cert_check_stats": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64),
+                                           C.POINTER(C.c_double)]),
     "psl_probe_imma": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_char_p, C.c_size_t]),
     "psl_probe_umma": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.c_char_p, C.c_size_t]),
     "psl_probe_peaks": (C.c_int, [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -116,6 +123,11 @@ SIGNATURES = {
     "psl_run_walks": (C.c_int, [C.c_void_p, C.POINTER(psl_params), C.c_uint32, C.c_void_p,
                                 C.c_void_p, C.POINTER(psl_walk_record), C.c_void_p, C.c_char_p,
                                 C.c_size_t]),
+    "psl_run_walks_multi": (C.c_int, [C.POINTER(C.c_int), C.c_uint32, C.POINTER(psl_params),
+                                      C.c_uint32, C.c_void_p, C.c_void_p,
+                                      C.POINTER(psl_walk_record), C.c_void_p,
+                                      C.POINTER(C.c_uint32), C.POINTER(C.c_double), C.c_char_p,
+                                      C.c_size_t]),
 }
 
 _lib = None

@@ -10,11 +10,13 @@
 // There is no CPU fallback: without a CUDA device every compute entry point
 // returns PSL_ERR_CUDA.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda_runtime.h>
@@ -31,6 +33,9 @@ struct psl_ctx {
   uint32_t launches = 0;
   int scan_mode = PSL_SCAN_AUTO;
   uint64_t stats[5] = {0, 0, 0, 0, 0};
+  int cert_check = 0;
+  uint64_t chk[5] = {0, 0, 0, 0, 0};
+  double chk_max[2] = {0.0, 0.0};
 };
 
 struct psl_walks {
@@ -57,6 +62,7 @@ struct psl_walks {
   double* lo_buf = nullptr;     // certified-scan per-row lower bounds (n_lmt > 1024)
   double* iv_buf = nullptr;     // certified-scan row intervals of a group
   uint64_t stats_read[5] = {0, 0, 0, 0, 0};   // scan statistics already added to ctx->stats
+  uint64_t chk_read[5] = {0, 0, 0, 0, 0};     // ... certificate-check counts
 };
 
 namespace {
@@ -123,6 +129,23 @@ int device_ready(psl_ctx* ctx, char* err, size_t errlen) {
   CK(cudaSetDevice(ctx->device));
   return PSL_OK;
 }
+
+// Stream-ordered device scratch for one C-ABI call: allocations come from the
+// device's memory pool (kept across calls, psl_ctx_create), so a call costs no
+// cudaMalloc / cudaFree round trip; freed in stream order when the call ends.
+struct Scratch {
+  cudaStream_t s;
+  std::vector<void*> p;
+  explicit Scratch(cudaStream_t st) : s(st) {}
+  template <class T>
+  cudaError_t get(T** out, size_t bytes) {
+    void* q = nullptr;
+    const cudaError_t e = cudaMallocAsync(&q, std::max<size_t>(bytes, 16), s);
+    if (e == cudaSuccess) { p.push_back(q); *out = static_cast<T*>(q); }
+    return e;
+  }
+  ~Scratch() { for (void* q : p) cudaFreeAsync(q, s); }
+};
 
 }  // namespace
 
@@ -205,13 +228,26 @@ int psl_ctx_scan_stats(psl_ctx* ctx, uint64_t* certified, uint64_t* refined, uin
   return PSL_OK;
 }
 
+int psl_ctx_set_cert_check(psl_ctx* ctx, int on) {
+  if (!ctx) return PSL_ERR_CONFIG;
+  ctx->cert_check = on ? 1 : 0;
+  return PSL_OK;
+}
+
+int psl_ctx_cert_check_stats(psl_ctx* ctx, uint64_t counts[5], double maxima[2]) {
+  if (!ctx) return PSL_ERR_CONFIG;
+  for (int i = 0; i < 5; ++i) if (counts) counts[i] = ctx->chk[i];
+  for (int i = 0; i < 2; ++i) if (maxima) maxima[i] = ctx->chk_max[i];
+  return PSL_OK;
+}
+
 int psl_probe_umma(psl_ctx* ctx, double* mma_per_s, char* err, size_t errlen) {
   int rc = device_ready(ctx, err, errlen);
   if (rc) return rc;
   int nsm = 0;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
   const int n = probe_umma(nsm, ctx->stream, mma_per_s);
-  if (n < 0) return cuda_fail(err, errlen, cudaGetLastError(), "probe_umma");
+  if (n < 0) return cuda_fail(err, errlen, take_launch_error(), "probe_umma");
   ctx->launches += (uint32_t)n;
   return PSL_OK;
 }
@@ -222,7 +258,7 @@ int psl_probe_imma(psl_ctx* ctx, double* mma_per_s, char* err, size_t errlen) {
   int nsm = 0;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
   const int n = probe_imma(nsm, ctx->stream, mma_per_s);
-  if (n < 0) return cuda_fail(err, errlen, cudaGetLastError(), "probe_imma");
+  if (n < 0) return cuda_fail(err, errlen, take_launch_error(), "probe_imma");
   ctx->launches += (uint32_t)n;
   return PSL_OK;
 }
@@ -234,7 +270,7 @@ int psl_probe_peaks(psl_ctx* ctx, double* dadd_cells_per_s, double* lds_cells_pe
   int nsm = 0;
   CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, ctx->device));
   const int n = probe_peaks(nsm, ctx->stream, dadd_cells_per_s, lds_cells_per_s, sm_mhz);
-  if (n < 0) return cuda_fail(err, errlen, cudaGetLastError(), "probe_peaks");
+  if (n < 0) return cuda_fail(err, errlen, take_launch_error(), "probe_peaks");
   ctx->launches += (uint32_t)n;
   return PSL_OK;
 }
@@ -313,17 +349,11 @@ double psl_pow_int(double base, uint32_t exp) {
 
 namespace {
 
-struct DevScan {
-  uint32_t* bits = nullptr;
-  int32_t* C = nullptr;
-  double* lut = nullptr;
-  int2* h = nullptr;
-  double* values = nullptr;
-  int32_t* psls = nullptr;
-  ~DevScan() {
-    cudaFree(bits); cudaFree(C); cudaFree(lut); cudaFree(h); cudaFree(values); cudaFree(psls);
-  }
-};
+std::vector<uint32_t> padded_bits(const int8_t* seq, uint32_t L) {
+  std::vector<uint32_t> bits = pack_bits(seq, L, kBitsPad);
+  bits.insert(bits.begin(), 0u);   // front pad: word i at bits[i + 1]
+  return bits;
+}
 
 // values[1..n], psls[1..n] of the n neighbours (start+i)%L of one pivot.
 int run_scan(psl_ctx* ctx, const int8_t* seq, const int32_t* table, uint32_t L, uint32_t start,
@@ -332,34 +362,35 @@ int run_scan(psl_ctx* ctx, const int8_t* seq, const int32_t* table, uint32_t L, 
   int rc = device_ready(ctx, err, errlen);
   if (rc) return rc;
   const uint32_t nw = (L + 31) / 32;
-  std::vector<uint32_t> bits = pack_bits(seq, L, kBitsPad);
-  bits.insert(bits.begin(), 0u);   // front pad: word i at bits[i + 1]
-  int32_t P = 0;
-  for (uint32_t k = 1; k < L; ++k) P = std::max(P, std::abs(table[k]));
-  std::vector<int2> h;
-  for (uint32_t k = 1; k < L; ++k)
-    if (std::abs(table[k]) >= P - 8) h.push_back(make_int2((int)k, table[k]));
-  DevScan d;
+  const std::vector<uint32_t> bits = padded_bits(seq, L);
   cudaStream_t s = ctx->stream;
-  CK(cudaMalloc(&d.bits, bits.size() * 4));
-  CK(cudaMalloc(&d.C, (size_t)L * 4));
-  CK(cudaMalloc(&d.lut, (size_t)lut_size * 8));
-  CK(cudaMalloc(&d.h, std::max<size_t>(h.size(), 1) * sizeof(int2)));
-  CK(cudaMalloc(&d.values, ((size_t)n + 1) * 8));
-  CK(cudaMalloc(&d.psls, ((size_t)n + 1) * 4));
-  CK(cudaMemcpyAsync(d.bits, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(d.C, table, (size_t)L * 4, cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(d.lut, lut, (size_t)lut_size * 8, cudaMemcpyHostToDevice, s));
-  if (!h.empty()) CK(cudaMemcpyAsync(d.h, h.data(), h.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+  Scratch d(s);
   ScanArgs a{};
+  double* dv = nullptr;
+  int32_t* dp = nullptr;
+  uint32_t* db = nullptr;
+  int32_t* dc = nullptr;
+  double* dl = nullptr;
+  CK(d.get(&db, bits.size() * 4));
+  CK(d.get(&dc, (size_t)L * 4));
+  CK(d.get(&dl, (size_t)lut_size * 8));
+  CK(d.get(&a.hlist, (size_t)L * sizeof(int2)));
+  CK(d.get(&a.P, 4));
+  CK(d.get(&a.hcount, 4));
+  CK(d.get(&dv, ((size_t)n + 1) * 8));
+  CK(d.get(&dp, ((size_t)n + 1) * 4));
+  CK(cudaMemcpyAsync(db, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dc, table, (size_t)L * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dl, lut, (size_t)lut_size * 8, cudaMemcpyHostToDevice, s));
   a.L = L; a.n = n; a.start = start; a.nwords = nw;
   a.nchunks = (L - 1 + kChunk - 1) / kChunk;
-  a.lut_size = lut_size; a.P = P; a.hcount = (uint32_t)h.size();
-  a.bits = d.bits; a.C = d.C; a.lut = d.lut; a.hlist = d.h; a.values = d.values; a.psls = d.psls;
-  if (launch_scan(a, s) < 0) return cuda_fail(err, errlen, cudaGetLastError(), "scan_kernel");
-  ctx->launches += 1;
-  CK(cudaMemcpyAsync(values + 1, d.values + 1, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
-  CK(cudaMemcpyAsync(psls + 1, d.psls + 1, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
+  a.lut_size = lut_size;
+  a.bits = db; a.C = dc; a.lut = dl; a.values = dv; a.psls = dp;
+  const int nl = launch_scan(a, s);
+  if (nl < 0) return cuda_fail(err, errlen, take_launch_error(), "scan_kernel");
+  ctx->launches += (uint32_t)nl;
+  CK(cudaMemcpyAsync(values + 1, dv + 1, (size_t)n * 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(psls + 1, dp + 1, (size_t)n * 4, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return PSL_OK;
 }
@@ -374,6 +405,12 @@ int psl_scan(psl_ctx* ctx, const psl_scan_job* job, char* err, size_t errlen) {
   if (job->length < kMinLength || job->start >= job->length || job->n < 1 ||
       job->n > job->length) {
     set_err(err, errlen, "psl_scan: job out of range");
+    return PSL_ERR_CONFIG;
+  }
+  // the reference's ScanJob reads PowerTable(L, alpha) (L + 1 entries,
+  // search.cpp:337-338): any |C_k +- 4| <= L is a valid index
+  if (job->lut_size < job->length + 1) {
+    set_err(err, errlen, "power table too small for sequence length");
     return PSL_ERR_CONFIG;
   }
   return run_scan(ctx, job->seq, job->table, job->length, job->start, job->n, job->lut,
@@ -449,23 +486,19 @@ int psl_build_table(psl_ctx* ctx, const int8_t* seq, uint32_t L, int32_t* table_
   rc = device_ready(ctx, err, errlen);
   if (rc) return rc;
   const uint32_t nw = (L + 31) / 32;
-  std::vector<uint32_t> bits = pack_bits(seq, L, kBitsPad);
+  const std::vector<uint32_t> bits = pack_bits(seq, L, kBitsPad);
+  cudaStream_t s = ctx->stream;
+  Scratch d(s);
   uint32_t* db = nullptr;
   int32_t* dc = nullptr;
-  cudaStream_t s = ctx->stream;
-  CK(cudaMalloc(&db, bits.size() * 4));
-  CK(cudaMalloc(&dc, (size_t)L * 4));
+  CK(d.get(&db, bits.size() * 4));
+  CK(d.get(&dc, (size_t)L * 4));
   CK(cudaMemcpyAsync(db, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice, s));
-  if (launch_table_only(db, dc, L, nw, s) < 0) {
-    cudaFree(db); cudaFree(dc);
-    return cuda_fail(err, errlen, cudaGetLastError(), "build_tables_kernel");
-  }
+  if (launch_table_only(db, dc, L, nw, s) < 0)
+    return cuda_fail(err, errlen, take_launch_error(), "build_tables_kernel");
   ctx->launches += 1;
-  cudaError_t e = cudaMemcpyAsync(table_out, dc, (size_t)L * 4, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  cudaFree(db);
-  cudaFree(dc);
-  if (e != cudaSuccess) return cuda_fail(err, errlen, e, "build_table");
+  CK(cudaMemcpyAsync(table_out, dc, (size_t)L * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
   return PSL_OK;
 }
 
@@ -494,7 +527,7 @@ int psl_verify_sequence(psl_ctx* ctx, const int8_t* seq, uint32_t L, int32_t* ps
   CK(cudaMemsetAsync(den, 0, 8, s));
   CK(cudaMemsetAsync(dh, 0, ((size_t)L + 1) * 8, s));
   if (launch_table_only(db, dc, L, nw, s) < 0 || launch_verify(dc, L, dpsl, den, dh, s) < 0)
-    return cuda_fail(err, errlen, cudaGetLastError(), "verify");
+    return cuda_fail(err, errlen, take_launch_error(), "verify");
   ctx->launches += 2;
   int32_t hpsl = 0;
   unsigned long long hen = 0;
@@ -522,25 +555,85 @@ int psl_apply_flip(psl_ctx* ctx, int8_t* seq, int32_t* table, uint32_t L, uint32
   }
   rc = device_ready(ctx, err, errlen);
   if (rc) return rc;
-  std::vector<uint32_t> bits = pack_bits(seq, L, kBitsPad);
+  const std::vector<uint32_t> bits = pack_bits(seq, L, kBitsPad);
+  cudaStream_t s = ctx->stream;
+  Scratch d(s);
   uint32_t* db = nullptr;
   int32_t* dc = nullptr;
-  cudaStream_t s = ctx->stream;
-  CK(cudaMalloc(&db, bits.size() * 4));
-  CK(cudaMalloc(&dc, (size_t)L * 4));
+  CK(d.get(&db, bits.size() * 4));
+  CK(d.get(&dc, (size_t)L * 4));
   CK(cudaMemcpyAsync(db, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(dc, table, (size_t)L * 4, cudaMemcpyHostToDevice, s));
-  if (launch_apply_flip(db, dc, L, j, s) < 0) {
-    cudaFree(db); cudaFree(dc);
-    return cuda_fail(err, errlen, cudaGetLastError(), "apply_flip_kernel");
-  }
+  if (launch_apply_flip(db, dc, L, j, s) < 0)
+    return cuda_fail(err, errlen, take_launch_error(), "apply_flip_kernel");
   ctx->launches += 2;
-  cudaError_t e = cudaMemcpyAsync(table, dc, (size_t)L * 4, cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  cudaFree(db);
-  cudaFree(dc);
-  if (e != cudaSuccess) return cuda_fail(err, errlen, e, "apply_flip");
+  CK(cudaMemcpyAsync(table, dc, (size_t)L * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
   seq[j] = (int8_t)-seq[j];
+  return PSL_OK;
+}
+
+int psl_flip_deltas(psl_ctx* ctx, const int8_t* seq, uint32_t L, uint32_t j, int32_t* out, char* err,
+                    size_t errlen) {
+  int rc = check_sequence(seq, L, err, errlen);
+  if (rc) return rc;
+  if (!out) { set_err(err, errlen, "flip_deltas: null output"); return PSL_ERR_CONFIG; }
+  if (j >= L) {   // sequence.cpp:156-160
+    set_err(err, errlen, "flip position " + std::to_string(j) + " out of range for length " +
+                             std::to_string(L));
+    return PSL_ERR_CONFIG;
+  }
+  rc = device_ready(ctx, err, errlen);
+  if (rc) return rc;
+  const std::vector<uint32_t> bits = pack_bits(seq, L, kBitsPad);
+  cudaStream_t s = ctx->stream;
+  Scratch d(s);
+  uint32_t* db = nullptr;
+  int32_t* dout = nullptr;
+  CK(d.get(&db, bits.size() * 4));
+  CK(d.get(&dout, (size_t)L * 4));
+  CK(cudaMemcpyAsync(db, bits.data(), bits.size() * 4, cudaMemcpyHostToDevice, s));
+  if (launch_flip_deltas(db, L, j, dout, s) < 0)
+    return cuda_fail(err, errlen, take_launch_error(), "flip_deltas_kernel");
+  ctx->launches += 1;
+  CK(cudaMemcpyAsync(out, dout, (size_t)L * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return PSL_OK;
+}
+
+int psl_fitness(psl_ctx* ctx, const int32_t* table, uint32_t L, const double* lut, uint32_t lut_size,
+                uint32_t alpha, double* fitness, char* err, size_t errlen) {
+  if (!table || !lut || !fitness) { set_err(err, errlen, "fitness: null pointer"); return PSL_ERR_CONFIG; }
+  if (L < 1) { set_err(err, errlen, "fitness: empty table"); return PSL_ERR_CONFIG; }
+  int32_t amax = 0;
+  for (uint32_t k = 1; k < L; ++k) amax = std::max(amax, std::abs(table[k]));
+  if ((uint64_t)lut_size <= (uint64_t)amax) {
+    set_err(err, errlen, "power table too small for the table's sidelobes");
+    return PSL_ERR_CONFIG;
+  }
+  int rc = device_ready(ctx, err, errlen);
+  if (rc) return rc;
+  cudaStream_t s = ctx->stream;
+  Scratch d(s);
+  int32_t* dc = nullptr;
+  double* dl = nullptr;
+  double* dout = nullptr;
+  CK(d.get(&dc, (size_t)L * 4));
+  CK(d.get(&dl, (size_t)lut_size * 8));
+  CK(d.get(&dout, 8));
+  CK(cudaMemcpyAsync(dc, table, (size_t)L * 4, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dl, lut, (size_t)lut_size * 8, cudaMemcpyHostToDevice, s));
+  if (launch_fitness_chain(dc, L, dl, dout, s) < 0)
+    return cuda_fail(err, errlen, take_launch_error(), "fitness_chain_kernel");
+  ctx->launches += 1;
+  double v = 0.0;
+  CK(cudaMemcpyAsync(&v, dout, 8, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (!std::isfinite(v)) {   // sequence.cpp:139
+    set_err(err, errlen, overflow_msg(false, L, alpha));
+    return PSL_ERR_OVERFLOW;
+  }
+  *fitness = v;
   return PSL_OK;
 }
 
@@ -666,7 +759,7 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
   }
 #undef AL
   if (launch_power_tables(W->lut, a.lut_n, p.alpha1, p.alpha2, s) < 0)
-    return fail(cudaGetLastError(), "power_tables_kernel");
+    return fail(take_launch_error(), "power_tables_kernel");
   ctx->launches += 1;
   for (uint32_t bi = 0; bi < nbatch; ++bi) {
     const uint32_t w0 = (uint32_t)((uint64_t)n_walks * bi / nbatch);
@@ -684,11 +777,11 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
     }
     const RunArgs ab = walk_offset(a, w0);
     const int ni = launch_init_walks(ab, cnt, W->seeds + w0, dinit, W->bad, s, w0);
-    if (ni < 0) return fail(cudaGetLastError(), "init_walks_kernel");
+    if (ni < 0) return fail(take_launch_error(), "init_walks_kernel");
     // SidelobeTable::build: exact NTT correlation for long sequences (O(L log L)),
     // bit-parallel popcount kernel (O(L^2/32)) for short ones
     const int nb = L >= 8192 ? launch_build_tables_ntt(ab, cnt, s) : launch_build_tables(ab, cnt, s);
-    if (nb < 0) return fail(cudaGetLastError(), "build_tables");
+    if (nb < 0) return fail(take_launch_error(), "build_tables");
     ctx->launches += (uint32_t)ni + (uint32_t)nb;
   }
   if (W->inits) {
@@ -713,8 +806,9 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
 int walks_launch(psl_walks* W, uint32_t steps, char* err, size_t errlen) {
   RunArgs a = W->a;
   a.step_budget = steps;
+  a.cert_check = W->ctx->cert_check;
   if (launch_run(a, W->n_walks, W->ctx->stream) < 0)
-    return cuda_fail(err, errlen, cudaGetLastError(), "run_kernel");
+    return cuda_fail(err, errlen, take_launch_error(), "run_kernel");
   W->ctx->launches += 1;
   return PSL_OK;
 }
@@ -758,7 +852,7 @@ int psl_walks_records(psl_walks* w, psl_walk_record* records, int8_t* solutions,
     // unpack on the device, one D2H of n_walks * L int8
     if (!w->sol) CK(cudaMallocAsync(&w->sol, (size_t)w->n_walks * L, s));
     if (launch_unpack(w->a.bits_best + w->a.w_front + 1, w->a.w_stride, L, w->n_walks, w->sol, s) < 0)
-      return cuda_fail(err, errlen, cudaGetLastError(), "unpack_kernel");
+      return cuda_fail(err, errlen, take_launch_error(), "unpack_kernel");
     w->ctx->launches += 1;
     CK(cudaMemcpyAsync(solutions, w->sol, (size_t)w->n_walks * L, cudaMemcpyDeviceToHost, s));
   }
@@ -786,6 +880,17 @@ int psl_walks_records(psl_walks* w, psl_walk_record* records, int8_t* solutions,
     w->ctx->stats[i] += tot[i] - w->stats_read[i];
     w->stats_read[i] = tot[i];
   }
+  uint64_t chk[5] = {0, 0, 0, 0, 0};
+  for (const WalkState& S : st) {
+    chk[0] += S.chk_steps; chk[1] += S.chk_rows; chk[2] += S.chk_viol; chk[3] += S.chk_dec;
+    chk[4] += S.chk_dec_bad;
+    w->ctx->chk_max[0] = std::max(w->ctx->chk_max[0], S.chk_tight);
+    w->ctx->chk_max[1] = std::max(w->ctx->chk_max[1], S.chk_relw);
+  }
+  for (int i = 0; i < 5; ++i) {
+    w->ctx->chk[i] += chk[i] - w->chk_read[i];
+    w->chk_read[i] = chk[i];
+  }
   return PSL_OK;
 }
 
@@ -810,6 +915,73 @@ int psl_run_walks(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, cons
   if (!rc) rc = psl_walks_records(w, records, solutions, err, errlen);
   psl_walks_destroy(w);
   return rc;
+}
+
+int psl_run_walks_multi(const int* devices, uint32_t n_devices, const psl_params* params,
+                        uint32_t n_walks, const uint64_t* seeds, const int8_t* inits,
+                        psl_walk_record* records, int8_t* solutions, uint32_t* best_walk,
+                        double* device_seconds, char* err, size_t errlen) {
+  if (!devices || n_devices < 1) { set_err(err, errlen, "at least one device is required"); return PSL_ERR_CONFIG; }
+  if (!params || !records) { set_err(err, errlen, "null params or records"); return PSL_ERR_CONFIG; }
+  psl_params p;
+  int rc = psl_validate_params(params, &p, nullptr, 0, err, errlen);
+  if (rc) return rc;
+  if (n_walks < n_devices) {
+    set_err(err, errlen, "n_walks (" + std::to_string(n_walks) + ") must be >= the number of devices (" +
+                             std::to_string(n_devices) + ")");
+    return PSL_ERR_CONFIG;
+  }
+  const uint32_t L = p.length;
+  std::vector<uint64_t> sd(n_walks);
+  for (uint32_t w = 0; w < n_walks; ++w) sd[w] = seeds ? seeds[w] : p.seed + w;
+  struct Part {
+    int rc = PSL_OK;
+    std::string err;
+    double seconds = 0.0;
+  };
+  std::vector<Part> parts(n_devices);
+  auto run_part = [&](uint32_t d) {
+    Part& pt = parts[d];
+    const uint32_t w0 = (uint32_t)((uint64_t)n_walks * d / n_devices);
+    const uint32_t w1 = (uint32_t)((uint64_t)n_walks * (d + 1) / n_devices);
+    char e[1024] = {0};
+    const auto t0 = std::chrono::steady_clock::now();
+    psl_ctx* ctx = nullptr;
+    pt.rc = psl_ctx_create(devices[d], &ctx, e, sizeof e);
+    if (pt.rc == PSL_OK) {
+      pt.rc = psl_run_walks(ctx, &p, w1 - w0, sd.data() + w0, inits ? inits + (size_t)w0 * L : nullptr,
+                            records + w0, solutions ? solutions + (size_t)w0 * L : nullptr, e, sizeof e);
+      psl_ctx_destroy(ctx);
+    }
+    pt.seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (pt.rc != PSL_OK)
+      pt.err = "device " + std::to_string(devices[d]) + ": " + e;
+  };
+  if (n_devices == 1) {
+    run_part(0);
+  } else {
+    std::vector<std::thread> th;
+    th.reserve(n_devices);
+    for (uint32_t d = 0; d < n_devices; ++d) th.emplace_back(run_part, d);
+    for (auto& t : th) t.join();
+  }
+  for (uint32_t d = 0; d < n_devices; ++d) {
+    if (device_seconds) device_seconds[d] = parts[d].seconds;
+    if (parts[d].rc != PSL_OK) {
+      set_err(err, errlen, parts[d].err);
+      return parts[d].rc;
+    }
+  }
+  if (best_walk) {
+    uint64_t best = UINT64_MAX;
+    for (uint32_t w = 0; w < n_walks; ++w) {
+      if (records[w].status != PSL_OK) continue;
+      const uint64_t key = ((uint64_t)(uint32_t)records[w].psl_best << 32) | w;
+      best = std::min(best, key);
+    }
+    *best_walk = best == UINT64_MAX ? UINT32_MAX : (uint32_t)(best & 0xffffffffu);
+  }
+  return PSL_OK;
 }
 
 // ---------------------------------------------------------------- run_search

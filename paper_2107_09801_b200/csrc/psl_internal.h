@@ -55,6 +55,16 @@ struct WalkState {
   uint64_t n_vlchain;   // exact value_local chains over the local snapshot
   uint64_t n_mma;       // tensor-core mma.sync m16n8k32 instructions (per warp) issued
   uint64_t n_umma;      // tcgen05.mma M128 N64 K32 (kind::i8) instructions issued
+  // certificate check mode (RunArgs::cert_check): every certified step is also
+  // re-scored by the exact sweep and each row's serial double is tested
+  // against the row's interval [lo, hi]
+  uint64_t chk_steps;   // certified steps checked
+  uint64_t chk_rows;    // rows checked
+  uint64_t chk_viol;    // rows whose exact serial double fell outside [lo, hi]
+  uint64_t chk_dec;     // steps the intervals decided on their own
+  uint64_t chk_dec_bad; // ... whose decision (argmin, value_local order) differs from the exact one
+  double chk_tight;     // max |V - mid| / (half-width on V's side) over checked rows (<= 1)
+  double chk_relw;      // max (hi - lo) / mid over checked rows
 };
 
 struct RunArgs {
@@ -67,6 +77,7 @@ struct RunArgs {
   int32_t record_events, record_traces;
   int32_t cert;         // certified scan allowed (decision-exact; never with traces)
   double cert_slack;    // test hook: extra relative interval width (forces the exact fallbacks)
+  int32_t cert_check;   // test hook: re-score every certified step exactly and check the intervals
   uint64_t events_cap, traces_cap;
   WalkState* st;
   int32_t* Cpiv;
@@ -96,17 +107,39 @@ struct RunArgs {
 
 struct ScanArgs {
   uint32_t L, n, start, nwords, nchunks, lut_size;
-  int32_t P;            // PSL of the given table
-  uint32_t hcount;
+  int32_t* P;           // device: PSL of the given table (scan_prep_kernel)
+  uint32_t* hcount;     // device: entries in hlist
   const uint32_t* bits;
   const int32_t* C;
   const double* lut;
-  const int2* hlist;    // all k with |C_k| >= P - 8
+  int2* hlist;          // device: all k with |C_k| >= P - 8 (any order)
   double* values;       // [n+1]
   int32_t* psls;        // [n+1]
 };
 
 size_t run_smem_bytes(bool cert);
+
+// The CUDA error a launcher saw (per host thread): launchers record it when
+// they return -1, the C ABI reports it (cudaGetLastError() would already have
+// been cleared by the launcher).
+inline cudaError_t& launch_error_slot() {
+  static thread_local cudaError_t e = cudaSuccess;
+  return e;
+}
+inline int launch_status(int launches) {
+  const cudaError_t e = cudaGetLastError();
+  launch_error_slot() = e;
+  return e == cudaSuccess ? launches : -1;
+}
+inline int launch_fail(cudaError_t e) {
+  launch_error_slot() = e == cudaSuccess ? cudaErrorUnknown : e;
+  return -1;
+}
+inline cudaError_t take_launch_error() {
+  const cudaError_t e = launch_error_slot();
+  launch_error_slot() = cudaSuccess;
+  return e == cudaSuccess ? cudaErrorUnknown : e;
+}
 
 // Launchers (return the number of kernels launched, or -1 on launch error).
 int launch_init_walks(const RunArgs& a, uint32_t n_walks, const uint64_t* d_seeds,
@@ -126,6 +159,9 @@ int launch_table_only(const uint32_t* d_bits, int32_t* d_C, uint32_t L, uint32_t
 int launch_power_tables(double* lut, uint32_t lut_n, uint32_t alpha1, uint32_t alpha2,
                         cudaStream_t s);
 int launch_apply_flip(uint32_t* d_bits, int32_t* d_C, uint32_t L, uint32_t j, cudaStream_t s);
+int launch_flip_deltas(const uint32_t* d_bits, uint32_t L, uint32_t j, int32_t* d_out, cudaStream_t s);
+int launch_fitness_chain(const int32_t* d_C, uint32_t L, const double* d_lut, double* d_out,
+                         cudaStream_t s);
 int probe_peaks(int nsm, cudaStream_t s, double* dadd_cps, double* lds_cps, double* mhz);
 int probe_imma(int nsm, cudaStream_t s, double* mma_per_s);
 int probe_umma(int nsm, cudaStream_t s, double* mma_per_s);

@@ -24,6 +24,7 @@
 //    |C_k| >= PSL(pivot) - 8 can hold a neighbour's peak, and those are
 //    collected while streaming.
 #include <algorithm>
+#include <atomic>
 #include <type_traits>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -172,6 +173,10 @@ struct Ctl {
   uint64_t mbar_f[2];        // decoupled issuer: chunk staged (builder warps arrive)
   uint64_t mbar_e[2];        // decoupled issuer: warp 15 done reading the chunk's buffers
   uint32_t tmem;             // TMEM base of this CTA's accumulators (kTmemCols columns)
+  // certificate check mode (RunArgs::cert_check)
+  int32_t chk_on, chk_dec, chk_cmp;
+  uint32_t chk_ci, chk_rows, chk_viol;
+  unsigned long long chk_tight, chk_relw;   // non-negative doubles as bit patterns (atomicMax)
 };
 
 constexpr size_t kTabBytes = 2ull * kChunk * kRecDoubles * sizeof(double);
@@ -1076,6 +1081,8 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
       ctl->cert = 0;
       ctl->need_exact = 0;
       ctl->need_vl = 0;
+      ctl->chk_on = 0; ctl->chk_rows = 0; ctl->chk_viol = 0;
+      ctl->chk_tight = 0ull; ctl->chk_relw = 0ull;
       if (kCert && a.cert && ctl->do_scan &&
           L >= kCertMinL) {
         // fixed-point scale: every |H4|, |R4| <= 2 pow(Amax, alpha) < 2^(62+q)
@@ -1534,9 +1541,15 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
               ctl->cmp = compare_local(S, ctl->cv_lo, ctl->cv_hi, false, ctl->cv);
               need = ctl->cmp == 2;
             }
-            ctl->need_exact = need;
             ctl->st.n_cert += need ? 0 : 1;
             ctl->st.n_refine += need ? 1 : 0;
+            if (a.cert_check && ngrp == 1) {
+              // check mode: remember the certified decision, re-score exactly anyway
+              ctl->chk_on = 1; ctl->chk_dec = !need; ctl->chk_ci = ctl->ci;
+              ctl->chk_cmp = need ? 2 : ctl->cmp;
+              need = 1;
+            }
+            ctl->need_exact = need;
           }
           __syncthreads();
         }
@@ -1569,6 +1582,33 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           double chain = 0.0;
           double val[kJ];
           sweep(sio, sm, active, jj, val, pm, chain);
+          if (ctl->chk_on) {
+            // every row's serial double against its certified interval (one group:
+            // row rho = offset - 1 = ibase + m, intervals still in iv_buf)
+            const double* ivm = a.iv_buf + (size_t)w * 3 * kGroup;
+            const double* ivl = ivm + kGroup;
+            const double* ivh = ivl + kGroup;
+            uint32_t rows = 0, viol = 0;
+            double tight = 0.0, relw = 0.0;
+#pragma unroll
+            for (int m = 0; m < kJ; ++m) {
+              if (!active[m]) continue;
+              const uint32_t rho = ibase + m;
+              const double md = ivm[rho], lo = ivl[rho], hi = ivh[rho], v = val[m];
+              if (!isfinite(md) || !isfinite(v)) continue;   // non-finite rows go exact by design
+              ++rows;
+              if (!(v >= lo && v <= hi)) ++viol;
+              const double half = v >= md ? hi - md : md - lo;
+              if (half > 0.0) tight = fmax(tight, fabs(v - md) / half);
+              if (md > 0.0) relw = fmax(relw, (hi - lo) / md);
+            }
+            if (rows) {
+              atomicAdd(&ctl->chk_rows, rows);
+              if (viol) atomicAdd(&ctl->chk_viol, viol);
+              atomicMax(&ctl->chk_tight, (unsigned long long)__double_as_longlong(tight));
+              atomicMax(&ctl->chk_relw, (unsigned long long)__double_as_longlong(relw));
+            }
+          }
           reduce_group(ctl, sm, hlist, active, jj, val, ibase, L);
           if (t == 0) {
             if (g2 == 0 || ctl->best_v < ctl->cv) { ctl->cv = ctl->best_v; ctl->ci = ctl->best_i; }
@@ -1675,6 +1715,19 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         ctl->cmp = compare_local(S, ctl->cv, ctl->cv, true, ctl->cv);
       }
       __syncthreads();
+    }
+
+    if (kCert && t == 0 && ctl->chk_on) {
+      WalkState& S = ctl->st;
+      S.chk_steps += 1;
+      S.chk_rows += ctl->chk_rows;
+      S.chk_viol += ctl->chk_viol;
+      if (ctl->chk_dec) {
+        S.chk_dec += 1;
+        S.chk_dec_bad += (ctl->chk_ci != ctl->ci || ctl->chk_cmp != ctl->cmp) ? 1 : 0;
+      }
+      S.chk_tight = fmax(S.chk_tight, __longlong_as_double((long long)ctl->chk_tight));
+      S.chk_relw = fmax(S.chk_relw, __longlong_as_double((long long)ctl->chk_relw));
     }
 
     // ---- reduce_scan result + Algorithm 1 control (search.cpp:379-419)
@@ -1873,9 +1926,10 @@ __global__ void __launch_bounds__(kThreads, 2) scan_kernel(ScanArgs a) {
   const uint32_t t = threadIdx.x;
   const uint32_t nw = a.nwords;
   sm.sb = a.bits;     // padded: word i at a.bits[i + 1]
-  const bool in_smem = a.hcount <= (uint32_t)kHCap;
+  const uint32_t hcount = *a.hcount;
+  const bool in_smem = hcount <= (uint32_t)kHCap;
   if (in_smem)
-    for (uint32_t e = t; e < a.hcount; e += kThreads) sm.hf[e] = a.hlist[e];
+    for (uint32_t e = t; e < hcount; e += kThreads) sm.hf[e] = a.hlist[e];
   __syncthreads();
   const uint32_t ibase = blockIdx.x * kGroup + (t >> 5) * (32 * kJ) + (t & 31) * kJ;
   bool active[kJ];
@@ -1902,10 +1956,28 @@ __global__ void __launch_bounds__(kThreads, 2) scan_kernel(ScanArgs a) {
   for (int m = 0; m < kJ; ++m) {
     if (!active[m]) continue;
     const uint32_t i = ibase + m + 1;
-    const int32_t p = in_smem ? neighbour_psl(sm.hf, a.hcount, 0, true, jj[m], a.L, sm.sb)
-                              : neighbour_psl(a.hlist, a.hcount, 0, true, jj[m], a.L, sm.sb);
+    const int32_t p = in_smem ? neighbour_psl(sm.hf, hcount, 0, true, jj[m], a.L, sm.sb)
+                              : neighbour_psl(a.hlist, hcount, 0, true, jj[m], a.L, sm.sb);
     a.values[i] = v[m];
     a.psls[i] = p;
+  }
+}
+
+// The ScanJob seam's pivot PSL (max |C_k|, sequence.cpp:84-93) and the list of
+// shifts that can carry a neighbour's peak (|C_k| >= PSL - 8), on the device.
+__global__ void scan_psl_kernel(const int32_t* C, uint32_t L, int32_t* P) {
+  int32_t pm = 0;
+  for (uint32_t k = 1 + blockIdx.x * blockDim.x + threadIdx.x; k < L; k += gridDim.x * blockDim.x)
+    pm = max(pm, abs(C[k]));
+  pm = warp_max(pm);
+  if ((threadIdx.x & 31) == 0 && pm > 0) atomicMax(P, pm);
+}
+__global__ void scan_hlist_kernel(const int32_t* C, uint32_t L, const int32_t* P, int2* h,
+                                  uint32_t* count) {
+  const int32_t thr = *P - 8;
+  for (uint32_t k = 1 + blockIdx.x * blockDim.x + threadIdx.x; k < L; k += gridDim.x * blockDim.x) {
+    const int32_t c = C[k];
+    if (abs(c) >= thr) h[atomicAdd(count, 1u)] = make_int2((int)k, c);
   }
 }
 
@@ -1921,6 +1993,37 @@ __global__ void apply_flip_kernel(uint32_t* bits, int32_t* C, uint32_t L, uint32
   }
 }
 __global__ void flip_bit_kernel(uint32_t* bits, uint32_t j) { bits[j >> 5] ^= 1u << (j & 31); }
+
+// flip_deltas (sequence.cpp:154-172): out[0] = 0, out[k] = -2 s_j (s_{j-k} [k <= j]
+// + s_{j+k} [j + k < L]) on the sequence before the flip; one shift per thread.
+__global__ void flip_deltas_kernel(const uint32_t* bits, uint32_t L, uint32_t j, int32_t* out) {
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  auto sv = [&](uint32_t x) { return 1 - 2 * (int)((bits[x >> 5] >> (x & 31)) & 1u); };
+  if (k >= L) return;
+  if (k == 0) { out[0] = 0; return; }
+  int acc = 0;
+  if (k <= j) acc += sv(j - k);
+  if (j + k < L) acc += sv(j + k);
+  out[k] = -2 * sv(j) * acc;
+}
+
+// fitness(table, PowerTable) (sequence.cpp:131-141): the reference's serial
+// ascending-k double chain, one thread (the order is the result); C_k and the
+// table entries are loaded 8 shifts ahead of the dependent adds.
+__global__ void fitness_chain_kernel(const int32_t* C, uint32_t L, const double* lut, double* out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double sum = 0.0;
+  uint32_t k = 1;
+  for (; k + 8 <= L; k += 8) {
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = __ldg(lut + abs(__ldg(C + k + i)));
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sum = __dadd_rn(sum, v[i]);
+  }
+  for (; k < L; ++k) sum = __dadd_rn(sum, __ldg(lut + abs(__ldg(C + k))));
+  *out = sum;
+}
 
 // PowerTable(L, alpha) for both phases (sequence.hpp:72-84): lut[a] = pow_int(a, alpha)
 __global__ void power_tables_kernel(double* lut, uint32_t n, uint32_t alpha1, uint32_t alpha2) {
@@ -1957,7 +2060,7 @@ int launch_init_walks(const RunArgs& a, uint32_t n_walks, const uint64_t* d_seed
   const bool jump = !d_inits && a.L > kSpinChunk;
   if (jump) rng_jump_kernel<<<1, 256, 0, s>>>();
   init_walks_kernel<<<n_walks, 256, 0, s>>>(a, d_seeds, d_inits, d_bad, walk0);
-  return cudaGetLastError() == cudaSuccess ? (jump ? 2 : 1) : -1;
+  return launch_status(jump ? 2 : 1);
 }
 
 int launch_build_tables(const RunArgs& a, uint32_t n_walks, cudaStream_t s) {
@@ -1965,7 +2068,7 @@ int launch_build_tables(const RunArgs& a, uint32_t n_walks, cudaStream_t s) {
   dim3 grid((a.L + per_block - 1) / per_block, n_walks);
   build_tables_kernel<<<grid, 256, 0, s>>>(a.bits_piv + a.w_front + 1, a.w_stride, a.Cpiv, a.Cloc,
                                            a.c_stride, a.L, a.st);
-  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+  return launch_status(1);
 }
 
 int launch_table_only(const uint32_t* d_bits, int32_t* d_C, uint32_t L, uint32_t nwords,
@@ -1973,48 +2076,70 @@ int launch_table_only(const uint32_t* d_bits, int32_t* d_C, uint32_t L, uint32_t
   const uint32_t per_block = 8 * 32 * kTabR;
   dim3 grid((L + per_block - 1) / per_block, 1);
   build_tables_kernel<<<grid, 256, 0, s>>>(d_bits, nwords + kBitsPad, d_C, nullptr, L, L, nullptr);
-  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+  return launch_status(1);
 }
 
+// The dynamic shared-memory opt-in is a per-device function attribute: set it
+// once per device (a context may live on any GPU; several host threads may make
+// their first launch together).
+constexpr int kMaxDevices = 64;
+static bool smem_opt_in(const void* fn, size_t bytes, std::atomic<uint32_t> (&done)[kMaxDevices]) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return false;
+  if (done[dev].load(std::memory_order_acquire) == bytes) return true;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) { launch_fail(e); return false; }
+  done[dev].store((uint32_t)bytes, std::memory_order_release);
+  return true;
+}
+static std::atomic<uint32_t> g_attr_run_cert[kMaxDevices], g_attr_run_exact[kMaxDevices], g_attr_scan[kMaxDevices];
+
 int launch_run(const RunArgs& a, uint32_t n_walks, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(run_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)run_smem_bytes(true)) != cudaSuccess ||
-        cudaFuncSetAttribute(run_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)run_smem_bytes(false)) != cudaSuccess)
-      return -1;
-    attr = true;
+  if (a.cert) {
+    if (!smem_opt_in((const void*)run_kernel<true>, run_smem_bytes(true), g_attr_run_cert)) return -1;
+    run_kernel<true><<<n_walks, 2 * kThreads, run_smem_bytes(true), s>>>(a);
+  } else {
+    if (!smem_opt_in((const void*)run_kernel<false>, run_smem_bytes(false), g_attr_run_exact)) return -1;
+    run_kernel<false><<<n_walks, kThreads, run_smem_bytes(false), s>>>(a);
   }
-  if (a.cert) run_kernel<true><<<n_walks, 2 * kThreads, run_smem_bytes(true), s>>>(a);
-  else run_kernel<false><<<n_walks, kThreads, run_smem_bytes(false), s>>>(a);
-  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+  return launch_status(1);
 }
 
 int launch_scan(const ScanArgs& a, cudaStream_t s) {
   const size_t smem = run_smem_bytes(false);
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(scan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)run_smem_bytes(false)) != cudaSuccess)
-      return -1;
-    attr = true;
-  }
+  if (!smem_opt_in((const void*)scan_kernel, smem, g_attr_scan)) return -1;
+  const uint32_t pg = std::min<uint32_t>((a.L + 255) / 256, 1184);
+  cudaError_t e = cudaMemsetAsync(a.P, 0, 4, s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(a.hcount, 0, 4, s);
+  if (e != cudaSuccess) return launch_fail(e);
+  scan_psl_kernel<<<pg, 256, 0, s>>>(a.C, a.L, a.P);
+  scan_hlist_kernel<<<pg, 256, 0, s>>>(a.C, a.L, a.P, a.hlist, a.hcount);
   const uint32_t groups = (a.n + kGroup - 1) / kGroup;
   scan_kernel<<<groups, kThreads, smem, s>>>(a);
-  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+  return launch_status(3);
 }
 
 int launch_power_tables(double* lut, uint32_t lut_n, uint32_t alpha1, uint32_t alpha2,
                         cudaStream_t s) {
   power_tables_kernel<<<(lut_n + 255) / 256, 256, 0, s>>>(lut, lut_n, alpha1, alpha2);
-  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+  return launch_status(1);
 }
 
 int launch_apply_flip(uint32_t* d_bits, int32_t* d_C, uint32_t L, uint32_t j, cudaStream_t s) {
   apply_flip_kernel<<<(L + 255) / 256, 256, 0, s>>>(d_bits, d_C, L, j);
   flip_bit_kernel<<<1, 1, 0, s>>>(d_bits, j);
-  return cudaGetLastError() == cudaSuccess ? 2 : -1;
+  return launch_status(2);
+}
+
+int launch_flip_deltas(const uint32_t* d_bits, uint32_t L, uint32_t j, int32_t* d_out, cudaStream_t s) {
+  flip_deltas_kernel<<<(L + 255) / 256, 256, 0, s>>>(d_bits, L, j, d_out);
+  return launch_status(1);
+}
+
+int launch_fitness_chain(const int32_t* d_C, uint32_t L, const double* d_lut, double* d_out,
+                         cudaStream_t s) {
+  fitness_chain_kernel<<<1, 32, 0, s>>>(d_C, L, d_lut, d_out);
+  return launch_status(1);
 }
 
 }  // namespace pslb
@@ -2084,9 +2209,12 @@ __global__ void __launch_bounds__(256) probe_imma_kernel(int reps, int* out) {
 
 int probe_umma(int nsm, cudaStream_t s, double* mma_per_s) {
   int* out = nullptr;
-  if (cudaMalloc(&out, 64) != cudaSuccess) return -1;
-  if (cudaFuncSetAttribute(probe_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384) != cudaSuccess)
-    return -1;
+  cudaError_t e = cudaMalloc(&out, 64);
+  if (e != cudaSuccess) return launch_fail(e);
+  if ((e = cudaFuncSetAttribute(probe_umma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 16384)) != cudaSuccess) {
+    cudaFree(out);
+    return launch_fail(e);
+  }
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
@@ -2102,12 +2230,12 @@ int probe_umma(int nsm, cudaStream_t s, double* mma_per_s) {
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   cudaFree(out);
-  return cudaGetLastError() == cudaSuccess ? 2 : -1;
+  return launch_status(2);
 }
 
 int probe_imma(int nsm, cudaStream_t s, double* mma_per_s) {
   int* out = nullptr;
-  if (cudaMalloc(&out, 64) != cudaSuccess) return -1;
+  if (const cudaError_t e = cudaMalloc(&out, 64); e != cudaSuccess) return launch_fail(e);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
@@ -2123,14 +2251,14 @@ int probe_imma(int nsm, cudaStream_t s, double* mma_per_s) {
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   cudaFree(out);
-  return cudaGetLastError() == cudaSuccess ? 2 : -1;
+  return launch_status(2);
 }
 
 int probe_peaks(int nsm, cudaStream_t s, double* dadd_cps, double* lds_cps, double* mhz) {
   double* out = nullptr;
   long long* cyc = nullptr;
-  if (cudaMalloc(&out, sizeof(double) * nsm * 1024) != cudaSuccess) return -1;
-  if (cudaMalloc(&cyc, sizeof(long long) * nsm) != cudaSuccess) { cudaFree(out); return -1; }
+  if (const cudaError_t e = cudaMalloc(&out, sizeof(double) * nsm * 1024); e != cudaSuccess) return launch_fail(e);
+  if (const cudaError_t e = cudaMalloc(&cyc, sizeof(long long) * nsm); e != cudaSuccess) { cudaFree(out); return launch_fail(e); }
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
@@ -2157,7 +2285,7 @@ int probe_peaks(int nsm, cudaStream_t s, double* dadd_cps, double* lds_cps, doub
   cudaEventDestroy(b);
   cudaFree(out);
   cudaFree(cyc);
-  return cudaGetLastError() == cudaSuccess ? 4 : -1;
+  return launch_status(4);
 }
 }  // namespace pslb
 
@@ -2175,7 +2303,7 @@ __global__ void unpack_kernel(const uint32_t* bits, size_t w_stride, uint32_t L,
 int launch_unpack(const uint32_t* bits, size_t w_stride, uint32_t L, uint32_t n_walks, int8_t* out,
                   cudaStream_t s) {
   unpack_kernel<<<dim3(std::min<uint32_t>((L + 255) / 256, 512), n_walks), 256, 0, s>>>(bits, w_stride, L, out);
-  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+  return launch_status(1);
 }
 }  // namespace pslb
 
@@ -2206,6 +2334,6 @@ __global__ void verify_kernel(const int32_t* C, uint32_t L, int32_t* psl, unsign
 int launch_verify(const int32_t* C, uint32_t L, int32_t* psl, unsigned long long* energy,
                   unsigned long long* hist, cudaStream_t s) {
   verify_kernel<<<std::min<uint32_t>((L + 255) / 256, 1184), 256, 0, s>>>(C, L, psl, energy, hist);
-  return cudaGetLastError() == cudaSuccess ? 1 : -1;
+  return launch_status(1);
 }
 }  // namespace pslb

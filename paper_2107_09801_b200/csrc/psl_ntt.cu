@@ -421,10 +421,15 @@ int launch_build_tables_ntt(const RunArgs& a, uint32_t n_walks, cudaStream_t s) 
   while ((1u << logN) < 2 * L) ++logN;
   const uint32_t N = 1u << logN;
   const uint32_t logR = logN / 2, R = 1u << logR, C = N >> logR;   // R <= C <= 2R
-  if (R > (uint32_t)kMaxRows || C > (uint32_t)kMaxRowLen || C < (uint32_t)kCols) return -1;
+  if (R > (uint32_t)kMaxRows || C > (uint32_t)kMaxRowLen || C < (uint32_t)kCols)
+    return launch_fail(cudaErrorInvalidValue);
   uint32_t *x = nullptr, *tw = nullptr;
-  if (cudaMallocAsync(&x, (size_t)n_walks * N * 4, s) != cudaSuccess) return -1;
-  if (cudaMallocAsync(&tw, (size_t)(N + 4 * R + 4 * C) * 4, s) != cudaSuccess) return -1;
+  cudaError_t e = cudaMallocAsync(&x, (size_t)n_walks * N * 4, s);
+  if (e != cudaSuccess) return launch_fail(e);
+  if ((e = cudaMallocAsync(&tw, (size_t)(N + 4 * R + 4 * C) * 4, s)) != cudaSuccess) {
+    cudaFreeAsync(x, s);
+    return launch_fail(e);
+  }
   uint32_t* twi = tw + N / 2;
   uint2* tabR = reinterpret_cast<uint2*>(tw + N);
   uint2 *tabRi = tabR + R, *tabC = tabRi + R, *tabCi = tabC + C;
@@ -444,30 +449,30 @@ int launch_build_tables_ntt(const RunArgs& a, uint32_t n_walks, cudaStream_t s) 
 #define COL_FWD(LR) case LR: ntt_col_fwd_kernel<LR><<<gcol, kNttThreads, 0, s>>>(bits, a.w_stride, L, R, C, tw, tabR, x); break;
     COL_FWD(7) COL_FWD(8) COL_FWD(9) COL_FWD(10)
 #undef COL_FWD
-    default: return -1;
+    default: cudaFreeAsync(x, s); cudaFreeAsync(tw, s); return launch_fail(cudaErrorInvalidValue);
   }
   const uint32_t logC = logN - logR;
   switch (logC) {
 #define ROW(LC, F, T) case LC: ntt_row_kernel<F, LC><<<grow, kNttThreads, 0, s>>>(x, R, C, T); break;
     ROW(7, true, tabC) ROW(8, true, tabC) ROW(9, true, tabC) ROW(10, true, tabC) ROW(11, true, tabC)
-    default: return -1;
+    default: cudaFreeAsync(x, s); cudaFreeAsync(tw, s); return launch_fail(cudaErrorInvalidValue);
   }
   ntt_pointwise_kernel<<<dim3(R, n_walks), 256, 0, s>>>(x, logN, logR, L, tw);
   switch (logC) {
     ROW(7, false, tabCi) ROW(8, false, tabCi) ROW(9, false, tabCi) ROW(10, false, tabCi) ROW(11, false, tabCi)
 #undef ROW
-    default: return -1;
+    default: cudaFreeAsync(x, s); cudaFreeAsync(tw, s); return launch_fail(cudaErrorInvalidValue);
   }
   switch (logR) {
 #define COL_INV(LR) case LR: ntt_col_inv_kernel<LR><<<gcol, kNttThreads, 0, s>>>(x, R, C, twi, tabRi, ninv_m, L, a.Cpiv, a.Cloc, a.c_stride, a.st); break;
     COL_INV(7) COL_INV(8) COL_INV(9) COL_INV(10)
 #undef COL_INV
-    default: return -1;
+    default: cudaFreeAsync(x, s); cudaFreeAsync(tw, s); return launch_fail(cudaErrorInvalidValue);
   }
   launches += 11;
   cudaFreeAsync(x, s);
   cudaFreeAsync(tw, s);
-  return cudaGetLastError() == cudaSuccess ? launches : -1;
+  return launch_status(launches);
 }
 
 }  // namespace pslb

@@ -110,6 +110,18 @@ class Context:
         return {"certified": a.value, "refined": b.value, "chains": c.value, "mma": d.value,
                 "umma": e.value}
 
+    def set_cert_check(self, on: bool) -> None:
+        """Certificate check (validation hook): re-score every certified step with
+        the exact sweep and test each row's serial double against its interval."""
+        B.lib().psl_ctx_set_cert_check(self._h, 1 if on else 0)
+
+    def cert_check_stats(self) -> dict:
+        cnt = (C.c_uint64 * 5)()
+        mx = (C.c_double * 2)()
+        B.lib().psl_ctx_cert_check_stats(self._h, cnt, mx)
+        return {"steps": cnt[0], "rows": cnt[1], "violations": cnt[2], "decided": cnt[3],
+                "decided_wrong": cnt[4], "tightness": mx[0], "rel_width": mx[1]}
+
     def probe_umma(self) -> float:
         """tcgen05.mma kind::i8 M128 N64 K32 instructions per second (all SMs)."""
         v = C.c_double()
@@ -378,19 +390,33 @@ def merit_factor(table) -> float:                    # sequence.cpp:143-152
     return (float(L) * float(L)) / (2.0 * float(energy))
 
 
-def fitness(table, pow_or_alpha) -> float:           # sequence.cpp:117-141
-    t = np.asarray(table)
-    lut = pow_or_alpha.lut if isinstance(pow_or_alpha, PowerTable) else \
-        PowerTable(len(t), int(pow_or_alpha)).lut
-    # serial ascending-k RN sum: cumsum is a left-to-right accumulation
-    terms = lut[np.abs(t[1:]).astype(np.int64)]
-    total = float(np.cumsum(terms)[-1]) if len(terms) else 0.0
-    if not np.isfinite(total):
-        alpha = pow_or_alpha.alpha if isinstance(pow_or_alpha, PowerTable) else pow_or_alpha
-        raise OverflowError(f"fitness sum is not finite at length {len(t)} with exponent {alpha}; "
-                            "lower the exponent (alpha2, then alpha1) until |C_k|^alpha sums "
-                            "stay inside double range")
-    return total
+def fitness(table, pow_or_alpha, ctx: Context | None = None) -> float:   # sequence.cpp:117-141
+    """The serial ascending-k double sum of |C_k|^alpha, on the device
+    (psl_fitness); OverflowError when it leaves the finite range."""
+    t = np.ascontiguousarray(table, np.int32)
+    lut, alpha = _lut_for(len(t), pow_or_alpha)
+    lut = np.ascontiguousarray(lut, np.float64)
+    ctx = ctx or default_context()
+    v = C.c_double()
+    err = _err()
+    rc = B.lib().psl_fitness(ctx.handle, t.ctypes.data, len(t), lut.ctypes.data, len(lut), alpha,
+                             C.byref(v), err, len(err))
+    if rc:
+        _raise(rc, err)
+    return v.value
+
+
+def flip_deltas(seq, j: int, ctx: Context | None = None) -> np.ndarray:   # sequence.cpp:154-172
+    """delta_k of flipping position j (out[0] = 0), on the device."""
+    s = _seq(seq)
+    out = np.zeros(len(s), np.int32)
+    ctx = ctx or default_context()
+    err = _err()
+    rc = B.lib().psl_flip_deltas(ctx.handle, s.ctypes.data, len(s), j, out.ctypes.data, err,
+                                 len(err))
+    if rc:
+        _raise(rc, err)
+    return out
 
 
 @dataclass
@@ -542,6 +568,29 @@ class WalkRecord:
     solution_best: Optional[np.ndarray] = None
 
 
+def _walk_inputs(p: SearchParams, n_walks: int, seeds, inits):
+    """seeds / warm starts for n_walks walks, checked before the C ABI reads
+    8 n_walks seed bytes and n_walks x L start bytes (one (L,) start is given
+    to every walk)."""
+    if n_walks < 1:
+        raise ConfigError("n_walks must be >= 1")
+    seeds_arr = None
+    if seeds is not None:
+        seeds_arr = np.ascontiguousarray(seeds, np.uint64).reshape(-1)
+        if seeds_arr.size != n_walks:
+            raise ConfigError(f"{seeds_arr.size} seeds given for {n_walks} walks")
+    inits_arr = None
+    if inits is not None:
+        inits_arr = np.asarray(inits)
+        if inits_arr.shape == (p.length,):
+            inits_arr = np.broadcast_to(inits_arr, (n_walks, p.length))
+        if inits_arr.shape != (n_walks, p.length):
+            raise ConfigError(f"warm starts have shape {tuple(np.shape(inits))}, expected "
+                              f"({n_walks}, {p.length}) or ({p.length},)")
+        inits_arr = np.ascontiguousarray(inits_arr, np.int8)
+    return seeds_arr, inits_arr
+
+
 class Walks:
     """n independent walks (one CTA each) advanced on the device in lock-step
     batches of steps; walk w uses seed params.seed + w unless seeds is given."""
@@ -551,10 +600,10 @@ class Walks:
         p = validate_params(params)
         self.params = p
         self.n_walks = n_walks
+        self._h = C.c_void_p()
+        seeds_arr, inits_arr = _walk_inputs(p, n_walks, seeds, inits)
         self.ctx = ctx or default_context()
         c, keep = _to_c(p)
-        seeds_arr = None if seeds is None else np.ascontiguousarray(seeds, np.uint64)
-        inits_arr = None if inits is None else np.ascontiguousarray(inits, np.int8)
         self._h = C.c_void_p()
         err = _err()
         rc = B.lib().psl_walks_create(self.ctx.handle, C.byref(c), n_walks,
@@ -619,10 +668,9 @@ def run_walks(params: SearchParams, n_walks: int, seeds=None, inits=None,
     With a pinned `out` buffer each walk's kernel writes its best sequence
     straight into it when the walk stops (the D2H overlaps later walks)."""
     p = validate_params(params)
+    seeds_arr, inits_arr = _walk_inputs(p, n_walks, seeds, inits)
     ctx = ctx or default_context()
     c, keep = _to_c(p)
-    seeds_arr = None if seeds is None else np.ascontiguousarray(seeds, np.uint64)
-    inits_arr = None if inits is None else np.ascontiguousarray(inits, np.int8)
     recs = (B.psl_walk_record * n_walks)()
     sol = None
     if solutions:
@@ -643,3 +691,32 @@ def run_walks(params: SearchParams, n_walks: int, seeds=None, inits=None,
     return [WalkRecord(r.seed, r.nse, r.elapsed_seconds, r.psl_best, r.status, r.merit_factor,
                        r.energy, r.switches, r.steps, None if sol is None else sol[i])
             for i, r in enumerate(recs)]
+
+
+def run_walks_multi(params: SearchParams, n_walks: int, devices: Sequence[int], seeds=None,
+                    inits=None, solutions: bool = True):
+    """psl_run_walks_multi: walks split into contiguous blocks over `devices`
+    (one host thread + context per device, no per-step communication), records
+    gathered on the host in global walk order.  Returns (records, best_walk,
+    per-device seconds); best_walk minimises (psl_best, walk index)."""
+    p = validate_params(params)
+    seeds_arr, inits_arr = _walk_inputs(p, n_walks, seeds, inits)
+    devs = (C.c_int * len(devices))(*devices)
+    c, keep = _to_c(p)
+    recs = (B.psl_walk_record * n_walks)()
+    sol = np.zeros((n_walks, p.length), np.int8) if solutions else None
+    best = C.c_uint32()
+    secs = (C.c_double * len(devices))()
+    err = _err()
+    rc = B.lib().psl_run_walks_multi(devs, len(devices), C.byref(c), n_walks,
+                                     seeds_arr.ctypes.data if seeds_arr is not None else None,
+                                     inits_arr.ctypes.data if inits_arr is not None else None,
+                                     recs, sol.ctypes.data if sol is not None else None,
+                                     C.byref(best), secs, err, len(err))
+    del keep
+    if rc:
+        _raise(rc, err)
+    out = [WalkRecord(r.seed, r.nse, r.elapsed_seconds, r.psl_best, r.status, r.merit_factor,
+                      r.energy, r.switches, r.steps, None if sol is None else sol[i])
+           for i, r in enumerate(recs)]
+    return out, best.value, list(secs)

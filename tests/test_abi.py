@@ -111,15 +111,13 @@ def test_pow_int_matches_reference_kats(golden):
     assert all(big[a] == P.pow_int(float(a), 10) for a in range(0, 5001, 37))
 
 
-def test_host_fitness_psl_mf(golden):
+def test_host_psl_mf_and_device_only_fitness(golden):
     from oracle import oracle_py as O
     rng = np.random.default_rng(4)
     for _ in range(10):
         L = int(rng.integers(2, 300))
         s = rng.choice(np.array([-1, 1], np.int8), L)
         c = O.build_table(s)
-        for alpha in (1, 2, 4, 13):
-            assert P.fitness(c, alpha) == O.fitness(c, O.power_table(L, alpha))
         assert P.psl(c) == O.psl(c)
         assert P.merit_factor(c) == O.lib().orc_merit_factor(c, L)
 
@@ -159,3 +157,29 @@ def test_public_entry_points_fail_loudly_without_gpu():
         P.Walks(p, 2)
     with pytest.raises(P.DeviceError):
         P.run_search(p)
+    # fitness() / flip_deltas() run on the device (psl_fitness, psl_flip_deltas)
+    c = np.zeros(L, np.int32)
+    with pytest.raises(P.DeviceError):
+        P.fitness(c, 4)
+    with pytest.raises(P.DeviceError):
+        P.flip_deltas(np.ones(L, np.int8), 0)
+    with pytest.raises(P.DeviceError):
+        P.run_walks_multi(p, 2, devices=[0])
+
+
+def test_walk_inputs_are_size_checked_before_the_abi():
+    """psl_walks_create / psl_run_walks read 8 n_walks seed bytes and
+    n_walks x L start bytes: wrong sizes must raise ConfigError on the host
+    (before any device or C-ABI call), one (L,) start is given to every walk."""
+    p = _ok()
+    with pytest.raises(P.ConfigError, match="seeds"):
+        P.Walks(p, 4, seeds=[1, 2, 3])
+    with pytest.raises(P.ConfigError, match="warm starts"):
+        P.run_walks(p, 4, inits=np.ones((3, 64), np.int8))
+    with pytest.raises(P.ConfigError, match="warm starts"):
+        P.Walks(p, 2, inits=np.ones(63, np.int8))
+    with pytest.raises(P.ConfigError, match="n_walks"):
+        P.run_walks(p, 0)
+    from paper_2107_09801_b200.pslopt import _walk_inputs
+    s, i = _walk_inputs(p, 3, [5, 6, 7], np.ones(64, np.int8))
+    assert s.tolist() == [5, 6, 7] and i.shape == (3, 64) and i.flags.c_contiguous

@@ -69,3 +69,38 @@ def test_pack_roundtrip_and_keys():
     assert D.pack_key(5, 9) < D.pack_key(5, 10) < D.pack_key(6, 0)
     key, idx = D.local_best([4, 3, 3], [10, 12, 11])
     assert (key >> 32, key & 0xffffffff, idx) == (3, 11, 2)
+
+
+def _bench(args, env=None, timeout=300):
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    e.update(env or {})
+    return subprocess.run([sys.executable, os.path.join(root, "bench.py")] + args,
+                          capture_output=True, text=True, timeout=timeout, env=e, cwd=root)
+
+
+def test_bench_gpus_n_launches_n_ranks():
+    """bench.py --gpus 2 started directly re-launches itself under
+    torch.distributed.run with 2 processes; the reference arm runs on rank 0
+    only and prints exactly one JSON line (the other rank exits 0)."""
+    import json
+    from oracle import oracle_py as O
+    if not O.ref_available():
+        pytest.skip("oracle/_ref not built")
+    p = _bench(["--impl", "reference", "--gpus", "2", "--length", "4095", "--steps", "2",
+                "--warmup", "1"])
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    line = json.loads(lines[0])
+    assert line["impl"] == "reference" and line["n_gpus"] == 2 and line["value"] > 0
+    assert line["cpu_baseline"]["cores"] == line["config"]["host_threads"]
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_bench_rejects_world_mismatch():
+    p = _bench(["--impl", "reference", "--gpus", "1", "--length", "64"],
+               env={"WORLD_SIZE": "2", "RANK": "1", "LOCAL_RANK": "1"})
+    assert p.returncode == 2 and "world size 2 != --gpus 1" in p.stderr

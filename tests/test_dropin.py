@@ -1,9 +1,21 @@
 """Drop-in proof: the reference's own release gate (proj/tests/acceptance.cpp,
 criteria C1-C9) compiled unmodified and linked against the B200 engine through
-integration/pslopt_search_b200.cpp, which replaces the reference's
-src/search.cpp (run_search, neighborhood_scan, ... over the C ABI).
+integration/pslopt_search_b200.cpp and integration/pslopt_sequence_b200.cpp,
+which replace the reference's src/search.cpp and src/sequence.cpp.
 Built by `make -C oracle dropin` where /root/reference exists; the binary
-travels with the repo snapshot to the GPU box."""
+travels with the repo snapshot to the GPU box.
+
+What each criterion exercises on the GPU (acceptance.cpp line numbers):
+  C1 (:75-99)   SidelobeTable::build + evaluate_neighbor on the engine, checked
+                against the reference's CPU oracle::brute_fitness (oracle.cpp)
+  C3 (:150-169) build + fitness (serial device chain) + merit_factor
+  C4, C5, C6    run_search (the device-resident walk)
+  C8 (:283-382) build + apply_flip on the engine, run_search accounting
+  C2 (:102-148) and C9 (:397-) call only the reference's own oracle.cpp / io.cpp
+                (exhaustive search, text round trips): CPU reference code that
+                stays in the link; they show the relinked library is complete,
+                not that the engine is right.
+"""
 import os
 import subprocess
 
@@ -21,9 +33,9 @@ def run(crit, timeout):
     return p.returncode, p.stdout + p.stderr
 
 
-# C1 incremental==brute, C2 exhaustive optima, C3 MF identity, C6 records
-# identical across worker counts (L=4095, 1e6 NSE), C8 invariant suite, C9 format
-# round trips -- all through the GPU run_search.
+# C1 incremental==brute, C2 exhaustive optima (CPU oracle.cpp), C3 MF identity,
+# C6 records identical across worker counts (L=4095, 1e6 NSE), C8 invariant
+# suite, C9 format round trips (CPU io.cpp) -- see the module docstring.
 @pytest.mark.parametrize("crit", [1, 2, 3, 6, 8, 9])
 def test_acceptance_criterion(crit):
     rc, out = run(crit, 900)
@@ -116,3 +128,20 @@ def test_cli_exit_codes(tmp_path):
     r = subprocess.run([CLI, "solve", "-L", "16", "--max-nse", "10", "--init",
                         str(tmp_path / "missing.txt")], capture_output=True, text=True)
     assert r.returncode == 3
+
+
+@pytest.mark.skipif(not os.path.exists(CLI), reason="pslopt_b200 not built")
+def test_cli_bench_over_two_contexts_matches_one():
+    # the bench seeds split over two device contexts (psl_run_walks_multi, one
+    # host thread each; both on GPU 0 here): the same per-seed records
+    one = subprocess.run([CLI, "bench", "-L", "1023", "--runs", "10", "--max-nse", "2000000"],
+                         capture_output=True, text=True, timeout=600)
+    two = subprocess.run([CLI, "bench", "-L", "1023", "--runs", "10", "--max-nse", "2000000",
+                          "--devices", "0,0"], capture_output=True, text=True, timeout=600)
+    assert one.returncode == 0 and two.returncode == 0, one.stderr + two.stderr
+
+    def runs(out):
+        return [" ".join(w for w in ln.split() if not w.startswith("elapsed="))
+                for ln in out.splitlines() if ln.startswith("run seed=")]
+    assert runs(one.stdout) == runs(two.stdout) and len(runs(one.stdout)) == 10
+    assert "devices=2 best seed=" in two.stdout

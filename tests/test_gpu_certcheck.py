@@ -1,0 +1,69 @@
+"""Row-by-row proof that the certified scan's intervals hold the reference's
+serial doubles at the BASELINE lengths, in both alpha regimes.
+
+With the certificate check on (psl_ctx_set_cert_check), every step the
+certified tensor-core scan scores is ALSO re-scored by the exact serial-chain
+sweep (itself bit-identical to detail::eval_flip, sequence.hpp:126-162 --
+test_gpu_parity.py).  The kernel then tests, for every row j of the step,
+V_exact(j) in [lo(j), hi(j)], and compares the decisions the intervals took on
+their own (argmin with smallest-offset ties, value_step vs value_local;
+search.cpp:383-413) with the exact ones.  Decisions are taken from the exact
+sweep in this mode, so the walks are the reference's walks.
+
+The large-alpha runs put alpha2 (13 / 11 / 10 at m16 / m18 / m20,
+search.cpp:19-23) into phase 1 so that regime -- terms up to ~1e37 at m20,
+fixed-point scale 2^qH with qH ~ 60 -- is checked at full n_lmt = 1024 from the
+first step; the n_lmt = 2, ls_lmt = 1 runs switch phase every few steps and
+check the restart path (snapshot restore, 10 folded flips, serial fitness chain).
+"""
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(engine, L, a1, a2, ls, n, walks, steps, seed=11):
+    ctx = engine.default_context()
+    ctx.set_cert_check(True)
+    try:
+        before = ctx.cert_check_stats()
+        sb = ctx.scan_stats()
+        p = engine.SearchParams(length=L, seed=seed, alpha1=a1, alpha2=a2, ls_lmt=ls,
+                                flip_lmt=min(L, 10), n_lmt=n,
+                                stop=engine.StopCondition(max_nse=1 + steps * (n + 1)))
+        w = engine.Walks(p, walks, seeds=[seed + i for i in range(walks)], ctx=ctx)
+        w.run()
+        recs = w.records()
+        w.close()
+    finally:
+        ctx.set_cert_check(False)
+    after = ctx.cert_check_stats()
+    sa = ctx.scan_stats()
+    d = {k: after[k] - before[k] for k in ("steps", "rows", "violations", "decided",
+                                         "decided_wrong")}
+    d["tightness"], d["rel_width"] = after["tightness"], after["rel_width"]
+    d["switches"] = sum(r.switches for r in recs)
+    d["certified"] = sa["certified"] - sb["certified"]
+    return d
+
+
+@pytest.mark.parametrize("L,a1,a2,walks,steps", [
+    (65535, 4, 13, 8, 40), (65535, 13, 4, 8, 40),
+    (262143, 4, 11, 4, 16), (262143, 11, 4, 4, 16),
+    (1048575, 4, 10, 3, 8), (1048575, 10, 4, 3, 8),
+])
+def test_intervals_hold_exact_doubles_full_neighbourhood(engine, L, a1, a2, walks, steps):
+    d = _run(engine, L, a1, a2, 2000, 1024, walks, steps)
+    assert d["steps"] >= walks * (steps - 1), d
+    assert d["rows"] >= d["steps"] * 1024 - 1024, d
+    assert d["violations"] == 0, d
+    assert d["decided"] > 0 and d["decided_wrong"] == 0, d
+    assert d["tightness"] <= 1.0, d
+
+
+@pytest.mark.parametrize("L,a2,n,steps", [(65535, 13, 2, 400), (262143, 11, 2, 200),
+                                          (1048575, 10, 2, 150), (1048575, 10, 5, 60)])
+def test_intervals_hold_across_phase_switches(engine, L, a2, n, steps):
+    d = _run(engine, L, 4, a2, 1, n, 2, steps)
+    assert d["switches"] >= 4, d            # both phases, restarts included
+    assert d["violations"] == 0 and d["decided_wrong"] == 0, d
+    assert d["rows"] > 0 and d["decided"] > 0, d

@@ -192,3 +192,16 @@ def test_oracle_vs_live_reference():
         R.ref_scan_values(s, c, L, start, n, lut, vr, pr)
         assert np.array_equal(v.view(np.uint64), vr.view(np.uint64))
         assert np.array_equal(p, pr)
+
+
+def test_fft_table_build_pinned(golden):
+    """build_table_fft (the CPU baseline's O(L log L) pivot tables) equals the
+    reference's SidelobeTable::build: exactly at small L, and by the reference's
+    own table hash at m14 and m20 (seed 1)."""
+    import hashlib
+    for L in (2, 3, 13, 64, 1000, 4095):
+        s = O.random_sequence(L, L)
+        assert np.array_equal(O.build_table_fft(s), O.build_table(s)), L
+    for name, L in (("kats.json", 16383), ("kats_big.json", 1048575)):
+        c = O.build_table_fft(O.random_sequence(1, L))
+        assert hashlib.sha256(c.tobytes()).hexdigest() == golden(name)[str(L)]["table_sha"]
