@@ -349,9 +349,15 @@ double psl_pow_int(double base, uint32_t exp) {
 
 namespace {
 
-std::vector<uint32_t> padded_bits(const int8_t* seq, uint32_t L) {
-  std::vector<uint32_t> bits = pack_bits(seq, L, kBitsPad);
-  bits.insert(bits.begin(), 0u);   // front pad: word i at bits[i + 1]
+// The sequence bits in the walks' padded layout (walks_create): nw + 48 zero
+// words on both sides, because the sweep's sliding windows run past either end
+// of the sequence unclamped.  Word i sits at [sb0 + 1 + i].
+std::vector<uint32_t> padded_bits(const int8_t* seq, uint32_t L, size_t* sb0) {
+  const size_t nw = (L + 31) / 32, front = nw + 48;
+  std::vector<uint32_t> bits(front + nw + nw + 48 + kBitsPad, 0u);
+  for (uint32_t i = 0; i < L; ++i)
+    if (seq[i] < 0) bits[front + (i >> 5)] |= 1u << (i & 31);
+  *sb0 = front - 1;
   return bits;
 }
 
@@ -362,7 +368,8 @@ int run_scan(psl_ctx* ctx, const int8_t* seq, const int32_t* table, uint32_t L, 
   int rc = device_ready(ctx, err, errlen);
   if (rc) return rc;
   const uint32_t nw = (L + 31) / 32;
-  const std::vector<uint32_t> bits = padded_bits(seq, L);
+  size_t sb0 = 0;
+  const std::vector<uint32_t> bits = padded_bits(seq, L, &sb0);
   cudaStream_t s = ctx->stream;
   Scratch d(s);
   ScanArgs a{};
@@ -385,7 +392,7 @@ int run_scan(psl_ctx* ctx, const int8_t* seq, const int32_t* table, uint32_t L, 
   a.L = L; a.n = n; a.start = start; a.nwords = nw;
   a.nchunks = (L - 1 + kChunk - 1) / kChunk;
   a.lut_size = lut_size;
-  a.bits = db; a.C = dc; a.lut = dl; a.values = dv; a.psls = dp;
+  a.bits = db + sb0; a.C = dc; a.lut = dl; a.values = dv; a.psls = dp;
   const int nl = launch_scan(a, s);
   if (nl < 0) return cuda_fail(err, errlen, take_launch_error(), "scan_kernel");
   ctx->launches += (uint32_t)nl;

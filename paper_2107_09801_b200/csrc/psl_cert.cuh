@@ -205,6 +205,7 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
   int32_t cv = 0;
   if (k < io.L) {
     cv = cpre;
+    if (io.Cloc) io.Cloc[k] = cpre;   // lazy local snapshot: the pre-fold table
 #ifndef PSL_ABLATE_FOLD
     if (io.F == 1) {
       // the common single move: C_k += 2 s_f (s_{f-k} + s_{f+k}), s_f after the flip
@@ -220,7 +221,6 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
 #endif
     if (io.fsum) part[3] = __dadd_rn(part[3], io.lut[abs(cv)]);
     if (io.Cdst) io.Cdst[k] = cv;
-    if (io.Cloc) io.Cloc[k] = cv;
     const int32_t a = abs(cv);
     pmax = max(pmax, a);
     want = io.hlist != nullptr && a >= io.hthr;

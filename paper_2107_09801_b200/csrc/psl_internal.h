@@ -39,7 +39,11 @@ struct WalkState {
   uint32_t phase;
   uint32_t n_pending;   // pending flips the next pass folds into C
   uint32_t src_local;   // next pass reads C from the local snapshot (restart)
-  uint32_t local_pending;    // next pass also writes the local snapshot C
+  uint32_t local_pending;    // next pass copies its PRE-fold C into the local snapshot
+                             // (the snapshot is materialised lazily: only when the
+                             // pivot first moves away from the local best)
+  uint32_t loc_at_pivot;     // the local best IS the current pivot (snapshot not
+                             // materialised; its table is Cpiv after the next fold)
   uint32_t fitness_pending;  // next pass runs the serial pivot-fitness chain
   int32_t status;       // PSL_OK / PSL_ERR_OVERFLOW
   uint32_t err_alpha;

@@ -273,9 +273,9 @@ __device__ __forceinline__ void build_chunk(const SweepIO& io, uint32_t c, doubl
     int32_t cv = 0;
     if (k < io.L) {
       cv = io.Csrc[k];
+      if (io.Cloc) io.Cloc[k] = cv;   // lazy local snapshot: the pre-fold table
       if (io.F) cv = fold_flips(cv, k, io, sb);
       if (io.Cdst) io.Cdst[k] = cv;
-      if (io.Cloc) io.Cloc[k] = cv;
       const int32_t av = abs(cv);
       pmax = max(pmax, av);
       want = io.hlist != nullptr && av >= io.hthr;
@@ -698,6 +698,7 @@ __global__ void __launch_bounds__(256) init_walks_kernel(RunArgs a, const uint64
     z.nse = 1;                 // the initial fitness evaluation (search.cpp:349)
     z.phase = 1;
     z.fitness_pending = 1;
+    z.loc_at_pivot = 1;        // local best = the start pivot (search.cpp:354-355)
     z.psl_best = -1;           // set from P on the first pass
     *S = z;
   }
@@ -919,9 +920,11 @@ __device__ __forceinline__ void reduce_group(Ctl* ctl, const Smem& sm, const int
 __device__ __forceinline__ void first_pass_state(Ctl* ctl, const RunArgs& a, uint32_t w,
                                                  int32_t Pn, double chain, uint32_t alpha) {
   WalkState& S = ctl->st;
+  // the lazily materialised snapshot is the PRE-fold table: its PSL is the
+  // previous pass's
+  if (S.local_pending) { S.P_local = S.P; S.local_pending = 0; }
   ctl->P_new = Pn;
   S.P = Pn;
-  if (S.local_pending) { S.P_local = Pn; S.local_pending = 0; }
   S.n_pending = 0;
   S.src_local = 0;
   if (S.fitness_pending) {
@@ -1702,7 +1705,9 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
       sio.L = L; sio.nwords = nw; sio.nchunks = a.nchunks;
       sio.alpha = alpha; sio.lut = lut; sio.lut_size = a.lut_n;
       sio.scan = false; sio.hcount = &ctl->hcount;
-      sio.Csrc = Cloc; sio.Cdst = nullptr; sio.Cloc = nullptr;
+      // (not yet materialised: the local best is the pivot, whose table this
+      // step's pass just wrote to Cpiv)
+      sio.Csrc = ctl->st.loc_at_pivot ? Cpiv : Cloc; sio.Cdst = nullptr; sio.Cloc = nullptr;
       sio.flips = flips; sio.F = 0; sio.hlist = nullptr; sio.hthr = 0; sio.chain = true;
       int32_t pm = 0;
       double chain = 0.0;
@@ -1803,6 +1808,17 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
       if (t == 0) ctl->st.energy_best = e;
     }
     __syncthreads();
+    // Local-best snapshot (search.cpp:394-399), materialised lazily: while the
+    // walk keeps improving the local best IS the pivot and nothing is copied.
+    // The first non-improving move leaves it behind: its bits are the pivot's
+    // before this move, its table the next pass's pre-fold C (no 4 MB copy per
+    // improving step).  A restart needs >= 2 worsening steps after the last
+    // improvement (ls_lmt >= 1), so the snapshot is materialised before any
+    // restart reads it.
+    const bool materialise = !ctl->restart && !ctl->improve && ctl->st.loc_at_pivot;
+    if (materialise)
+      for (uint32_t i = t; i < nw; i += blockDim.x) bits_loc[i + 1] = bits_piv[i + 1];
+    __syncthreads();
     if (ctl->restart) {
       // back to the phase-local best (:405-406): bits from the snapshot, C via
       // the next pass (src_local); then flip_random_distinct (:407, :131-148)
@@ -1830,12 +1846,14 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
       flips[0] = js;
       ctl->st.n_pending = 1;
       ctl->st.src_local = 0;
-      if (ctl->improve) ctl->st.local_pending = 1;
+      if (ctl->improve) {
+        ctl->st.loc_at_pivot = 1;
+      } else if (materialise) {
+        ctl->st.loc_at_pivot = 0;
+        ctl->st.local_pending = 1;
+      }
     }
-    __syncthreads();
-    if (ctl->improve) {
-      for (uint32_t i = t; i < nw; i += blockDim.x) bits_loc[i + 1] = bits_piv[i + 1];
-    }
+    if (ctl->restart && t == 0) ctl->st.loc_at_pivot = 0;
     __syncthreads();
   }
 

@@ -4,7 +4,7 @@ Runs here (where /root/reference exists) against oracle/_ref/libpslref.so, which
 oracle/Makefile compiles from the reference sources.  The fixtures are small and
 committed; the GPU box never reads /root/reference.
 
-    make -C oracle && python tests/golden/make_golden.py [--big]
+    make -C oracle && python tests/golden/make_golden.py [--big | --phase2]
 
 Doubles are stored as float.hex() strings so comparisons are bit-exact;
 sequences as '+'/'-' strings (formats.md alphabet).  --big adds the m18/m20
@@ -259,8 +259,57 @@ def gen_kats(big: bool):
     return out
 
 
+PHASE2_CASES = [
+    # (name, L, seed, a1, a2, ls, flip, n, steps): small n + ls_lmt 1 switch phase
+    # every few steps at the BASELINE lengths (restart: snapshot restore, flip_lmt
+    # folded flips, serial fitness chain, alpha2 = default_alpha2(L))
+    ("m16_n2_ls1", 65535, 3, 4, 13, 1, 10, 2, 400),
+    ("m16_n16_ls1", 65535, 4, 4, 13, 1, 10, 16, 150),
+    ("m18_n2_ls1", 262143, 3, 4, 11, 1, 10, 2, 200),
+    ("m20_n2_ls1", 1048575, 3, 4, 10, 1, 10, 2, 150),
+    ("m20_n5_ls1", 1048575, 5, 4, 10, 1, 10, 5, 60),
+    # the large-alpha regime at full n_lmt = 1024 from the first step (alpha2 of
+    # the length put into phase 1): terms up to ~1e37 at m20
+    ("m16_a13_full", 65535, 7, 13, 4, 2000, 10, 1024, 20),
+    ("m18_a11_full", 262143, 7, 11, 4, 2000, 10, 1024, 8),
+    ("m20_a10_full", 1048575, 7, 10, 4, 2000, 10, 1024, 3),
+]
+
+
+def _phase2_case(case):
+    name, L, seed, a1, a2, ls, flip, n, steps = case
+    rec = run(L, seed, a1, a2, ls, flip, n, 1 + steps * n, cap=1 << 16)
+    sol = rec.pop("solution_best", None)
+    if sol is not None:
+        rec["solution_sha"] = hashlib.sha256(sol.encode()).hexdigest()
+    rec.update(name=name, params=[L, seed, a1, a2, ls, flip, n, 1 + steps * n],
+               switches=sum(1 for e in rec["events"] if e[3] == 1),
+               phases=sorted({t[4] for t in rec.get("traces", [])}))
+    return rec
+
+
+def gen_phase2():
+    """Reference run_search records, events and every ScanTrace (hex doubles) in
+    both phases at m16 / m18 / m20 (phase 2 pinned at every BASELINE
+    length).  Solutions as sha256 of the '+'/'-' string.  ~10 min of reference
+    CPU time (the m20 O(L^2) builds), cases in parallel processes."""
+    from multiprocessing import Pool
+    with Pool(min(len(PHASE2_CASES), os.cpu_count() or 1)) as pool:
+        out = pool.map(_phase2_case, PHASE2_CASES, chunksize=1)
+    for r in out:
+        print(f"phase2 {r['name']}: psl {r.get('psl_best')} nse {r.get('nse')} "
+              f"switches {r['switches']} phases {r['phases']}", flush=True)
+    return {r["name"]: r for r in out}
+
+
 def main():
     big = "--big" in sys.argv
+    if "--phase2" in sys.argv:
+        obj = gen_phase2()
+        with open(os.path.join(HERE, "phase2.json"), "w") as f:
+            json.dump(obj, f, separators=(",", ":"))
+        print("wrote phase2.json", os.path.getsize(os.path.join(HERE, "phase2.json")), "bytes")
+        return
     def dump(name, obj):
         with open(os.path.join(HERE, name), "w") as f:
             json.dump(obj, f, separators=(",", ":"))
