@@ -14,9 +14,8 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-import numpy as np  # noqa: E402
-
 import paper_2107_09801_b200 as P  # noqa: E402
+from paper_2107_09801_b200.chain import run_chain  # noqa: E402
 
 
 def main():
@@ -26,28 +25,26 @@ def main():
     ap.add_argument("--seconds", type=float, default=30.0)
     ap.add_argument("--walks", type=int, default=0)
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--devices", type=int, nargs="+", default=[0])
     args = ap.parse_args()
     import torch
-    walks = args.walks or torch.cuda.get_device_properties(0).multi_processor_count   # one wave
-    ctx = P.Context(0)
+    nsm = torch.cuda.get_device_properties(args.devices[0]).multi_processor_count
+    walks = args.walks or nsm * len(args.devices)     # one wave of walk CTAs per GPU
     L = (1 << args.m) - 1
-    best_seq, best_psl = None, None
-    for r in range(args.rounds):
-        p = P.default_params(L)
-        p.seed = args.seed + r * walks
-        p.stop = P.StopCondition(max_seconds=args.seconds)
-        inits = None if best_seq is None else np.repeat(best_seq[None, :], walks, axis=0)
-        t0 = time.perf_counter()
-        recs = P.run_walks(p, walks, inits=inits, ctx=ctx, solutions=True)
-        i = int(np.argmin([x.psl_best for x in recs]))
-        if best_psl is None or recs[i].psl_best < best_psl:
-            best_psl, best_seq = recs[i].psl_best, recs[i].solution_best.copy()
-        rep = P.verify_sequence(best_seq, ctx)
-        assert rep.psl == best_psl
-        print(json.dumps({"m": args.m, "round": r + 1, "walks": walks, "seconds": args.seconds,
-                          "wall": time.perf_counter() - t0, "round_best_psl": recs[i].psl_best,
-                          "chain_best_psl": best_psl, "chain_best_mf": rep.merit_factor,
-                          "nse": int(sum(x.nse for x in recs))}), flush=True)
+    p = P.default_params(L)
+    p.seed = args.seed
+    p.stop = P.StopCondition(max_seconds=args.seconds)
+    t0 = [time.perf_counter()]
+
+    def report(r):
+        print(json.dumps({"m": args.m, "round": r.round, "walks": walks, "devices": len(args.devices),
+                          "seconds": args.seconds, "wall": time.perf_counter() - t0[0],
+                          "round_best_psl": r.round_best_psl, "chain_best_psl": r.chain_best_psl,
+                          "chain_best_mf": r.chain_best_mf, "nse": r.nse,
+                          "switches": r.switches}), flush=True)
+        t0[0] = time.perf_counter()
+
+    run_chain(p, walks, args.rounds, devices=args.devices, on_round=report)
 
 
 if __name__ == "__main__":
