@@ -36,15 +36,10 @@
 #pragma once
 
 // The certified kernel's CTA (one walk per SM) is 16 warps: every thread
-// builds one shift per chunk (kCC = 512) and lane 0 of warp 15 also issues the
-// chunk's tcgen05 MMAs; all 16 warps run the cross MMAs.  (-DPSL_CC=480 builds
-// the decoupled variant: warp 15 a dedicated issuer synchronised by mbarriers,
-// warps 0-14 building; correct, measured 11 % slower.)
+// builds one shift per chunk (kCC = 512); warps 15 and 14 also issue the
+// chunk's forward / reversed tcgen05 MMAs; all 16 warps run the cross MMAs.
 constexpr uint32_t kCertThreads = 2 * kThreads;
-#ifndef PSL_CC
-#define PSL_CC kCertThreads
-#endif
-constexpr uint32_t kCC = PSL_CC;              // shifts per certified chunk (one per builder thread)
+constexpr uint32_t kCC = kCertThreads;        // shifts per certified chunk (one per builder thread)
 constexpr int kCCols = kCC / 32;              // 32-shift columns per chunk
 constexpr int kCertTiles = 4;                 // mma.sync m16 row tiles per warp (64 rows, 16 warps)
 constexpr uint32_t kLag = 2;                  // reversed MMAs trail the builder by 2 chunks (>= 896 shifts)
@@ -337,6 +332,68 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
   }
 }
 
+// Tail chunks c0 <= c < nch (every shift past M_hi: H4 = R4 = 0, the term of
+// every row is e2 = |C_k|^alpha).  No staging and no per-chunk barrier: each
+// thread streams its shift of four chunks at a time from C (loads first), folds
+// the move, writes C back (and the lazy local snapshot's pre-fold value),
+// collects PSL / high sidelobes and adds 4 e2 to the window constant part[2] --
+// the same per-thread serial order and term count as cert_build, so the
+// rounding budget of the window sums is unchanged.
+__device__ __forceinline__ void cert_tail(const CertIO& io, uint32_t c0, uint32_t nch,
+                                          const uint32_t* sb, int32_t& pmax, double (&part)[5]) {
+  constexpr uint32_t U = 4;
+  const uint32_t t = threadIdx.x;
+#pragma unroll 1
+  for (uint32_t c = c0; c < nch; c += U) {
+    int32_t cp[U];
+    uint2 fw[U];
+#pragma unroll
+    for (uint32_t u = 0; u < U; ++u) {
+      const uint32_t k = cert_kb((int32_t)(c + u)) + t;
+      const bool in = c + u < nch && k < io.L;
+      cp[u] = in ? __ldcg(io.Csrc + k) : 0;
+      fw[u] = (in && io.F == 1) ? cert_fold_words(io, c + u, sb) : make_uint2(0u, 0u);
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < U; ++u) {
+      if (c + u >= nch) break;                         // warp-uniform
+      const uint32_t k = cert_kb((int32_t)(c + u)) + t;
+      bool want = false;
+      int32_t cv = 0;
+      if (k < io.L) {
+        cv = cp[u];
+        if (io.Cloc) io.Cloc[k] = cv;                  // lazy local snapshot: pre-fold
+        if (io.F == 1) {
+          const uint32_t f = io.f1;
+          const int bA = (int)((fw[u].x >> ((f - k) & 31)) & 1u), bB = (int)((fw[u].y >> ((f + k) & 31)) & 1u);
+          const int acc = (k <= f ? 1 - 2 * bA : 0) + (f + k < io.L ? 1 - 2 * bB : 0);
+          cv += 2 * io.sf1 * acc;
+        } else if (io.F) {
+          SweepIO fio;
+          fio.L = io.L; fio.flips = io.flips; fio.F = io.F;
+          cv = fold_flips(cv, k, fio, sb);
+        }
+        const int32_t a = abs(cv);
+        if (io.fsum) part[3] = __dadd_rn(part[3], io.lut[a]);
+        if (io.Cdst) io.Cdst[k] = cv;
+        pmax = max(pmax, a);
+        want = io.hlist != nullptr && a >= io.hthr;
+        part[2] = __dadd_rn(part[2], __dmul_rn(4.0, io.lut[a]));
+      }
+      if (io.hlist) {
+        const uint32_t m = __ballot_sync(FULL, want);
+        if (m) {
+          const int lane = t & 31, leader = __ffs(m) - 1;
+          uint32_t base = 0;
+          if (lane == leader) base = atomicAdd(io.hcount, (uint32_t)__popc(m));
+          base = __shfl_sync(FULL, base, leader);
+          if (want) io.hlist[base + __popc(m & ((1u << lane) - 1))] = make_int2((int)k, cv);
+        }
+      }
+    }
+  }
+}
+
 // Zero digit cores for chunk c (ring slots of chunks past the end / before the start)
 __device__ __forceinline__ void cert_zero_digits(const CertSmem& cs, long long c) {
   constexpr uint32_t kCores = kCC / 16, kParts = kCores * 8;   // 16-byte parts per mapping
@@ -424,50 +481,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
   }
 }
 
-// The tensor-core MMAs of iteration c, issued by a whole warp (warp-uniform
-// descriptors, one lane elected inside the asm: no per-MMA waterfall over a
-// divergent thread): forward kappa-chunk c and reversed kappa'-chunk c - kLag,
-// kCCols K-steps of 32 shifts each.  Descriptors advance by constants per
-// K-step: A by 4 cores (512 B), B by 2 digit cores (256 B; the double-mapped
-// ring keeps every span contiguous).  Then committed to the iteration's
-// barrier by the elected lane.
+// One tcgen05 MMA issued by a whole warp: warp-uniform descriptors, one lane
+// elected inside the asm (no per-MMA waterfall over a divergent thread).
 __device__ __forceinline__ void umma_i8_elect(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %4, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(kIdesc), "r"(acc));
-}
-__device__ __forceinline__ void cert_issue_warp(const CertSmem& cs, uint32_t tmem, int32_t c, bool fwd,
-                                                bool rev, uint32_t started, uint64_t* mbar) {
-  const uint32_t abuf = smem_u32(cs.acore) + (uint32_t)(c & 1) * (uint32_t)kABuf;
-  const uint32_t ring = smem_u32(cs.dring);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (fwd) {
-    const long long q0 = (long long)(kCC / 16) * c - 56;
-    uint64_t da = umma_desc(abuf, 256, 128);
-    uint64_t db = umma_desc(ring + (uint32_t)((((q0 % kRing) + kRing) % kRing) * 128), 128, 1024);
-#pragma unroll
-    for (int s = 0; s < kCCols; ++s) {
-      umma_i8_elect(tmem, da, db, (s > 0 || (started & 1u)) ? 1u : 0u);
-      da += 512 >> 4;
-      db += 256 >> 4;
-    }
-  }
-  if (rev) {
-    const long long q0 = (long long)(kCC / 16) * (c - (int32_t)kLag);
-    uint64_t da = umma_desc(abuf + (uint32_t)(kACores * 128), 256, 128);
-    uint64_t db = umma_desc(ring + (uint32_t)((((q0 % kRing) + kRing) % kRing) * 128), 128, 1024);
-#pragma unroll
-    for (int s = 0; s < kCCols; ++s) {
-      umma_i8_elect(tmem + 64, da, db, (s > 0 || (started & 2u)) ? 1u : 0u);
-      da += 512 >> 4;
-      db += 256 >> 4;
-    }
-  }
-  asm volatile(
-      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
-          smem_u32(mbar)) : "memory");
 }
 
 // One direction's MMAs of iteration c (dir 0: forward kappa-chunk c, 1:

@@ -170,8 +170,6 @@ struct Ctl {
   double rs5[5][16];
   uint32_t cfw[72], crv[72]; // per-chunk tcgen05 flags of the pass segment (bit c: fwd / rev MMAs)
   uint64_t mbar[2];          // tcgen05 commit barriers (iteration parity)
-  uint64_t mbar_f[2];        // decoupled issuer: chunk staged (builder warps arrive)
-  uint64_t mbar_e[2];        // decoupled issuer: warp 15 done reading the chunk's buffers
   uint32_t tmem;             // TMEM base of this CTA's accumulators (kTmemCols columns)
   // certificate check mode (RunArgs::cert_check)
   int32_t chk_on, chk_dec, chk_cmp;
@@ -1040,7 +1038,6 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
   __syncthreads();
   if (ctl->st.done || ctl->st.status != PSL_OK) return;
   uint32_t mb_par[2] = {0u, 0u};   // next phase parity to wait for on ctl->mbar[0/1]
-  uint32_t mf_par[2] = {0u, 0u}, me_par[2] = {0u, 0u};   // ... on ctl->mbar_f / mbar_e
   if (kCert) {
     if (t < 32) {   // the certified scan's tcgen05 accumulators live in TMEM
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -1048,15 +1045,9 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     if (t == 0) {
-      for (int i = 0; i < 2; ++i) {
-        // two committing warps per iteration (forward: warp 15, reversed: warp 14);
-        // the decoupled variant commits once
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&ctl->mbar[i])),
-                     "r"(kCC < kCertThreads ? 1 : 2) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&ctl->mbar_f[i])),
-                     "r"(kCC / 32) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&ctl->mbar_e[i])) : "memory");
-      }
+      // two committing warps per iteration (forward: warp 15, reversed: warp 14)
+      for (int i = 0; i < 2; ++i)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"(smem_u32(&ctl->mbar[i])) : "memory");
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1217,11 +1208,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         for (int32_t cz = -(int32_t)kLag; cz < 0; ++cz) cert_zero_digits(cs, cz);
         // C_k streams into shared memory by cp.async two chunks ahead
         const uint32_t nch = io.nchunks;
-        const bool builder = t < kCC;   // warp 15 issues the tcgen05 MMAs instead
-        if (builder) {
-          cert_prefetch(io, cs, 0);
-          if (nch > 1) cert_prefetch(io, cs, 1);
-        }
+        const bool builder = t < kCC;   // every thread builds one shift per chunk
         // which iterations issue forward (kappa-chunk c) / reversed (c - kLag) MMAs
         for (uint32_t c = t; c < (nch + kLag + 31) / 32 * 32; c += blockDim.x) {
           bool fw = false, rv = false;
@@ -1235,88 +1222,35 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           if ((t & 31) == 0) { ctl->cfw[c >> 5] = mf; ctl->crv[c >> 5] = mr; }
         }
         __syncthreads();
+        // Chunks from c_end on are pure tail (zone 5: H4 = R4 = 0, every row's term
+        // is |C_k|^alpha, no MMA reads their digit cores, no band constants): they
+        // skip the chunk pipeline and are streamed by cert_tail after it.  The
+        // serial fitness chain (restart passes) needs every chunk's record in
+        // order, so chain passes keep the pipeline to the end.
+        uint32_t c_end = nch;
+        if (!io.chain) {
+          uint32_t cl = io.M_hi >= 1 ? (io.M_hi - 1) / kCC : 0u;   // last chunk with kb <= M_hi
+          while (cl + 1 < nch && ((ctl->cfw[(cl + 1) >> 5] >> ((cl + 1) & 31)) & 1u)) ++cl;
+          c_end = min(nch, cl + 1);
+        }
+        if (builder) {
+          cert_prefetch(io, cs, 0);
+          if (c_end > 1) cert_prefetch(io, cs, 1);
+        }
         uint2 fwords = (builder && io.F == 1) ? cert_fold_words(io, 0, sm.sb) : make_uint2(0u, 0u);
         uint32_t issued = 0;        // bit (c & 1): iteration c committed MMAs not yet waited for
         // iteration c: build chunk c, stage the sequence cores of forward kappa-chunk c and
         // reversed kappa'-chunk c - kLag, issue their tcgen05 MMAs (one thread, async),
         // then the zone-1 cross MMAs (mma.sync) and band-1 cells of chunk c
         PT_MARK(7);
-        if (kCC < kCertThreads) {
-          // ---- decoupled issuer (kCC = 480): warps 0-14 build / stage / cross and
-          // sync among themselves (named barrier 1); warp 15 waits for each staged
-          // chunk on an mbarrier, issues its tcgen05 MMAs (blocking while the
-          // tensor pipe drains them), runs its own cross rows and band cells and
-          // releases the chunk's buffers on a second mbarrier.
-          if (builder) {
-            uint32_t used = 0;
-            for (uint32_t c = 0; c < nch + kLag; ++c) {
-              const uint32_t b = c & 1;
-              if (used & (1u << b)) {       // iteration c - 2 used buffer b
-                if (issued & (1u << b)) { mbar_wait(&ctl->mbar[b], mb_par[b]); mb_par[b] ^= 1u; }
-                mbar_wait(&ctl->mbar_e[b], me_par[b]);
-                me_par[b] ^= 1u;
-                issued &= ~(1u << b);
-              }
-              used |= 1u << b;
-              const bool fw = (ctl->cfw[c >> 5] >> (c & 31)) & 1u, rv = (ctl->crv[c >> 5] >> (c & 31)) & 1u;
-              if (c < nch) {
-                if (c + 2 < nch) cert_prefetch(io, cs, c + 2);
-                const uint2 fnext = (io.F == 1 && c + 1 < nch) ? cert_fold_words(io, c + 1, sm.sb) : fwords;
-                const int pending = (int)min(2u, nch - 1 - c);
-                cert_build(io, cs, c, sm.sb, pmax, part, cert_take(cs, c, pending), fwords, ovf);
-                fwords = fnext;
-              } else {
-                cert_zero_digits(cs, c);
-              }
-              cert_cores(io, cs, (int32_t)c, sm.sb, fw, rv);
-              asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-              asm volatile("bar.sync 1, %0;" ::"n"(kCC) : "memory");
-              if ((t & 31) == 0)
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&ctl->mbar_f[b])) : "memory");
-              if (fw || rv) {
-                started |= (fw ? 1u : 0u) | (rv ? 2u : 0u);
-                numma += (fw ? kCCols : 0) + (rv ? kCCols : 0);
-                issued |= 1u << b;
-              }
-              if (c < nch) {
-                cert_cross_chunk(io, ln, c, acc, nmma);
-                if (io.chain && t == kCertThreads - 64) cert_chain_chunk(io, cs, c, chain);
-                if (t >= (uint32_t)kThreads && cert_band_chunk(io, c)) cert_band_cells(io, cs, c, sm.sb, Bs, t - kThreads);
-              }
-            }
-            for (uint32_t bb = 0; bb < 2; ++bb) {
-              if (issued & (1u << bb)) { mbar_wait(&ctl->mbar[bb], mb_par[bb]); mb_par[bb] ^= 1u; }
-              if (used & (1u << bb)) { mbar_wait(&ctl->mbar_e[bb], me_par[bb]); me_par[bb] ^= 1u; }
-            }
-            issued = 0;
-          } else {
-            for (uint32_t c = 0; c < nch + kLag; ++c) {
-              const uint32_t b = c & 1;
-              mbar_wait(&ctl->mbar_f[b], mf_par[b]);
-              mf_par[b] ^= 1u;
-              const bool fw = (ctl->cfw[c >> 5] >> (c & 31)) & 1u, rv = (ctl->crv[c >> 5] >> (c & 31)) & 1u;
-              if (fw || rv) {
-                cert_issue_warp(cs, tmem, (int32_t)c, fw, rv, started, &ctl->mbar[b]);
-                started |= (fw ? 1u : 0u) | (rv ? 2u : 0u);
-                numma += (fw ? kCCols : 0) + (rv ? kCCols : 0);
-              }
-              if (c < nch) {
-                cert_cross_chunk(io, ln, c, acc, nmma);
-                if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, sm.sb, Bs, t - kThreads);
-              }
-              __syncwarp();
-              if ((t & 31) == 0)
-                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&ctl->mbar_e[b])) : "memory");
-            }
-          }
-        } else {
+        {
         // warp 15 issues the forward MMAs of chunk c right after its barrier,
         // warp 14 the reversed ones at the top of the next iteration (after the
         // forward ones drained): the tensor-pipe wait is split over two warps
         int32_t pend_c = -1;
         bool pend_rv = false;
         uint32_t pend_started = 0;
-        for (uint32_t c = 0; c < nch + kLag; ++c) {
+        for (uint32_t c = 0; c < c_end + kLag; ++c) {
           if (pend_c >= 0) {
             if ((t >> 5) == PSL_REV_WARP) cert_issue_dir(cs, tmem, pend_c, 1, pend_rv, pend_started, &ctl->mbar[pend_c & 1]);
             pend_c = -1;
@@ -1330,11 +1264,11 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           }
           PT_MARK(0);
           const bool fw = (ctl->cfw[c >> 5] >> (c & 31)) & 1u, rv = (ctl->crv[c >> 5] >> (c & 31)) & 1u;
-          if (c < nch) {
+          if (c < c_end) {
             if (builder) {
-              if (c + 2 < nch) cert_prefetch(io, cs, c + 2);
-              const uint2 fnext = (io.F == 1 && c + 1 < nch) ? cert_fold_words(io, c + 1, sm.sb) : fwords;
-              const int pending = (int)min(2u, nch - 1 - c);
+              if (c + 2 < c_end) cert_prefetch(io, cs, c + 2);
+              const uint2 fnext = (io.F == 1 && c + 1 < c_end) ? cert_fold_words(io, c + 1, sm.sb) : fwords;
+              const int pending = (int)min(2u, c_end - 1 - c);
               cert_build(io, cs, c, sm.sb, pmax, part, cert_take(cs, c, pending), fwords, ovf);
               fwords = fnext;
             }
@@ -1361,7 +1295,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
             issued |= 1u << (c & 1);
           }
           PT_MARK(4);
-          if (c < nch) {   // zone-1 cross MMAs (all warps); band-1 cells (warps 8-15)
+          if (c < c_end) {   // zone-1 cross MMAs (all warps); band-1 cells (warps 8-15)
             cert_cross_chunk(io, ln, c, acc, nmma);          // all 16 warps, 64 rows each
             PT_MARK(5);
             if (io.chain && t == kCertThreads - 64) cert_chain_chunk(io, cs, c, chain);
@@ -1372,6 +1306,8 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         if (pend_c >= 0 && (t >> 5) == PSL_REV_WARP) cert_issue_dir(cs, tmem, pend_c, 1, pend_rv, pend_started, &ctl->mbar[pend_c & 1]);
         }
         PT_MARK(0);
+        // the tail chunks, streamed while the last MMAs drain
+        cert_tail(io, c_end, nch, sm.sb, pmax, part);
         for (uint32_t bb = 0; bb < 2; ++bb)
           if (issued & (1u << bb)) { mbar_wait(&ctl->mbar[bb], mb_par[bb]); mb_par[bb] ^= 1u; }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");

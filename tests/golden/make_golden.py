@@ -4,7 +4,7 @@ Runs here (where /root/reference exists) against oracle/_ref/libpslref.so, which
 oracle/Makefile compiles from the reference sources.  The fixtures are small and
 committed; the GPU box never reads /root/reference.
 
-    make -C oracle && python tests/golden/make_golden.py [--big | --phase2]
+    make -C oracle && python tests/golden/make_golden.py [--big | --phase2 [--only=name,...]]
 
 Doubles are stored as float.hex() strings so comparisons are bit-exact;
 sequences as '+'/'-' strings (formats.md alphabet).  --big adds the m18/m20
@@ -273,12 +273,31 @@ PHASE2_CASES = [
     ("m16_a13_full", 65535, 7, 13, 4, 2000, 10, 1024, 20),
     ("m18_a11_full", 262143, 7, 11, 4, 2000, 10, 1024, 8),
     ("m20_a10_full", 1048575, 7, 10, 4, 2000, 10, 1024, 3),
+    # full n_lmt = 1024 in BOTH phases: a deep warm start (the best sequence of a
+    # 20000-step GPU descent, tools/deep_starts.py; stored with the fixture as
+    # packed bits) from which 1024-neighbour steps stop improving, ls_lmt 1
+    ("m16_deep_ls1", 65535, 21, 4, 13, 1, 10, 1024, 150, "deep_m16"),
 ]
 
 
+def init_to_hex(s: np.ndarray) -> str:
+    return np.packbits((np.asarray(s) < 0).astype(np.uint8), bitorder="little").tobytes().hex()
+
+
+def init_from_hex(h: str, L: int) -> np.ndarray:
+    bits = np.unpackbits(np.frombuffer(bytes.fromhex(h), np.uint8), bitorder="little")[:L]
+    return np.where(bits == 1, -1, 1).astype(np.int8)
+
+
 def _phase2_case(case):
-    name, L, seed, a1, a2, ls, flip, n, steps = case
-    rec = run(L, seed, a1, a2, ls, flip, n, 1 + steps * n, cap=1 << 16)
+    name, L, seed, a1, a2, ls, flip, n, steps = case[:9]
+    init = None
+    if len(case) > 9:
+        init = np.load(os.path.join(HERE, "..", "..", "gpurun_out", case[9] + ".npy"))
+        assert len(init) == L
+    rec = run(L, seed, a1, a2, ls, flip, n, 1 + steps * n, init=init, cap=1 << 16)
+    if init is not None:
+        rec["init_bits_hex"] = init_to_hex(init)
     sol = rec.pop("solution_best", None)
     if sol is not None:
         rec["solution_sha"] = hashlib.sha256(sol.encode()).hexdigest()
@@ -294,8 +313,10 @@ def gen_phase2():
     length).  Solutions as sha256 of the '+'/'-' string.  ~10 min of reference
     CPU time (the m20 O(L^2) builds), cases in parallel processes."""
     from multiprocessing import Pool
-    with Pool(min(len(PHASE2_CASES), os.cpu_count() or 1)) as pool:
-        out = pool.map(_phase2_case, PHASE2_CASES, chunksize=1)
+    only = [a.split("=", 1)[1] for a in sys.argv if a.startswith("--only=")]
+    cases = [c for c in PHASE2_CASES if not only or c[0] in only[0].split(",")]
+    with Pool(max(1, min(len(cases), os.cpu_count() or 1))) as pool:
+        out = pool.map(_phase2_case, cases, chunksize=1)
     for r in out:
         print(f"phase2 {r['name']}: psl {r.get('psl_best')} nse {r.get('nse')} "
               f"switches {r['switches']} phases {r['phases']}", flush=True)
@@ -305,7 +326,11 @@ def gen_phase2():
 def main():
     big = "--big" in sys.argv
     if "--phase2" in sys.argv:
-        obj = gen_phase2()
+        obj = {}
+        path = os.path.join(HERE, "phase2.json")
+        if any(a.startswith("--only=") for a in sys.argv) and os.path.exists(path):
+            obj = json.load(open(path))            # regenerate a subset, keep the rest
+        obj.update(gen_phase2())
         with open(os.path.join(HERE, "phase2.json"), "w") as f:
             json.dump(obj, f, separators=(",", ":"))
         print("wrote phase2.json", os.path.getsize(os.path.join(HERE, "phase2.json")), "bytes")
