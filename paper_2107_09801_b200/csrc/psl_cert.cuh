@@ -161,6 +161,7 @@ __device__ __forceinline__ void cert_prefetch(const CertIO& io, const CertSmem& 
   const uint32_t k = cert_kb(c) + threadIdx.x;
   int32_t* dst = cs.cring + (size_t)(c % 3) * kCC + threadIdx.x;
   const bool in = k < io.L;
+  PSL_CHK(in_buf(dst, cs.cring, 3 * kCertCBuf, 4), 1);
   const int32_t* src = io.Csrc + (in ? k : 0);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src),
                "r"(in ? 4 : 0) : "memory");
@@ -187,6 +188,7 @@ __device__ __forceinline__ unsigned char* dcore(const CertSmem& cs, long long q)
 __device__ __forceinline__ uint2 cert_fold_words(const CertIO& io, uint32_t c, const uint32_t* sb) {
   const int32_t k = (int32_t)cert_kb(c) + (int32_t)threadIdx.x;
   const int32_t f = (int32_t)io.f1;
+  PSL_CHK(sb_ok(((f - k) >> 5) + 1, io.L) && sb_ok(((f + k) >> 5) + 1, io.L), 2);
   return make_uint2(sb[((f - k) >> 5) + 1], sb[((f + k) >> 5) + 1]);
 }
 
@@ -200,6 +202,7 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
   int32_t cv = 0;
   if (k < io.L) {
     cv = cpre;
+    PSL_CHK(k >= 1, 3);
     if (io.Cloc) io.Cloc[k] = cpre;   // lazy local snapshot: the pre-fold table
 #ifndef PSL_ABLATE_FOLD
     if (io.F == 1) {
@@ -227,6 +230,7 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
       uint32_t base = 0;
       if (lane == leader) base = atomicAdd(io.hcount, (uint32_t)__popc(m));
       base = __shfl_sync(FULL, base, leader);
+      PSL_CHK(!want || base + __popc(m & ((1u << lane) - 1)) < io.L, 4);
       if (want) io.hlist[base + __popc(m & ((1u << lane) - 1))] = make_int2((int)k, cv);
     }
   }
@@ -247,6 +251,7 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
       if (k <= io.M_lo) {
         part[1] = __dadd_rn(part[1], m4);
       } else {                                        // band 2: per-row prefix sums
+        PSL_CHK(k - io.M_lo - 1 < (uint32_t)kGroup, 5);
         io.b2M[k - io.M_lo - 1] = m4;
         io.b2E[k - io.M_lo - 1] = __dmul_rn(4.0, io.lut[abs(cv)]);
       }
@@ -280,12 +285,14 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
     const uint32_t col = (t & 15) & ~3u;                 // first of the group's 4 shifts in the core
     unsigned char* p0 = dcore(cs, (long long)(kCC / 16) * c + (t >> 4)) + col;
     unsigned char* p1 = p0 + kRing * 128;
+    PSL_CHK(in_buf(p0 + 16 * x, cs.dring, kDRing, 4) && in_buf(p1 + 16 * (4 + x), cs.dring, kDRing, 4), 6);
     *reinterpret_cast<uint32_t*>(p0 + 16 * x) = wl;
     *reinterpret_cast<uint32_t*>(p0 + 16 * (4 + x)) = wh;
     *reinterpret_cast<uint32_t*>(p1 + 16 * x) = wl;
     *reinterpret_cast<uint32_t*>(p1 + 16 * (4 + x)) = wh;
   }
 #endif
+  PSL_CHK(b * kCC + t < 2 * kCC, 7);
   if (io.chain || cert_band_chunk(io, c)) cs.rec[b * kCC + t] = cv;
   if (kb > io.m_lo) return;
   // zone-1 chunk: R4 digit rows and the sequence windows of the cross MMAs
@@ -294,6 +301,7 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
     ovf |= (((unsigned long long)rv + (1ull << 61)) >> 62) != 0;
     const unsigned long long dr = ((unsigned long long)rv + 0x8080808080808080ull) ^ 0x8080808080808080ull;
     unsigned char* lr = cs.limbR + (size_t)b * kLimbBuf + t;
+    PSL_CHK(in_buf(lr + 7 * kLimbStride, cs.limbR, 2 * kLimbBuf), 8);
 #pragma unroll
     for (int d = 0; d < 8; ++d) lr[d * kLimbStride] = (unsigned char)(dr >> (8 * d));
   }
@@ -313,6 +321,7 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
     uint32_t w0 = 0, w1 = 0;
     if (hi >= 0 && lo < L) {
       if (lo >= 0 && hi < L) {
+        PSL_CHK(sb_ok((lo >> 5) + 2, io.L), 9);
         uint32_t x = __funnelshift_r(sb[(lo >> 5) + 1], sb[(lo >> 5) + 2], (uint32_t)lo & 31) & 0xFFu;
         if (dir) x = __brev(x) >> 24;
         w0 = nib_bytes(x & 0xFu);
@@ -325,6 +334,7 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
       }
     }
     unsigned char* dst = (dir == 0 ? cs.winF : cs.winV) + (size_t)b * kWinBuf + 4 * q;
+    PSL_CHK(in_buf(dst + 3 * kWinBytes, dir == 0 ? cs.winF : cs.winV, 2 * kWinBuf, 4), 10);
     *reinterpret_cast<uint32_t*>(dst) = w0;
     *reinterpret_cast<uint32_t*>(dst + kWinBytes) = __funnelshift_r(w0, w1, 8);
     *reinterpret_cast<uint32_t*>(dst + 2 * kWinBytes) = __funnelshift_r(w0, w1, 16);
@@ -351,6 +361,7 @@ __device__ __forceinline__ void cert_tail(const CertIO& io, uint32_t c0, uint32_
     for (uint32_t u = 0; u < U; ++u) {
       const uint32_t k = cert_kb((int32_t)(c + u)) + t;
       const bool in = c + u < nch && k < io.L;
+      PSL_CHK(!in || k >= 1, 11);
       cp[u] = in ? __ldcg(io.Csrc + k) : 0;
       fw[u] = (in && io.F == 1) ? cert_fold_words(io, c + u, sb) : make_uint2(0u, 0u);
     }
@@ -387,6 +398,7 @@ __device__ __forceinline__ void cert_tail(const CertIO& io, uint32_t c0, uint32_
           uint32_t base = 0;
           if (lane == leader) base = atomicAdd(io.hcount, (uint32_t)__popc(m));
           base = __shfl_sync(FULL, base, leader);
+          PSL_CHK(!want || base + __popc(m & ((1u << lane) - 1)) < io.L, 12);
           if (want) io.hlist[base + __popc(m & ((1u << lane) - 1))] = make_int2((int)k, cv);
         }
       }
@@ -400,6 +412,7 @@ __device__ __forceinline__ void cert_zero_digits(const CertSmem& cs, long long c
   for (uint32_t i = threadIdx.x; i < 2 * kParts; i += blockDim.x) {
     const uint32_t part = i % kParts, map = i / kParts;
     unsigned char* p = dcore(cs, (long long)kCores * c + part / 8) + 16 * (part & 7) + map * kRing * 128;
+    PSL_CHK(in_buf(p, cs.dring, kDRing, 16), 13);
     *reinterpret_cast<uint4*>(p) = make_uint4(0u, 0u, 0u, 0u);
   }
 }
@@ -408,6 +421,7 @@ __device__ __forceinline__ void cert_zero_digits(const CertSmem& cs, long long c
 __device__ __forceinline__ void seq20(const uint32_t* sb, int32_t p0, int dir, int32_t L, uint32_t (&w)[5]) {
   const int32_t lo = dir > 0 ? p0 : p0 - 19, hi = lo + 19;
   if (lo >= 0 && hi < L) {
+    PSL_CHK(sb_ok((lo >> 5) + 2, (uint32_t)L), 14);
     uint32_t x = __funnelshift_r(sb[(lo >> 5) + 1], sb[(lo >> 5) + 2], (uint32_t)lo & 31) & 0xFFFFFu;
     if (dir < 0) x = __brev(x) >> 12;
 #pragma unroll
@@ -443,6 +457,7 @@ __device__ __forceinline__ void cert_cores(const CertIO& io, const CertSmem& cs,
   uint32_t w[5];
   seq20(sb, p0, dir == 0 ? 1 : -1, (int32_t)io.L, w);
   uint4* dst = reinterpret_cast<uint4*>(base + (size_t)dir * kACores * 128 + 64 * g);
+  PSL_CHK(in_buf(dst + 3, cs.acore, 2 * kABuf, 16), 15);
   // row r of the quad = the 16 bytes from byte r; rows in a lane-rotated order
   // (r = i + g/2 mod 4) so each quarter-warp store covers 8 distinct 16-byte bank groups
 #pragma unroll
@@ -624,7 +639,7 @@ __device__ __forceinline__ void cert_cross_run(uint32_t f, uint32_t v, uint32_t 
 }
 
 // The cross MMAs of zone-1 chunk c (buffer c & 1) for this warp's 128 rows.
-__device__ __forceinline__ void cert_cross_chunk(const CertIO& io, const CertLane& ln, uint32_t c,
+__device__ __forceinline__ void cert_cross_chunk(const CertIO& io, const CertSmem& cs, const CertLane& ln, uint32_t c,
                                                  int (&acc)[kCertTiles][4], uint32_t& nmma) {
   const uint32_t kb = cert_kb(c);
   if (kb > io.m_lo) return;
@@ -637,6 +652,20 @@ __device__ __forceinline__ void cert_cross_chunk(const CertIO& io, const CertLan
   // columns whose first shift is still in zone 1 (the rest of the chunk has R4 = 0)
   const int n = (int)min((uint32_t)kCCols, (io.m_lo - kb) / 32 + 1);
   const uint32_t b = c & 1;
+#ifdef PSL_DEBUG_BOUNDS
+  {
+    // every LDS whose value is used stays inside its own window copy / digit row
+    // (cert_cross_run's final ring refill after the last column is dead: it may
+    // read one column past the copy, still inside the CTA's shared memory)
+    const uint32_t wf = smem_u32(cs.winF), wv = smem_u32(cs.winV), lb = smem_u32(cs.limbR);
+    const uint32_t f0 = ln.f + b * (uint32_t)kWinBuf - wf, v0 = ln.v + b * (uint32_t)kWinBuf - wv;
+    const uint32_t cf = f0 % kWinBytes, cvv = v0 % kWinBytes;
+    const uint32_t cb = ((ln.bd + b * (uint32_t)kLimbBuf - lb) % (uint32_t)kLimbBuf) % (uint32_t)kLimbStride;
+    PSL_CHK(cf + 32u * (uint32_t)n + 28u <= (uint32_t)kWinBytes, 16);
+    PSL_CHK(cvv >= 56u && cvv + 32u * (uint32_t)n - 12u <= (uint32_t)kWinBytes, 17);
+    PSL_CHK(cb + 32u * (uint32_t)n - 12u <= (uint32_t)kLimbStride, 18);
+  }
+#endif
   nmma += (uint32_t)(n * kCertTiles);
   cert_cross_run(ln.f + b * (uint32_t)kWinBuf, ln.v + b * (uint32_t)kWinBuf,
                  ln.bd + b * (uint32_t)kLimbBuf, n, acc);
@@ -717,6 +746,7 @@ __device__ __forceinline__ void cert_band_cells(const CertIO& io, const CertSmem
       // bit q: s_{j+k0+q} and s_{j-k0-q} (1 <-> -1; zero pads beyond the ends)
       const long long pB = (long long)j + k0, pA = (long long)j - k0 - 31;
       const long long wB = pB >> 5, wA = pA >> 5;
+      PSL_CHK(sb_ok(wB + 2, L) && sb_ok(wA + 1, L) && sb_ok(wA + 2, L), 19);
       const uint32_t Bw = __funnelshift_r(sb[wB + 1], sb[wB + 2], (uint32_t)(pB & 31));
       const uint32_t Aw = __brev(__funnelshift_r(sb[wA + 1], sb[wA + 2], (uint32_t)(pA & 31)));
       const uint32_t nq = min(32u, bhi - k0 + 1);
@@ -725,6 +755,7 @@ __device__ __forceinline__ void cert_band_cells(const CertIO& io, const CertSmem
         const int u = ((Bw >> q) & 1u) == sjb ? 1 : -1;
         const int v = ((Aw >> q) & 1u) == sjb ? 1 : -1;
         const int x = (k <= j ? v : 0) + (j + k < L ? u : 0);
+        PSL_CHK(k - kb < kCC, 20);
         s = __dadd_rn(s, lut[abs(rec[k - kb] - 2 * x)]);
       }
     }

@@ -37,6 +37,41 @@ namespace {
 
 constexpr uint32_t FULL = 0xffffffffu;
 
+// Device bounds checks (-DPSL_DEBUG_BOUNDS; tools/ablate.sh bounds=PSL_DEBUG_BOUNDS):
+// every shared-memory buffer write of the certified pipeline, every C / high-
+// sidelobe / scratch index and every padded bit-array word index is tested;
+// a violation prints its site and traps.  The stand-in for compute-sanitizer
+// memcheck, which this GPU pool does not allow (profiles/r02_bounds_check.md).
+#ifdef PSL_DEBUG_BOUNDS
+}  // namespace
+}  // namespace pslb
+#include <cstdio>
+namespace pslb {
+namespace {
+#define PSL_CHK(cond, site)                                                                  \
+  do {                                                                                       \
+    if (!(cond)) {                                                                           \
+      printf("PSL bounds violation: site %d block %d thread %d\n", (int)(site), (int)blockIdx.x, \
+             (int)threadIdx.x);                                                              \
+      __trap();                                                                              \
+    }                                                                                        \
+  } while (0)
+#else
+#define PSL_CHK(cond, site) do {} while (0)
+#endif
+// valid word indices of a walk's padded bit array around sb (sb[0] = the last
+// front pad word; nw + 47 pad words before it, nw + 48 + kBitsPad after the
+// sequence): [-(nw + 47), 2 nw + 57)
+__device__ __forceinline__ bool sb_ok(long long idx, uint32_t L) {
+  const long long nw = ((long long)L + 31) / 32;
+  return idx >= -(nw + 47) && idx < 2 * nw + 49 + kBitsPad;
+}
+__device__ __forceinline__ bool in_buf(const void* p, const void* base, size_t bytes, size_t len = 1) {
+  const char* q = static_cast<const char*>(p);
+  const char* b = static_cast<const char*>(base);
+  return q >= b && q + len <= b + bytes;
+}
+
 // ------------------------------------------------------------ primitives
 
 __device__ __forceinline__ uint64_t rotl64(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
@@ -290,6 +325,7 @@ __device__ __forceinline__ void build_chunk(const SweepIO& io, uint32_t c, doubl
         uint32_t base = 0;
         if (lane == leader) base = atomicAdd(io.hcount, (uint32_t)__popc(m));
         base = __shfl_sync(FULL, base, leader);
+        PSL_CHK(!want || base + __popc(m & ((1u << lane) - 1)) < io.L, 33);
         if (want) io.hlist[base + __popc(m & ((1u << lane) - 1))] = make_int2((int)k, cv);
       }
     }
@@ -410,6 +446,7 @@ __device__ __forceinline__ void sweep(const SweepIO& io, const Smem& sm, const b
         uint32_t Bp[kJ], Ap[kJ];
         if (cls != CLS_TAIL) {
           if (adj) {
+            PSL_CHK(sb_ok(pB + 2 - sb, L) && sb_ok(pA - sb, L), 30);
             const uint32_t b0 = pB[0], b1 = pB[1], b2 = pB[2];
             const uint32_t a0 = pA[0], a1 = pA[1], a2 = pA[2];
             XB = __funnelshift_r(b0, b1, shB); YB = __funnelshift_r(b1, b2, shB);
@@ -1296,7 +1333,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           }
           PT_MARK(4);
           if (c < c_end) {   // zone-1 cross MMAs (all warps); band-1 cells (warps 8-15)
-            cert_cross_chunk(io, ln, c, acc, nmma);          // all 16 warps, 64 rows each
+            cert_cross_chunk(io, cs, ln, c, acc, nmma);          // all 16 warps, 64 rows each
             PT_MARK(5);
             if (io.chain && t == kCertThreads - 64) cert_chain_chunk(io, cs, c, chain);
             if (t >= (uint32_t)kThreads && cert_band_chunk(io, c)) cert_band_cells(io, cs, c, sm.sb, Bs, t - kThreads);
@@ -1412,6 +1449,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
             const double Err = E0 + 2.0 * gB * B4 + 2.0 * g8 * Abs + u * (fabs(lin) + fabs(xv)) +
                                a.cert_slack * Abs;
             const double hv = 0.25 * (T4 + Err) * (1.0 + gL) * (1.0 + 8.0 * u);
+            PSL_CHK(rho < (uint32_t)kGroup, 31);
             ivm[rho] = isfinite(hv) ? 0.25 * T4 : __longlong_as_double(0x7ff8000000000000ll);   // -> bad
             ivl[rho] = fmax(0.0, 0.25 * (T4 - Err)) * (1.0 - gL) * (1.0 - 8.0 * u);
             ivh[rho] = hv;
@@ -1449,6 +1487,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
 #pragma unroll
         for (int m = 0; m < kJ; ++m) {
           if (active[m] && ibase + m + 1 == bi) { ctl->gv_lo = lo[m]; ctl->gv_hi = hi[m]; }
+          PSL_CHK(!(active[m] && ngrp > 1) || ibase + m < a.n, 32);
           if (active[m] && ngrp > 1) lo_all[ibase + m] = lo[m];
         }
         __syncthreads();

@@ -25,6 +25,8 @@ def main():
     steps = [int(x) for x in sys.argv[1:4]] or [20000, 6000, 2500]
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     for (m, S) in zip((16, 18, 20), steps):
+        if S <= 0:
+            continue
         L = (1 << m) - 1
         p = P.SearchParams(length=L, seed=11, alpha1=4, alpha2=P.default_alpha2(L),
                            ls_lmt=1 << 30, flip_lmt=10, n_lmt=1024,
