@@ -506,31 +506,37 @@ __device__ __forceinline__ void umma_i8_elect(uint32_t tmem_d, uint64_t da, uint
 }
 
 // One direction's MMAs of iteration c (dir 0: forward kappa-chunk c, 1:
-// reversed kappa'-chunk c - kLag), issued by a whole warp, then committed.  The
-// commit also arrives when the warp issued nothing (two issuing warps, one
-// barrier arrival each per iteration).
+// reversed kappa'-chunk c - kLag), K-steps s0 <= s < s1, issued by a whole warp;
+// with `commit` the warp then commits them (and its earlier ones) to the
+// iteration's barrier.  The commit also arrives when the warp issued nothing (two
+// issuing warps, one barrier arrival each per iteration).  The 16 K-steps are
+// issued in two halves around other work: the issuing thread blocks while the
+// tensor pipe's queue (2-3 MMAs) is full, so each half mostly finds it drained.
 __device__ __forceinline__ void cert_issue_dir(const CertSmem& cs, uint32_t tmem, int32_t c, int dir,
-                                               bool active, uint32_t started, uint64_t* mbar) {
+                                               bool active, uint32_t started, uint64_t* mbar,
+                                               int s0, int s1, bool commit) {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (active) {
     const uint32_t abuf = smem_u32(cs.acore) + (uint32_t)(c & 1) * (uint32_t)kABuf +
                           (dir ? (uint32_t)(kACores * 128) : 0u);
     const uint32_t ring = smem_u32(cs.dring);
     const long long q0 = dir ? (long long)(kCC / 16) * (c - (int32_t)kLag) : (long long)(kCC / 16) * c - 56;
-    uint64_t da = umma_desc(abuf, 256, 128);
-    uint64_t db = umma_desc(ring + (uint32_t)((((q0 % kRing) + kRing) % kRing) * 128), 128, 1024);
+    uint64_t da = umma_desc(abuf, 256, 128) + (uint64_t)(s0 * (512 >> 4));
+    uint64_t db = umma_desc(ring + (uint32_t)((((q0 % kRing) + kRing) % kRing) * 128), 128, 1024) +
+                  (uint64_t)(s0 * (256 >> 4));
     const uint32_t bit = dir ? 2u : 1u;
-#pragma unroll
-    for (int s = 0; s < kCCols; ++s) {
+#pragma unroll 4
+    for (int s = s0; s < s1; ++s) {
       umma_i8_elect(tmem + (dir ? 64u : 0u), da, db, (s > 0 || (started & bit)) ? 1u : 0u);
       da += 512 >> 4;
       db += 256 >> 4;
     }
   }
-  asm volatile(
-      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
-          smem_u32(mbar)) : "memory");
+  if (commit)
+    asm volatile(
+        "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(
+            smem_u32(mbar)) : "memory");
 }
 
 // ---- the cross term on mma.sync (zone-1 chunks)

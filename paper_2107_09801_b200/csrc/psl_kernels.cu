@@ -1021,6 +1021,9 @@ __device__ __forceinline__ int compare_local(const WalkState& S, double lo, doub
 #ifndef PSL_REV_WARP
 #define PSL_REV_WARP 14
 #endif
+#ifndef PSL_ISSUE_SPLIT
+#define PSL_ISSUE_SPLIT 1          // 2: issue a direction in two halves around other work (measured: +-1 %)
+#endif
 
 // Timing-only instrumentation (-DPSL_PHASE_TIMING, tools/ablate.sh): per-warp
 // cycles per phase of the certified chunk loop, printed by CTA 0 at exit.
@@ -1281,15 +1284,21 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         // then the zone-1 cross MMAs (mma.sync) and band-1 cells of chunk c
         PT_MARK(7);
         {
-        // warp 15 issues the forward MMAs of chunk c right after its barrier,
-        // warp 14 the reversed ones at the top of the next iteration (after the
-        // forward ones drained): the tensor-pipe wait is split over two warps
+        // warp 15 issues the forward MMAs of chunk c: half right after the chunk
+        // barrier, half after its cross / band work; warp 14 the reversed ones
+        // in the next iteration: half at the loop top, half after its build.  So
+        // the tensor-pipe waits are split over two warps and two points each.
+        constexpr int kHalf = PSL_ISSUE_SPLIT > 1 ? kCCols / 2 : kCCols;
         int32_t pend_c = -1;
         bool pend_rv = false;
         uint32_t pend_started = 0;
         for (uint32_t c = 0; c < c_end + kLag; ++c) {
+          int32_t rv_c = -1;         // this iteration finishes the reversed MMAs of rv_c
           if (pend_c >= 0) {
-            if ((t >> 5) == PSL_REV_WARP) cert_issue_dir(cs, tmem, pend_c, 1, pend_rv, pend_started, &ctl->mbar[pend_c & 1]);
+            if ((t >> 5) == PSL_REV_WARP)
+              cert_issue_dir(cs, tmem, pend_c, 1, pend_rv, pend_started, &ctl->mbar[pend_c & 1], 0, kHalf,
+                             kHalf == kCCols);
+            rv_c = pend_c;
             pend_c = -1;
           }
           if (issued & (1u << (c & 1))) {      // MMAs of iteration c - 2 read this buffer
@@ -1312,6 +1321,8 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           } else {
             cert_zero_digits(cs, c);
           }
+          if (kHalf < kCCols && rv_c >= 0 && (t >> 5) == PSL_REV_WARP)
+            cert_issue_dir(cs, tmem, rv_c, 1, pend_rv, pend_started, &ctl->mbar[rv_c & 1], kHalf, kCCols, true);
           PT_MARK(1);
           cert_cores(io, cs, (int32_t)c, sm.sb, fw, rv);
           PT_MARK(2);
@@ -1325,7 +1336,8 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           if ((fw || rv)) {
 #endif
             // warp 15 (stages no cores) issues, one lane elected per MMA
-            if ((t >> 5) == PSL_FWD_WARP) cert_issue_dir(cs, tmem, (int32_t)c, 0, fw, started, &ctl->mbar[c & 1]);
+            if ((t >> 5) == PSL_FWD_WARP)
+              cert_issue_dir(cs, tmem, (int32_t)c, 0, fw, started, &ctl->mbar[c & 1], 0, kHalf, kHalf == kCCols);
             pend_c = (int32_t)c; pend_rv = rv; pend_started = started;
             started |= (fw ? 1u : 0u) | (rv ? 2u : 0u);   // uniform copy of the issuer's flags
             numma += (fw ? kCCols : 0) + (rv ? kCCols : 0);
@@ -1339,8 +1351,11 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
             if (t >= (uint32_t)kThreads && cert_band_chunk(io, c)) cert_band_cells(io, cs, c, sm.sb, Bs, t - kThreads);
             PT_MARK(6);
           }
+          if (kHalf < kCCols && pend_c == (int32_t)c && (t >> 5) == PSL_FWD_WARP)
+            cert_issue_dir(cs, tmem, (int32_t)c, 0, fw, pend_started, &ctl->mbar[c & 1], kHalf, kCCols, true);
         }
-        if (pend_c >= 0 && (t >> 5) == PSL_REV_WARP) cert_issue_dir(cs, tmem, pend_c, 1, pend_rv, pend_started, &ctl->mbar[pend_c & 1]);
+        if (pend_c >= 0 && (t >> 5) == PSL_REV_WARP)
+          cert_issue_dir(cs, tmem, pend_c, 1, pend_rv, pend_started, &ctl->mbar[pend_c & 1], 0, kCCols, true);
         }
         PT_MARK(0);
         // the tail chunks, streamed while the last MMAs drain
