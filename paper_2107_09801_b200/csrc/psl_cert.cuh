@@ -724,11 +724,14 @@ __device__ __forceinline__ void cert_lin_rows(uint32_t tmem, bool rev, uint32_t 
   }
 }
 
-// Exact band-1 terms of chunk c for this thread's rows rho = 4t + m: per cell
-// pow_int(|C_k - 2x|, alpha), x = s_j (s_{j-k} [k <= j] + s_{j+k} [j+k < L]).
+// Exact band-1 terms of chunk c for this thread's rows rho = kBandRows t + m: per
+// cell pow_int(|C_k - 2x|, alpha), x = s_j (s_{j-k} [k <= j] + s_{j+k} [j+k < L]),
+// each row's terms added serially in ascending k.  All 16 warps take rows (two
+// each), so the few band chunks of a pass do not stall half the CTA.
+constexpr int kBandRows = kGroup / kCertThreads;
 __device__ __forceinline__ void cert_band_cells(const CertIO& io, const CertSmem& cs, uint32_t c,
-                                                const uint32_t* __restrict__ sb, double (&Bs)[kJ],
-                                                uint32_t owner) {
+                                                const uint32_t* __restrict__ sb,
+                                                double (&Bs)[kBandRows], uint32_t owner) {
   const uint32_t kb = cert_kb(c);
   const uint32_t ke = min(kb + kCC - 1, io.L - 1);
   const int32_t* rec = cs.rec + (size_t)(c & 1) * kCC;
@@ -741,8 +744,8 @@ __device__ __forceinline__ void cert_band_cells(const CertIO& io, const CertSmem
   const uint32_t bhi = min(ke, io.m_hi);
   if (blo > bhi) return;
 #pragma unroll
-  for (int m = 0; m < kJ; ++m) {
-    const uint32_t rho = 4 * owner + m;
+  for (int m = 0; m < kBandRows; ++m) {
+    const uint32_t rho = kBandRows * owner + m;
     if (rho < io.r_lo || rho >= io.r_hi) continue;
     const uint32_t j = (uint32_t)(io.j0 + (int32_t)rho);
     const uint32_t sjb = (sb[(j >> 5) + 1] >> (j & 31)) & 1u;

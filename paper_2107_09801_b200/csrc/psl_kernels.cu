@@ -1240,7 +1240,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           for (int e = 0; e < 4; ++e) acc[r][e] = 0;
         bool ovf = false;
         double part[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
-        double Bs[kJ] = {0.0, 0.0, 0.0, 0.0};
+        double Bs[kBandRows] = {0.0, 0.0};   // band-1 sums of rows kBandRows t + m
         int32_t pmax = 0;
         uint32_t nmma = 0, numma = 0, started = 0;
         const uint32_t tmem = ctl->tmem;
@@ -1348,7 +1348,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
             cert_cross_chunk(io, cs, ln, c, acc, nmma);          // all 16 warps, 64 rows each
             PT_MARK(5);
             if (io.chain && t == kCertThreads - 64) cert_chain_chunk(io, cs, c, chain);
-            if (t >= (uint32_t)kThreads && cert_band_chunk(io, c)) cert_band_cells(io, cs, c, sm.sb, Bs, t - kThreads);
+            if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, sm.sb, Bs, t);
             PT_MARK(6);
           }
           if (kHalf < kCCols && pend_c == (int32_t)c && (t >> 5) == PSL_FWD_WARP)
@@ -1360,6 +1360,12 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         PT_MARK(0);
         // the tail chunks, streamed while the last MMAs drain
         cert_tail(io, c_end, nch, sm.sb, pmax, part);
+        // band-1 row sums to the row-interval scratch (read back by the row owners)
+#pragma unroll
+        for (int m = 0; m < kBandRows; ++m) {
+          const uint32_t rho = kBandRows * t + m;
+          if (rho >= r_lo && rho < r_hi) ivm[rho] = Bs[m];
+        }
         for (uint32_t bb = 0; bb < 2; ++bb)
           if (issued & (1u << bb)) { mbar_wait(&ctl->mbar[bb], mb_par[bb]); mb_par[bb] ^= 1u; }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -1456,7 +1462,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
             const uint32_t j = (uint32_t)(j0 + (int32_t)rho);
             const double lin = linrow[rho], xv = xrow[rho];
             const uint32_t Mj = max(j, L - 1 - j);
-            const double B4 = __dadd_rn(__dmul_rn(4.0, Bs[m]),
+            const double B4 = __dadd_rn(__dmul_rn(4.0, ivm[rho]),   // band-1 sum, stored above
                                         cert_band2_const(io, ctl->M_hi - ctl->M_lo, Mj - ctl->M_lo));
             const int sj = sval(sm.sb, j);
             const double T4 = __dadd_rn(__dadd_rn(__dadd_rn(Sc, B4), sj > 0 ? lin : -lin), xv);
