@@ -39,6 +39,12 @@
 // builds one shift per chunk (kCC = 512); warps 15 and 14 also issue the
 // chunk's forward / reversed tcgen05 MMAs; all 16 warps run the cross MMAs.
 constexpr uint32_t kCertThreads = 2 * kThreads;
+#ifndef PSL_WIN_BALANCE
+#define PSL_WIN_BALANCE 1
+#endif
+#ifndef PSL_REV_WARP_C
+#define PSL_REV_WARP_C 14u         // the warp that issues the reversed MMAs (PSL_REV_WARP)
+#endif
 constexpr uint32_t kCC = kCertThreads;        // shifts per certified chunk (one per builder thread)
 constexpr int kCCols = kCC / 32;              // 32-shift columns per chunk
 constexpr int kCertTiles = 4;                 // mma.sync m16 row tiles per warp (64 rows, 16 warps)
@@ -260,9 +266,12 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
     }
   }
   // fixed point -> 8 balanced base-256 digits
-  const long long hv = __double2ll_rn(__dmul_rn(H, io.scaleH));
-  // |v| < 2^61 (the units leave a 4x margin under 2^62 < kMaxD): top 3 bits all equal
-  ovf |= (((unsigned long long)hv + (1ull << 61)) >> 62) != 0;
+  const double hs = __dmul_rn(H, io.scaleH);
+  // |v| < 2^61 (the units leave a 4x margin under 2^62 < kMaxD), tested on the
+  // double (doubles near 2^61 are 512 apart, so the rounded value is below it too;
+  // NaN fails the test)
+  ovf |= !(fabs(hs) < 0x1p61);
+  const long long hv = __double2ll_rn(hs);
   const unsigned long long dh = ((unsigned long long)hv + 0x8080808080808080ull) ^ 0x8080808080808080ull;
   // H4 digit core: core q = 16 c + t / 16 holds rows d (16 shifts each).  Lane
   // x of a 4-lane group assembles row (x & 3) / row 4 + (x & 3) of the group's
@@ -297,8 +306,9 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
   if (kb > io.m_lo) return;
   // zone-1 chunk: R4 digit rows and the sequence windows of the cross MMAs
   {
-    const long long rv = __double2ll_rn(__dmul_rn(R, io.scaleR));
-    ovf |= (((unsigned long long)rv + (1ull << 61)) >> 62) != 0;
+    const double rs = __dmul_rn(R, io.scaleR);
+    ovf |= !(fabs(rs) < 0x1p61);
+    const long long rv = __double2ll_rn(rs);
     const unsigned long long dr = ((unsigned long long)rv + 0x8080808080808080ull) ^ 0x8080808080808080ull;
     unsigned char* lr = cs.limbR + (size_t)b * kLimbBuf + t;
     PSL_CHK(in_buf(lr + 7 * kLimbStride, cs.limbR, 2 * kLimbBuf), 8);
@@ -312,7 +322,7 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
   constexpr int kW = kWinBytes / 4;
   // thread -> base word q of one direction: bytes 4q..4q+7 of the base copy
   // from one bit window, copy a word q = base bytes 4q+a..4q+a+3
-  for (int idx = (int)t; idx < 2 * kW; idx += (int)kCC) {
+  auto stage = [&](int idx) {
     const int dir = idx >= kW ? 1 : 0;
     const int q = dir ? idx - kW : idx;
     // fwd: byte i <-> position p0 + i; rev: byte i <-> position p0 - i (i = 0..7)
@@ -339,7 +349,20 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
     *reinterpret_cast<uint32_t*>(dst + kWinBytes) = __funnelshift_r(w0, w1, 8);
     *reinterpret_cast<uint32_t*>(dst + 2 * kWinBytes) = __funnelshift_r(w0, w1, 16);
     *reinterpret_cast<uint32_t*>(dst + 3 * kWinBytes) = __funnelshift_r(w0, w1, 24);
+  };
+  // 2 kW = 784 words per chunk: one per thread, the other 272 to the warps that
+  // stage no sequence cores and issue no reversed MMAs before the barrier
+  // (11, 12, 13, 15), so the chunk barrier waits for no doubly loaded warp
+  stage((int)t);
+#if PSL_WIN_BALANCE
+  const uint32_t wp = t >> 5;
+  if (wp >= 11 && wp != PSL_REV_WARP_C) {
+    const int sidx = (int)((wp == 15 ? 3u : wp - 11u) * 32u + (t & 31u));
+    for (int e = (int)kCC + sidx; e < 2 * kW; e += 128) stage(e);
   }
+#else
+  if ((int)(t + kCC) < 2 * kW) stage((int)(t + kCC));
+#endif
 }
 
 // Tail chunks c0 <= c < nch (every shift past M_hi: H4 = R4 = 0, the term of

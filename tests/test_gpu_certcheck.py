@@ -67,3 +67,63 @@ def test_intervals_hold_across_phase_switches(engine, L, a2, n, steps):
     assert d["switches"] >= 4, d            # both phases, restarts included
     assert d["violations"] == 0 and d["decided_wrong"] == 0, d
     assert d["rows"] > 0 and d["decided"] > 0, d
+
+
+def _deep_m16():
+    import json
+    import os
+    import numpy as np
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "phase2.json")))
+    d = g["m16_deep_ls1"]
+    bits = np.unpackbits(np.frombuffer(bytes.fromhex(d["init_bits_hex"]), np.uint8),
+                         bitorder="little")[:65535]
+    return np.where(bits == 1, -1, 1).astype(np.int8)
+
+
+def test_intervals_hold_full_neighbourhood_in_both_phases(engine):
+    """Deep m16 warm start (the phase2.json fixture's), n_lmt 1024, ls_lmt 1: the
+    walks switch phase, so alpha2 = 13 steps score the full neighbourhood."""
+    ctx = engine.default_context()
+    init = _deep_m16()
+    ctx.set_cert_check(True)
+    try:
+        before = ctx.cert_check_stats()
+        p = engine.SearchParams(length=65535, seed=21, alpha1=4, alpha2=13, ls_lmt=1,
+                                flip_lmt=10, n_lmt=1024,
+                                stop=engine.StopCondition(max_nse=1 + 150 * 1024))
+        w = engine.Walks(p, 4, seeds=[21, 22, 23, 24], inits=init, ctx=ctx)
+        w.run()
+        recs = w.records()
+        w.close()
+    finally:
+        ctx.set_cert_check(False)
+    after = ctx.cert_check_stats()
+    assert sum(r.switches for r in recs) >= 4
+    assert after["violations"] == before["violations"]
+    assert after["decided_wrong"] == before["decided_wrong"]
+    assert after["rows"] - before["rows"] >= 4 * 100 * 1024
+
+
+@pytest.mark.slow
+def test_m20_auto_vs_exact_at_bench_scale(engine):
+    """The benchmarked configuration (m20, 444 walks = three waves, n_lmt 1024) with
+    ls_lmt 2, 50 steps: every walk's record and best sequence from the certified
+    scan equals the exact sweep's (A/B at scale)."""
+    import numpy as np
+    ctx = engine.default_context()
+    L = 1048575
+    p = engine.SearchParams(length=L, seed=1, alpha1=4, alpha2=10, ls_lmt=2, flip_lmt=10,
+                            n_lmt=1024, stop=engine.StopCondition(max_nse=1 + 50 * 1024))
+    out = {}
+    for mode in (ctx.SCAN_AUTO, ctx.SCAN_EXACT):
+        ctx.set_scan_mode(mode)
+        before = ctx.scan_stats()
+        out[mode] = engine.run_walks(p, 444, ctx=ctx)
+        after = ctx.scan_stats()
+        if mode == ctx.SCAN_AUTO:
+            assert after["certified"] - before["certified"] >= 444 * 45
+    ctx.set_scan_mode(ctx.SCAN_AUTO)
+    for a, b in zip(out[ctx.SCAN_AUTO], out[ctx.SCAN_EXACT]):
+        assert (a.seed, a.nse, a.psl_best, a.energy, a.switches, a.steps) == \
+            (b.seed, b.nse, b.psl_best, b.energy, b.switches, b.steps)
+        assert np.array_equal(a.solution_best, b.solution_best)
