@@ -58,7 +58,11 @@ constexpr int kY0 = 1031;                     // origin of the reversed window
 constexpr size_t kLimbBuf = 8ull * kLimbStride;
 constexpr size_t kWinBuf = 4ull * kWinBytes;
 constexpr size_t kCertRecBuf = (size_t)kCC * sizeof(int32_t);
-constexpr size_t kCertCBuf = (size_t)kCC * sizeof(int32_t);
+#ifndef PSL_BULK_C
+#define PSL_BULK_C 1               // C chunks by one bulk async copy (TMA engine); 0: per-thread cp.async
+#endif
+constexpr uint32_t kCSlot = kCC + 4;          // C ring slot: the 16-byte aligned span C[kb-1, kb+515)
+constexpr size_t kCertCBuf = (size_t)kCSlot * sizeof(int32_t);
 constexpr size_t kDRing = 2ull * kRing * 128;            // digit cores, double mapped
 constexpr size_t kABuf = 2ull * kACores * 128;           // fwd + rev cores, one buffer
 // [digit ring][A cores 2][R digit rows 2][win_f 2][win_r 2][rec 2][C ring 3]
@@ -94,6 +98,8 @@ struct CertIO {
   bool chain;                                 // also the serial fitness() of the folded table
   bool fsum;                                  // the initial fitness() as a certified interval:
                                               // builders add lut[|C_k|] into part[3]
+  size_t c_stride;                            // C entries per walk (a multiple of 32)
+  uint64_t* cbar;                             // [3] mbarriers of the C ring's bulk copies
 };
 
 struct CertSmem {
@@ -161,23 +167,59 @@ __device__ __forceinline__ uint4 seq16(const uint32_t* sb, long long p0, int dir
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-// C_k of this thread's shift of chunk c -> ring slot c % 3, asynchronously
-// (cp.async, zero-filled past L); the thread itself consumes it in cert_build
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}\n" : "=r"(done) : "r"(smem_u32(mbar)), "r"(parity) : "memory");
+  }
+}
+
+// C_k of chunk c -> ring slot c % 3, asynchronously.  PSL_BULK_C: thread 0
+// issues ONE bulk copy (cp.async.bulk, the TMA engine) of the 16-byte aligned
+// span C[kb-1, kb+515) (clamped to the walk's c_stride entries; shifts >= L are
+// never used) that completes on the slot's mbarrier; otherwise every thread
+// copies its own 4 bytes with cp.async (zero-filled past L).
 __device__ __forceinline__ void cert_prefetch(const CertIO& io, const CertSmem& cs, uint32_t c) {
+#if PSL_BULK_C
+  if (threadIdx.x != 0) return;
+  const uint32_t slot = c % 3;
+  const size_t base = (size_t)cert_kb((int32_t)c) - 1;                 // = kCC * c, 16-byte aligned
+  const uint32_t n = (uint32_t)min((size_t)kCSlot, io.c_stride - base);
+  const uint32_t bytes = n * 4u;                                         // a multiple of 128
+  int32_t* dst = cs.cring + (size_t)slot * kCSlot;
+  PSL_CHK(in_buf(dst, cs.cring, 3 * kCertCBuf, bytes) && n > 0 && (base & 3) == 0, 1);
+  const uint32_t bar = smem_u32(io.cbar + slot);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(io.Csrc + base), "r"(bytes), "r"(bar) : "memory");
+#else
   const uint32_t k = cert_kb(c) + threadIdx.x;
-  int32_t* dst = cs.cring + (size_t)(c % 3) * kCC + threadIdx.x;
+  int32_t* dst = cs.cring + (size_t)(c % 3) * kCSlot + 1 + threadIdx.x;
   const bool in = k < io.L;
   PSL_CHK(in_buf(dst, cs.cring, 3 * kCertCBuf, 4), 1);
   const int32_t* src = io.Csrc + (in ? k : 0);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src),
                "r"(in ? 4 : 0) : "memory");
   asm volatile("cp.async.commit_group;" ::: "memory");
+#endif
 }
-__device__ __forceinline__ int32_t cert_take(const CertSmem& cs, uint32_t c, int pending) {
+// This thread's C_k of chunk c (after the slot's copy landed).  cphase: bit s =
+// the parity of slot s's next completion (kept by every thread across passes).
+__device__ __forceinline__ int32_t cert_take(const CertIO& io, const CertSmem& cs, uint32_t c,
+                                             int pending, uint32_t& cphase) {
+  const uint32_t slot = c % 3;
+#if PSL_BULK_C
+  (void)pending;
+  mbar_wait(io.cbar + slot, (cphase >> slot) & 1u);
+  cphase ^= 1u << slot;
+#else
+  (void)io; (void)cphase;
   if (pending >= 2) asm volatile("cp.async.wait_group 2;" ::: "memory");
   else if (pending == 1) asm volatile("cp.async.wait_group 1;" ::: "memory");
   else asm volatile("cp.async.wait_group 0;" ::: "memory");
-  return cs.cring[(size_t)(c % 3) * kCC + threadIdx.x];
+#endif
+  return cs.cring[(size_t)slot * kCSlot + 1 + threadIdx.x];
 }
 
 __device__ __forceinline__ unsigned char* dcore(const CertSmem& cs, long long q) {
@@ -510,13 +552,6 @@ __device__ __forceinline__ void umma_i8(uint32_t tmem_d, uint64_t da, uint64_t d
 __device__ __forceinline__ void umma_commit(uint64_t* mbar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                    smem_u32(mbar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-                 "selp.u32 %0, 1, 0, p;\n\t}\n" : "=r"(done) : "r"(smem_u32(mbar)), "r"(parity) : "memory");
-  }
 }
 
 // One tcgen05 MMA issued by a whole warp: warp-uniform descriptors, one lane

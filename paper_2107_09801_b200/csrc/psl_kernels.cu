@@ -205,6 +205,7 @@ struct Ctl {
   double rs5[5][16];
   uint32_t cfw[72], crv[72]; // per-chunk tcgen05 flags of the pass segment (bit c: fwd / rev MMAs)
   uint64_t mbar[2];          // tcgen05 commit barriers (iteration parity)
+  uint64_t cbar[3];          // bulk-copy barriers of the certified C ring (one per slot)
   uint32_t tmem;             // TMEM base of this CTA's accumulators (kTmemCols columns)
   // certificate check mode (RunArgs::cert_check)
   int32_t chk_on, chk_dec, chk_cmp;
@@ -218,7 +219,7 @@ constexpr size_t kHfBytes = (size_t)kHCap * sizeof(int2);
 constexpr size_t kCtlBytes = (sizeof(Ctl) + 15) & ~size_t(15);
 // the exact sweep's records and the certified scan's buffers share one region
 // (psl_cert.cuh: 4 digit rows + 4 window copies + 2 record buffers)
-constexpr size_t kCertRegion = 2ull * 256 * 128 + 2ull * (2 * 82 * 128) + 2ull * 8 * (512 + 16) +
+constexpr size_t kCertRegion = 2ull * 256 * 128 + 2ull * (2 * 82 * 128) + 2ull * 8 * (512 + 16) + 48 +
                                  4ull * 4 * 1568 + 2ull * 512 * 4 + 3ull * 512 * 4;
 constexpr size_t kExactMain = kTabBytes + kTailBytes;
 
@@ -1078,6 +1079,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
   __syncthreads();
   if (ctl->st.done || ctl->st.status != PSL_OK) return;
   uint32_t mb_par[2] = {0u, 0u};   // next phase parity to wait for on ctl->mbar[0/1]
+  uint32_t cphase = 0u;             // ... on ctl->cbar[0..2] (bit per slot)
   if (kCert) {
     if (t < 32) {   // the certified scan's tcgen05 accumulators live in TMEM
       asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -1088,6 +1090,8 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
       // two committing warps per iteration (forward: warp 15, reversed: warp 14)
       for (int i = 0; i < 2; ++i)
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 2;" ::"r"(smem_u32(&ctl->mbar[i])) : "memory");
+      for (int i = 0; i < 3; ++i)   // C ring: thread 0's arrive.expect_tx + the copy's bytes
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&ctl->cbar[i])) : "memory");
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1222,6 +1226,8 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         io.m_lo = ctl->m_lo; io.m_hi = ctl->m_hi; io.M_lo = ctl->M_lo; io.M_hi = ctl->M_hi;
         io.b2M = a.b2 + (size_t)w * 2 * kGroup;
         io.b2E = io.b2M + kGroup;
+        io.c_stride = a.c_stride;
+        io.cbar = ctl->cbar;
         // first step / restart: fitness() of the folded table, serially, by one
         // thread of warp 14 behind the builder (search.cpp:348, :409)
         // the first step's value_local (search.cpp:348) as an interval from a
@@ -1315,7 +1321,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
               if (c + 2 < c_end) cert_prefetch(io, cs, c + 2);
               const uint2 fnext = (io.F == 1 && c + 1 < c_end) ? cert_fold_words(io, c + 1, sm.sb) : fwords;
               const int pending = (int)min(2u, c_end - 1 - c);
-              cert_build(io, cs, c, sm.sb, pmax, part, cert_take(cs, c, pending), fwords, ovf);
+              cert_build(io, cs, c, sm.sb, pmax, part, cert_take(io, cs, c, pending, cphase), fwords, ovf);
               fwords = fnext;
             }
           } else {
