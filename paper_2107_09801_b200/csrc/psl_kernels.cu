@@ -1022,6 +1022,9 @@ __device__ __forceinline__ int compare_local(const WalkState& S, double lo, doub
 #ifndef PSL_REV_WARP
 #define PSL_REV_WARP 14
 #endif
+#ifndef PSL_STAGGER
+#define PSL_STAGGER 1              // half the warps cross-then-build, half build-then-cross
+#endif
 #ifndef PSL_ISSUE_SPLIT
 #define PSL_ISSUE_SPLIT 1          // 2: issue a direction in two halves around other work (measured: +-1 %)
 #endif
@@ -1295,6 +1298,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         // in the next iteration: half at the loop top, half after its build.  So
         // the tensor-pipe waits are split over two warps and two points each.
         constexpr int kHalf = PSL_ISSUE_SPLIT > 1 ? kCCols / 2 : kCCols;
+        const bool early = t < (uint32_t)kThreads;   // warps 0-7 (PSL_STAGGER)
         int32_t pend_c = -1;
         bool pend_rv = false;
         uint32_t pend_started = 0;
@@ -1330,6 +1334,14 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           if (kHalf < kCCols && rv_c >= 0 && (t >> 5) == PSL_REV_WARP)
             cert_issue_dir(cs, tmem, rv_c, 1, pend_rv, pend_started, &ctl->mbar[rv_c & 1], kHalf, kCCols, true);
           PT_MARK(1);
+          // PSL_STAGGER: warps 0-7 run the cross MMAs / band cells of chunk c - 1
+          // after building chunk c, warps 8-15 before (end of the previous
+          // iteration), so one half's builder overlaps the other half's IMMA work
+          // inside every barrier interval (buffers of c - 1 live until iteration c + 1)
+          if (PSL_STAGGER && early && c >= 1 && c - 1 < c_end) {
+            cert_cross_chunk(io, cs, ln, c - 1, acc, nmma);
+            if (cert_band_chunk(io, c - 1)) cert_band_cells(io, cs, c - 1, sm.sb, Bs, t);
+          }
           cert_cores(io, cs, (int32_t)c, sm.sb, fw, rv);
           PT_MARK(2);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1350,8 +1362,8 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
             issued |= 1u << (c & 1);
           }
           PT_MARK(4);
-          if (c < c_end) {   // zone-1 cross MMAs (all warps); band-1 cells (warps 8-15)
-            cert_cross_chunk(io, cs, ln, c, acc, nmma);          // all 16 warps, 64 rows each
+          if (c < c_end && !(PSL_STAGGER && early)) {   // zone-1 cross MMAs, band-1 cells
+            cert_cross_chunk(io, cs, ln, c, acc, nmma);          // 64 rows per warp
             PT_MARK(5);
             if (io.chain && t == kCertThreads - 64) cert_chain_chunk(io, cs, c, chain);
             if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, sm.sb, Bs, t);

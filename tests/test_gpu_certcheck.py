@@ -127,3 +127,25 @@ def test_m20_auto_vs_exact_at_bench_scale(engine):
         assert (a.seed, a.nse, a.psl_best, a.energy, a.switches, a.steps) == \
             (b.seed, b.nse, b.psl_best, b.energy, b.switches, b.steps)
         assert np.array_equal(a.solution_best, b.solution_best)
+
+
+@pytest.mark.parametrize("L,a1,a2", [(1048575, 4, 10), (262143, 11, 4)])
+def test_forced_fallbacks_at_baseline_lengths(engine, monkeypatch, L, a1, a2):
+    """Widened intervals (PSLB200_CERT_SLACK) at m20 / m18 push many steps onto the
+    exact re-score and the exact value_local chain (the fallback the benchmark
+    never needed at m20): the records still equal the exact sweep's."""
+    import numpy as np
+    ctx = engine.default_context()
+    p = engine.SearchParams(length=L, seed=9, alpha1=a1, alpha2=a2, ls_lmt=2, flip_lmt=10,
+                            n_lmt=1024, stop=engine.StopCondition(max_nse=1 + 6 * 1024))
+    ctx.set_scan_mode(ctx.SCAN_EXACT)
+    ref = engine.run_walks(p, 3, ctx=ctx)
+    ctx.set_scan_mode(ctx.SCAN_AUTO)
+    monkeypatch.setenv("PSLB200_CERT_SLACK", "1e-5")
+    before = ctx.scan_stats()
+    got = engine.run_walks(p, 3, ctx=ctx)
+    after = ctx.scan_stats()
+    assert after["refined"] - before["refined"] > 0
+    for a, b in zip(got, ref):
+        assert (a.nse, a.psl_best, a.energy) == (b.nse, b.psl_best, b.energy)
+        assert np.array_equal(a.solution_best, b.solution_best)
