@@ -40,7 +40,7 @@
 // chunk's forward / reversed tcgen05 MMAs; all 16 warps run the cross MMAs.
 constexpr uint32_t kCertThreads = 2 * kThreads;
 #ifndef PSL_WIN_BALANCE
-#define PSL_WIN_BALANCE 1
+#define PSL_WIN_BALANCE 0          // 1: window words moved to the warps without core/issue work (measured +3 %)
 #endif
 #ifndef PSL_REV_WARP_C
 #define PSL_REV_WARP_C 14u         // the warp that issues the reversed MMAs (PSL_REV_WARP)
