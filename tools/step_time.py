@@ -38,11 +38,14 @@ def main():
     ap.add_argument("--walks", type=int, default=296)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--mode", default="both")
+    ap.add_argument("--n-lmt", type=int, default=0)
     a = ap.parse_args()
     ctx = P.Context(0)
     p = P.default_params(a.length)
+    if a.n_lmt:
+        p.n_lmt = a.n_lmt
     p.stop = P.StopCondition(max_nse=1 << 62)
-    out = {"L": a.length, "walks": a.walks, "steps": a.steps}
+    out = {"L": a.length, "walks": a.walks, "steps": a.steps, "n_lmt": p.n_lmt}
     for name, mode in (("auto", ctx.SCAN_AUTO), ("exact", ctx.SCAN_EXACT)):
         if a.mode not in ("both", name):
             continue
