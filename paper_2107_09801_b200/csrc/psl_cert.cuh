@@ -509,9 +509,12 @@ __device__ __forceinline__ void cert_cores(const CertIO& io, const CertSmem& cs,
   unsigned char* base = cs.acore + (size_t)(c & 1) * kABuf;
   constexpr uint32_t kQuads = kACores * 2;    // 100 groups of 4 rows per direction
   const uint32_t t = threadIdx.x;
+  // forward quads on threads 0..163, reversed on 192..355: no warp runs both
+  // directions' code (a mixed warp took twice as long and held up the barrier)
+  constexpr uint32_t kRevT = (kQuads + 31) / 32 * 32;
   uint32_t dir, g;
   if (t < kQuads) { dir = 0; g = t; }
-  else if (t < 2 * kQuads) { dir = 1; g = t - kQuads; }
+  else if (t >= kRevT && t < kRevT + kQuads) { dir = 1; g = t - kRevT; }
   else return;
   if (dir == 0 ? !fwd : !rev) return;
 #ifdef PSL_ABLATE_CORES
