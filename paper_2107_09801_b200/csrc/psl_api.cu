@@ -10,6 +10,8 @@
 // There is no CPU fallback: without a CUDA device every compute entry point
 // returns PSL_ERR_CUDA.
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -36,6 +38,11 @@ struct psl_ctx {
   int cert_check = 0;
   uint64_t chk[5] = {0, 0, 0, 0, 0};
   double chk_max[2] = {0.0, 0.0};
+  // pinned staging of host-packed warm starts (grow-only) and the event after
+  // its last upload (the next packing waits for it)
+  uint32_t* pack_host = nullptr;
+  size_t pack_cap = 0;
+  cudaEvent_t pack_done = nullptr;
 };
 
 struct psl_walks {
@@ -53,8 +60,7 @@ struct psl_walks {
   psl_event* events = nullptr;
   psl_trace* traces = nullptr;
   uint64_t* seeds = nullptr;
-  int8_t* inits = nullptr;      // device copy of warm starts (int8 +-1)
-  uint32_t* bad = nullptr;      // [first bad flat index + 1, value]
+  uint32_t* packed = nullptr;   // device copy of the host-packed warm starts (setup only)
   int8_t* sol = nullptr;        // unpack scratch for solutions
   int8_t* sol_direct = nullptr; // host buffer the run kernel wrote the solutions into (psl_run_walks)
   double* lut = nullptr;        // [2][lut_n] power tables
@@ -147,6 +153,43 @@ struct Scratch {
   ~Scratch() { for (void* q : p) cudaFreeAsync(q, s); }
 };
 
+// One walk's warm start -> nw bit words (bit = 1 <-> -1), validating every
+// element as the BinarySequence ctor does (sequence.cpp:20-35).  Returns the first
+// offending position + 1 (0 when valid) and its value in *badv.  8 elements per
+// 64-bit word: (b + 1) mod 256 in {0x00, 0x02} <=> b in {+1, -1}; the sign bits
+// are gathered by the 0x0102040810204080 multiply.
+uint64_t pack_walk(const int8_t* s, uint32_t L, uint32_t* dst, int* badv) {
+  const uint32_t full = L / 32;
+  for (uint32_t i = 0; i < full; ++i) {
+    uint32_t word = 0;
+    uint64_t badm = 0;
+    for (int q = 0; q < 4; ++q) {
+      uint64_t v;
+      std::memcpy(&v, s + 32 * (size_t)i + 8 * q, 8);
+      const uint64_t inc = ((v & 0x7F7F7F7F7F7F7F7Full) + 0x0101010101010101ull) ^ (v & 0x8080808080808080ull);
+      badm |= inc & 0xFDFDFDFDFDFDFDFDull;
+      word |= (uint32_t)((((v >> 7) & 0x0101010101010101ull) * 0x0102040810204080ull) >> 56) << (8 * q);
+    }
+    if (badm) {
+      for (uint32_t j = 0; j < 32; ++j) {
+        const int8_t e = s[32 * (size_t)i + j];
+        if (e != 1 && e != -1) { *badv = e; return 32ull * i + j + 1; }
+      }
+    }
+    dst[i] = word;
+  }
+  if (full * 32 < L) {
+    uint32_t word = 0;
+    for (uint32_t j = full * 32; j < L; ++j) {
+      const int8_t e = s[j];
+      if (e != 1 && e != -1) { *badv = e; return (uint64_t)j + 1; }
+      word |= (uint32_t)(e < 0) << (j & 31);
+    }
+    dst[full] = word;
+  }
+  return 0;
+}
+
 }  // namespace
 
 extern "C" {
@@ -196,6 +239,8 @@ void psl_ctx_destroy(psl_ctx* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->own) cudaStreamDestroy(ctx->own);
   if (ctx->copy) cudaStreamDestroy(ctx->copy);
+  if (ctx->pack_done) { cudaEventSynchronize(ctx->pack_done); cudaEventDestroy(ctx->pack_done); }
+  if (ctx->pack_host) cudaFreeHost(ctx->pack_host);
   delete ctx;
 }
 
@@ -652,7 +697,7 @@ void psl_walks_destroy(psl_walks* w) {
   cudaStream_t s = w->ctx->stream;
   for (void* p : {(void*)w->st, (void*)w->Cpiv, (void*)w->Cloc, (void*)w->bits, (void*)w->hlist,
                   (void*)w->flips, (void*)w->events, (void*)w->traces, (void*)w->seeds,
-                  (void*)w->inits, (void*)w->bad, (void*)w->sol, (void*)w->lut, (void*)w->b2,
+                  (void*)w->packed, (void*)w->sol, (void*)w->lut, (void*)w->b2,
                   (void*)w->lo_buf, (void*)w->iv_buf})
     if (p) cudaFreeAsync(p, s);
   delete w;
@@ -736,75 +781,134 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
   for (uint32_t w = 0; w < n_walks; ++w) sd[w] = seeds ? seeds[w] : p.seed + w;
   if ((e = cudaMemcpyAsync(W->seeds, sd.data(), 8ull * n_walks, cudaMemcpyHostToDevice, s)) != cudaSuccess)
     return fail(e, "seeds");
-  // warm starts travel as int8 and are validated + packed on the device
-  AL(W->bad, 8);
-  if ((e = cudaMemsetAsync(W->bad, 0xff, 4, s)) != cudaSuccess) return fail(e, "bad flag");
-  if ((e = cudaMemsetAsync(W->bad + 1, 0, 4, s)) != cudaSuccess) return fail(e, "bad flag");
-  // per-walk warm starts of many long walks: uploaded in batches on a copy
-  // stream, each batch validated / packed and its tables built while the next
-  // batch is in flight
+  // Warm starts are validated and bit-packed on the host (8x fewer PCIe bytes
+  // than the int8 elements), by all host threads, walk by walk in order; a batch
+  // of packed walks is uploaded on the copy stream as soon as it is complete, and
+  // its validation / table build runs while the next batch is still being packed.
+  const bool shared_init = !inits && p.init;
   const uint32_t nbatch = (inits && L >= 8192 && n_walks >= 32) ? 4u : 1u;
   if (inits || p.init) {
-    const size_t bytes = (size_t)n_walks * L;
-    AL(W->inits, bytes);
-    if (inits && nbatch > 1) {
-      if (!ctx->copy && (e = cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking)) != cudaSuccess)
-        return fail(e, "copy stream");
-      cudaEvent_t ready;
-      if ((e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming)) != cudaSuccess) return fail(e, "event");
-      cudaEventRecord(ready, s);                    // the allocation is stream-ordered on s
-      cudaStreamWaitEvent(ctx->copy, ready, 0);
-      cudaEventDestroy(ready);
-    } else if (inits) {
-      if ((e = cudaMemcpyAsync(W->inits, inits, bytes, cudaMemcpyHostToDevice, s)) != cudaSuccess)
-        return fail(e, "inits");
-    } else {
-      for (uint32_t w = 0; w < n_walks; ++w)
-        if ((e = cudaMemcpyAsync(W->inits + (size_t)w * L, p.init, L, cudaMemcpyHostToDevice, s)) != cudaSuccess)
-          return fail(e, "init");
+    const size_t words = (shared_init ? 1 : (size_t)n_walks) * nw;
+    if (ctx->pack_done) cudaEventSynchronize(ctx->pack_done);   // staging free again
+    else if ((e = cudaEventCreateWithFlags(&ctx->pack_done, cudaEventDisableTiming)) != cudaSuccess)
+      return fail(e, "event");
+    if (ctx->pack_cap < words) {
+      if (ctx->pack_host) cudaFreeHost(ctx->pack_host);
+      ctx->pack_host = nullptr;
+      ctx->pack_cap = 0;
+      if ((e = cudaHostAlloc(&ctx->pack_host, words * 4, cudaHostAllocPortable)) != cudaSuccess)
+        return fail(e, "pinned staging");
+      ctx->pack_cap = words;
     }
+    AL(W->packed, words * 4);
+    if (nbatch > 1 && !ctx->copy &&
+        (e = cudaStreamCreateWithFlags(&ctx->copy, cudaStreamNonBlocking)) != cudaSuccess)
+      return fail(e, "copy stream");
   }
 #undef AL
   if (launch_power_tables(W->lut, a.lut_n, p.alpha1, p.alpha2, s) < 0)
     return fail(take_launch_error(), "power_tables_kernel");
   ctx->launches += 1;
+  // host packing: walks claimed in order by the worker threads; done[b] counts the
+  // packed walks of batch b; the first invalid element over all walks is reported
+  std::atomic<uint32_t> next{0};
+  std::vector<std::atomic<uint32_t>> done(nbatch);
+  for (auto& d : done) d.store(0);
+  std::atomic<uint64_t> bad_flat{UINT64_MAX};
+  int bad_val = 0;
+  std::mutex bad_mu;
+  const uint32_t n_pack = shared_init ? 0u : (inits ? n_walks : 0u);
+  auto batch_of = [&](uint32_t w) { return (uint32_t)(((uint64_t)(w + 1) * nbatch - 1) / n_walks); };
+  auto worker = [&]() {
+    for (;;) {
+      const uint32_t w = next.fetch_add(1);
+      if (w >= n_pack) return;
+      int bv = 0;
+      const uint64_t b = pack_walk(inits + (size_t)w * L, L, ctx->pack_host + (size_t)w * nw, &bv);
+      if (b) {
+        const uint64_t flat = (uint64_t)w * L + b - 1;
+        std::lock_guard<std::mutex> lk(bad_mu);
+        if (flat < bad_flat.load()) { bad_flat.store(flat); bad_val = bv; }
+      }
+      done[batch_of(w)].fetch_add(1);
+    }
+  };
+  std::vector<std::thread> pool;
+  if (shared_init) {
+    int bv = 0;
+    pack_walk(p.init, L, ctx->pack_host, &bv);              // validated by psl_validate_params
+  } else if (n_pack) {
+    const uint32_t hw = std::max(1u, std::thread::hardware_concurrency());
+    const uint32_t nt = ((size_t)n_pack * L < (1u << 20)) ? 0u : std::min({hw, 16u, n_pack});
+    for (uint32_t i = 0; i < nt; ++i) pool.emplace_back(worker);
+    if (nt == 0) worker();
+  }
+  auto join_pool = [&]() { for (auto& th : pool) if (th.joinable()) th.join(); };
   for (uint32_t bi = 0; bi < nbatch; ++bi) {
     const uint32_t w0 = (uint32_t)((uint64_t)n_walks * bi / nbatch);
     const uint32_t cnt = (uint32_t)((uint64_t)n_walks * (bi + 1) / nbatch) - w0;
-    int8_t* dinit = W->inits ? W->inits + (size_t)w0 * L : nullptr;
-    if (nbatch > 1) {
-      cudaEvent_t done;
-      if ((e = cudaMemcpyAsync(dinit, inits + (size_t)w0 * L, (size_t)cnt * L, cudaMemcpyHostToDevice,
-                               ctx->copy)) != cudaSuccess ||
-          (e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming)) != cudaSuccess)
-        return fail(e, "inits");
-      cudaEventRecord(done, ctx->copy);
-      cudaStreamWaitEvent(s, done, 0);
-      cudaEventDestroy(done);
+    const uint32_t* dpacked = nullptr;
+    size_t pstride = 0;
+    if (n_pack) {
+      while (done[bi].load() < cnt) std::this_thread::yield();
+      if (bad_flat.load() != UINT64_MAX) break;                // reported below
+      cudaStream_t cs_ = nbatch > 1 ? ctx->copy : s;
+      if (nbatch > 1) {
+        cudaEvent_t ready;
+        if ((e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming)) != cudaSuccess) {
+          join_pool();
+          return fail(e, "event");
+        }
+        cudaEventRecord(ready, s);                           // W->packed is stream-ordered on s
+        cudaStreamWaitEvent(cs_, ready, 0);
+        cudaEventDestroy(ready);
+      }
+      if ((e = cudaMemcpyAsync(W->packed + (size_t)w0 * nw, ctx->pack_host + (size_t)w0 * nw,
+                               (size_t)cnt * nw * 4, cudaMemcpyHostToDevice, cs_)) != cudaSuccess) {
+        join_pool();
+        return fail(e, "warm starts");
+      }
+      if (nbatch > 1) {
+        cudaEvent_t landed;
+        if ((e = cudaEventCreateWithFlags(&landed, cudaEventDisableTiming)) != cudaSuccess) {
+          join_pool();
+          return fail(e, "event");
+        }
+        cudaEventRecord(landed, cs_);
+        cudaStreamWaitEvent(s, landed, 0);
+        cudaEventDestroy(landed);
+      }
+      dpacked = W->packed + (size_t)w0 * nw;
+      pstride = nw;
+    } else if (shared_init) {
+      if (bi == 0 && (e = cudaMemcpyAsync(W->packed, ctx->pack_host, (size_t)nw * 4,
+                                          cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return fail(e, "warm start");
+      dpacked = W->packed;
+      pstride = 0;
     }
     const RunArgs ab = walk_offset(a, w0);
-    const int ni = launch_init_walks(ab, cnt, W->seeds + w0, dinit, W->bad, s, w0);
-    if (ni < 0) return fail(take_launch_error(), "init_walks_kernel");
+    const int ni = launch_init_walks(ab, cnt, W->seeds + w0, dpacked, pstride, s);
+    if (ni < 0) { join_pool(); return fail(take_launch_error(), "init_walks_kernel"); }
     // SidelobeTable::build: exact NTT correlation for long sequences (O(L log L)),
     // bit-parallel popcount kernel (O(L^2/32)) for short ones
     const int nb = L >= 8192 ? launch_build_tables_ntt(ab, cnt, s) : launch_build_tables(ab, cnt, s);
-    if (nb < 0) return fail(take_launch_error(), "build_tables");
+    if (nb < 0) { join_pool(); return fail(take_launch_error(), "build_tables"); }
     ctx->launches += (uint32_t)ni + (uint32_t)nb;
   }
-  if (W->inits) {
-    uint32_t bad[2];
-    if ((e = cudaMemcpyAsync(bad, W->bad, 8, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
-        (e = cudaStreamSynchronize(s)) != cudaSuccess)
-      return fail(e, "init check");
-    if (bad[0] != 0xffffffffu) {
-      const uint32_t flat = bad[0] - 1;
-      psl_walks_destroy(W);
-      set_err(err, errlen, "sequence element at position " + std::to_string(flat % L) + " is " +
-                               std::to_string((int)(int32_t)bad[1]) + "; elements must be +1 or -1");
-      return PSL_ERR_CONFIG;
-    }
-    cudaFreeAsync(W->inits, s);
-    W->inits = nullptr;
+  join_pool();
+  if (n_pack && bad_flat.load() != UINT64_MAX) {
+    const uint64_t flat = bad_flat.load();
+    cudaStreamSynchronize(s);
+    psl_walks_destroy(W);
+    set_err(err, errlen, "sequence element at position " + std::to_string(flat % L) + " is " +
+                             std::to_string(bad_val) + "; elements must be +1 or -1");
+    return PSL_ERR_CONFIG;
+  }
+  if (W->packed) {
+    cudaEventRecord(ctx->pack_done, nbatch > 1 ? ctx->copy : s);   // staging reusable after this
+    cudaFreeAsync(W->packed, s);
+    W->packed = nullptr;
   }
   *out = W;
   return PSL_OK;

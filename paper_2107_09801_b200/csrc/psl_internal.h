@@ -146,8 +146,10 @@ inline cudaError_t take_launch_error() {
 }
 
 // Launchers (return the number of kernels launched, or -1 on launch error).
+// packed: warm starts as nw bit words per walk (stride 0: one shared start), or
+// nullptr for random_sequence starts drawn on the device
 int launch_init_walks(const RunArgs& a, uint32_t n_walks, const uint64_t* d_seeds,
-                      const int8_t* d_inits, uint32_t* d_bad, cudaStream_t s, uint32_t walk0 = 0);
+                      const uint32_t* d_packed, size_t packed_stride, cudaStream_t s);
 // RunArgs whose per-walk arrays start at walk w0 (batched setup)
 RunArgs walk_offset(const RunArgs& a, uint32_t w0);
 int launch_verify(const int32_t* C, uint32_t L, int32_t* psl, unsigned long long* energy,

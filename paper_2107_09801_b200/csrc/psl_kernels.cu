@@ -718,8 +718,7 @@ __global__ void __launch_bounds__(256) rng_jump_kernel() {
 // Walk setup: RNG, pivot (random_sequence, search.cpp:120-129, or warm start),
 // snapshot copies.  One CTA per walk.
 __global__ void __launch_bounds__(256) init_walks_kernel(RunArgs a, const uint64_t* seeds,
-                                                         const int8_t* inits, uint32_t* bad,
-                                                         uint32_t walk0) {
+                                                         const uint32_t* packed, size_t packed_stride) {
   const uint32_t w = blockIdx.x;
   WalkState* S = a.st + w;
   uint32_t* bp = a.bits_piv + (size_t)w * a.w_stride + a.w_front;
@@ -738,7 +737,7 @@ __global__ void __launch_bounds__(256) init_walks_kernel(RunArgs a, const uint64
     z.psl_best = -1;           // set from P on the first pass
     *S = z;
   }
-  if (!inits) {
+  if (!packed) {
     // L spin() draws in position order; bit = top bit of next() (1 <-> -1)
     __shared__ uint64_t cs[kMaxSpinChunks][4];
     __shared__ uint64_t jm[256][4];
@@ -789,44 +788,11 @@ __global__ void __launch_bounds__(256) init_walks_kernel(RunArgs a, const uint64
       }
     }
   }
-  if (inits) {
-    // warm starts: validate (BinarySequence ctor, sequence.cpp:20-35) and pack;
-    // bad[0] = first offending flat index + 1, bad[1] = its value
-    const int8_t* src = inits + (size_t)w * a.L;
-    const size_t base = (size_t)(walk0 + w) * a.L;   // flat index over all walks (first offender)
-    for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) {
-      uint32_t word = 0;
-      const uint32_t nb = min(32u, a.L - i * 32);
-      if (nb == 32) {
-        // 8 byte quads (aligned loads + funnel shifts): -1 bytes -> bits, any
-        // byte not in {+1, -1} flagged
-        const uintptr_t pa = reinterpret_cast<uintptr_t>(src + (size_t)i * 32);
-        const uint32_t* q = reinterpret_cast<const uint32_t*>(pa & ~uintptr_t(3));
-        const uint32_t sh = 8u * (uint32_t)(pa & 3);
-        uint32_t qw[9];
-#pragma unroll
-        for (int r = 0; r < 8; ++r) qw[r] = __ldg(q + r);
-        qw[8] = sh ? __ldg(q + 8) : 0u;
-        uint32_t badm = 0;
-#pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const uint32_t v = __funnelshift_r(qw[r], qw[r + 1], sh);
-          badm |= (~(__vcmpeq4(v, 0x01010101u) | __vcmpeq4(v, 0xFFFFFFFFu)) != 0u) << r;
-          word |= ((((v >> 7) & 0x01010101u) * 0x01020408u) >> 24) << (4 * r);
-        }
-        if (!badm) { bp[i + 1] = word; continue; }
-        word = 0;
-      }
-      for (uint32_t b = 0; b < nb; ++b) {
-        const int8_t v = src[i * 32 + b];
-        if (v != 1 && v != -1) {
-          const uint32_t flat = (uint32_t)(base + i * 32 + b) + 1;
-          if (atomicMin(&bad[0], flat) > flat) bad[1] = (uint32_t)(int32_t)v;
-        }
-        word |= (uint32_t)(v < 0) << b;
-      }
-      bp[i + 1] = word;
-    }
+  if (packed) {
+    // warm starts, validated and bit-packed on the host (psl_api.cu pack_walk):
+    // nw words per walk (stride 0: one start shared by every walk)
+    const uint32_t* src = packed + (size_t)w * packed_stride;
+    for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) bp[i + 1] = src[i];
   }
   __syncthreads();
   // padded layout: zero pads around words 1..nw (relative to the walk base);
@@ -2088,10 +2054,10 @@ RunArgs walk_offset(const RunArgs& a, uint32_t w0) {
 }
 
 int launch_init_walks(const RunArgs& a, uint32_t n_walks, const uint64_t* d_seeds,
-                      const int8_t* d_inits, uint32_t* d_bad, cudaStream_t s, uint32_t walk0) {
-  const bool jump = !d_inits && a.L > kSpinChunk;
+                      const uint32_t* d_packed, size_t packed_stride, cudaStream_t s) {
+  const bool jump = !d_packed && a.L > kSpinChunk;
   if (jump) rng_jump_kernel<<<1, 256, 0, s>>>();
-  init_walks_kernel<<<n_walks, 256, 0, s>>>(a, d_seeds, d_inits, d_bad, walk0);
+  init_walks_kernel<<<n_walks, 256, 0, s>>>(a, d_seeds, d_packed, packed_stride);
   return launch_status(jump ? 2 : 1);
 }
 
