@@ -462,14 +462,17 @@ def main():
     torch.cuda.synchronize()
     e2e_ms = D.max_over_ranks(ea.elapsed_time(eb), cdev)
     e2e_nse = D.sum_over_ranks(e2e_nse_local, cdev)
+    nwords = (L + 31) // 32
     e2e = {"value": e2e_nse / (e2e_ms * 1e-3), "unit": "NSE/s",
            "h2d_bytes_per_step": int(inits.nbytes + 8 * n_walks),
+           "pcie_h2d_bytes_per_step": int(n_walks * nwords * 4 + 8 * n_walks),
            "d2h_bytes_per_step": int(n_walks * L + n_walks * 80),
            "steps": args.e2e_reps, "ms_per_step": e2e_ms / args.e2e_reps,
            "step": f"one psl_run_walks call per GPU: {n_walks} host start sequences (pinned "
-                   f"int8) -> device validation/packing + NTT table build + {args.e2e_steps} "
-                   f"search steps -> records + best sequences (int8, into a pinned host buffer) "
-                   f"on the host; 1 untimed warm-up call"}
+                   f"int8, h2d_bytes_per_step) -> validated and bit-packed by the host threads, "
+                   f"uploaded as bits (pcie_h2d_bytes_per_step) -> NTT table build + "
+                   f"{args.e2e_steps} search steps -> records + best sequences (int8, into a "
+                   f"pinned host buffer) on the host; 1 untimed warm-up call"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
