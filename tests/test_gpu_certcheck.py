@@ -149,3 +149,22 @@ def test_forced_fallbacks_at_baseline_lengths(engine, monkeypatch, L, a1, a2):
     for a, b in zip(got, ref):
         assert (a.nse, a.psl_best, a.energy) == (b.nse, b.psl_best, b.energy)
         assert np.array_equal(a.solution_best, b.solution_best)
+
+
+@pytest.mark.parametrize("L,steps", [(262143, 4), (1048575, 2)])
+def test_paper_neighbourhood_6912_auto_equals_exact(engine, L, steps):
+    """The paper's N_lmt = 6912: seven certified 1024-row groups
+    per step combined in ascending offset order; records equal the exact sweep's."""
+    import numpy as np
+    ctx = engine.default_context()
+    p = engine.SearchParams(length=L, seed=4, alpha1=4, alpha2=engine.default_alpha2(L),
+                            ls_lmt=2000, flip_lmt=10, n_lmt=6912,
+                            stop=engine.StopCondition(max_nse=1 + steps * 6912))
+    out = {}
+    for mode in (ctx.SCAN_EXACT, ctx.SCAN_AUTO):
+        ctx.set_scan_mode(mode)
+        out[mode] = engine.run_walks(p, 2, ctx=ctx)
+    ctx.set_scan_mode(ctx.SCAN_AUTO)
+    for a, b in zip(out[ctx.SCAN_AUTO], out[ctx.SCAN_EXACT]):
+        assert (a.nse, a.psl_best, a.energy, a.steps) == (b.nse, b.psl_best, b.energy, b.steps)
+        assert np.array_equal(a.solution_best, b.solution_best)
