@@ -1047,7 +1047,8 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
   sm.sb = bits_piv;   // padded: word i at bits_piv[i + 1]
   __syncthreads();
   if (ctl->st.done || ctl->st.status != PSL_OK) return;
-  uint32_t mb_par[2] = {0u, 0u};   // next phase parity to wait for on ctl->mbar[0/1]
+  uint32_t mb_par = 0u;            // bit b: next phase parity to wait for on ctl->mbar[b]
+                                   // (a bit mask: an indexed 2-array lived in local memory)
   uint32_t cphase = 0u;             // ... on ctl->cbar[0..2] (bit per slot)
   if (kCert) {
     if (t < 32) {   // the certified scan's tcgen05 accumulators live in TMEM
@@ -1279,9 +1280,9 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           }
           if (issued & (1u << (c & 1))) {      // MMAs of iteration c - 2 read this buffer
             PT_MARK(0);
-            mbar_wait(&ctl->mbar[c & 1], mb_par[c & 1]);
+            mbar_wait(&ctl->mbar[c & 1], (mb_par >> (c & 1)) & 1u);
             PT_MARK(8);
-            mb_par[c & 1] ^= 1u;
+            mb_par ^= 1u << (c & 1);
             issued &= ~(1u << (c & 1));
           }
           PT_MARK(0);
@@ -1351,7 +1352,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           if (rho >= r_lo && rho < r_hi) ivm[rho] = Bs[m];
         }
         for (uint32_t bb = 0; bb < 2; ++bb)
-          if (issued & (1u << bb)) { mbar_wait(&ctl->mbar[bb], mb_par[bb]); mb_par[bb] ^= 1u; }
+          if (issued & (1u << bb)) { mbar_wait(&ctl->mbar[bb], (mb_par >> bb) & 1u); mb_par ^= 1u << bb; }
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if ((t & 31) == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&ctl->st.n_mma),
                                      (unsigned long long)nmma);
