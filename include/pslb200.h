@@ -194,7 +194,11 @@ int psl_validate_params(const psl_params* in, psl_params* out, char* warning,
 double psl_pow_int(double base, uint32_t exp);         /* sequence.cpp:95-105 */
 
 /* ---- operator seam ----------------------------------------------------- */
-/* scan_chunk(job, 1, n+1) / ScanPool::run (search.cpp:167-175, :202-218). */
+/* scan_chunk(job, 1, n+1) / ScanPool::run (search.cpp:167-175, :202-218):
+ * values[i], psls[i] of neighbour (start + i) % length for i = 1..n.  lut must be
+ * PowerTable(length, alpha)'s length + 1 entries (search.cpp:337-338; else
+ * PSL_ERR_CONFIG).  The pivot's PSL and high-sidelobe list are built on the
+ * device; device scratch comes from the context's memory pool. */
 int psl_scan(psl_ctx* ctx, const psl_scan_job* job, char* err, size_t errlen);
 /* neighborhood_scan (search.cpp:296-321); absolute positions in `out`. */
 int psl_neighborhood_scan(psl_ctx* ctx, const int8_t* seq, const int32_t* table,
