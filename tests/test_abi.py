@@ -183,3 +183,18 @@ def test_walk_inputs_are_size_checked_before_the_abi():
     from paper_2107_09801_b200.pslopt import _walk_inputs
     s, i = _walk_inputs(p, 3, [5, 6, 7], np.ones(64, np.int8))
     assert s.tolist() == [5, 6, 7] and i.shape == (3, 64) and i.flags.c_contiguous
+
+
+def test_scan_seam_rejects_short_power_table():
+    """psl_scan reads PowerTable(L, alpha) (L + 1 entries, search.cpp:337-338): a
+    shorter table is a ConfigError before any device work (no GPU needed)."""
+    L = 64
+    s = np.ones(L, np.int8)
+    t = np.arange(L, 0, -1).astype(np.int32)
+    lut = np.ones(L, np.float64)
+    values, psls = np.zeros(9, np.float64), np.zeros(9, np.int32)
+    job = B.psl_scan_job(s.ctypes.data, t.ctypes.data, L, 0, 8, lut.ctypes.data, len(lut),
+                         values.ctypes.data, psls.ctypes.data)
+    err = C.create_string_buffer(256)
+    rc = B.lib().psl_scan(None, C.byref(job), err, 256)       # checked before any device use
+    assert rc == B.PSL_ERR_CONFIG and b"power table too small" in err.value
