@@ -36,9 +36,6 @@ namespace pslb {
 namespace {
 
 constexpr uint32_t FULL = 0xffffffffu;
-#ifndef PSL_ONE_PREDADD
-#define PSL_ONE_PREDADD 1          // exact sweep, one-side cells: predicated DADDs (see sweep)
-#endif
 
 // Device bounds checks (-DPSL_DEBUG_BOUNDS; tools/ablate.sh bounds=PSL_DEBUG_BOUNDS):
 // every shared-memory buffer write of the certified pipeline, every C / high-
@@ -526,14 +523,7 @@ __device__ __forceinline__ void sweep(const SweepIO& io, const Smem& sm, const b
               const uint32_t x = P[m] >> (g * kG);
 #pragma unroll
               for (int qq = 0; qq < kG; ++qq)
-#if PSL_ONE_PREDADD
-                // two predicated adds instead of a 64-bit select (2 FSEL) + add:
-                // one FP64 issue more, two ALU issues fewer per cell
-                if ((x >> qq) & 1u) sum[m] = __dadd_rn(sum[m], e1[qq]);
-                else sum[m] = __dadd_rn(sum[m], e3[qq]);
-#else
                 sum[m] = __dadd_rn(sum[m], ((x >> qq) & 1u) ? e1[qq] : e3[qq]);
-#endif
             }
           }
         } else if (cls == CLS_TAIL) {

@@ -26,8 +26,7 @@ for r in range(rounds):
             print(f"{lib}: failed: {p.stderr[-800:]}")
             continue
         d = json.loads(lines[-1])
-        key = "auto_ms_per_step" if "auto_ms_per_step" in d else "exact_ms_per_step"
-        res[lib].append(round(d[key], 3))
+        res[lib].append(round(d["auto_ms_per_step"], 3))
 for lib in libs:
     v = sorted(res[lib])
     if v:

@@ -5,5 +5,3 @@ for i in 1 2; do
 PSLB200_RUN_PIPELINE=0 NW=444 python tools/e2e_breakdown.py 10 2>&1 | tail -2
 PSLB200_RUN_PIPELINE=1 NW=444 python tools/e2e_breakdown.py 10 2>&1 | tail -2
 done
-python tools/ab_time.py build_ablate/lib_nopred.so paper_2107_09801_b200/libpslb200.so 3 -- --walks 444 --steps 4 --mode exact 2>&1 | tail -2
-python tools/ab_time.py build_ablate/lib_nopred.so paper_2107_09801_b200/libpslb200.so 3 -- --length 65535 --walks 444 --steps 10 --mode exact 2>&1 | tail -2
