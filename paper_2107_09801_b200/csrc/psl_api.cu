@@ -1075,11 +1075,8 @@ int psl_run_walks(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, cons
     cudaGetLastError();
   }
   psl_walks* w = nullptr;
-  // setup and run pipelined over the upload batches (walks_create run_now);
-  // PSLB200_RUN_PIPELINE=0 runs all setup first, then one launch for all walks
-  const char* pe = std::getenv("PSLB200_RUN_PIPELINE");
-  const bool pipeline = !(pe && std::string(pe) == "0");
-  int rc = walks_create(ctx, params, n_walks, seeds, inits, 0, 0, &w, err, errlen, pipeline, sol_out,
+  // setup and run pipelined over the upload batches (walks_create run_now)
+  int rc = walks_create(ctx, params, n_walks, seeds, inits, 0, 0, &w, err, errlen, true, sol_out,
                         sol_direct);
   if (rc) return rc;
   if (!w->launched) rc = psl_walks_run(w, err, errlen);
