@@ -43,10 +43,6 @@ struct psl_ctx {
   uint32_t* pack_host = nullptr;
   size_t pack_cap = 0;
   cudaEvent_t pack_done = nullptr;
-  // psl_run_walks pipelining: one stream per setup batch (setup of batch b, then
-  // its walks' run kernel, while later batches are still being set up)
-  cudaStream_t batch[4] = {nullptr, nullptr, nullptr, nullptr};
-  int32_t* abort_host = nullptr;          // mapped pinned flag (RunArgs::abort)
 };
 
 struct psl_walks {
@@ -73,7 +69,6 @@ struct psl_walks {
   double* iv_buf = nullptr;     // certified-scan row intervals of a group
   uint64_t stats_read[5] = {0, 0, 0, 0, 0};   // scan statistics already added to ctx->stats
   uint64_t chk_read[5] = {0, 0, 0, 0, 0};     // ... certificate-check counts
-  bool launched = false;        // walks_create already launched the run (psl_run_walks pipelining)
 };
 
 namespace {
@@ -245,9 +240,6 @@ void psl_ctx_destroy(psl_ctx* ctx) {
   if (ctx->own) cudaStreamDestroy(ctx->own);
   if (ctx->copy) cudaStreamDestroy(ctx->copy);
   if (ctx->pack_done) { cudaEventSynchronize(ctx->pack_done); cudaEventDestroy(ctx->pack_done); }
-  for (cudaStream_t b : ctx->batch)
-    if (b) cudaStreamDestroy(b);
-  if (ctx->abort_host) cudaFreeHost(ctx->abort_host);
   if (ctx->pack_host) cudaFreeHost(ctx->pack_host);
   delete ctx;
 }
@@ -713,13 +705,9 @@ void psl_walks_destroy(psl_walks* w) {
 
 namespace {
 
-// run_now (psl_run_walks): with several setup batches, batch b's table build and
-// then its walks' run kernel go to their own stream, so the run of early batches
-// overlaps the setup of later ones; sol_out / sol_direct as in psl_run_walks.
 int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const uint64_t* seeds,
                  const int8_t* inits, uint64_t events_cap, uint64_t traces_cap, psl_walks** out,
-                 char* err, size_t errlen, bool run_now = false, int8_t* sol_out = nullptr,
-                 int8_t* sol_direct = nullptr) {
+                 char* err, size_t errlen) {
   *out = nullptr;
   psl_params p;
   int rc = psl_validate_params(params, &p, nullptr, 0, err, errlen);
@@ -755,13 +743,8 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
   a.w_stride = ((size_t)nw + 48 + nw + (size_t)nw + 48 + kBitsPad + 3) & ~size_t(3);
   a.h_stride = L;
   a.f_stride = std::max<uint32_t>(p.flip_lmt, 1);
-  a.sol_out = sol_out;
-  W->sol_direct = sol_direct;
   cudaStream_t s = ctx->stream;
   auto fail = [&](cudaError_t e, const char* what) {
-    if (ctx->abort_host) *ctx->abort_host = 1;          // stop any walks already running
-    for (cudaStream_t b : ctx->batch)
-      if (b) cudaStreamSynchronize(b);
     psl_walks_destroy(W);
     return cuda_fail(err, errlen, e, what);
   };
@@ -826,24 +809,6 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
   if (launch_power_tables(W->lut, a.lut_n, p.alpha1, p.alpha2, s) < 0)
     return fail(take_launch_error(), "power_tables_kernel");
   ctx->launches += 1;
-  const bool pipe = run_now && nbatch > 1;
-  if (pipe) {
-    if (!ctx->abort_host &&
-        (e = cudaHostAlloc(&ctx->abort_host, sizeof(int32_t), cudaHostAllocMapped)) != cudaSuccess)
-      return fail(e, "abort flag");
-    *ctx->abort_host = 0;
-    int32_t* dabort = nullptr;
-    if ((e = cudaHostGetDevicePointer(&dabort, ctx->abort_host, 0)) != cudaSuccess) return fail(e, "abort flag");
-    a.abort = dabort;
-    for (uint32_t bi = 0; bi < nbatch; ++bi)
-      if (!ctx->batch[bi] && (e = cudaStreamCreateWithFlags(&ctx->batch[bi], cudaStreamNonBlocking)) != cudaSuccess)
-        return fail(e, "batch stream");
-    cudaEvent_t set;                                   // allocations, seeds, power tables
-    if ((e = cudaEventCreateWithFlags(&set, cudaEventDisableTiming)) != cudaSuccess) return fail(e, "event");
-    cudaEventRecord(set, s);
-    for (uint32_t bi = 0; bi < nbatch; ++bi) cudaStreamWaitEvent(ctx->batch[bi], set, 0);
-    cudaEventDestroy(set);
-  }
   // host packing: walks claimed in order by the worker threads; done[b] counts the
   // packed walks of batch b; the first invalid element over all walks is reported
   std::atomic<uint32_t> next{0};
@@ -882,7 +847,6 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
   for (uint32_t bi = 0; bi < nbatch; ++bi) {
     const uint32_t w0 = (uint32_t)((uint64_t)n_walks * bi / nbatch);
     const uint32_t cnt = (uint32_t)((uint64_t)n_walks * (bi + 1) / nbatch) - w0;
-    const cudaStream_t sb = pipe ? ctx->batch[bi] : s;   // this batch's setup (and run) stream
     const uint32_t* dpacked = nullptr;
     size_t pstride = 0;
     if (n_pack) {
@@ -911,7 +875,7 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
           return fail(e, "event");
         }
         cudaEventRecord(landed, cs_);
-        cudaStreamWaitEvent(sb, landed, 0);
+        cudaStreamWaitEvent(s, landed, 0);
         cudaEventDestroy(landed);
       }
       dpacked = W->packed + (size_t)w0 * nw;
@@ -924,34 +888,17 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
       pstride = 0;
     }
     const RunArgs ab = walk_offset(a, w0);
-    const int ni = launch_init_walks(ab, cnt, W->seeds + w0, dpacked, pstride, sb);
+    const int ni = launch_init_walks(ab, cnt, W->seeds + w0, dpacked, pstride, s);
     if (ni < 0) { join_pool(); return fail(take_launch_error(), "init_walks_kernel"); }
     // SidelobeTable::build: exact NTT correlation for long sequences (O(L log L)),
     // bit-parallel popcount kernel (O(L^2/32)) for short ones
-    const int nb = L >= 8192 ? launch_build_tables_ntt(ab, cnt, sb) : launch_build_tables(ab, cnt, sb);
+    const int nb = L >= 8192 ? launch_build_tables_ntt(ab, cnt, s) : launch_build_tables(ab, cnt, s);
     if (nb < 0) { join_pool(); return fail(take_launch_error(), "build_tables"); }
     ctx->launches += (uint32_t)ni + (uint32_t)nb;
-    if (pipe) {                                        // this batch's walks start now
-      if (launch_run(ab, cnt, sb) < 0) { join_pool(); return fail(take_launch_error(), "run_kernel"); }
-      ctx->launches += 1;
-    }
   }
   join_pool();
-  if (pipe) {                                          // join the batch streams back into s
-    for (uint32_t bi = 0; bi < nbatch; ++bi) {
-      cudaEvent_t fin;
-      if ((e = cudaEventCreateWithFlags(&fin, cudaEventDisableTiming)) != cudaSuccess) return fail(e, "event");
-      cudaEventRecord(fin, ctx->batch[bi]);
-      cudaStreamWaitEvent(s, fin, 0);
-      cudaEventDestroy(fin);
-    }
-    W->launched = true;
-  }
   if (n_pack && bad_flat.load() != UINT64_MAX) {
     const uint64_t flat = bad_flat.load();
-    if (pipe) *ctx->abort_host = 1;     // earlier batches' walks stop at their next step
-    for (cudaStream_t b : ctx->batch)
-      if (b) cudaStreamSynchronize(b);
     cudaStreamSynchronize(s);
     psl_walks_destroy(W);
     set_err(err, errlen, "sequence element at position " + std::to_string(flat % L) + " is " +
@@ -1061,25 +1008,21 @@ int psl_walks_records(psl_walks* w, psl_walk_record* records, int8_t* solutions,
 int psl_run_walks(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const uint64_t* seeds,
                   const int8_t* inits, psl_walk_record* records, int8_t* solutions, char* err,
                   size_t errlen) {
-  int8_t* sol_out = nullptr;
-  int8_t* sol_direct = nullptr;
+  psl_walks* w = nullptr;
+  int rc = psl_walks_create(ctx, params, n_walks, seeds, inits, &w, err, errlen);
+  if (rc) return rc;
   if (solutions) {
     // a pinned (mapped) caller buffer: each walk's kernel writes its best
     // sequence there when it stops, overlapping the D2H with later walks' steps
     cudaPointerAttributes pa;
     if (cudaPointerGetAttributes(&pa, solutions) == cudaSuccess && pa.type == cudaMemoryTypeHost &&
         pa.devicePointer) {
-      sol_out = static_cast<int8_t*>(pa.devicePointer);
-      sol_direct = solutions;
+      w->a.sol_out = static_cast<int8_t*>(pa.devicePointer);
+      w->sol_direct = solutions;
     }
     cudaGetLastError();
   }
-  psl_walks* w = nullptr;
-  // setup and run pipelined over the upload batches (walks_create run_now)
-  int rc = walks_create(ctx, params, n_walks, seeds, inits, 0, 0, &w, err, errlen, true, sol_out,
-                        sol_direct);
-  if (rc) return rc;
-  if (!w->launched) rc = psl_walks_run(w, err, errlen);
+  rc = psl_walks_run(w, err, errlen);
   if (!rc) rc = psl_walks_records(w, records, solutions, err, errlen);
   psl_walks_destroy(w);
   return rc;

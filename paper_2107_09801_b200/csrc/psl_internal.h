@@ -107,8 +107,6 @@ struct RunArgs {
   uint32_t lut_n;       // entries per table (> max |C_k| + 4)
   int8_t* sol_out;      // optional: mapped pinned host [walk][L]; a walk that stops writes its
                         // best sequence there from the kernel (overlaps later walks' steps)
-  const volatile int32_t* abort;   // optional: mapped pinned host flag; nonzero stops every walk
-                                   // at its next step boundary (psl_run_walks error path)
 };
 
 struct ScanArgs {

@@ -1076,8 +1076,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
       WalkState& S = ctl->st;
       const double elapsed = (double)(globaltimer() - S.t0_ns) * 1e-9;
       const bool stop = (a.has_max_nse && S.nse >= a.max_nse) ||
-                        (a.has_max_seconds && elapsed >= a.max_seconds) ||
-                        (a.abort != nullptr && *a.abort != 0);
+                        (a.has_max_seconds && elapsed >= a.max_seconds);
       const bool room = ctl->steps_this_launch < a.step_budget &&
                         (!a.record_events || S.n_events + 2 <= a.events_cap) &&
                         (!a.record_traces || S.n_traces + 1 <= a.traces_cap);

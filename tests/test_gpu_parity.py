@@ -440,26 +440,3 @@ def test_verify_sequence_matches_oracle(engine):
         assert rep.merit_factor == O.lib().orc_merit_factor(c, L)
         hist = np.bincount(np.abs(c[1:]), minlength=rep.psl + 1)
         assert np.array_equal(rep.sidelobe_histogram, hist)
-
-
-def test_run_walks_pipelined_abort_on_late_bad_start(engine):
-    """psl_run_walks runs early upload batches while later ones are still being set
-    up; an invalid element found in a late batch stops the walks already running at
-    their next step (no waiting for a 60 s stop condition) and reports the error."""
-    import time
-    L, nw = 9001, 40
-    rng = np.random.default_rng(13)
-    inits = np.where(rng.integers(0, 2, (nw, L)) == 1, -1, 1).astype(np.int8)
-    inits[39, 17] = 5
-    p = engine.SearchParams(length=L, seed=3, alpha1=4, alpha2=13, ls_lmt=2000, flip_lmt=10,
-                            n_lmt=256, stop=engine.StopCondition(max_seconds=60.0))
-    t0 = time.time()
-    with pytest.raises(engine.ConfigError, match="position 17 is 5;"):
-        engine.run_walks(p, nw, inits=inits)
-    assert time.time() - t0 < 20.0
-    # and the context is usable afterwards
-    inits[39, 17] = 1
-    p2 = engine.SearchParams(length=L, seed=3, alpha1=4, alpha2=13, ls_lmt=2000, flip_lmt=10,
-                             n_lmt=256, stop=engine.StopCondition(max_nse=1 + 3 * 256))
-    recs = engine.run_walks(p2, nw, inits=inits)
-    assert all(r.nse == 1 + 3 * 256 for r in recs)
