@@ -277,6 +277,8 @@ PHASE2_CASES = [
     # 20000-step GPU descent, tools/deep_starts.py; stored with the fixture as
     # packed bits) from which 1024-neighbour steps stop improving, ls_lmt 1
     ("m16_deep_ls1", 65535, 21, 4, 13, 1, 10, 1024, 150, "deep_m16"),
+    # the same at m18 (a 60000-step descent): alpha2 = 11 at full n_lmt in phase 2
+    ("m18_deep_ls1", 262143, 21, 4, 11, 1, 10, 1024, 40, "deep_m18"),
 ]
 
 

@@ -69,39 +69,41 @@ def test_intervals_hold_across_phase_switches(engine, L, a2, n, steps):
     assert d["rows"] > 0 and d["decided"] > 0, d
 
 
-def _deep_m16():
+def _deep_start(name, L):
     import json
     import os
     import numpy as np
     g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "phase2.json")))
-    d = g["m16_deep_ls1"]
+    d = g[name]
     bits = np.unpackbits(np.frombuffer(bytes.fromhex(d["init_bits_hex"]), np.uint8),
-                         bitorder="little")[:65535]
+                         bitorder="little")[:L]
     return np.where(bits == 1, -1, 1).astype(np.int8)
 
 
-def test_intervals_hold_full_neighbourhood_in_both_phases(engine):
-    """Deep m16 warm start (the phase2.json fixture's), n_lmt 1024, ls_lmt 1: the
-    walks switch phase, so alpha2 = 13 steps score the full neighbourhood."""
+@pytest.mark.parametrize("name,L,a2,steps,walks", [("m16_deep_ls1", 65535, 13, 150, 4),
+                                                  ("m18_deep_ls1", 262143, 11, 40, 3)])
+def test_intervals_hold_full_neighbourhood_in_both_phases(engine, name, L, a2, steps, walks):
+    """Deep warm starts (the phase2.json fixtures'), n_lmt 1024, ls_lmt 1: the walks
+    switch phase, so alpha2 steps score the full neighbourhood under the check."""
     ctx = engine.default_context()
-    init = _deep_m16()
+    init = _deep_start(name, L)
     ctx.set_cert_check(True)
     try:
         before = ctx.cert_check_stats()
-        p = engine.SearchParams(length=65535, seed=21, alpha1=4, alpha2=13, ls_lmt=1,
+        p = engine.SearchParams(length=L, seed=21, alpha1=4, alpha2=a2, ls_lmt=1,
                                 flip_lmt=10, n_lmt=1024,
-                                stop=engine.StopCondition(max_nse=1 + 150 * 1024))
-        w = engine.Walks(p, 4, seeds=[21, 22, 23, 24], inits=init, ctx=ctx)
+                                stop=engine.StopCondition(max_nse=1 + steps * 1024))
+        w = engine.Walks(p, walks, seeds=[21 + i for i in range(walks)], inits=init, ctx=ctx)
         w.run()
         recs = w.records()
         w.close()
     finally:
         ctx.set_cert_check(False)
     after = ctx.cert_check_stats()
-    assert sum(r.switches for r in recs) >= 4
+    assert sum(r.switches for r in recs) >= walks
     assert after["violations"] == before["violations"]
     assert after["decided_wrong"] == before["decided_wrong"]
-    assert after["rows"] - before["rows"] >= 4 * 100 * 1024
+    assert after["rows"] - before["rows"] >= walks * (steps // 2) * 1024
 
 
 @pytest.mark.slow
