@@ -6,20 +6,24 @@
 // run_search step loop (search.cpp:327-430).
 //
 // B200 design (DESIGN.md has the full derivation):
-//  * one persistent CTA (1024 threads) per walk; thread t scores neighbour
-//    i = t+1 of the pivot.  The whole step loop -- scan, argmin/PSL
-//    reduction, move, snapshots, restarts, RNG, events -- stays on device.
+//  * one persistent CTA per walk (the exact sweep: 256 threads, two CTAs per
+//    SM; the certified scan, psl_cert.cuh: 512 threads, one per SM).  The whole
+//    step loop -- scan, argmin/PSL reduction, move, snapshots, restarts, RNG,
+//    events -- stays on device.
 //  * C_k lives in HBM/L2 and is streamed through shared memory in chunks of
 //    512 shifts.  While streaming, the builder threads fold the previous
 //    step's accepted flip(s) into C (the O(L) apply_flip is fused into the
-//    next sweep) and expand every C_k into a 64-byte record of the five
-//    possible terms |C_k + d|^alpha, d in {-4,-2,0,+2,+4}.
-//  * every neighbour's fitness is the reference's serial ascending-k double
-//    chain (one DADD per cell, RN, no reassociation), so values are
-//    bit-identical.  Per cell a thread only turns two sequence bits into a
-//    record offset (SHF + LOP3), loads the term (LDS.64) and adds it.
-//  * the sequence is bit-packed in shared memory (bit = 1 <-> -1); per
-//    32-shift block each lane slides two 32-bit windows (s_{j-k}, s_{j+k}).
+//    next sweep); the exact sweep expands every C_k into a 64-byte record of
+//    the five possible terms |C_k + d|^alpha, d in {-4,-2,0,+2,+4}.
+//  * exact sweep: every neighbour's fitness is the reference's serial
+//    ascending-k double chain (one DADD per cell, RN, no reassociation), so
+//    values are bit-identical; each thread owns 4 adjacent neighbours and per
+//    32-shift block turns two sequence-bit windows into term selections.
+//  * certified scan (the default): per-row intervals from tcgen05 / mma.sync
+//    correlations that provably hold the serial doubles; undecided steps go
+//    to the exact sweep (decision-exact records).
+//  * the pivot is bit-packed in global memory (L1-resident; bit = 1 <-> -1)
+//    with zero pads so sliding windows run off either end unclamped.
 //  * neighbour PSL is exact but not computed per cell: only shifts with
 //    |C_k| >= PSL(pivot) - 8 can hold a neighbour's peak, and those are
 //    collected while streaming.
