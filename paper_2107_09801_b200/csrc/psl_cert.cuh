@@ -132,10 +132,6 @@ static_assert(2 * kWinBuf >= kGroup * sizeof(double) && 2 * kABuf >= kGroup * si
 
 __device__ __forceinline__ uint32_t cert_kb(int32_t c) { return (uint32_t)(1 + c * (int32_t)kCC); }
 
-__device__ __forceinline__ bool cert_band_chunk(const CertIO& io, uint32_t c) {
-  const uint32_t kb = cert_kb(c), ke = kb + kCC - 1;
-  return kb <= io.m_hi && ke > io.m_lo;      // band 1 (band 2 is linear: MMA + prefix sums)
-}
 // shifts with nonzero H4 (zone 1, past band 1 up to M_hi) intersect [lo, hi]?
 __device__ __forceinline__ bool cert_lin_in(const CertIO& io, long long lo, long long hi) {
   if (hi < 1 || lo > (long long)io.L - 1) return false;
@@ -344,7 +340,7 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
   }
 #endif
   PSL_CHK(b * kCC + t < 2 * kCC, 7);
-  if (io.chain || cert_band_chunk(io, c)) cs.rec[b * kCC + t] = cv;
+  if (io.chain) cs.rec[b * kCC + t] = cv;
   if (kb > io.m_lo) return;
   // zone-1 chunk: R4 digit rows and the sequence windows of the cross MMAs
   {
@@ -785,51 +781,138 @@ __device__ __forceinline__ void cert_lin_rows(uint32_t tmem, bool rev, uint32_t 
   }
 }
 
-// Exact band-1 terms of chunk c for this thread's rows rho = kBandRows t + m: per
-// cell pow_int(|C_k - 2x|, alpha), x = s_j (s_{j-k} [k <= j] + s_{j+k} [j+k < L]),
-// each row's terms added serially in ascending k.  All 16 warps take rows (two
-// each), so the few band chunks of a pass do not stall half the CTA.
-constexpr int kBandRows = kGroup / kCertThreads;
-__device__ __forceinline__ void cert_band_cells(const CertIO& io, const CertSmem& cs, uint32_t c,
-                                                const uint32_t* __restrict__ sb,
-                                                double (&Bs)[kBandRows], uint32_t owner) {
-  const uint32_t kb = cert_kb(c);
-  const uint32_t ke = min(kb + kCC - 1, io.L - 1);
-  const int32_t* rec = cs.rec + (size_t)(c & 1) * kCC;
+// Band 1 (k in (m_lo, m_hi], <= n shifts wide), scored exactly per cell after
+// the chunk loop.  In band 1 row j's cell is two-sided for k <= m_j and
+// one-sided past it (s_{j+k} for rows left of the middle, s_{j-k} right of
+// it; m_hi <= (L-1)/2 <= M_j), so with du = [s_{j+k} != s_j], dv = [s_{j-k} != s_j]
+// its term is entry code of the shift's 8-entry record
+//   code = 2 du + dv (two-sided: e4, e2, e2, e0),  4 + dw (one-sided: e3, e1),
+// e_x = pow_int(|C_k - 2(x - 2)|, alpha).  The records live in the digit ring
+// (free once the MMAs drained): one LDS.64 per cell, no dependent lookups.
+constexpr int kBandRows = kGroup / kCertThreads;    // rows per thread (rho = kBandRows t + m)
+constexpr uint32_t kBandRec = 8;                     // doubles per band record
+static_assert((size_t)kGroup * kBandRec * sizeof(double) <= kDRing, "band records fit the digit ring");
+
+// The pivot words band 1 reads (logical word w = sb[w + 1]), staged in the
+// record buffer: forward positions j + k, backward j - k - 31, the rows' own bits.
+constexpr uint32_t kBandWF = 80, kBandWB = 80, kBandWR = 40;
+static_assert((kBandWF + kBandWB + kBandWR) * 4 <= kCertRecBuf * 2, "band bit windows fit the record buffer");
+struct BandBits {
+  long long f0, b0, r0;     // first logical word of each window
+};
+__device__ __forceinline__ BandBits cert_band_bits(const CertIO& io) {
+  const long long jlo = (long long)io.j0 + io.r_lo, jhi = (long long)io.j0 + io.r_hi - 1;
+  const long long blo = (long long)io.m_lo + 1, bhi = min((long long)io.m_hi, (long long)io.L - 1);
+  BandBits w;
+  w.f0 = (jlo + blo) >> 5;
+  w.b0 = (jlo - bhi - 62) >> 5;
+  w.r0 = jlo >> 5;
+  return w;
+}
+
+// Records of the band shifts and the staged pivot words (all threads; C after
+// the fold, visible after a barrier).
+__device__ __forceinline__ void cert_band_records(const CertIO& io, const CertSmem& cs, const int32_t* Cf,
+                                                  const uint32_t* sb) {
+  const uint32_t blo = io.m_lo + 1, bhi = min(io.m_hi, io.L - 1);
+  {
+    const BandBits bw = cert_band_bits(io);
+    const long long jlo = (long long)io.j0 + io.r_lo, jhi = (long long)io.j0 + io.r_hi - 1;
+    const uint32_t nf = (uint32_t)(((jhi + bhi + 63) >> 5) - bw.f0 + 1);
+    const uint32_t nb = (uint32_t)(((jhi - (long long)blo) >> 5) + 2 - bw.b0);
+    const uint32_t nr = (uint32_t)((jhi >> 5) - bw.r0 + 1);
+    PSL_CHK(nf <= kBandWF && nb <= kBandWB && nr <= kBandWR, 21);
+    uint32_t* wf = reinterpret_cast<uint32_t*>(cs.rec);
+    for (uint32_t i = threadIdx.x; i < nf + nb + nr; i += blockDim.x) {
+      const long long lw = i < nf ? bw.f0 + i : (i < nf + nb ? bw.b0 + (i - nf) : bw.r0 + (i - nf - nb));
+      const uint32_t slot = i < nf ? i : (i < nf + nb ? kBandWF + (i - nf) : kBandWF + kBandWB + (i - nf - nb));
+      PSL_CHK(sb_ok(lw + 1, io.L), 21);
+      wf[slot] = sb[lw + 1];
+    }
+  }
+  double* tab = reinterpret_cast<double*>(cs.dring);
+  for (uint32_t i = threadIdx.x; blo + i <= bhi; i += blockDim.x) {
+    PSL_CHK(i < (uint32_t)kGroup && blo + i >= 1 && blo + i < io.L, 19);
+    const int32_t c = __ldcg(Cf + blo + i);
+    const double e4 = io.lut[abs(c - 4)], e3 = io.lut[abs(c - 2)], e2 = io.lut[abs(c)];
+    const double e1 = io.lut[abs(c + 2)], e0 = io.lut[abs(c + 4)];
+    double2* r = reinterpret_cast<double2*>(tab + (size_t)kBandRec * i);
+    r[0] = make_double2(e4, e2);
+    r[1] = make_double2(e2, e0);
+    r[2] = make_double2(e3, e1);
+    r[3] = make_double2(0.0, 0.0);
+  }
+}
+
+// 4 bits -> 4 bytes (bit i -> byte i = 0 / 1)
+__device__ __forceinline__ uint32_t spread4(uint32_t x) { return ((x & 0xFu) * 0x00204081u) & 0x01010101u; }
+
+// Row sums of band-1 cells for this thread's rows (in ascending k, two
+// interleaved partial sums per row: depth <= n / 2 + 2, inside the gamma_2100
+// budget of the bound).
+__device__ __forceinline__ void cert_band_rows(const CertIO& io, const CertSmem& cs, double (&Bs)[kBandRows]) {
+  const uint32_t blo = io.m_lo + 1, bhi = min(io.m_hi, io.L - 1);
+  if (blo > bhi) return;
   const uint32_t L = io.L;
+  const unsigned char* tab = cs.dring;
+  const BandBits bw = cert_band_bits(io);
+  const uint32_t* sF = reinterpret_cast<const uint32_t*>(cs.rec);
+  const uint32_t* sB = sF + kBandWF;
+  const uint32_t* sR = sB + kBandWB;
 #ifdef PSL_ABLATE_BAND
   return;
 #endif
-  const double* __restrict__ lut = io.lut;
-  const uint32_t blo = max(kb, io.m_lo + 1);
-  const uint32_t bhi = min(ke, io.m_hi);
-  if (blo > bhi) return;
-#pragma unroll
+#pragma unroll 1
   for (int m = 0; m < kBandRows; ++m) {
-    const uint32_t rho = kBandRows * owner + m;
+    const uint32_t rho = kBandRows * threadIdx.x + m;
     if (rho < io.r_lo || rho >= io.r_hi) continue;
     const uint32_t j = (uint32_t)(io.j0 + (int32_t)rho);
-    const uint32_t sjb = (sb[(j >> 5) + 1] >> (j & 31)) & 1u;
-    double s = Bs[m];
+    const uint32_t mj = min(j, L - 1 - j);
+    const bool left = j <= L - 1 - j;                  // one-sided cells use s_{j+k}
+    const uint32_t sjm = ((sR[(long long)(j >> 5) - bw.r0] >> (j & 31)) & 1u) ? 0xFFFFFFFFu : 0u;
+    double s0 = 0.0, s1 = 0.0;
 #pragma unroll 1
     for (uint32_t k0 = blo; k0 <= bhi; k0 += 32) {
-      // bit q: s_{j+k0+q} and s_{j-k0-q} (1 <-> -1; zero pads beyond the ends)
+      // bit q: s_{j+k0+q} and s_{j-k0-q} (1 <-> -1; zero pads beyond the ends are never selected)
       const long long pB = (long long)j + k0, pA = (long long)j - k0 - 31;
-      const long long wB = pB >> 5, wA = pA >> 5;
-      PSL_CHK(sb_ok(wB + 2, L) && sb_ok(wA + 1, L) && sb_ok(wA + 2, L), 19);
-      const uint32_t Bw = __funnelshift_r(sb[wB + 1], sb[wB + 2], (uint32_t)(pB & 31));
-      const uint32_t Aw = __brev(__funnelshift_r(sb[wA + 1], sb[wA + 2], (uint32_t)(pA & 31)));
-      const uint32_t nq = min(32u, bhi - k0 + 1);
-      for (uint32_t q = 0; q < nq; ++q) {
-        const uint32_t k = k0 + q;
-        const int u = ((Bw >> q) & 1u) == sjb ? 1 : -1;
-        const int v = ((Aw >> q) & 1u) == sjb ? 1 : -1;
-        const int x = (k <= j ? v : 0) + (j + k < L ? u : 0);
-        PSL_CHK(k - kb < kCC, 20);
-        s = __dadd_rn(s, lut[abs(rec[k - kb] - 2 * x)]);
+      const int32_t wB = (int32_t)((pB >> 5) - bw.f0), wA = (int32_t)((pA >> 5) - bw.b0);
+      PSL_CHK(wB >= 0 && wB + 1 < (int32_t)kBandWF && wA >= 0 && wA + 1 < (int32_t)kBandWB, 20);
+      const uint32_t Du = __funnelshift_r(sF[wB], sF[wB + 1], (uint32_t)(pB & 31)) ^ sjm;
+      const uint32_t Dv = __brev(__funnelshift_r(sB[wA], sB[wA + 1], (uint32_t)(pA & 31))) ^ sjm;
+      // two-sided cells: q < d = m_j - k0 + 1
+      const int d = (int)mj - (int)k0 + 1;
+      const uint32_t A = d >= 32 ? 0xFFFFFFFFu : (d <= 0 ? 0u : (1u << d) - 1u);
+      const uint32_t W4 = ~A, W2 = Du & A, W1 = left ? ((A & Dv) | (~A & Du)) : Dv;
+      const unsigned char* base = tab + (k0 - blo) * (uint32_t)(kBandRec * sizeof(double));
+      const uint32_t nq = min(32u, bhi - k0 + 1);     // CTA-uniform
+      // 8 x code per byte, 4 cells per word
+      uint32_t c8[8];
+#pragma unroll
+      for (int g = 0; g < 8; ++g)
+        c8[g] = ((((spread4(W4 >> (4 * g)) << 1) + spread4(W2 >> (4 * g))) << 1) + spread4(W1 >> (4 * g))) << 3;
+      PSL_CHK(k0 - blo + nq <= (uint32_t)kGroup, 20);
+      if (nq == 32) {                                   // full block: branch-free, loads hoisted
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double e[16];
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            e[q] = *reinterpret_cast<const double*>(
+                base + __byte_perm(c8[4 * h + (q >> 2)], 0u, 0x4440u + (uint32_t)(q & 3)) +
+                (16 * h + q) * kBandRec * sizeof(double));
+#pragma unroll
+          for (int q = 0; q < 16; q += 2) { s0 = __dadd_rn(s0, e[q]); s1 = __dadd_rn(s1, e[q + 1]); }
+        }
+      } else {
+#pragma unroll 1
+        for (uint32_t q = 0; q < nq; ++q) {
+          const uint32_t off = (((W4 >> q) & 1u) << 5) | (((W2 >> q) & 1u) << 4) | (((W1 >> q) & 1u) << 3);
+          const double e = *reinterpret_cast<const double*>(base + off + q * kBandRec * sizeof(double));
+          if (q & 1) s1 = __dadd_rn(s1, e); else s0 = __dadd_rn(s0, e);
+        }
       }
     }
-    Bs[m] = s;
+    Bs[m] = __dadd_rn(s0, s1);
   }
 }
 
@@ -844,26 +927,43 @@ __device__ __forceinline__ void cert_chain_chunk(const CertIO& io, const CertSme
 }
 
 // Band 2 (k in (M_lo, M_hi]): row j's constant is sum_{k <= M_j} 4M_k +
-// sum_{k > M_j} 4 e2_k.  Warp 0 turns b2M into inclusive prefix sums and b2E
-// into inclusive suffix sums (32 serial terms per lane + a shuffle scan).
-__device__ __forceinline__ void cert_band2_scan(const CertIO& io, uint32_t nb2) {
-  if (threadIdx.x >= 32) return;
-  const uint32_t lane = threadIdx.x;
-  const uint32_t per = (nb2 + 31) / 32, lo = lane * per, hi = min(nb2, lo + per);
-  double sm = 0.0, se = 0.0;
-  for (uint32_t i = lo; i < hi; ++i) { sm = __dadd_rn(sm, io.b2M[i]); io.b2M[i] = sm; }
-  for (uint32_t i = hi; i-- > lo;) { se = __dadd_rn(se, io.b2E[i]); io.b2E[i] = se; }
-  double pm = sm, ps = se;   // inclusive scans over lanes (prefix for M, suffix for E)
+// sum_{k > M_j} 4 e2_k.  b2M becomes its inclusive prefix sums, b2E its
+// inclusive suffix sums, over the whole CTA (two elements per thread, warp
+// shuffle scans, one pass over the warp totals in `wsum` [2][32] shared):
+// every sum has depth <= 2 + 5 + 5 + 2, inside the bound's gamma_128.
+__device__ __forceinline__ void cert_band2_scan(const CertIO& io, uint32_t nb2, double* wsum) {
+  const uint32_t t = threadIdx.x, lane = t & 31, warp = t >> 5, nwp = blockDim.x >> 5;
+  const uint32_t i0 = 2 * t, i1 = 2 * t + 1;          // b2M index / b2E index from the top
+  PSL_CHK(nb2 <= 2 * blockDim.x && nb2 <= (uint32_t)kGroup, 5);
+  const double m0 = i0 < nb2 ? __ldcg(io.b2M + i0) : 0.0, m1 = i1 < nb2 ? __ldcg(io.b2M + i1) : 0.0;
+  const double e0 = i0 < nb2 ? __ldcg(io.b2E + (nb2 - 1 - i0)) : 0.0;
+  const double e1 = i1 < nb2 ? __ldcg(io.b2E + (nb2 - 1 - i1)) : 0.0;
+  const double qm = __dadd_rn(m0, m1), qe = __dadd_rn(e0, e1);
+  double pm = qm, pe = qe;                              // inclusive over the warp's pairs
   for (int o = 1; o < 32; o <<= 1) {
-    const double a = __shfl_up_sync(FULL, pm, o), bb = __shfl_down_sync(FULL, ps, o);
-    if ((int)lane >= o) pm = __dadd_rn(pm, a);
-    if ((int)lane + o < 32) ps = __dadd_rn(ps, bb);
+    const double a = __shfl_up_sync(FULL, pm, o), b = __shfl_up_sync(FULL, pe, o);
+    if ((int)lane >= o) { pm = __dadd_rn(pm, a); pe = __dadd_rn(pe, b); }
   }
-  const double offm = __dsub_rn(pm, sm), offe = __dsub_rn(ps, se);   // exclusive carries
-  for (uint32_t i = lo; i < hi; ++i) {
-    io.b2M[i] = __dadd_rn(io.b2M[i], offm);
-    io.b2E[i] = __dadd_rn(io.b2E[i], offe);
+  double xm = __shfl_up_sync(FULL, pm, 1), xe = __shfl_up_sync(FULL, pe, 1);   // exclusive
+  if (lane == 0) { xm = 0.0; xe = 0.0; }
+  if (lane == 31) { wsum[warp] = pm; wsum[32 + warp] = pe; }
+  __syncthreads();
+  if (warp == 0) {                                      // exclusive scan of the warp totals
+    double a = lane < nwp ? wsum[lane] : 0.0, b = lane < nwp ? wsum[32 + lane] : 0.0;
+    for (int o = 1; o < 32; o <<= 1) {
+      const double u = __shfl_up_sync(FULL, a, o), v = __shfl_up_sync(FULL, b, o);
+      if ((int)lane >= o) { a = __dadd_rn(a, u); b = __dadd_rn(b, v); }
+    }
+    double ea = __shfl_up_sync(FULL, a, 1), eb = __shfl_up_sync(FULL, b, 1);
+    if (lane == 0) { ea = 0.0; eb = 0.0; }
+    __syncwarp();
+    if (lane < nwp) { wsum[lane] = ea; wsum[32 + lane] = eb; }
   }
+  __syncthreads();
+  const double cm = __dadd_rn(wsum[warp], xm), ce = __dadd_rn(wsum[32 + warp], xe);
+  const double am = __dadd_rn(cm, m0), ae = __dadd_rn(ce, e0);
+  if (i0 < nb2) { io.b2M[i0] = am; io.b2E[nb2 - 1 - i0] = ae; }
+  if (i1 < nb2) { io.b2M[i1] = __dadd_rn(am, m1); io.b2E[nb2 - 1 - i1] = __dadd_rn(ae, e1); }
 }
 __device__ __forceinline__ double cert_band2_const(const CertIO& io, uint32_t nb2, uint32_t i) {
   return __dadd_rn(i > 0 ? io.b2M[i - 1] : 0.0, i < nb2 ? io.b2E[i] : 0.0);

@@ -1007,7 +1007,8 @@ __device__ __forceinline__ int compare_local(const WalkState& S, double lo, doub
 #include <cstdio>
 namespace pslb {
 namespace {
-constexpr int kPT = 10;  // loop top, build, cores, barrier, issue, cross, band, outside the loop, mbar wait, fence
+constexpr int kPT = 19;  // loop top, build, cores, barrier, issue, cross, band, pass prologue, mbar wait, fence,
+                         // tail, row intervals, reduce, exact/vl, control, step top
 #define PT_MARK(i)                                                   \
   do {                                                               \
     const long long _n = clock64();                                  \
@@ -1120,6 +1121,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
       }
     }
     __syncthreads();
+    PT_MARK(15);
     if (!ctl->need_pass) break;
     const bool do_scan = ctl->do_scan;
     const uint32_t start = ctl->start;
@@ -1311,7 +1313,6 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           // inside every barrier interval (buffers of c - 1 live until iteration c + 1)
           if (PSL_STAGGER && early && c >= 1 && c - 1 < c_end) {
             cert_cross_chunk(io, cs, ln, c - 1, acc, nmma);
-            if (cert_band_chunk(io, c - 1)) cert_band_cells(io, cs, c - 1, sm.sb, Bs, t);
           }
           cert_cores(io, cs, (int32_t)c, sm.sb, fw, rv);
           PT_MARK(2);
@@ -1337,7 +1338,6 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
             cert_cross_chunk(io, cs, ln, c, acc, nmma);          // 64 rows per warp
             PT_MARK(5);
             if (io.chain && t == kCertThreads - 64) cert_chain_chunk(io, cs, c, chain);
-            if (cert_band_chunk(io, c)) cert_band_cells(io, cs, c, sm.sb, Bs, t);
             PT_MARK(6);
           }
           if (kHalf < kCCols && pend_c == (int32_t)c && (t >> 5) == PSL_FWD_WARP)
@@ -1349,15 +1349,28 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         PT_MARK(0);
         // the tail chunks, streamed while the last MMAs drain
         cert_tail(io, c_end, nch, sm.sb, pmax, part);
+        PT_MARK(10);
+        for (uint32_t bb = 0; bb < 2; ++bb)
+          if (issued & (1u << bb)) { mbar_wait(&ctl->mbar[bb], (mb_par >> bb) & 1u); mb_par ^= 1u << bb; }
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        PT_MARK(16);
+        // band-1 cells (the digit ring is free now; C of the band is folded and
+        // written once every thread passed the barrier)
+        if (io.m_hi > io.m_lo) {
+          __syncthreads();
+          PT_MARK(17);
+          cert_band_records(io, cs, io.Cdst ? io.Cdst : io.Csrc, sm.sb);
+          __syncthreads();
+          PT_MARK(18);
+          cert_band_rows(io, cs, Bs);
+        }
+        PT_MARK(6);
         // band-1 row sums to the row-interval scratch (read back by the row owners)
 #pragma unroll
         for (int m = 0; m < kBandRows; ++m) {
           const uint32_t rho = kBandRows * t + m;
           if (rho >= r_lo && rho < r_hi) ivm[rho] = Bs[m];
         }
-        for (uint32_t bb = 0; bb < 2; ++bb)
-          if (issued & (1u << bb)) { mbar_wait(&ctl->mbar[bb], (mb_par >> bb) & 1u); mb_par ^= 1u << bb; }
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         if ((t & 31) == 0) atomicAdd(reinterpret_cast<unsigned long long*>(&ctl->st.n_mma),
                                      (unsigned long long)nmma);
         if (t == 0) ctl->st.n_umma += numma;
@@ -1430,7 +1443,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
                             1024.0 * u * (double)L * (ctl->c_unitH + ctl->c_unitR);
         }
         __syncthreads();
-        if (ctl->M_hi > ctl->M_lo) cert_band2_scan(io, ctl->M_hi - ctl->M_lo);
+        if (ctl->M_hi > ctl->M_lo) cert_band2_scan(io, ctl->M_hi - ctl->M_lo, reinterpret_cast<double*>(cs.rec));
         __syncthreads();
         if (t == 0 && ctl->M_hi > ctl->M_lo) {
           // scan rounding, absolute: relative to the band-2 totals
@@ -1466,6 +1479,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           }
         }
         __syncthreads();
+        PT_MARK(11);
       }
       if (first) {
         filter_hlist(ctl, sm, hlist);
@@ -1543,6 +1557,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         }
       }
       }   // groups
+      PT_MARK(12);
       if (ctl->need_exact) {
         // exact re-score of the same pivot (flips already folded into Cpiv), in
         // groups of kJ * blockDim.x rows combined in ascending offset order
@@ -1721,6 +1736,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
     }
 
     // ---- reduce_scan result + Algorithm 1 control (search.cpp:379-419)
+    PT_MARK(13);
     if (t == 0) {
       WalkState& S = ctl->st;
       S.nse += a.n;                                            // :379
@@ -1840,6 +1856,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
     }
     if (ctl->restart && t == 0) ctl->st.loc_at_pivot = 0;
     __syncthreads();
+    PT_MARK(14);
   }
 
   // ---- persist
@@ -1849,8 +1866,10 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
   if (kCert && t == 0) printf("PTCTA %u %lld\n", w, clock64() - pt_t0);
   if (kCert && w == 0 && t < 16) {
     const long long* q = pt_acc[t];
-    printf("PT warp %2u top %lld build %lld cores %lld bar %lld issue %lld cross %lld band %lld other %lld mbarwait %lld fence %lld\n", t,
-           q[0], q[1], q[2], q[3], q[4], q[5], q[6], q[7], q[8], q[9]);
+    printf("PT warp %2u top %lld build %lld cores %lld bar %lld issue %lld cross %lld band %lld prologue %lld mbarwait %lld fence %lld "
+           "tail %lld rows %lld reduce %lld exact %lld control %lld steptop %lld epimbar %lld episync %lld epirec %lld\n", t,
+           q[0], q[1], q[2], q[3], q[4], q[5], q[6], q[7], q[8], q[9], q[10], q[11], q[12], q[13], q[14], q[15],
+           q[16], q[17], q[18]);
   }
 #endif
   if (t == 0) {
