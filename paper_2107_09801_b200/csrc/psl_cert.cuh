@@ -70,7 +70,13 @@ constexpr size_t kCertBytes = kDRing + 2 * kABuf + 2 * kLimbBuf + 4 * kWinBuf +
                               2 * kCertRecBuf + 3 * kCertCBuf;
 constexpr long long kMaxD = 0x7F7F7F7F7F7F7F7Fll;      // 8 balanced base-256 digits
 constexpr uint32_t kCertMinL = 2048;
-constexpr uint32_t kTmemCols = 128;
+#ifndef PSL_XTMEM
+#define PSL_XTMEM 0                // 1: cross term on 8 row tiles x half the columns per warp, accumulators
+                                   // parked in TMEM between zone-1 chunks (half the LDS per MMA).  Correct, but
+                                   // measured 21.6 vs 16.4 ms/step at m20 (its -DPSL_PHASE_TIMING build: -2 %);
+                                   // 0: 4 tiles x all columns, accumulators in registers
+#endif
+constexpr uint32_t kTmemCols = PSL_XTMEM ? 256 : 128;   // fwd 0-63, rev 64-127, cross 128-255
 constexpr uint32_t kLutS = 6144;             // PowerTable entries staged in shared memory           // fwd accumulator cols 0-63, rev 64-127
 
 struct CertIO {
@@ -163,11 +169,20 @@ __device__ __forceinline__ uint4 seq16(const uint32_t* sb, long long p0, int dir
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
+#ifndef PSL_MBAR_HINT
+#define PSL_MBAR_HINT 0            // > 0: try_wait suspend-time hint (ns) instead of the default
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
   uint32_t done = 0;
   while (!done) {
+#if PSL_MBAR_HINT > 0
+    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}\n" : "=r"(done) : "r"(smem_u32(mbar)), "r"(parity),
+                 "n"(PSL_MBAR_HINT) : "memory");
+#else
     asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
                  "selp.u32 %0, 1, 0, p;\n\t}\n" : "=r"(done) : "r"(smem_u32(mbar)), "r"(parity) : "memory");
+#endif
   }
 }
 
@@ -701,6 +716,178 @@ __device__ __forceinline__ void cert_cross_run(uint32_t f, uint32_t v, uint32_t 
   if (c + 1 < n) column(std::integral_constant<int, 1>{});
 }
 
+#if PSL_XTMEM
+// ---- the cross term with TMEM-parked accumulators.  Warp w scores row group
+// g = (w & 3) | (w >> 3) << 2 (rows 128 g .. 128 g + 127, 8 m16 tiles) over
+// the column half h = (w >> 2) & 1 of every zone-1 chunk (columns 8h .. 8h + 7):
+// per column one new forward and one new reversed quad feed 8 MMAs (half the
+// shared-memory loads per MMA of 4 tiles x 16 columns).  The 32 accumulator
+// registers live in TMEM between chunks (lanes 32 (w & 3) + lane, columns
+// 128 + 32 (w >> 2)); warps w and w + 4 hold the two halves of the same rows.
+constexpr int kXTiles = 8;
+__device__ __forceinline__ uint32_t cert_xgroup(uint32_t w) { return (w & 3u) | ((w >> 3) << 2); }
+__device__ __forceinline__ uint32_t cert_xhalf(uint32_t w) { return (w >> 2) & 1u; }
+__device__ __forceinline__ uint32_t cert_xtaddr(uint32_t tmem, uint32_t w) {
+  return tmem + ((32u * (w & 3u)) << 16) + 128u + 32u * (w >> 2);
+}
+__device__ __forceinline__ CertLane cert_lane8(const CertSmem& cs) {
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t gid = lane >> 2, tig = lane & 3;
+  const uint32_t g = cert_xgroup(w), h = cert_xhalf(w);
+  const uint32_t base_f = 128 * g + gid + 4 * tig, af = gid & 3;
+  const uint32_t base_v = kY0 - 128 * g - gid + 4 * tig, av = base_v & 3;
+  CertLane l;
+  l.f = smem_u32(cs.winF) + af * kWinBytes + (base_f - af) + 256 * h;
+  l.v = smem_u32(cs.winV) + av * kWinBytes + (base_v - av) + 256 * h;
+  l.bd = smem_u32(cs.limbR) + gid * kLimbStride + 4 * tig + 256 * h;
+  return l;
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int (&a)[kXTiles][4]) {
+  __syncwarp();
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(a[0][0]), "=r"(a[0][1]), "=r"(a[0][2]), "=r"(a[0][3]), "=r"(a[1][0]), "=r"(a[1][1]),
+        "=r"(a[1][2]), "=r"(a[1][3]), "=r"(a[2][0]), "=r"(a[2][1]), "=r"(a[2][2]), "=r"(a[2][3]),
+        "=r"(a[3][0]), "=r"(a[3][1]), "=r"(a[3][2]), "=r"(a[3][3]), "=r"(a[4][0]), "=r"(a[4][1]),
+        "=r"(a[4][2]), "=r"(a[4][3]), "=r"(a[5][0]), "=r"(a[5][1]), "=r"(a[5][2]), "=r"(a[5][3]),
+        "=r"(a[6][0]), "=r"(a[6][1]), "=r"(a[6][2]), "=r"(a[6][3]), "=r"(a[7][0]), "=r"(a[7][1]),
+        "=r"(a[7][2]), "=r"(a[7][3])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const int (&a)[kXTiles][4]) {
+  __syncwarp();
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};"
+      ::"r"(taddr), "r"(a[0][0]), "r"(a[0][1]), "r"(a[0][2]), "r"(a[0][3]), "r"(a[1][0]), "r"(a[1][1]),
+        "r"(a[1][2]), "r"(a[1][3]), "r"(a[2][0]), "r"(a[2][1]), "r"(a[2][2]), "r"(a[2][3]),
+        "r"(a[3][0]), "r"(a[3][1]), "r"(a[3][2]), "r"(a[3][3]), "r"(a[4][0]), "r"(a[4][1]),
+        "r"(a[4][2]), "r"(a[4][3]), "r"(a[5][0]), "r"(a[5][1]), "r"(a[5][2]), "r"(a[5][3]),
+        "r"(a[6][0]), "r"(a[6][1]), "r"(a[6][2]), "r"(a[6][3]), "r"(a[7][0]), "r"(a[7][1]),
+        "r"(a[7][2]), "r"(a[7][3]) : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// n consecutive columns for 8 tiles: tile 2i (+1), i = 0..3, reads the forward
+// quad E (O) at e = c + i and the reversed quad E (O) at e = c - i; rings of
+// five (F(c .. c+4), V(c-4 .. c); slot = e mod 5, resolved at compile time).
+__device__ __forceinline__ void cert_cross_run8(uint32_t f, uint32_t v, uint32_t bd, int n,
+                                                int (&acc)[kXTiles][4]) {
+  constexpr int R = 5;
+  Quad F[R], V[R];
+  F[0] = qfe<0>(f); F[1] = qfe<1>(f); F[2] = qfe<2>(f); F[3] = qfe<3>(f); F[4] = qfe<4>(f);
+  V[0] = qve<0>(v); V[4] = qve<-1>(v); V[3] = qve<-2>(v); V[2] = qve<-3>(v);   // V(e) -> slot e mod 5
+  V[1] = {0u, 0u, lds32<-112>(v), lds32<-120>(v)};                            // V(-4): only z, w are used
+  auto column = [&](auto U_) {
+    constexpr int U = decltype(U_)::value;                  // column mod 5
+    const uint32_t b0 = lds32<0>(bd), b1 = lds32<16>(bd);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const Quad& fa = F[(U + i) % R];
+      const Quad& fb = F[(U + i + 1) % R];
+      const Quad& va = V[(U - i + 2 * R) % R];
+      const Quad& vb = V[(U - i - 1 + 2 * R) % R];
+      imma_q(acc[2 * i], uv_q(fa, va), b0, b1);
+      imma_q(acc[2 * i + 1], uv_q(Quad{fa.z, fa.w, fb.x, fb.y}, Quad{vb.z, vb.w, va.x, va.y}), b0, b1);
+    }
+    // advance: F(c + 5) -> slot U, V(c + 1) -> slot U + 1
+    f += 32; v += 32; bd += 32;
+    F[U] = qfe<4>(f);
+    V[(U + 1) % R] = qve<0>(v);
+  };
+  // always the full half chunk: columns past m_lo have R4 = 0 (zero digit rows)
+  (void)n;
+  column(std::integral_constant<int, 0>{}); column(std::integral_constant<int, 1>{});
+  column(std::integral_constant<int, 2>{}); column(std::integral_constant<int, 3>{});
+  column(std::integral_constant<int, 4>{}); column(std::integral_constant<int, 0>{});
+  column(std::integral_constant<int, 1>{}); column(std::integral_constant<int, 2>{});
+}
+
+// The cross MMAs of zone-1 chunk c (buffer c & 1) for this warp's rows and
+// column half; the accumulators come from / go back to TMEM (zero at chunk 0,
+// the first zone-1 chunk of every pass).
+#ifndef PSL_XT_NOINLINE
+#define PSL_XT_NOINLINE 0
+#endif
+#if PSL_XT_NOINLINE
+__device__ __noinline__ void cert_cross_chunk(const CertIO& io, const CertSmem& cs, const CertLane& ln, uint32_t c,
+                                              uint32_t tmem, uint32_t& nmma) {
+#else
+__device__ __forceinline__ void cert_cross_chunk(const CertIO& io, const CertSmem& cs, const CertLane& ln, uint32_t c,
+                                                 uint32_t tmem, uint32_t& nmma) {
+#endif
+  const uint32_t kb = cert_kb(c);
+  if (kb > io.m_lo) return;
+#ifdef PSL_ABLATE_MMA
+  return;
+#endif
+  const uint32_t w = threadIdx.x >> 5, g = cert_xgroup(w), h = cert_xhalf(w);
+  const int rw_lo = max(128 * (int)g, (int)io.r_lo), rw_hi = min(128 * (int)g + 127, (int)io.r_hi - 1);
+  if (rw_lo > rw_hi) return;
+  // columns whose first shift is still in zone 1 (the rest of the chunk has R4 = 0), this half
+  const int nall = (int)min((uint32_t)kCCols, (io.m_lo - kb) / 32 + 1);
+  if (nall <= 8 * (int)h) return;
+  const int n = 8;            // the whole half: its columns past m_lo add zero digits
+  const uint32_t b = c & 1;
+#ifdef PSL_DEBUG_BOUNDS
+  {
+    // every LDS whose value is used stays inside its own window copy / digit row
+    // (the final ring refill after the last column is dead: it may read one
+    // column past the copy, still inside the CTA's shared memory)
+    const uint32_t wf = smem_u32(cs.winF), wv = smem_u32(cs.winV), lb = smem_u32(cs.limbR);
+    const uint32_t f0 = ln.f + b * (uint32_t)kWinBuf - wf, v0 = ln.v + b * (uint32_t)kWinBuf - wv;
+    const uint32_t cf = f0 % kWinBytes, cvv = v0 % kWinBytes;
+    const uint32_t cb = ((ln.bd + b * (uint32_t)kLimbBuf - lb) % (uint32_t)kLimbBuf) % (uint32_t)kLimbStride;
+    PSL_CHK(cf + 32u * (uint32_t)n + 124u <= (uint32_t)kWinBytes, 16);
+    PSL_CHK(cvv >= 120u && cvv + 32u * (uint32_t)n - 12u <= (uint32_t)kWinBytes, 17);
+    PSL_CHK(cb + 32u * (uint32_t)n - 12u <= (uint32_t)kLimbStride, 18);
+  }
+#endif
+  nmma += (uint32_t)(n * kXTiles);
+  int acc[kXTiles][4];
+  const uint32_t ta = cert_xtaddr(tmem, w);
+  if (c == 0) {
+#pragma unroll
+    for (int r = 0; r < kXTiles; ++r)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[r][e] = 0;
+  } else {
+    tmem_ld32(ta, acc);
+  }
+  cert_cross_run8(ln.f + b * (uint32_t)kWinBuf, ln.v + b * (uint32_t)kWinBuf,
+                  ln.bd + b * (uint32_t)kLimbBuf, n, acc);
+  tmem_st32(ta, acc);
+}
+
+// Cross accumulators -> per-row doubles: the half-0 warp of each row group adds
+// its partner's (column half 1) int32 digit sums exactly, then rows 128 g + 16 r
+// + gid (+8) as before (weights 256^d x 2^qR).  Call after a barrier with
+// tcgen05.fence::after_thread_sync.
+__device__ __forceinline__ void cert_cross_rows(uint32_t tmem, uint32_t m_lo, double unitR, double* xrow) {
+  const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5, gid = lane >> 2, tig = lane & 3;
+  if (cert_xhalf(w) != 0) return;
+  const uint32_t g = cert_xgroup(w);
+  int acc[kXTiles][4], acc1[kXTiles][4];
+  const bool s0 = m_lo >= 1, s1 = m_lo >= 1 + 256;       // the halves ran in chunk 0 (zone 1 is a prefix)
+  tmem_ld32(cert_xtaddr(tmem, w), acc);
+  tmem_ld32(cert_xtaddr(tmem, w + 4), acc1);
+  const double w0 = ldexp(unitR, 16 * tig), w1 = ldexp(unitR, 16 * tig + 8);
+#pragma unroll
+  for (int r = 0; r < kXTiles; ++r) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[r][e] = (s0 ? acc[r][e] : 0) + (s1 ? acc1[r][e] : 0);
+#pragma unroll
+    for (int hh = 0; hh < 2; ++hh) {
+      double p = __dadd_rn(__dmul_rn((double)acc[r][2 * hh], w0), __dmul_rn((double)acc[r][2 * hh + 1], w1));
+      p = __dadd_rn(p, __shfl_xor_sync(FULL, p, 1));
+      p = __dadd_rn(p, __shfl_xor_sync(FULL, p, 2));
+      if (tig == 0) xrow[128 * g + 16 * r + gid + 8 * hh] = p;
+    }
+  }
+}
+#else
 // The cross MMAs of zone-1 chunk c (buffer c & 1) for this warp's 128 rows.
 __device__ __forceinline__ void cert_cross_chunk(const CertIO& io, const CertSmem& cs, const CertLane& ln, uint32_t c,
                                                  int (&acc)[kCertTiles][4], uint32_t& nmma) {
@@ -751,6 +938,8 @@ __device__ __forceinline__ void cert_cross_rows(const int (&acc)[kCertTiles][4],
     }
   }
 }
+
+#endif  // PSL_XTMEM
 
 // TMEM accumulators -> linrow[r_lo + u] (threads 0..127 = TMEM lanes): forward
 // lane rho, N-group g -> u = rho + 128 (7 - g); reversed lane r -> u = 127 - r +

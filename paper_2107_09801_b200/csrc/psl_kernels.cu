@@ -1137,7 +1137,11 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
       // (offset i) are neighbours j = start + i mod L; a window that wraps past
       // L - 1 is scored in two passes, one per contiguous row segment.
       const CertSmem cs = cert_carve(smem_raw);
+#if PSL_XTMEM
+      const CertLane ln = cert_lane8(cs);
+#else
       const CertLane ln = cert_lane(cs);
+#endif
       // row intervals [lo, hi] and midpoints of the current group, through global
       // scratch (not registers across the chunk loop)
       double* ivm = a.iv_buf + (size_t)w * 3 * kGroup;
@@ -1215,17 +1219,24 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         io.fsum = first && seg == 0 && s_fitness_pending != 0 && initial;
         io.chain = first && seg == 0 && s_fitness_pending != 0 && !initial;
         double chain = 0.0;
+#if !PSL_XTMEM
         int acc[kCertTiles][4];
 #pragma unroll
         for (int r = 0; r < kCertTiles; ++r)
 #pragma unroll
           for (int e = 0; e < 4; ++e) acc[r][e] = 0;
+#endif
         bool ovf = false;
         double part[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
         double Bs[kBandRows] = {0.0, 0.0};   // band-1 sums of rows kBandRows t + m
         int32_t pmax = 0;
         uint32_t nmma = 0, numma = 0, started = 0;
         const uint32_t tmem = ctl->tmem;
+#if PSL_XTMEM
+#define XACC tmem
+#else
+#define XACC acc
+#endif
         // digit cores of shifts <= 0 (read by the first chunks' shifted N-groups) are zero
         for (int32_t cz = -(int32_t)kLag; cz < 0; ++cz) cert_zero_digits(cs, cz);
         // C_k streams into shared memory by cp.async two chunks ahead
@@ -1312,7 +1323,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           // iteration), so one half's builder overlaps the other half's IMMA work
           // inside every barrier interval (buffers of c - 1 live until iteration c + 1)
           if (PSL_STAGGER && early && c >= 1 && c - 1 < c_end) {
-            cert_cross_chunk(io, cs, ln, c - 1, acc, nmma);
+            cert_cross_chunk(io, cs, ln, c - 1, XACC, nmma);
           }
           cert_cores(io, cs, (int32_t)c, sm.sb, fw, rv);
           PT_MARK(2);
@@ -1335,7 +1346,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           }
           PT_MARK(4);
           if (c < c_end && !(PSL_STAGGER && early)) {   // zone-1 cross MMAs, band-1 cells
-            cert_cross_chunk(io, cs, ln, c, acc, nmma);          // 64 rows per warp
+            cert_cross_chunk(io, cs, ln, c, XACC, nmma);
             PT_MARK(5);
             if (io.chain && t == kCertThreads - 64) cert_chain_chunk(io, cs, c, chain);
             PT_MARK(6);
@@ -1418,10 +1429,19 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
             if (lane == 0) ctl->rs5[i][warp] = v;
           }
         }
+#if PSL_XTMEM
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");   // cross accumulators in TMEM
+#endif
         __syncthreads();                       // windows / cores are free: row arrays alias them
         double* linrow = cs.linrow;
         const double* xrow = cs.xrow;
+#if PSL_XTMEM
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        cert_cross_rows(tmem, ctl->m_lo, ctl->c_unitR, cs.xrow);
+#else
         cert_cross_rows(acc, ctl->c_unitR, cs.xrow);
+#endif
+#undef XACC
         cert_lin_rows(tmem, false, started, ctl->c_unitH, io, linrow);
         __syncthreads();
         cert_lin_rows(tmem, true, started, ctl->c_unitH, io, linrow);
