@@ -39,8 +39,8 @@
 // builds one shift per chunk (kCC = 512); warps 15 and 14 also issue the
 // chunk's forward / reversed tcgen05 MMAs; all 16 warps run the cross MMAs.
 constexpr uint32_t kCertThreads = 2 * kThreads;
-#ifndef PSL_WIN_BALANCE
-#define PSL_WIN_BALANCE 0          // 1: window words moved to the warps without core/issue work (measured +3 %)
+#ifndef PSL_STAGE_PRE
+#define PSL_STAGE_PRE 1            // zone-1 window staging: pivot words loaded at the top of the build
 #endif
 #ifndef PSL_REV_WARP_C
 #define PSL_REV_WARP_C 14u         // the warp that issues the reversed MMAs (PSL_REV_WARP)
@@ -257,6 +257,28 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
   const uint32_t t = threadIdx.x;
   const uint32_t kb = cert_kb(c), k = kb + t;
   const uint32_t b = c & 1;
+  const int L = (int)io.L, j0 = io.j0;
+  constexpr int kW = kWinBytes / 4;
+  // window-staging word q of direction dir: bytes 4q..4q+7 (fwd: positions p0 + i, rev: p0 - i)
+  auto stage_p0 = [&](int idx, int& dir) {
+    dir = idx >= kW ? 1 : 0;
+    const int q = dir ? idx - kW : idx;
+    return dir == 0 ? j0 + (int)kb + 4 * q : j0 - (int)kb + kY0 - 4 * q;
+  };
+#if PSL_STAGE_PRE
+  // zone-1 chunks: the staging's pivot words, loaded before the build (L2 latency off the barrier path)
+  uint2 pw0 = make_uint2(0u, 0u), pw1 = make_uint2(0u, 0u);
+  if (kb <= io.m_lo) {
+    auto pre = [&](int idx) {
+      int dir;
+      const int p0 = stage_p0(idx, dir);
+      const int lo = dir == 0 ? p0 : p0 - 7;
+      return (lo >= 0 && lo + 7 < L) ? make_uint2(sb[(lo >> 5) + 1], sb[(lo >> 5) + 2]) : make_uint2(0u, 0u);
+    };
+    pw0 = pre((int)t);
+    if ((int)(t + kCC) < 2 * kW) pw1 = pre((int)(t + kCC));
+  }
+#endif
   bool want = false;
   int32_t cv = 0;
   if (k < io.L) {
@@ -371,21 +393,24 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
 #ifdef PSL_ABLATE_STAGE
   return;
 #endif
-  const int L = (int)io.L, j0 = io.j0;
-  constexpr int kW = kWinBytes / 4;
   // thread -> base word q of one direction: bytes 4q..4q+7 of the base copy
   // from one bit window, copy a word q = base bytes 4q+a..4q+a+3
-  auto stage = [&](int idx) {
-    const int dir = idx >= kW ? 1 : 0;
+  auto stage = [&](int idx, uint2 pw) {
+    int dir;
+    const int p0 = stage_p0(idx, dir);
     const int q = dir ? idx - kW : idx;
     // fwd: byte i <-> position p0 + i; rev: byte i <-> position p0 - i (i = 0..7)
-    const int p0 = dir == 0 ? j0 + (int)kb + 4 * q : j0 - (int)kb + kY0 - 4 * q;
     const int lo = dir == 0 ? p0 : p0 - 7, hi = lo + 7;
     uint32_t w0 = 0, w1 = 0;
     if (hi >= 0 && lo < L) {
       if (lo >= 0 && hi < L) {
         PSL_CHK(sb_ok((lo >> 5) + 2, io.L), 9);
+#if PSL_STAGE_PRE
+        uint32_t x = __funnelshift_r(pw.x, pw.y, (uint32_t)lo & 31) & 0xFFu;
+#else
+        (void)pw;
         uint32_t x = __funnelshift_r(sb[(lo >> 5) + 1], sb[(lo >> 5) + 2], (uint32_t)lo & 31) & 0xFFu;
+#endif
         if (dir) x = __brev(x) >> 24;
         w0 = nib_bytes(x & 0xFu);
         w1 = nib_bytes(x >> 4);
@@ -406,16 +431,11 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
   // 2 kW = 784 words per chunk: one per thread, the other 272 to the warps that
   // stage no sequence cores and issue no reversed MMAs before the barrier
   // (11, 12, 13, 15), so the chunk barrier waits for no doubly loaded warp
-  stage((int)t);
-#if PSL_WIN_BALANCE
-  const uint32_t wp = t >> 5;
-  if (wp >= 11 && wp != PSL_REV_WARP_C) {
-    const int sidx = (int)((wp == 15 ? 3u : wp - 11u) * 32u + (t & 31u));
-    for (int e = (int)kCC + sidx; e < 2 * kW; e += 128) stage(e);
-  }
-#else
-  if ((int)(t + kCC) < 2 * kW) stage((int)(t + kCC));
+#if !PSL_STAGE_PRE
+  const uint2 pw0 = make_uint2(0u, 0u), pw1 = pw0;
 #endif
+  stage((int)t, pw0);
+  if ((int)(t + kCC) < 2 * kW) stage((int)(t + kCC), pw1);
 }
 
 // Tail chunks c0 <= c < nch (every shift past M_hi: H4 = R4 = 0, the term of
@@ -494,11 +514,18 @@ __device__ __forceinline__ void cert_zero_digits(const CertSmem& cs, long long c
 }
 
 // 20 sequence bytes for positions p0 + dir * x, x = 0..19, as 5 words (0 outside [0, L))
-__device__ __forceinline__ void seq20(const uint32_t* sb, int32_t p0, int dir, int32_t L, uint32_t (&w)[5]) {
+__device__ __forceinline__ void seq20(const uint32_t* sb, int32_t p0, int dir, int32_t L, uint32_t (&w)[5],
+                                      uint2 pre) {
   const int32_t lo = dir > 0 ? p0 : p0 - 19, hi = lo + 19;
   if (lo >= 0 && hi < L) {
     PSL_CHK(sb_ok((lo >> 5) + 2, (uint32_t)L), 14);
+#if PSL_CORE_PRE
+    (void)sb;
+    uint32_t x = __funnelshift_r(pre.x, pre.y, (uint32_t)lo & 31) & 0xFFFFFu;
+#else
+    (void)pre;
     uint32_t x = __funnelshift_r(sb[(lo >> 5) + 1], sb[(lo >> 5) + 2], (uint32_t)lo & 31) & 0xFFFFFu;
+#endif
     if (dir < 0) x = __brev(x) >> 12;
 #pragma unroll
     for (int q = 0; q < 5; ++q) w[q] = nib_bytes((x >> (4 * q)) & 0xFu);
@@ -515,8 +542,41 @@ __device__ __forceinline__ void seq20(const uint32_t* sb, int32_t p0, int dir, i
 // (core m row i = s[JT + 127 - kb' - 8m - i - x]).  Core row (m, i) is the 16
 // bytes at position offset r = 8m + i (address 16 r); a thread expands 20 bytes
 // once and emits the four rows r0..r0+3 by byte shifts.
+#ifndef PSL_CORE_PRE
+#define PSL_CORE_PRE 0             // 1 (measured neutral): the cores' two pivot words loaded at the top of the iteration
+#endif
+// This thread's core quad (dir, g) of iteration c, or false (cert_cores' mapping).
+__device__ __forceinline__ bool cert_core_quad(const CertIO& io, int32_t c, bool fwd, bool rev, int32_t& p0,
+                                               int& dir) {
+  constexpr uint32_t kQuads = kACores * 2;
+  constexpr uint32_t kRevT = (kQuads + 31) / 32 * 32;
+  const uint32_t t = threadIdx.x;
+  uint32_t g;
+  if (t < kQuads) { dir = 0; g = t; }
+  else if (t >= kRevT && t < kRevT + kQuads) { dir = 1; g = t - kRevT; }
+  else return false;
+  if (dir == 0 ? !fwd : !rev) return false;
+  p0 = dir == 0 ? io.JT + (int32_t)cert_kb(c) + 4 * (int32_t)g
+                : io.JT + 127 - (int32_t)cert_kb(c - (int32_t)kLag) - 4 * (int32_t)g;
+  return true;
+}
+// The two pivot words seq20's fast path reads for this thread's quad (issued
+// early so the L2 latency overlaps the builder).
+__device__ __forceinline__ uint2 cert_core_words(const CertIO& io, int32_t c, const uint32_t* sb, bool fwd, bool rev) {
+#if PSL_CORE_PRE
+  int32_t p0;
+  int dir;
+  if (!cert_core_quad(io, c, fwd, rev, p0, dir)) return make_uint2(0u, 0u);
+  const int32_t lo = dir == 0 ? p0 : p0 - 19;
+  if (lo < 0 || lo + 19 >= (int32_t)io.L) return make_uint2(0u, 0u);
+  return make_uint2(sb[(lo >> 5) + 1], sb[(lo >> 5) + 2]);
+#else
+  (void)io; (void)c; (void)sb; (void)fwd; (void)rev;
+  return make_uint2(0u, 0u);
+#endif
+}
 __device__ __forceinline__ void cert_cores(const CertIO& io, const CertSmem& cs, int32_t c,
-                                           const uint32_t* sb, bool fwd, bool rev) {
+                                           const uint32_t* sb, bool fwd, bool rev, uint2 pre) {
   unsigned char* base = cs.acore + (size_t)(c & 1) * kABuf;
   constexpr uint32_t kQuads = kACores * 2;    // 100 groups of 4 rows per direction
   const uint32_t t = threadIdx.x;
@@ -534,7 +594,7 @@ __device__ __forceinline__ void cert_cores(const CertIO& io, const CertSmem& cs,
   const int32_t p0 = dir == 0 ? io.JT + (int32_t)cert_kb(c) + 4 * (int32_t)g
                               : io.JT + 127 - (int32_t)cert_kb(c - (int32_t)kLag) - 4 * (int32_t)g;
   uint32_t w[5];
-  seq20(sb, p0, dir == 0 ? 1 : -1, (int32_t)io.L, w);
+  seq20(sb, p0, dir == 0 ? 1 : -1, (int32_t)io.L, w, pre);
   uint4* dst = reinterpret_cast<uint4*>(base + (size_t)dir * kACores * 128 + 64 * g);
   PSL_CHK(in_buf(dst + 3, cs.acore, 2 * kABuf, 16), 15);
   // row r of the quad = the 16 bytes from byte r; rows in a lane-rotated order

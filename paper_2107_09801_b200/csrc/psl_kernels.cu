@@ -1271,6 +1271,9 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           if (c_end > 1) cert_prefetch(io, cs, 1);
         }
         uint2 fwords = (builder && io.F == 1) ? cert_fold_words(io, 0, sm.sb) : make_uint2(0u, 0u);
+#ifndef PSL_LATE_WAIT
+#define PSL_LATE_WAIT 1
+#endif
         uint32_t issued = 0;        // bit (c & 1): iteration c committed MMAs not yet waited for
         // iteration c: build chunk c, stage the sequence cores of forward kappa-chunk c and
         // reversed kappa'-chunk c - kLag, issue their tcgen05 MMAs (one thread, async),
@@ -1295,6 +1298,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
             rv_c = pend_c;
             pend_c = -1;
           }
+#if !PSL_LATE_WAIT
           if (issued & (1u << (c & 1))) {      // MMAs of iteration c - 2 read this buffer
             PT_MARK(0);
             mbar_wait(&ctl->mbar[c & 1], (mb_par >> (c & 1)) & 1u);
@@ -1302,8 +1306,10 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
             mb_par ^= 1u << (c & 1);
             issued &= ~(1u << (c & 1));
           }
+#endif
           PT_MARK(0);
           const bool fw = (ctl->cfw[c >> 5] >> (c & 31)) & 1u, rv = (ctl->crv[c >> 5] >> (c & 31)) & 1u;
+          const uint2 corew = cert_core_words(io, (int32_t)c, sm.sb, fw, rv);
           if (c < c_end) {
             if (builder) {
               if (c + 2 < c_end) cert_prefetch(io, cs, c + 2);
@@ -1325,7 +1331,19 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           if (PSL_STAGGER && early && c >= 1 && c - 1 < c_end) {
             cert_cross_chunk(io, cs, ln, c - 1, XACC, nmma);
           }
-          cert_cores(io, cs, (int32_t)c, sm.sb, fw, rv);
+#if PSL_LATE_WAIT
+          // the MMAs of iteration c - 2 read A-core buffer c & 1 (and nothing the
+          // builder writes: its digit-ring slots are 8 chunks apart), so their
+          // completion is awaited only before this iteration's cores
+          if (issued & (1u << (c & 1))) {
+            PT_MARK(2);
+            mbar_wait(&ctl->mbar[c & 1], (mb_par >> (c & 1)) & 1u);
+            PT_MARK(8);
+            mb_par ^= 1u << (c & 1);
+            issued &= ~(1u << (c & 1));
+          }
+#endif
+          cert_cores(io, cs, (int32_t)c, sm.sb, fw, rv, corew);
           PT_MARK(2);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           PT_MARK(9);
