@@ -9,9 +9,11 @@ def funcs(path):
     """line -> enclosing function name (top-level definitions)."""
     names, cur = {}, "?"
     for i, l in enumerate(open(path), 1):
-        m = re.match(r"(?:template <[^>]*>\s*)?(?:__device__|__global__)[^(]*?\b(\w+)\(", l)
-        if m:
-            cur = m.group(1)
+        if re.match(r"(?:template <[^>]*>\s*)?(?:__device__|__global__)", l):
+            l2 = re.sub(r"__launch_bounds__\([^)]*\([^)]*\)[^)]*\)|__launch_bounds__\([^)]*\)", "", l)
+            m = re.search(r"\b(\w+)\(", l2)
+            if m:
+                cur = m.group(1)
         names[i] = cur
     return names
 
