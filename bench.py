@@ -396,6 +396,11 @@ def main():
         "frac_of_tcgen05_issue_peak": (achieved / (umma_per_s * 128 * 64 * 32 * 2.0))
         if umma_per_s else None,
         "mma_sync_peak_tops": (mma_per_s * 16 * 8 * 32 * 2.0 / 1e12) if mma_per_s else None,
+        # tcgen05 (UMMA) and mma.sync (IMMA) serialise on the SM's tensor pipe
+        # (profiles/r02_tensor_pipe_sharing.txt): the step's exclusive tensor-pipe
+        # time at the probed rates (probe_umma walks the scan's descriptors)
+        "tensor_pipe_busy_frac": ((scan["umma"] / umma_per_s + scan["mma"] / mma_per_s) / (ms * 1e-3))
+        if (umma_per_s and mma_per_s) else None,
         "umma_per_step": scan["umma"] / args.steps,
         "mma_per_step": scan["mma"] / args.steps,
         "cells_per_s": cells_per_step / per_step_s,

@@ -1979,8 +1979,11 @@ __global__ void __launch_bounds__(128) probe_umma_kernel(int reps, int per, int*
   uint32_t par = 0;
   for (int r = 0; r < reps; ++r) {
     if (threadIdx.x == 0) {
+      // the certified scan's descriptors and K-step walk (16 steps of 512 B of A, 256 B of B)
       const uint64_t da = umma_desc(base, 256, 128), db = umma_desc(base + 4096, 128, 1024);
-      for (int i = 0; i < per; ++i) umma_i8(tmem_base, da, db, i > 0 ? 1u : 0u);
+      for (int i = 0; i < per; ++i)
+        umma_i8(tmem_base, da + (uint64_t)((i & 15) * (512 >> 4)), db + (uint64_t)((i & 15) * (256 >> 4)),
+                i > 0 ? 1u : 0u);
       umma_commit(&mbar);
     }
     mbar_wait(&mbar, par);
