@@ -818,7 +818,17 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
   int bad_val = 0;
   std::mutex bad_mu;
   const uint32_t n_pack = shared_init ? 0u : (inits ? n_walks : 0u);
-  auto batch_of = [&](uint32_t w) { return (uint32_t)(((uint64_t)(w + 1) * nbatch - 1) / n_walks); };
+  // batch boundaries: a small first batch (1/16 of the walks) so the first
+  // table builds start after little packing; the GPU is the slower stage after it
+  auto bound = [&](uint32_t b) -> uint32_t {
+    static const uint32_t num[5] = {0, 1, 4, 8, 16};
+    return nbatch == 4 ? (uint32_t)((uint64_t)n_walks * num[b] / 16) : (uint32_t)((uint64_t)n_walks * b / nbatch);
+  };
+  auto batch_of = [&](uint32_t w) {
+    uint32_t b = 0;
+    while (b + 1 < nbatch && w >= bound(b + 1)) ++b;
+    return b;
+  };
   auto worker = [&]() {
     for (;;) {
       const uint32_t w = next.fetch_add(1);
@@ -845,8 +855,8 @@ int walks_create(psl_ctx* ctx, const psl_params* params, uint32_t n_walks, const
   }
   auto join_pool = [&]() { for (auto& th : pool) if (th.joinable()) th.join(); };
   for (uint32_t bi = 0; bi < nbatch; ++bi) {
-    const uint32_t w0 = (uint32_t)((uint64_t)n_walks * bi / nbatch);
-    const uint32_t cnt = (uint32_t)((uint64_t)n_walks * (bi + 1) / nbatch) - w0;
+    const uint32_t w0 = bound(bi);
+    const uint32_t cnt = bound(bi + 1) - w0;
     const uint32_t* dpacked = nullptr;
     size_t pstride = 0;
     if (n_pack) {
