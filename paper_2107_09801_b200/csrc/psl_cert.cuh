@@ -1134,11 +1134,23 @@ __device__ __forceinline__ void cert_band_rows(const CertIO& io, const CertSmem&
       const uint32_t W4 = ~A, W2 = Du & A, W1 = left ? ((A & Dv) | (~A & Du)) : Dv;
       const unsigned char* base = tab + (k0 - blo) * (uint32_t)(kBandRec * sizeof(double));
       const uint32_t nq = min(32u, bhi - k0 + 1);     // CTA-uniform
-      // 8 x code per byte, 4 cells per word
+      // 8 x code per byte, 4 cells per word; blocks where every lane of the warp is
+      // two-sided (code 2du + dv) or one-sided (4 + dw) skip the third bit plane
+      const uint32_t am = __activemask();
+      const bool allA = __all_sync(am, d >= 32), allB = __all_sync(am, d <= 0);
       uint32_t c8[8];
+      if (allA) {
 #pragma unroll
-      for (int g = 0; g < 8; ++g)
-        c8[g] = ((((spread4(W4 >> (4 * g)) << 1) + spread4(W2 >> (4 * g))) << 1) + spread4(W1 >> (4 * g))) << 3;
+        for (int g = 0; g < 8; ++g) c8[g] = ((spread4(Du >> (4 * g)) << 1) + spread4(Dv >> (4 * g))) << 3;
+      } else if (allB) {
+        const uint32_t Dw = left ? Du : Dv;
+#pragma unroll
+        for (int g = 0; g < 8; ++g) c8[g] = 0x20202020u + (spread4(Dw >> (4 * g)) << 3);
+      } else {
+#pragma unroll
+        for (int g = 0; g < 8; ++g)
+          c8[g] = ((((spread4(W4 >> (4 * g)) << 1) + spread4(W2 >> (4 * g))) << 1) + spread4(W1 >> (4 * g))) << 3;
+      }
       PSL_CHK(k0 - blo + nq <= (uint32_t)kGroup, 20);
       if (nq == 32) {                                   // full block: branch-free, loads hoisted
 #pragma unroll
