@@ -47,8 +47,8 @@ INT_OPS_PER_CELL = 4     # delta, +c, abs, max per flip x shift cel
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20,
-                    help="timed search steps, all in one launch (long launches amortise the end-of-launch tail of the walk CTAs)")
+    ap.add_argument("--steps", type=int, default=40,
+                    help="timed search steps, all in one launch like psl_walks_run (long launches amortise the end-of-launch tail of the walk CTAs)")
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--length", type=int, default=L_DEFAULT)
