@@ -169,20 +169,11 @@ __device__ __forceinline__ uint4 seq16(const uint32_t* sb, long long p0, int dir
   return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-#ifndef PSL_MBAR_HINT
-#define PSL_MBAR_HINT 0            // > 0: try_wait suspend-time hint (ns) instead of the default
-#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
   uint32_t done = 0;
   while (!done) {
-#if PSL_MBAR_HINT > 0
-    asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-                 "selp.u32 %0, 1, 0, p;\n\t}\n" : "=r"(done) : "r"(smem_u32(mbar)), "r"(parity),
-                 "n"(PSL_MBAR_HINT) : "memory");
-#else
     asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
                  "selp.u32 %0, 1, 0, p;\n\t}\n" : "=r"(done) : "r"(smem_u32(mbar)), "r"(parity) : "memory");
-#endif
   }
 }
 
@@ -514,18 +505,11 @@ __device__ __forceinline__ void cert_zero_digits(const CertSmem& cs, long long c
 }
 
 // 20 sequence bytes for positions p0 + dir * x, x = 0..19, as 5 words (0 outside [0, L))
-__device__ __forceinline__ void seq20(const uint32_t* sb, int32_t p0, int dir, int32_t L, uint32_t (&w)[5],
-                                      uint2 pre) {
+__device__ __forceinline__ void seq20(const uint32_t* sb, int32_t p0, int dir, int32_t L, uint32_t (&w)[5]) {
   const int32_t lo = dir > 0 ? p0 : p0 - 19, hi = lo + 19;
   if (lo >= 0 && hi < L) {
     PSL_CHK(sb_ok((lo >> 5) + 2, (uint32_t)L), 14);
-#if PSL_CORE_PRE
-    (void)sb;
-    uint32_t x = __funnelshift_r(pre.x, pre.y, (uint32_t)lo & 31) & 0xFFFFFu;
-#else
-    (void)pre;
     uint32_t x = __funnelshift_r(sb[(lo >> 5) + 1], sb[(lo >> 5) + 2], (uint32_t)lo & 31) & 0xFFFFFu;
-#endif
     if (dir < 0) x = __brev(x) >> 12;
 #pragma unroll
     for (int q = 0; q < 5; ++q) w[q] = nib_bytes((x >> (4 * q)) & 0xFu);
@@ -542,41 +526,8 @@ __device__ __forceinline__ void seq20(const uint32_t* sb, int32_t p0, int dir, i
 // (core m row i = s[JT + 127 - kb' - 8m - i - x]).  Core row (m, i) is the 16
 // bytes at position offset r = 8m + i (address 16 r); a thread expands 20 bytes
 // once and emits the four rows r0..r0+3 by byte shifts.
-#ifndef PSL_CORE_PRE
-#define PSL_CORE_PRE 0             // 1 (measured neutral): the cores' two pivot words loaded at the top of the iteration
-#endif
-// This thread's core quad (dir, g) of iteration c, or false (cert_cores' mapping).
-__device__ __forceinline__ bool cert_core_quad(const CertIO& io, int32_t c, bool fwd, bool rev, int32_t& p0,
-                                               int& dir) {
-  constexpr uint32_t kQuads = kACores * 2;
-  constexpr uint32_t kRevT = (kQuads + 31) / 32 * 32;
-  const uint32_t t = threadIdx.x;
-  uint32_t g;
-  if (t < kQuads) { dir = 0; g = t; }
-  else if (t >= kRevT && t < kRevT + kQuads) { dir = 1; g = t - kRevT; }
-  else return false;
-  if (dir == 0 ? !fwd : !rev) return false;
-  p0 = dir == 0 ? io.JT + (int32_t)cert_kb(c) + 4 * (int32_t)g
-                : io.JT + 127 - (int32_t)cert_kb(c - (int32_t)kLag) - 4 * (int32_t)g;
-  return true;
-}
-// The two pivot words seq20's fast path reads for this thread's quad (issued
-// early so the L2 latency overlaps the builder).
-__device__ __forceinline__ uint2 cert_core_words(const CertIO& io, int32_t c, const uint32_t* sb, bool fwd, bool rev) {
-#if PSL_CORE_PRE
-  int32_t p0;
-  int dir;
-  if (!cert_core_quad(io, c, fwd, rev, p0, dir)) return make_uint2(0u, 0u);
-  const int32_t lo = dir == 0 ? p0 : p0 - 19;
-  if (lo < 0 || lo + 19 >= (int32_t)io.L) return make_uint2(0u, 0u);
-  return make_uint2(sb[(lo >> 5) + 1], sb[(lo >> 5) + 2]);
-#else
-  (void)io; (void)c; (void)sb; (void)fwd; (void)rev;
-  return make_uint2(0u, 0u);
-#endif
-}
 __device__ __forceinline__ void cert_cores(const CertIO& io, const CertSmem& cs, int32_t c,
-                                           const uint32_t* sb, bool fwd, bool rev, uint2 pre) {
+                                           const uint32_t* sb, bool fwd, bool rev) {
   unsigned char* base = cs.acore + (size_t)(c & 1) * kABuf;
   constexpr uint32_t kQuads = kACores * 2;    // 100 groups of 4 rows per direction
   const uint32_t t = threadIdx.x;
@@ -594,7 +545,7 @@ __device__ __forceinline__ void cert_cores(const CertIO& io, const CertSmem& cs,
   const int32_t p0 = dir == 0 ? io.JT + (int32_t)cert_kb(c) + 4 * (int32_t)g
                               : io.JT + 127 - (int32_t)cert_kb(c - (int32_t)kLag) - 4 * (int32_t)g;
   uint32_t w[5];
-  seq20(sb, p0, dir == 0 ? 1 : -1, (int32_t)io.L, w, pre);
+  seq20(sb, p0, dir == 0 ? 1 : -1, (int32_t)io.L, w);
   uint4* dst = reinterpret_cast<uint4*>(base + (size_t)dir * kACores * 128 + 64 * g);
   PSL_CHK(in_buf(dst + 3, cs.acore, 2 * kABuf, 16), 15);
   // row r of the quad = the 16 bytes from byte r; rows in a lane-rotated order

@@ -1274,9 +1274,6 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
 #ifndef PSL_LATE_WAIT
 #define PSL_LATE_WAIT 1
 #endif
-#ifndef PSL_FWD_LATE
-#define PSL_FWD_LATE 0             // 1: forward MMAs of chunk c issued at the top of iteration c + 1 (measured +0.6 % m20, +1.5 % m16)
-#endif
         uint32_t issued = 0;        // bit (c & 1): iteration c committed MMAs not yet waited for
         // iteration c: build chunk c, stage the sequence cores of forward kappa-chunk c and
         // reversed kappa'-chunk c - kLag, issue their tcgen05 MMAs (one thread, async),
@@ -1290,7 +1287,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         constexpr int kHalf = PSL_ISSUE_SPLIT > 1 ? kCCols / 2 : kCCols;
         const bool early = t < (uint32_t)kThreads;   // warps 0-7 (PSL_STAGGER)
         int32_t pend_c = -1;
-        bool pend_rv = false, pend_fw = false;
+        bool pend_rv = false;
         uint32_t pend_started = 0;
         for (uint32_t c = 0; c < c_end + kLag; ++c) {
           int32_t rv_c = -1;         // this iteration finishes the reversed MMAs of rv_c
@@ -1298,12 +1295,6 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
             if ((t >> 5) == PSL_REV_WARP)
               cert_issue_dir(cs, tmem, pend_c, 1, pend_rv, pend_started, &ctl->mbar[pend_c & 1], 0, kHalf,
                              kHalf == kCCols);
-#if PSL_FWD_LATE
-            // forward MMAs of the previous chunk too: the tensor pipe (shared with
-            // mma.sync, tcgen05 first) runs them under the build, not under the cross term
-            if ((t >> 5) == PSL_FWD_WARP)
-              cert_issue_dir(cs, tmem, pend_c, 0, pend_fw, pend_started, &ctl->mbar[pend_c & 1], 0, kCCols, true);
-#endif
             rv_c = pend_c;
             pend_c = -1;
           }
@@ -1318,7 +1309,6 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
 #endif
           PT_MARK(0);
           const bool fw = (ctl->cfw[c >> 5] >> (c & 31)) & 1u, rv = (ctl->crv[c >> 5] >> (c & 31)) & 1u;
-          const uint2 corew = cert_core_words(io, (int32_t)c, sm.sb, fw, rv);
           if (c < c_end) {
             if (builder) {
               if (c + 2 < c_end) cert_prefetch(io, cs, c + 2);
@@ -1352,7 +1342,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
             issued &= ~(1u << (c & 1));
           }
 #endif
-          cert_cores(io, cs, (int32_t)c, sm.sb, fw, rv, corew);
+          cert_cores(io, cs, (int32_t)c, sm.sb, fw, rv);
           PT_MARK(2);
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
           PT_MARK(9);
@@ -1364,31 +1354,25 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           if ((fw || rv)) {
 #endif
             // warp 15 (stages no cores) issues, one lane elected per MMA
-#if !PSL_FWD_LATE
             if ((t >> 5) == PSL_FWD_WARP)
               cert_issue_dir(cs, tmem, (int32_t)c, 0, fw, started, &ctl->mbar[c & 1], 0, kHalf, kHalf == kCCols);
-#endif
-            pend_c = (int32_t)c; pend_rv = rv; pend_fw = fw; pend_started = started;
+            pend_c = (int32_t)c; pend_rv = rv; pend_started = started;
             started |= (fw ? 1u : 0u) | (rv ? 2u : 0u);   // uniform copy of the issuer's flags
             numma += (fw ? kCCols : 0) + (rv ? kCCols : 0);
             issued |= 1u << (c & 1);
           }
           PT_MARK(4);
-          if (c < c_end && !(PSL_STAGGER && early)) {   // zone-1 cross MMAs, band-1 cells
+          if (c < c_end && !(PSL_STAGGER && early)) {   // zone-1 cross MMAs
             cert_cross_chunk(io, cs, ln, c, XACC, nmma);
             PT_MARK(5);
             if (io.chain && t == kCertThreads - 64) cert_chain_chunk(io, cs, c, chain);
             PT_MARK(6);
           }
-          if (!PSL_FWD_LATE && kHalf < kCCols && pend_c == (int32_t)c && (t >> 5) == PSL_FWD_WARP)
+          if (kHalf < kCCols && pend_c == (int32_t)c && (t >> 5) == PSL_FWD_WARP)
             cert_issue_dir(cs, tmem, (int32_t)c, 0, fw, pend_started, &ctl->mbar[c & 1], kHalf, kCCols, true);
         }
         if (pend_c >= 0 && (t >> 5) == PSL_REV_WARP)
           cert_issue_dir(cs, tmem, pend_c, 1, pend_rv, pend_started, &ctl->mbar[pend_c & 1], 0, kCCols, true);
-#if PSL_FWD_LATE
-        if (pend_c >= 0 && (t >> 5) == PSL_FWD_WARP)
-          cert_issue_dir(cs, tmem, pend_c, 0, pend_fw, pend_started, &ctl->mbar[pend_c & 1], 0, kCCols, true);
-#endif
         }
         PT_MARK(0);
         // the tail chunks, streamed while the last MMAs drain
