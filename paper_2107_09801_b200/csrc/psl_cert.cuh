@@ -952,32 +952,42 @@ __device__ __forceinline__ void cert_cross_rows(const int (&acc)[kCertTiles][4],
 
 #endif  // PSL_XTMEM
 
-// TMEM accumulators -> linrow[r_lo + u] (threads 0..127 = TMEM lanes): forward
-// lane rho, N-group g -> u = rho + 128 (7 - g); reversed lane r -> u = 127 - r +
-// 128 g; value = sum_d digit-column d x 256^d x 2^qH.
-__device__ __forceinline__ void cert_lin_rows(uint32_t tmem, bool rev, uint32_t started,
-                                              double unitH, const CertIO& io, double* linrow) {
-  const uint32_t t = threadIdx.x;
-  if (t >= 128) return;
+// TMEM accumulators -> per-row doubles, all 16 warps: warps 0-7 the forward
+// accumulators (-> linrow), 8-15 the reversed ones (-> linrev); warp w reads TMEM
+// lanes 32 (w & 3) .. + 31 and N-groups 4 ((w >> 2) & 1) .. + 3, four loads in
+// flight before one wait.  Forward lane rho, N-group g -> u = rho + 128 (7 - g);
+// reversed lane r -> u = 127 - r + 128 g; value = sum_d digit-column d x 256^d x 2^qH.
+// The row's linear term is linrow + linrev (one rounding, as fwd then += rev).
+__device__ __forceinline__ void cert_lin_rows(uint32_t tmem, uint32_t started, double unitH, const CertIO& io,
+                                              double* linrow, double* linrev) {
+  const uint32_t w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool rev = w >= 8;
+  const uint32_t rho = 32 * (w & 3) + lane, g0 = 4 * ((w >> 2) & 1);
   const uint32_t col0 = rev ? 64u : 0u;
   const bool have = (started >> (rev ? 1 : 0)) & 1u;
-#pragma unroll 1
-  for (int g = 0; g < 8; ++g) {
-    uint32_t v[8];
-    const uint32_t addr = tmem + ((uint32_t)(32 * (t >> 5)) << 16) + col0 + 8 * g;
+  uint32_t v[4][8];
+#pragma unroll
+  for (int gg = 0; gg < 4; ++gg) {
+    const uint32_t addr = tmem + ((32u * (w & 3)) << 16) + col0 + 8 * (g0 + gg);
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "=r"(v[gg][0]), "=r"(v[gg][1]), "=r"(v[gg][2]), "=r"(v[gg][3]), "=r"(v[gg][4]),
+                   "=r"(v[gg][5]), "=r"(v[gg][6]), "=r"(v[gg][7])
                  : "r"(addr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  double* out = rev ? linrev : linrow;
+#pragma unroll
+  for (int gg = 0; gg < 4; ++gg) {
+    const uint32_t g = g0 + gg;
     double x = 0.0;
     if (have) {
 #pragma unroll
-      for (int d = 7; d >= 0; --d) x = __dadd_rn(__dmul_rn(x, 256.0), (double)(int32_t)v[d]);
+      for (int d = 7; d >= 0; --d) x = __dadd_rn(__dmul_rn(x, 256.0), (double)(int32_t)v[gg][d]);
       x = __dmul_rn(x, unitH);
     }
-    const uint32_t u = rev ? 127 - t + 128 * g : t + 128 * (7 - g);
-    const uint32_t rho = io.r_lo + u;
-    if (u < io.r_hi - io.r_lo && rho < (uint32_t)kGroup) linrow[rho] = rev ? __dadd_rn(linrow[rho], x) : x;
+    const uint32_t u = rev ? 127 - rho + 128 * g : rho + 128 * (7 - g);
+    const uint32_t r = io.r_lo + u;
+    if (u < io.r_hi - io.r_lo && r < (uint32_t)kGroup) out[r] = x;
   }
 }
 

@@ -589,7 +589,8 @@ __device__ __forceinline__ int32_t neighbour_psl(const int2* h, uint32_t nh, int
                                                  const uint32_t* sb) {
   const int sj = sval(sb, j);
   int32_t peak = 0;
-  for (uint32_t e = 0; e < nh; ++e) {
+#pragma unroll 4
+  for (uint32_t e = 0; e < nh; ++e) {          // unrolled: the entries' bit loads overlap
     const int2 kc = h[e];
     if (!filtered && abs(kc.y) < thr) continue;
     const uint32_t k = (uint32_t)kc.x;
@@ -1285,6 +1286,11 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         // in the next iteration: half at the loop top, half after its build.  So
         // the tensor-pipe waits are split over two warps and two points each.
         constexpr int kHalf = PSL_ISSUE_SPLIT > 1 ? kCCols / 2 : kCCols;
+#ifndef PSL_FWD_AFTER_CROSS
+#define PSL_FWD_AFTER_CROSS 1      // warp 15 runs its cross rows before issuing the forward MMAs
+                                   // (the tensor queue has drained by then; -1.7 % ms/step at m20)
+#endif
+        constexpr int kHalfF = PSL_FWD_AFTER_CROSS ? 0 : kHalf;
         const bool early = t < (uint32_t)kThreads;   // warps 0-7 (PSL_STAGGER)
         int32_t pend_c = -1;
         bool pend_rv = false;
@@ -1354,8 +1360,8 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           if ((fw || rv)) {
 #endif
             // warp 15 (stages no cores) issues, one lane elected per MMA
-            if ((t >> 5) == PSL_FWD_WARP)
-              cert_issue_dir(cs, tmem, (int32_t)c, 0, fw, started, &ctl->mbar[c & 1], 0, kHalf, kHalf == kCCols);
+            if (kHalfF > 0 && (t >> 5) == PSL_FWD_WARP)
+              cert_issue_dir(cs, tmem, (int32_t)c, 0, fw, started, &ctl->mbar[c & 1], 0, kHalfF, kHalfF == kCCols);
             pend_c = (int32_t)c; pend_rv = rv; pend_started = started;
             started |= (fw ? 1u : 0u) | (rv ? 2u : 0u);   // uniform copy of the issuer's flags
             numma += (fw ? kCCols : 0) + (rv ? kCCols : 0);
@@ -1368,8 +1374,8 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
             if (io.chain && t == kCertThreads - 64) cert_chain_chunk(io, cs, c, chain);
             PT_MARK(6);
           }
-          if (kHalf < kCCols && pend_c == (int32_t)c && (t >> 5) == PSL_FWD_WARP)
-            cert_issue_dir(cs, tmem, (int32_t)c, 0, fw, pend_started, &ctl->mbar[c & 1], kHalf, kCCols, true);
+          if (kHalfF < kCCols && pend_c == (int32_t)c && (t >> 5) == PSL_FWD_WARP)
+            cert_issue_dir(cs, tmem, (int32_t)c, 0, fw, pend_started, &ctl->mbar[c & 1], kHalfF, kCCols, true);
         }
         if (pend_c >= 0 && (t >> 5) == PSL_REV_WARP)
           cert_issue_dir(cs, tmem, pend_c, 1, pend_rv, pend_started, &ctl->mbar[pend_c & 1], 0, kCCols, true);
@@ -1459,17 +1465,17 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         cert_cross_rows(acc, ctl->c_unitR, cs.xrow);
 #endif
 #undef XACC
-        cert_lin_rows(tmem, false, started, ctl->c_unitH, io, linrow);
+        double* linrev = reinterpret_cast<double*>(cs.dring);   // free: band 1 is done
+        cert_lin_rows(tmem, started, ctl->c_unitH, io, linrow, linrev);
+        double v5 = 0.0;                       // window constant i = t: its warp sums in fixed order
+        if (t < 5)
+          for (int x = 0; x < (int)(blockDim.x >> 5); ++x) v5 = __dadd_rn(v5, ctl->rs5[t][x]);
         __syncthreads();
-        cert_lin_rows(tmem, true, started, ctl->c_unitH, io, linrow);
+        if (t < 5) ctl->rs5[t][0] = v5;
         __syncthreads();
         if (t == 0) {
           double sm5[5];
-          for (int i = 0; i < 5; ++i) {
-            double v = 0.0;
-            for (int x = 0; x < (int)(blockDim.x >> 5); ++x) v = __dadd_rn(v, ctl->rs5[i][x]);
-            sm5[i] = v;
-          }
+          for (int i = 0; i < 5; ++i) sm5[i] = ctl->rs5[i][0];
           const double u = 0x1p-53;
           const double Sc = __dadd_rn(__dadd_rn(sm5[0], sm5[1]), sm5[2]);
           ctl->c_sconst = Sc;
@@ -1499,7 +1505,7 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
             const uint32_t rho = kJ * (t - kThreads) + m;
             if (rho < r_lo || rho >= r_hi) continue;
             const uint32_t j = (uint32_t)(j0 + (int32_t)rho);
-            const double lin = linrow[rho], xv = xrow[rho];
+            const double lin = __dadd_rn(linrow[rho], linrev[rho]), xv = xrow[rho];
             const uint32_t Mj = max(j, L - 1 - j);
             const double B4 = __dadd_rn(__dmul_rn(4.0, ivm[rho]),   // band-1 sum, stored above
                                         cert_band2_const(io, ctl->M_hi - ctl->M_lo, Mj - ctl->M_lo));
