@@ -1291,6 +1291,11 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
                                    // (the tensor queue has drained by then; -1.7 % ms/step at m20)
 #endif
         constexpr int kHalfF = PSL_FWD_AFTER_CROSS ? 0 : kHalf;
+#ifndef PSL_REV_ISSUE
+#define PSL_REV_ISSUE 2            // reversed MMAs of chunk c: 0 top of c + 1, 1 after warp 14's
+                                   // build in c + 1 (+0.6 %), 2 after warp 14's cross rows in c (-0.7 %)
+#endif
+        constexpr int kHalfR = PSL_REV_ISSUE == 1 ? 0 : kHalf;
         const bool early = t < (uint32_t)kThreads;   // warps 0-7 (PSL_STAGGER)
         int32_t pend_c = -1;
         bool pend_rv = false;
@@ -1298,9 +1303,9 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
         for (uint32_t c = 0; c < c_end + kLag; ++c) {
           int32_t rv_c = -1;         // this iteration finishes the reversed MMAs of rv_c
           if (pend_c >= 0) {
-            if ((t >> 5) == PSL_REV_WARP)
-              cert_issue_dir(cs, tmem, pend_c, 1, pend_rv, pend_started, &ctl->mbar[pend_c & 1], 0, kHalf,
-                             kHalf == kCCols);
+            if (PSL_REV_ISSUE != 2 && kHalfR > 0 && (t >> 5) == PSL_REV_WARP)
+              cert_issue_dir(cs, tmem, pend_c, 1, pend_rv, pend_started, &ctl->mbar[pend_c & 1], 0, kHalfR,
+                             kHalfR == kCCols);
             rv_c = pend_c;
             pend_c = -1;
           }
@@ -1326,8 +1331,8 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           } else {
             cert_zero_digits(cs, c);
           }
-          if (kHalf < kCCols && rv_c >= 0 && (t >> 5) == PSL_REV_WARP)
-            cert_issue_dir(cs, tmem, rv_c, 1, pend_rv, pend_started, &ctl->mbar[rv_c & 1], kHalf, kCCols, true);
+          if (PSL_REV_ISSUE != 2 && kHalfR < kCCols && rv_c >= 0 && (t >> 5) == PSL_REV_WARP)
+            cert_issue_dir(cs, tmem, rv_c, 1, pend_rv, pend_started, &ctl->mbar[rv_c & 1], kHalfR, kCCols, true);
           PT_MARK(1);
           // PSL_STAGGER: warps 0-7 run the cross MMAs / band cells of chunk c - 1
           // after building chunk c, warps 8-15 before (end of the previous
@@ -1376,8 +1381,10 @@ __global__ void __launch_bounds__(kCert ? 2 * kThreads : kThreads, kCert ? 1 : 2
           }
           if (kHalfF < kCCols && pend_c == (int32_t)c && (t >> 5) == PSL_FWD_WARP)
             cert_issue_dir(cs, tmem, (int32_t)c, 0, fw, pend_started, &ctl->mbar[c & 1], kHalfF, kCCols, true);
+          if (PSL_REV_ISSUE == 2 && pend_c == (int32_t)c && (t >> 5) == PSL_REV_WARP)
+            cert_issue_dir(cs, tmem, (int32_t)c, 1, rv, pend_started, &ctl->mbar[c & 1], 0, kCCols, true);
         }
-        if (pend_c >= 0 && (t >> 5) == PSL_REV_WARP)
+        if (PSL_REV_ISSUE != 2 && pend_c >= 0 && (t >> 5) == PSL_REV_WARP)
           cert_issue_dir(cs, tmem, pend_c, 1, pend_rv, pend_started, &ctl->mbar[pend_c & 1], 0, kCCols, true);
         }
         PT_MARK(0);
