@@ -8,4 +8,4 @@ for cfg in "2048 auto" "5000 auto" "2048 exact" "70000 auto" "300000 auto"; do
   timeout 600 python tools/sanitize_run.py $cfg 12 >> gpurun_out/s2_bounds_runs.log 2>&1; echo "run $cfg = $?"
 done
 unset PSLB200_LIB
-timeout 900 ./tools/ubench/umma_imma > gpurun_out/s2_umma_imma.txt 2>&1; echo ub=$?; cat gpurun_out/s2_umma_imma.txt
+
