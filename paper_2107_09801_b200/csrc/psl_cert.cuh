@@ -438,7 +438,10 @@ __device__ __forceinline__ void cert_build(const CertIO& io, const CertSmem& cs,
 // rounding budget of the window sums is unchanged.
 __device__ __forceinline__ void cert_tail(const CertIO& io, uint32_t c0, uint32_t nch,
                                           const uint32_t* sb, int32_t& pmax, double (&part)[5]) {
-  constexpr uint32_t U = 4;
+#ifndef PSL_TAIL_U
+#define PSL_TAIL_U 8                // (4: +1.0 % at m20, 16: spills)
+#endif
+  constexpr uint32_t U = PSL_TAIL_U;   // chunks per streamed group (loads first)
   const uint32_t t = threadIdx.x;
 #pragma unroll 1
   for (uint32_t c = c0; c < nch; c += U) {
